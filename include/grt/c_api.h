@@ -1,0 +1,249 @@
+/*
+ * grt/c_api.h -- C ABI of the B200-native graphrt decode path.
+ *
+ * Every entry point replaces one piece of the reference's C++ runtime/operator
+ * API (reference = /root/reference/proj/core, namespace graphrt).  Plain C types,
+ * opaque handles, caller-owned host buffers, no exceptions: every call returns a
+ * grt_status whose numbering is the reference Errc list (error.hpp:10-39) in
+ * declaration order, followed by the device-side codes.
+ *
+ * Threading: one host thread per session (the reference is single-threaded,
+ * SPEC.md:217); sessions on different devices may run concurrently.  The library
+ * runs its own capture thread internally (asynchronous graph capture).
+ */
+#ifndef GRT_C_API_H
+#define GRT_C_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRT_ABI_VERSION 1
+
+/* Replaces graphrt::Errc (error.hpp:10-39) + Error exceptions. */
+typedef enum grt_status {
+  GRT_OK = 0,
+  GRT_ShapeMismatch = 1,
+  GRT_TokenOutOfRange = 2,
+  GRT_EmptyCache = 3,
+  GRT_CacheFull = 4,
+  GRT_InvalidConfig = 5,
+  GRT_LengthOutOfRange = 6,
+  GRT_PromptTooLong = 7,
+  GRT_EmptyPrompt = 8,
+  GRT_CaptureInProgress = 9,
+  GRT_CaptureViolation = 10,
+  GRT_ForeignBuffer = 11,
+  GRT_SessionClosed = 12,
+  GRT_EmptyCapture = 13,
+  GRT_ReplayShapeError = 14,
+  GRT_WrongLength = 15,
+  GRT_KeyMismatch = 16,
+  GRT_WarmupExceedsCapacity = 17,
+  GRT_StaticInFusedBlock = 18,
+  GRT_DeviceStopped = 19,
+  GRT_UnknownEvent = 20,
+  GRT_EmptySamples = 21,
+  GRT_IoError = 22,
+  /* device-side failures (no reference counterpart) */
+  GRT_CudaError = 100,
+  GRT_NvrtcError = 101,
+  GRT_NcclError = 102,
+  GRT_IpcError = 103,
+  GRT_Unsupported = 104,
+  GRT_NoDevice = 105
+} grt_status;
+
+typedef enum grt_arch { GRT_ARCH_REF = 0, GRT_ARCH_LLAMA = 1 } grt_arch;
+typedef enum grt_dtype { GRT_F32 = 0, GRT_BF16 = 1 } grt_dtype;
+typedef enum grt_init { GRT_INIT_MT19937 = 0, GRT_INIT_PHILOX = 1, GRT_INIT_NONE = 2 } grt_init;
+
+/* Replaces graphrt::RunMode (pipeline.hpp:18-24) -- same order. */
+typedef enum grt_run_mode {
+  GRT_MODE_EAGER = 0,
+  GRT_MODE_HYBRID = 1,
+  GRT_MODE_GRAPH_ONLY = 2,
+  GRT_MODE_ABLATE_ASYNC = 3,
+  GRT_MODE_ABLATE_FUSED = 4,
+  GRT_MODE_ABLATE_BOTH = 5
+} grt_run_mode;
+
+/* Replaces graphrt::EvictionPolicy (graph_cache.hpp:13). */
+typedef enum grt_eviction { GRT_EVICT_LEAST_USED = 0, GRT_EVICT_LRU = 1 } grt_eviction;
+
+/* Replaces graphrt::StepPath (pipeline.hpp:43). */
+typedef enum grt_step_path { GRT_PATH_REPLAYED = 0, GRT_PATH_EAGER_FALLBACK = 1 } grt_step_path;
+
+/* Replaces graphrt::SampleStrategy (kernels.hpp:105-115), extended with top-k/top-p. */
+typedef enum grt_sample_kind {
+  GRT_SAMPLE_GREEDY = 0,
+  GRT_SAMPLE_TEMPERATURE = 1, /* reference-compatible: mt19937_64 uniform01, inverse CDF */
+  GRT_SAMPLE_TOPKP = 2        /* integer-CDF top-k/top-p, Philox4x32-10 draws */
+} grt_sample_kind;
+
+/* Replaces graphrt::ModelConfig (model.hpp:17-29), extended for LLaMA/bf16/TP. */
+typedef struct grt_model_config {
+  int32_t arch;        /* grt_arch */
+  int32_t n_layers;
+  int32_t d_model;
+  int32_t n_heads;
+  int32_t vocab_size;
+  int32_t max_seq_len;
+  int32_t d_ff;        /* 0 => 4*d_model (model.hpp:26) */
+  float norm_eps;      /* ln_eps (model.hpp:23) */
+  uint64_t seed;       /* weight init seed (model.hpp:24) */
+  int32_t init;        /* grt_init */
+  int32_t weight_dtype;/* grt_dtype */
+  int32_t kv_dtype;    /* grt_dtype */
+  float rope_theta;
+  int32_t device;      /* CUDA ordinal */
+  int32_t tp_size;     /* 1 = single GPU */
+  int32_t tp_rank;
+} grt_model_config;
+
+/* Replaces graphrt::CacheConfig (pipeline.hpp:122-128), plus the bucket width. */
+typedef struct grt_cache_config {
+  uint64_t capacity;
+  int32_t warmup_lo;
+  int32_t warmup_hi;
+  int32_t prefill_uses_graphs;
+  int32_t policy;      /* grt_eviction */
+  int32_t bucket_size; /* KV positions per graph key; 1 = the reference's exact-length keys */
+  int32_t batched_prefill; /* 1 = one batched prefill pass (TTFT path); 0 = token-by-token like the reference */
+} grt_cache_config;
+
+typedef struct grt_sample_params {
+  int32_t kind;        /* grt_sample_kind */
+  float temperature;
+  int32_t top_k;       /* 0 = off */
+  float top_p;         /* >= 1 = off */
+  uint64_t seed;       /* sampler_seed (pipeline.hpp:138) */
+} grt_sample_params;
+
+/* Replaces graphrt::GenerationRequest (pipeline.hpp:133-141). */
+typedef struct grt_generation_request {
+  int32_t mode;        /* grt_run_mode */
+  const int32_t* prompt;
+  int32_t prompt_len;
+  int32_t gen_len;
+  grt_sample_params sampling;
+} grt_generation_request;
+
+/* Replaces graphrt::Counters (virtual_device.hpp:41-49) with real counts. */
+typedef struct grt_counters {
+  uint64_t dispatches;       /* host submissions (kernel launches + graph launches) */
+  uint64_t kernel_launches;  /* kernels launched directly by the host */
+  uint64_t fused_blocks;     /* dynamic blocks launched outside a graph */
+  uint64_t graph_replays;    /* cudaGraphLaunch calls */
+  uint64_t captures;         /* graphs captured + instantiated */
+  uint64_t events_recorded;
+  uint64_t events_waited;
+  uint64_t graph_kernel_nodes; /* kernels executed inside replayed graphs */
+} grt_counters;
+
+/* Replaces graphrt::CacheStats (graph_cache.hpp:18-24). */
+typedef struct grt_cache_stats {
+  uint64_t hits, misses, inserts, evictions, releases;
+} grt_cache_stats;
+
+/* Replaces graphrt::GenerationResult (pipeline.hpp:143-159).  Array fields are
+ * caller-owned buffers of the stated length (NULL = not requested). */
+typedef struct grt_generation_result {
+  int32_t* tokens;          /* [gen_len] */
+  double* per_token_us;     /* [gen_len]; [0] measured from prefill completion */
+  int32_t* prefill_paths;   /* [prompt_len] grt_step_path (or [1] for a batched prefill) */
+  int32_t* decode_paths;    /* [gen_len] */
+  double ttft_us;           /* request entry -> first token visible on the host */
+  double total_us;          /* request entry -> everything retired */
+  double prefill_us;        /* device time of the prefill (first pass start -> last pass end) */
+  grt_counters counters;
+  grt_cache_stats cache_delta;
+  int32_t captures_completed;
+  uint64_t cache_released;
+  double* host_token_us;    /* [gen_len] host time (us from request entry) each token became visible */
+} grt_generation_result;
+
+typedef struct grt_model grt_model;
+typedef struct grt_session grt_session;
+
+/* ---- library ---------------------------------------------------------------- */
+const char* grt_status_name(grt_status s);     /* errc_name (error.cpp:5-31) */
+const char* grt_last_error(void);              /* thread-local message of the last failure */
+int32_t grt_abi_version(void);
+grt_status grt_device_count(int32_t* n);
+/* Compiles the NVRTC dynamic-op module for a shape without loading it (no GPU needed). */
+grt_status grt_jit_compile_check(int32_t d_model, int32_t vocab, int32_t max_seq, int32_t weight_bf16, int32_t arch_ref,
+                                 uint64_t* cubin_bytes);
+void grt_model_config_default(grt_model_config* c); /* ModelConfig{} defaults */
+void grt_cache_config_default(grt_cache_config* c); /* CacheConfig{} defaults */
+
+/* ---- model (replaces graphrt::Model, model.hpp:58-132) --------------------- */
+grt_status grt_model_create(const grt_model_config* cfg, grt_model** out);   /* Model::Model */
+grt_status grt_model_destroy(grt_model* m);
+/* Overwrites one weight tensor from host memory given in the REFERENCE layout
+ * ([k,n] for matrices, model.hpp:33-45); name e.g. "layers.3.wq", "head". */
+grt_status grt_model_upload(grt_model* m, const char* tensor, const void* host, size_t bytes,
+                            int32_t host_dtype);
+/* Copies one weight tensor back in the reference layout as fp32. */
+grt_status grt_model_download(grt_model* m, const char* tensor, float* host, size_t numel);
+grt_status grt_model_weight_bytes(grt_model* m, uint64_t* bytes);            /* HBM bytes of weights */
+grt_status grt_model_decode_bytes(grt_model* m, int32_t length, uint64_t* bytes); /* algorithmic bytes/pass */
+
+/* ---- session (replaces graphrt::Session, pipeline.hpp:165-189) ------------- */
+grt_status grt_session_create(grt_model* m, const grt_cache_config* cc, grt_session** out);
+grt_status grt_session_destroy(grt_session* s);
+grt_status grt_generate(grt_session* s, const grt_generation_request* req,
+                        grt_generation_result* res);                           /* Session::run */
+grt_status grt_cache_stats_get(grt_session* s, grt_cache_stats* st, uint64_t* size);
+/* Times each kernel of the static plan for bucket `key` in isolation: `iters`
+ * back-to-back launches bracketed by CUDA events on the session's compute
+ * stream.  Fills up to `cap` entries of avg_ms / bytes (algorithmic HBM bytes)
+ * and names (NUL-separated into `names`, `names_len` bytes); *n = plan size. */
+grt_status grt_profile_plan(grt_session* s, int32_t key, int32_t iters, double* avg_ms, int64_t* bytes,
+                            char* names, int32_t names_len, int32_t cap, int32_t* n);
+grt_status grt_session_counters(grt_session* s, grt_counters* c);
+
+/* ---- step-level API (Model::step_math / prefill_math / reset, model.cpp:168-183) */
+grt_status grt_reset(grt_session* s);
+grt_status grt_step(grt_session* s, int32_t token);                 /* extend_position + slot append + plan(cur_len) */
+grt_status grt_prefill(grt_session* s, const int32_t* ids, int32_t n); /* prefill_math */
+grt_status grt_cur_len(grt_session* s, int32_t* len);
+grt_status grt_get_logits(grt_session* s, float* out, int32_t n);   /* model.logits() */
+grt_status grt_get_kv_row(grt_session* s, int32_t layer, int32_t slot, int32_t row, float* out); /* [h*dh] */
+grt_status grt_sample(grt_session* s, const grt_sample_params* p, int32_t* token); /* make_sample_op */
+grt_status grt_sampler_reset(grt_session* s, uint64_t seed);        /* SamplerRng::reset */
+
+/* ---- graph cache policy (replaces graphrt::GraphCache, graph_cache.hpp:29-81) ---
+ * The session owns its own cache of cudaGraphExec_t; this standalone handle runs
+ * the identical policy code on placeholder graphs (no GPU), for policy tests. */
+typedef struct grt_graph_cache grt_graph_cache;
+grt_status grt_graph_cache_create(uint64_t capacity, int32_t policy, grt_graph_cache** out);
+grt_status grt_graph_cache_destroy(grt_graph_cache* c);
+grt_status grt_graph_cache_lookup(grt_graph_cache* c, int32_t key, int32_t* hit);
+/* graph_key != key reproduces KeyMismatch; *evicted = INT32_MIN when nothing was evicted. */
+grt_status grt_graph_cache_insert(grt_graph_cache* c, int32_t key, int32_t graph_key, int32_t* evicted);
+grt_status grt_graph_cache_warmup(grt_graph_cache* c, int32_t lo, int32_t hi, int32_t* captured);
+grt_status grt_graph_cache_begin_session(grt_graph_cache* c);
+grt_status grt_graph_cache_release_inactive(grt_graph_cache* c, uint64_t* dropped);
+grt_status grt_graph_cache_query(grt_graph_cache* c, int32_t key, int32_t* contains, uint64_t* use_count,
+                                 uint64_t* size, grt_cache_stats* stats);
+
+/* ---- op-level API on device pointers (kernel parity tests) ----------------- */
+/* out[n] = W[n,k] . x[k] with W in the device ([n,k], row-major) layout. */
+grt_status grt_op_gemv(const void* w, int32_t w_dtype, const float* x, float* out, int32_t n, int32_t k,
+                       void* stream);
+/* Single-query attention over positions [0,len) of K/V laid out [h, max_seq, dh]. */
+grt_status grt_op_attention(const float* q, const void* k, const void* v, int32_t kv_dtype, float* out,
+                            int32_t n_heads, int32_t head_dim, int32_t max_seq, int32_t len, float scale,
+                            void* stream);
+/* Samples from device logits; writes the token to *token_dev (device int32). */
+grt_status grt_op_sample(const float* logits, int32_t vocab, const grt_sample_params* p, uint64_t step,
+                         double uniform, int32_t* token_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRT_C_API_H */

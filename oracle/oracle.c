@@ -134,7 +134,7 @@ float oc_round_bf16(float f) { return oc_bf16_to_f32(oc_f32_to_bf16(f)); }
  * reduction + degree-6 polynomial, every step an explicit fmaf or a single
  * rounded op (device twin: csrc/jit/sampler_math.cuh). */
 float oc_grt_expf(float z) {
-  if (!(z > -30.0f)) return 0.0f; /* e^-30 < 2^-43: below the 2^-32 weight quantum */
+  if (!(z > -30.0f)) return 0.0f; /* e^-30 < 2^-43: below the 2^-31 weight quantum */
   if (z > 0.0f) z = 0.0f;
   float n = rintf(z * 1.44269504088896341f);
   float r = fmaf(n, -0.693145751953125f, z);
@@ -643,14 +643,14 @@ int oc_sample_temperature(const float* logits, int vocab, double temperature, oc
  * and temperature).  Bit-exact between this file and the NVRTC kernel because
  * every reduction is over integers:
  *   1. m = max logits; z_i = (l_i - m) / T (fp32 div); e_i = grt_expf(z_i)
- *   2. w_i = (uint64)(e_i * 2^32)                        (exact scaling, truncation)
+ *   2. w_i = (uint64)(e_i * 2^31)                        (exact scaling, truncation; < 2^32)
  *   3. rank key K_i = w_i << 16 | (0xFFFF - i)           (larger weight first, then lower index)
  *   4. top-k (k in [1,V], 0 = off): keep the k largest keys
  *   5. top-p (p in (0,1), >=1 = off): W = sum kept w; thresh = max(1, (uint64)(p * (double)W));
  *      walk kept keys in descending order, keep the shortest prefix whose weight sum >= thresh
  *   6. S = sum kept w; u = 53-bit Philox(seed, step) draw; r = min(S-1, (uint64)(u * (double)S))
  *   7. token = smallest index i (ascending) among kept with inclusive prefix weight > r.
- * Temperature <= 0 means greedy.  If S == 0 (cannot happen: w_max = 2^32) -> argmax. */
+ * Temperature <= 0 means greedy.  If S == 0 (cannot happen: w_max = 2^31) -> argmax. */
 typedef struct {
   uint64_t key;
   int idx;
@@ -680,7 +680,7 @@ int oc_sample_topkp(const float* logits, int vocab, float temperature, int top_k
   for (int i = 0; i < vocab; ++i) {
     const float z = (logits[i] - m) / temperature;
     const float e = oc_grt_expf(z);
-    w[i] = (uint64_t)(e * 4294967296.0f);
+    w[i] = (uint64_t)(e * 2147483648.0f);
     ents[i].key = (w[i] << 16) | (uint64_t)(0xFFFF - i);
     ents[i].idx = i;
   }

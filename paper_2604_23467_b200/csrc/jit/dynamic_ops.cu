@@ -1,0 +1,395 @@
+// dynamic_ops.cu -- NVRTC source of the DYNAMIC ops (the JIT context path).
+//
+// The reference's dynamic set is exactly {extend_position, kv_append,
+// sample_token} (kernels.hpp:14-19).  Here they are hand-written
+// CUDA compiled at session start by NVRTC for sm_100a, specialised on the model
+// shape through -D defines (GRT_D, GRT_V, GRT_MAXSEQ, GRT_WBF16, GRT_ARCH_REF).
+// They read every runtime value (token, position, RNG state) from the device
+// control block (ctrl.h), so they are capturable into the step graph.
+//
+// Compiled with --fmad=false: the integer-CDF sampler must reproduce
+// oracle.c:oc_sample_topkp bit for bit.
+#include "ctrl.h"
+
+#ifndef GRT_D
+#error "GRT_D must be defined"
+#endif
+#ifndef GRT_V
+#error "GRT_V must be defined"
+#endif
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+#define GRT_SAMPLE_THREADS 1024
+#ifndef INFINITY
+#define INFINITY __int_as_float(0x7f800000)
+#endif
+
+__device__ __forceinline__ void grt_griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grt_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ u64 grt_globaltimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ float grt_bf16_to_f32(unsigned short h) { return __uint_as_float(((u32)h) << 16); }
+
+// ---------------------------------------------------------------------------
+// extend_position + slot append (kernels.cpp:238-259, :205-236; model.cpp:156-162)
+//   x = emb[token] (+ pos_table[position] in the reference arch); cur_len++.
+// The zero rows the reference appends are overwritten by the static pass before
+// they are read (build_plan writes row length-1 before attention), so the
+// append reduces to the length bump.
+extern "C" __global__ void grt_preprocess(GrtCtrl* ctrl, const void* emb, const void* pos_table, float* x) {
+  __shared__ int s_pos, s_tok, s_ok;
+  grt_launch_dependents();
+  grt_griddep_wait();
+  if (threadIdx.x == 0) {
+    const int pos = ctrl->seq_len;
+    int ok = 1;
+    int tok = 0;
+    if (pos >= GRT_MAXSEQ || pos < 0) {
+      atomicOr(&ctrl->err, 2); /* CacheFull / position outside table */
+      ok = 0;
+    } else {
+      tok = ctrl->tokens[pos];
+      if (tok < 0 || tok >= GRT_V) {
+        atomicOr(&ctrl->err, 4); /* TokenOutOfRange */
+        ok = 0;
+      }
+    }
+    s_pos = pos;
+    s_tok = tok;
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const long long erow = (long long)s_tok * GRT_D;
+#if GRT_ARCH_REF
+  const long long prow = (long long)s_pos * GRT_D;
+#else
+  (void)pos_table;
+#endif
+  for (int j = threadIdx.x; j < GRT_D; j += blockDim.x) {
+#if GRT_WBF16
+    float e = grt_bf16_to_f32(((const unsigned short*)emb)[erow + j]);
+#if GRT_ARCH_REF
+    e = e + grt_bf16_to_f32(((const unsigned short*)pos_table)[prow + j]);
+#endif
+#else
+    float e = ((const float*)emb)[erow + j];
+#if GRT_ARCH_REF
+    e = e + ((const float*)pos_table)[prow + j];
+#endif
+#endif
+    x[j] = e;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) ctrl->seq_len = s_pos + 1;
+}
+
+// ---------------------------------------------------------------------------
+// Sampler (run_sampler, kernels.cpp:263-289, plus the integer-CDF top-k/top-p).
+
+__device__ __forceinline__ void philox4x32_10(u32 c[4], u32 k0, u32 k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const u32 hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const u32 hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const u32 n0 = hi1 ^ c[1] ^ k0;
+    const u32 n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+// Twin of oracle.c:oc_grt_expf -- every step an explicit fmaf or one rounded op.
+__device__ __forceinline__ float grt_expf(float z) {
+  if (!(z > -30.0f)) return 0.0f;
+  if (z > 0.0f) z = 0.0f;
+  const float n = rintf(z * 1.44269504088896341f);
+  float r = fmaf(n, -0.693145751953125f, z);
+  r = fmaf(n, -1.428606765330187e-06f, r);
+  float p = 1.3981999507e-3f;
+  p = fmaf(p, r, 8.3334519073e-3f);
+  p = fmaf(p, r, 4.1665795894e-2f);
+  p = fmaf(p, r, 1.6666665459e-1f);
+  p = fmaf(p, r, 5.0000001201e-1f);
+  const float r2 = r * r;
+  float y = fmaf(p, r2, r);
+  y = y + 1.0f;
+  return ldexpf(y, (int)n);
+}
+
+__device__ __forceinline__ u64 topkp_weight(const float* logits, int i, float m, float t) {
+  const float z = (logits[i] - m) / t;
+  const float e = grt_expf(z);
+  return (u64)(e * 2147483648.0f);
+}
+__device__ __forceinline__ u64 topkp_key(u64 w, int i) { return (w << 16) | (u64)(0xFFFF - i); }
+
+__device__ float block_max_f(float v, float* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = red[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+__device__ u64 block_sum_u64(u64 v, u64* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    u64 t = red[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// Finds, among keys with (key & mask) == prefix and key >= floor, the digit
+// bucket where the descending cumulative (count or weight) reaches `need`.
+__device__ void radix_pick(u64* hist, int shift, u64& prefix, u64& mask, u64& need) {
+  __shared__ u64 s_prefix, s_need;
+  if (threadIdx.x == 0) {
+    u64 nd = need;
+    int dg = 255;
+    for (; dg > 0; --dg) {
+      if (hist[dg] >= nd) break;
+      nd -= hist[dg];
+    }
+    s_prefix = prefix | ((u64)dg << shift);
+    s_need = nd;
+  }
+  __syncthreads();
+  prefix = s_prefix;
+  need = s_need;
+  mask |= (u64)255 << shift;
+  __syncthreads();
+}
+
+extern "C" __global__ void __launch_bounds__(GRT_SAMPLE_THREADS) grt_sample(GrtCtrl* ctrl, const float* logits) {
+  __shared__ float redf[32];
+  __shared__ u64 redu[32];
+  __shared__ u64 hist[256];
+  __shared__ int s_tok;
+  __shared__ u64 s_t0;
+  grt_launch_dependents();
+  grt_griddep_wait();
+  const int pos = ctrl->seq_len;
+  if (pos < ctrl->prompt_len) return;  // prefill pass: the token is given
+  const int step = pos - ctrl->prompt_len;
+  if (threadIdx.x == 0) s_t0 = grt_globaltimer();
+  const int kind = ctrl->sample_kind;
+  const int tid = threadIdx.x;
+  const float temperature = ctrl->temperature;
+
+  if (kind == 0 || !(temperature > 0.0f)) {
+    // greedy: strict >, lowest index wins ties (kernels.cpp:265-270)
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+      const float v = logits[i];
+      if (v > bv || bi == 0x7fffffff) {
+        bv = v;
+        bi = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    if ((tid & 31) == 0) {
+      sv[tid >> 5] = bv;
+      si[tid >> 5] = bi;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      bv = sv[tid];
+      bi = si[tid];
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (tid == 0) s_tok = bi;
+    }
+    __syncthreads();
+  } else if (kind == 1) {
+    // temperature, reference-compatible (kernels.cpp:271-288): one uniform01
+    // draw per sample (pre-generated by the host from mt19937_64(seed) in step
+    // order), fp32 softmax numerators, fp32 denominator summed in ascending
+    // index order (serial, as in the reference), inverse CDF walked in double.
+    float m = -INFINITY;
+    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) m = fmaxf(m, logits[i]);
+    m = block_max_f(m, redf);
+    float* probs = ctrl->scratch;
+    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) probs[i] = expf((logits[i] - m) / temperature);
+    __syncthreads();
+    __shared__ float s_denom;
+    if (tid == 0) {
+      float denom = 0.0f;
+      for (int i = 0; i < GRT_V; ++i) denom += probs[i];
+      s_denom = denom;
+    }
+    __syncthreads();
+    const double u = ctrl->uniforms[step] * (double)s_denom;
+    // inclusive prefix sums in double over contiguous per-thread blocks
+    const int per = (GRT_V + GRT_SAMPLE_THREADS - 1) / GRT_SAMPLE_THREADS;
+    const int b0 = tid * per, b1 = min(GRT_V, b0 + per);
+    double local = 0.0;
+    for (int i = b0; i < b1; ++i) local += (double)probs[i];
+    __shared__ double sc[GRT_SAMPLE_THREADS];
+    sc[tid] = local;
+    __syncthreads();
+    if (tid == 0) {
+      double acc = 0.0;
+      for (int t = 0; t < GRT_SAMPLE_THREADS; ++t) {
+        const double v = sc[t];
+        sc[t] = acc;
+        acc += v;
+      }
+      s_tok = GRT_V - 1;
+    }
+    __syncthreads();
+    double acc = sc[tid];
+    int found = -1;
+    for (int i = b0; i < b1; ++i) {
+      acc += (double)probs[i];
+      if (u < acc) {
+        found = i;
+        break;
+      }
+    }
+    if (found >= 0) atomicMin(&s_tok, found);
+    __syncthreads();
+  } else {
+    // integer-CDF top-k / top-p (oracle.c:oc_sample_topkp)
+    float m = -INFINITY;
+    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) m = fmaxf(m, logits[i]);
+    m = block_max_f(m, redf);
+    const int top_k = ctrl->top_k;
+    const float top_p = ctrl->top_p;
+    // (1) top-k threshold key
+    u64 kth = 0;
+    if (top_k > 0 && top_k < GRT_V) {
+      u64 prefix = 0, mask = 0, need = (u64)top_k;
+      for (int shift = 40; shift >= 0; shift -= 8) {
+        for (int b = tid; b < 256; b += GRT_SAMPLE_THREADS) hist[b] = 0;
+        __syncthreads();
+        for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+          const u64 key = topkp_key(topkp_weight(logits, i, m, temperature), i);
+          if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1ull);
+        }
+        __syncthreads();
+        radix_pick(hist, shift, prefix, mask, need);
+      }
+      kth = prefix;
+    }
+    // (2) top-p threshold key among keys >= kth
+    u64 W = 0;
+    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+      const u64 w = topkp_weight(logits, i, m, temperature);
+      if (topkp_key(w, i) >= kth) W += w;
+    }
+    W = block_sum_u64(W, redu);
+    u64 kappa = kth;
+    if (top_p > 0.0f && top_p < 1.0f) {
+      u64 thresh = (u64)((double)top_p * (double)W);
+      if (thresh < 1) thresh = 1;
+      u64 prefix = 0, mask = 0, need = thresh;
+      for (int shift = 40; shift >= 0; shift -= 8) {
+        for (int b = tid; b < 256; b += GRT_SAMPLE_THREADS) hist[b] = 0;
+        __syncthreads();
+        for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+          const u64 w = topkp_weight(logits, i, m, temperature);
+          const u64 key = topkp_key(w, i);
+          if (key >= kth && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], w);
+        }
+        __syncthreads();
+        radix_pick(hist, shift, prefix, mask, need);
+      }
+      kappa = prefix > kth ? prefix : kth;
+    }
+    // (3) draw and inverse CDF in index order over the kept set
+    const int per = (GRT_V + GRT_SAMPLE_THREADS - 1) / GRT_SAMPLE_THREADS;
+    const int b0 = tid * per, b1 = min(GRT_V, b0 + per);
+    u64 local = 0;
+    for (int i = b0; i < b1; ++i) {
+      const u64 w = topkp_weight(logits, i, m, temperature);
+      if (topkp_key(w, i) >= kappa) local += w;
+    }
+    __shared__ u64 sc[GRT_SAMPLE_THREADS];
+    sc[tid] = local;
+    __syncthreads();
+    __shared__ u64 s_S;
+    if (tid == 0) {
+      u64 acc = 0;
+      for (int t = 0; t < GRT_SAMPLE_THREADS; ++t) {
+        const u64 v = sc[t];
+        sc[t] = acc;
+        acc += v;
+      }
+      s_S = acc;
+      s_tok = 0x7fffffff;
+    }
+    __syncthreads();
+    const u64 S = s_S;
+    u32 c[4] = {(u32)step, (u32)((u64)step >> 32), 0u, 0x53616D70u};
+    const u64 seed = ctrl->seed;
+    philox4x32_10(c, (u32)seed, (u32)(seed >> 32));
+    const u64 bits = (((u64)c[1] << 32) | (u64)c[0]) >> 11;
+    const double u = (double)bits * 0x1.0p-53;
+    u64 r = (u64)(u * (double)S);
+    if (r >= S) r = S - 1;
+    u64 acc = sc[tid];
+    if (S > 0 && acc <= r && r < acc + local) {
+      for (int i = b0; i < b1; ++i) {
+        const u64 w = topkp_weight(logits, i, m, temperature);
+        if (topkp_key(w, i) < kappa) continue;
+        acc += w;
+        if (acc > r) {
+          s_tok = i;
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  if (tid == 0) {
+    const int tok = s_tok;
+    ctrl->tokens[pos] = tok;
+    if (step < ctrl->max_gen) {
+      ctrl->out_tokens[step] = tok;
+      ctrl->out_stamps[2 * step] = s_t0;
+      ctrl->out_stamps[2 * step + 1] = grt_globaltimer();
+    }
+    __threadfence_system();
+  }
+}

@@ -1,0 +1,102 @@
+// kernels.h -- host-side declarations of the sm_100a decode kernels.
+//
+// Plain CUDA runtime types only (no torch).  Each launcher enqueues one kernel
+// on `stream`, optionally with Programmatic Dependent Launch so the kernel's
+// weight prefetch overlaps the previous kernel (see common.cuh).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace grt {
+
+enum class Dt : int { F32 = 0, BF16 = 1 };
+
+enum NormKind : int { NORM_NONE = 0, NORM_LN = 1, NORM_RMS = 2 };
+
+// Epilogues of the fused GEMV.  Rows are processed in adjacent PAIRS (2p, 2p+1)
+// of the device weight layout; the pairing is what lets RoPE (rotate-half) and
+// SwiGLU (gate,up) finish inside the GEMV.
+enum EpiKind : int {
+  EPI_STORE = 0,     // out[r] = v                                  (LM head, plain GEMV)
+  EPI_RESID = 1,     // out[r] += v   (residual add, kernels.cpp:162-174) (Wo, W2/down)
+  EPI_QKV = 2,       // q -> q_out, k/v -> KV row seq_len-1 (kernels.cpp:188-203)
+  EPI_QKV_ROPE = 3,  // as EPI_QKV with rotate-half RoPE on q,k (LLaMA)
+  EPI_SWIGLU = 4,    // act[p] = silu(gate_p) * up_p                 (LLaMA gate/up)
+  EPI_RELU = 5,      // act[r] = max(v, 0)  (make_relu, kernels.cpp:176-186) (ref W1)
+};
+
+struct GemvParams {
+  const void* w = nullptr;  // [n_rows, k] row-major device layout (transposed reference [k,n])
+  int n_rows = 0;
+  int k = 0;
+  int rowb = 0;             // bytes of one row chunk slot in shared memory (set by the launcher)
+  const float* x = nullptr; // input activation [k] fp32
+  const float* gamma = nullptr;
+  const float* beta = nullptr;
+  float eps = 1e-5f;
+  float* out = nullptr;     // STORE / RESID / SWIGLU / RELU target
+  // QKV epilogue
+  float* q_out = nullptr;
+  void* k_cache = nullptr;  // this layer's K [h][max_seq][dh]
+  void* v_cache = nullptr;
+  const int* seq_len = nullptr;  // device-resident live length; row written = seq_len-1
+  const float* rope_cos = nullptr;  // [max_seq][dh/2]
+  const float* rope_sin = nullptr;
+  int n_heads = 0, head_dim = 0, max_seq = 0, d_model = 0;
+  int kv_bf16 = 0;
+  int* err = nullptr;       // device error word (WrongLength / CacheFull flags)
+};
+
+struct AttnParams {
+  const float* q = nullptr;      // [h*dh], post-RoPE
+  const void* k_cache = nullptr; // [h][max_seq][dh]
+  const void* v_cache = nullptr;
+  float* out = nullptr;          // [h*dh]
+  float* part = nullptr;         // [h][nsplit][dh+2] split partials
+  int* counters = nullptr;       // [h] arrival counters (self-resetting)
+  const int* seq_len = nullptr;  // device live length (nullptr -> len_fixed)
+  int len_fixed = 0;
+  int n_heads = 0, head_dim = 0, max_seq = 0;
+  int span_cap = 0;              // max positions per split CTA (smem sizing)
+  float scale = 1.0f;
+  int* err = nullptr;
+};
+
+// Device error flags (bit set by kernels, read by the host after a run).
+enum DevErr : int {
+  DEVERR_WRONG_LENGTH = 1,  // live seq_len outside the graph bucket
+  DEVERR_CACHE_FULL = 2,
+  DEVERR_TOKEN_RANGE = 4,
+};
+
+int num_sms(int device);
+
+// Fused (norm) + GEMV + epilogue.  grid_ctas <= 0 picks one CTA per SM.
+cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s, bool pdl, int grid_ctas);
+size_t gemv_smem_bytes(Dt wdt, int k);
+cudaError_t gemv_prepare(int device);  // raises the dynamic smem limit once per process
+
+// Split-K flash-decode over the KV cache.
+cudaError_t launch_attention(Dt kvdt, AttnParams p, int nsplit, cudaStream_t s, bool pdl);
+int attention_nsplit(int max_len, int n_heads, int sms);
+cudaError_t attention_prepare();
+
+// Weight materialisation: writes a logical reference-layout tensor into its
+// device layout.  `src` (host-copied, fp32 or bf16 on device) or Philox init.
+struct MapDesc {
+  int64_t rows = 0, cols = 0;   // logical reference shape ([k,n] for matrices, [V,d] tables)
+  int transpose = 0;            // 1: matrix, physical row = f(j), col = p
+  int64_t ld = 0;               // physical row length (k) when transposed
+  int64_t row_base = 0;         // first physical row of this tensor's block
+  int row_stride = 1;           // 2 for interleaved gate/up
+  int row_offset = 0;           // 0 gate, 1 up
+  int rope_pair = 0;            // permute j within heads: (i, i+half) -> (2i, 2i+1)
+  int head_dim = 0;
+  int dst_dtype = 0;            // Dt
+};
+cudaError_t launch_map_init(const MapDesc& d, void* dst, uint64_t seed, uint32_t tensor_id, cudaStream_t s);
+cudaError_t launch_map_copy(const MapDesc& d, void* dst, const void* src, int src_dtype, cudaStream_t s);
+cudaError_t launch_map_read(const MapDesc& d, const void* dst, float* out_ref_layout, cudaStream_t s);
+
+}  // namespace grt

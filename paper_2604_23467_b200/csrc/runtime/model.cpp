@@ -1,0 +1,622 @@
+// model.cpp -- Model: device arena, weights, KV cache, static plans, dynamic ops.
+//
+// Mirrors graphrt::Model (model.hpp:58-132, model.cpp:30-183).  The reference's
+// 14 kernels per layer (model.hpp:74-83) become 5 fused sm_100a kernels:
+//   qkv   = ln1 + wq/wk/wv + (RoPE) + kv_write_k/v         (gemv.cu, EPI_QKV*)
+//   attn  = attention over [0, seq_len)                     (attention.cu)
+//   wo    = wo + residual_add                               (gemv.cu, EPI_RESID)
+//   up    = ln2 + w1 + relu  |  rms + gate/up + SwiGLU      (gemv.cu, EPI_RELU/SWIGLU)
+//   down  = w2 + residual_add                               (gemv.cu, EPI_RESID)
+// plus ln_f + head (EPI_STORE).  Every length-dependent value is read from the
+// device control block, so a plan is keyed by a BUCKET of lengths, not one.
+#include <cmath>
+#include <cstring>
+#include <random>
+
+#include "runtime.hpp"
+
+namespace grt {
+
+// ---------------------------------------------------------------------------
+// errors
+
+const char* errc_name(Errc c) noexcept {
+  switch (c) {
+    case GRT_OK: return "Ok";
+    case GRT_ShapeMismatch: return "ShapeMismatch";
+    case GRT_TokenOutOfRange: return "TokenOutOfRange";
+    case GRT_EmptyCache: return "EmptyCache";
+    case GRT_CacheFull: return "CacheFull";
+    case GRT_InvalidConfig: return "InvalidConfig";
+    case GRT_LengthOutOfRange: return "LengthOutOfRange";
+    case GRT_PromptTooLong: return "PromptTooLong";
+    case GRT_EmptyPrompt: return "EmptyPrompt";
+    case GRT_CaptureInProgress: return "CaptureInProgress";
+    case GRT_CaptureViolation: return "CaptureViolation";
+    case GRT_ForeignBuffer: return "ForeignBuffer";
+    case GRT_SessionClosed: return "SessionClosed";
+    case GRT_EmptyCapture: return "EmptyCapture";
+    case GRT_ReplayShapeError: return "ReplayShapeError";
+    case GRT_WrongLength: return "WrongLength";
+    case GRT_KeyMismatch: return "KeyMismatch";
+    case GRT_WarmupExceedsCapacity: return "WarmupExceedsCapacity";
+    case GRT_StaticInFusedBlock: return "StaticInFusedBlock";
+    case GRT_DeviceStopped: return "DeviceStopped";
+    case GRT_UnknownEvent: return "UnknownEvent";
+    case GRT_EmptySamples: return "EmptySamples";
+    case GRT_IoError: return "IoError";
+    case GRT_CudaError: return "CudaError";
+    case GRT_NvrtcError: return "NvrtcError";
+    case GRT_NcclError: return "NcclError";
+    case GRT_IpcError: return "IpcError";
+    case GRT_Unsupported: return "Unsupported";
+    case GRT_NoDevice: return "NoDevice";
+  }
+  return "UnknownError";
+}
+
+void raise(Errc code, const std::string& what) { throw Error(code, std::string(errc_name(code)) + ": " + what); }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) raise(GRT_NoDevice, std::string(what) + ": " + cudaGetErrorString(e));
+    raise(GRT_CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+void cu_check(CUresult e, const char* what) {
+  if (e != CUDA_SUCCESS) {
+    raise(GRT_CudaError, std::string(what) + ": " + cu_error_string(e));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// config
+
+void ModelConfig::validate() const {
+  // ModelConfig::validate (model.cpp:10-18)
+  if (n_layers < 1) raise(GRT_InvalidConfig, "n_layers must be >= 1");
+  if (d_model < 1) raise(GRT_InvalidConfig, "d_model must be >= 1");
+  if (n_heads < 1) raise(GRT_InvalidConfig, "n_heads must be >= 1");
+  if (d_model % n_heads != 0) raise(GRT_InvalidConfig, "d_model must be divisible by n_heads");
+  if (vocab_size < 1) raise(GRT_InvalidConfig, "vocab_size must be >= 1");
+  if (max_seq_len < 1) raise(GRT_InvalidConfig, "max_seq_len must be >= 1");
+  if (!(norm_eps > 0.0f)) raise(GRT_InvalidConfig, "ln_eps must be positive");
+  // device-layout requirements (16-byte bulk copies, 4-wide attention lanes)
+  if (d_model % 8 != 0) raise(GRT_InvalidConfig, "d_model must be a multiple of 8 (16-byte rows)");
+  if (d_ff() % 8 != 0) raise(GRT_InvalidConfig, "d_ff must be a multiple of 8");
+  const int dh = head_dim();
+  if (dh % 4 != 0 || dh > 128 || ((dh / 4) & (dh / 4 - 1)) != 0)
+    raise(GRT_InvalidConfig, "head_dim must be 4*2^k <= 128");
+  if (arch != GRT_ARCH_REF && arch != GRT_ARCH_LLAMA) raise(GRT_InvalidConfig, "unknown arch");
+  if (weight_dtype != GRT_F32 && weight_dtype != GRT_BF16) raise(GRT_InvalidConfig, "weight_dtype");
+  if (kv_dtype != GRT_F32 && kv_dtype != GRT_BF16) raise(GRT_InvalidConfig, "kv_dtype");
+  if (init != GRT_INIT_MT19937 && init != GRT_INIT_PHILOX && init != GRT_INIT_NONE) raise(GRT_InvalidConfig, "init");
+  if (tp_size != 1) raise(GRT_Unsupported, "tensor parallel sessions are created through grt_tp_* (tp_size must be 1 here)");
+}
+
+ModelConfig ModelConfig::from_c(const grt_model_config& c) {
+  ModelConfig m;
+  m.arch = c.arch;
+  m.n_layers = c.n_layers;
+  m.d_model = c.d_model;
+  m.n_heads = c.n_heads;
+  m.vocab_size = c.vocab_size;
+  m.max_seq_len = c.max_seq_len;
+  m.d_ff_ = c.d_ff;
+  m.norm_eps = c.norm_eps;
+  m.seed = c.seed;
+  m.init = c.init;
+  m.weight_dtype = c.weight_dtype;
+  m.kv_dtype = c.kv_dtype;
+  m.rope_theta = c.rope_theta;
+  m.device = c.device;
+  m.tp_size = c.tp_size < 1 ? 1 : c.tp_size;
+  m.tp_rank = c.tp_rank;
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// arena
+
+Arena::~Arena() {
+  if (base_) cudaFree(base_);
+}
+
+void Arena::reserve(size_t bytes) {
+  if (base_) raise(GRT_InvalidConfig, "arena already reserved");
+  cuda_check(cudaMalloc(&base_, bytes), "cudaMalloc(arena)");
+  cuda_check(cudaMemset(base_, 0, bytes), "cudaMemset(arena)");
+  cap_ = bytes;
+}
+
+void* Arena::alloc(size_t bytes, size_t align) {
+  size_t off = (used_ + align - 1) / align * align;
+  if (off + bytes > cap_) raise(GRT_InvalidConfig, "arena overflow");
+  used_ = off + bytes;
+  ++count_;
+  return base_ + off;
+}
+
+bool Arena::contains(const void* p, size_t n) const {
+  const char* c = static_cast<const char*>(p);
+  return base_ && c >= base_ && c + n <= base_ + cap_;
+}
+
+// ---------------------------------------------------------------------------
+// model
+
+namespace {
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// prng.hpp:15-17, :33-35 (std::mt19937_64's sequence is fixed by the standard)
+inline double uniform01(std::mt19937_64& eng) { return static_cast<double>(eng() >> 11) * 0x1.0p-53; }
+inline float uniform_symmetric(std::mt19937_64& eng, float limit) {
+  return static_cast<float>((2.0 * uniform01(eng) - 1.0) * limit);
+}
+
+}  // namespace
+
+void* Model::arena_buf(size_t bytes, const char* what) {
+  void* p = arena_.alloc(bytes);
+  buffers_.insert(p);
+  (void)what;
+  return p;
+}
+
+// Declares every logical tensor in the reference draw order (model.hpp:47-51);
+// the LLaMA arch drops pos_table and the betas and replaces w1/w2 by
+// w_gate/w_up/w_down (same order as oracle.c:declare_tensors).
+void Model::declare_tensors() {
+  const int64_t d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size;
+  const int wdt = cfg_.weight_dtype;
+  auto add = [&](const std::string& name, int64_t rows, int64_t cols, int dtype, void* dev, MapDesc m) {
+    LogicalTensor t;
+    t.name = name;
+    t.rows = rows;
+    t.cols = cols;
+    t.dtype = dtype;
+    t.dev = dev;
+    m.rows = rows;
+    m.cols = cols;
+    m.dst_dtype = dtype;
+    m.head_dim = cfg_.head_dim();
+    t.map = m;
+    t.id = static_cast<uint32_t>(tensors_.size());
+    tensors_.push_back(t);
+  };
+  auto mat = [&](int64_t ld, int64_t row_base, int stride, int offset, int rope) {
+    MapDesc m;
+    m.transpose = 1;
+    m.ld = ld;
+    m.row_base = row_base;
+    m.row_stride = stride;
+    m.row_offset = offset;
+    m.rope_pair = rope;
+    return m;
+  };
+  MapDesc plain;
+  add("embedding", V, d, wdt, emb_, plain);
+  if (!cfg_.llama()) add("pos_table", cfg_.max_seq_len, d, wdt, pos_, plain);
+  const int rope = cfg_.llama() ? 1 : 0;
+  for (int l = 0; l < cfg_.n_layers; ++l) {
+    const std::string p = "layers." + std::to_string(l) + ".";
+    LayerBuffers& L = layers_[l];
+    add(p + "wq", d, d, wdt, L.w_qkv, mat(d, 0, 1, 0, rope));
+    add(p + "wk", d, d, wdt, L.w_qkv, mat(d, d, 1, 0, rope));
+    add(p + "wv", d, d, wdt, L.w_qkv, mat(d, 2 * d, 1, 0, 0));
+    add(p + "wo", d, d, wdt, L.w_o, mat(d, 0, 1, 0, 0));
+    if (!cfg_.llama()) {
+      add(p + "w1", d, ff, wdt, L.w_up, mat(d, 0, 1, 0, 0));
+      add(p + "w2", ff, d, wdt, L.w_down, mat(ff, 0, 1, 0, 0));
+      add(p + "ln1_gamma", 1, d, GRT_F32, L.ln1_g, plain);
+      add(p + "ln1_beta", 1, d, GRT_F32, L.ln1_b, plain);
+      add(p + "ln2_gamma", 1, d, GRT_F32, L.ln2_g, plain);
+      add(p + "ln2_beta", 1, d, GRT_F32, L.ln2_b, plain);
+    } else {
+      add(p + "w_gate", d, ff, wdt, L.w_up, mat(d, 0, 2, 0, 0));
+      add(p + "w_up", d, ff, wdt, L.w_up, mat(d, 0, 2, 1, 0));
+      add(p + "w_down", ff, d, wdt, L.w_down, mat(ff, 0, 1, 0, 0));
+      add(p + "ln1_gamma", 1, d, GRT_F32, L.ln1_g, plain);
+      add(p + "ln2_gamma", 1, d, GRT_F32, L.ln2_g, plain);
+    }
+  }
+  add("lnf_gamma", 1, d, GRT_F32, lnf_g_, plain);
+  if (!cfg_.llama()) add("lnf_beta", 1, d, GRT_F32, lnf_b_, plain);
+  add("head", d, V, wdt, head_, mat(d, 0, 1, 0, 0));
+}
+
+Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
+  cfg_.validate();
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    raise(GRT_NoDevice, "no CUDA device visible");
+  }
+  if (cfg_.device < 0 || cfg_.device >= ndev) raise(GRT_InvalidConfig, "device ordinal out of range");
+  cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
+  cuda_check(gemv_prepare(cfg_.device), "gemv_prepare");
+  cuda_check(attention_prepare(), "attention_prepare");
+
+  const int64_t d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
+  const int64_t h = cfg_.n_heads, dh = cfg_.head_dim();
+  const size_t wb = cfg_.weight_dtype == GRT_BF16 ? 2 : 4;
+  const size_t kvb = kv_elem_bytes();
+  const int sms = num_sms(cfg_.device);
+  max_nsplit_ = attention_nsplit(static_cast<int>(S), static_cast<int>(h), sms);
+  max_gen_ = static_cast<int>(S);
+  const int64_t up_rows = cfg_.llama() ? 2 * ff : ff;
+
+  // size the arena: weights, KV, workspace, control
+  size_t need = 0;
+  auto acc = [&](size_t b) { need += round_up(b, 256) + 256; };
+  acc(V * d * wb);
+  if (!cfg_.llama()) acc(S * d * wb);
+  for (int l = 0; l < cfg_.n_layers; ++l) {
+    acc(3 * d * d * wb);
+    acc(d * d * wb);
+    acc(up_rows * d * wb);
+    acc(d * ff * wb);
+    for (int i = 0; i < 4; ++i) acc(d * 4);
+    acc(h * S * dh * kvb);
+    acc(h * S * dh * kvb);
+  }
+  acc(d * 4);
+  acc(d * 4);
+  acc(V * d * wb);
+  acc(d * 4);               // x
+  acc(d * 4);               // q
+  acc(d * 4);               // attn
+  acc(up_rows * 4);         // act
+  acc(V * 4);               // logits
+  acc(V * 4);               // sampler scratch
+  acc(h * max_nsplit_ * (dh + 2) * 4);
+  acc(h * 4);
+  acc(S * (dh / 2) * 4 * 2);
+  acc(sizeof(GrtCtrl));
+  acc(S * 4);
+  acc(max_gen_ * 8);
+  arena_.reserve(need);
+
+  layers_.resize(cfg_.n_layers);
+  emb_ = arena_buf(V * d * wb, "embedding");
+  if (!cfg_.llama()) pos_ = arena_buf(S * d * wb, "pos_table");
+  for (int l = 0; l < cfg_.n_layers; ++l) {
+    LayerBuffers& L = layers_[l];
+    L.w_qkv = arena_buf(3 * d * d * wb, "w_qkv");
+    L.w_o = arena_buf(d * d * wb, "w_o");
+    L.w_up = arena_buf(up_rows * d * wb, "w_up");
+    L.w_down = arena_buf(d * ff * wb, "w_down");
+    L.ln1_g = static_cast<float*>(arena_buf(d * 4, "ln1_g"));
+    L.ln1_b = static_cast<float*>(arena_buf(d * 4, "ln1_b"));
+    L.ln2_g = static_cast<float*>(arena_buf(d * 4, "ln2_g"));
+    L.ln2_b = static_cast<float*>(arena_buf(d * 4, "ln2_b"));
+    L.k = arena_buf(h * S * dh * kvb, "k");
+    L.v = arena_buf(h * S * dh * kvb, "v");
+  }
+  lnf_g_ = static_cast<float*>(arena_buf(d * 4, "lnf_g"));
+  lnf_b_ = static_cast<float*>(arena_buf(d * 4, "lnf_b"));
+  head_ = arena_buf(V * d * wb, "head");
+  x_ = static_cast<float*>(arena_buf(d * 4, "x"));
+  q_ = static_cast<float*>(arena_buf(d * 4, "q"));
+  attn_ = static_cast<float*>(arena_buf(d * 4, "attn"));
+  act_ = static_cast<float*>(arena_buf(up_rows * 4, "act"));
+  logits_ = static_cast<float*>(arena_buf(V * 4, "logits"));
+  scratch_ = static_cast<float*>(arena_buf(V * 4, "scratch"));
+  attn_part_ = static_cast<float*>(arena_buf(h * max_nsplit_ * (dh + 2) * 4, "attn_part"));
+  attn_counters_ = static_cast<int*>(arena_buf(h * 4, "attn_counters"));
+  rope_cos_ = static_cast<float*>(arena_buf(S * (dh / 2) * 4, "rope_cos"));
+  rope_sin_ = static_cast<float*>(arena_buf(S * (dh / 2) * 4, "rope_sin"));
+  ctrl_ = static_cast<GrtCtrl*>(arena_buf(sizeof(GrtCtrl), "ctrl"));
+  tokens_ = static_cast<int*>(arena_buf(S * 4, "tokens"));
+  uniforms_ = static_cast<double*>(arena_buf(max_gen_ * 8, "uniforms"));
+
+  weight_bytes_ = (V * d + (cfg_.llama() ? 0 : S * d) + V * d) * wb +
+                  static_cast<uint64_t>(cfg_.n_layers) * ((3 * d * d + d * d + up_rows * d + d * ff) * wb) +
+                  static_cast<uint64_t>(cfg_.n_layers) * 4 * d * 4 + 2 * d * 4;
+
+  declare_tensors();
+  init_weights();
+
+  // RoPE table: cos/sin of pos * theta^(-2i/dh) in double, rounded to fp32
+  // (identical to oracle.c:oc_rope_table).
+  {
+    const int64_t half = dh / 2;
+    std::vector<float> c(S * half), s(S * half);
+    for (int64_t p = 0; p < S; ++p)
+      for (int64_t i = 0; i < half; ++i) {
+        const double inv_freq = std::pow(static_cast<double>(cfg_.rope_theta), -(2.0 * i) / static_cast<double>(dh));
+        const double ang = static_cast<double>(p) * inv_freq;
+        c[p * half + i] = static_cast<float>(std::cos(ang));
+        s[p * half + i] = static_cast<float>(std::sin(ang));
+      }
+    cuda_check(cudaMemcpy(rope_cos_, c.data(), c.size() * 4, cudaMemcpyHostToDevice), "rope cos");
+    cuda_check(cudaMemcpy(rope_sin_, s.data(), s.size() * 4, cudaMemcpyHostToDevice), "rope sin");
+  }
+
+  // host-mapped outputs: sampled tokens + timestamps (zero-copy, no per-step sync)
+  void* ht = nullptr;
+  void* hs = nullptr;
+  cuda_check(cudaHostAlloc(&ht, max_gen_ * sizeof(int), cudaHostAllocMapped), "cudaHostAlloc tokens");
+  cuda_check(cudaHostAlloc(&hs, 2 * max_gen_ * sizeof(unsigned long long), cudaHostAllocMapped), "cudaHostAlloc stamps");
+  h_out_tokens_ = static_cast<volatile int*>(ht);
+  h_out_stamps_ = static_cast<volatile unsigned long long*>(hs);
+
+  // NVRTC: specialise the dynamic ops on this model's shape.
+  std::vector<std::string> opts = {
+      "-DGRT_D=" + std::to_string(d),
+      "-DGRT_V=" + std::to_string(V),
+      "-DGRT_MAXSEQ=" + std::to_string(S),
+      std::string("-DGRT_WBF16=") + (cfg_.weight_dtype == GRT_BF16 ? "1" : "0"),
+      std::string("-DGRT_ARCH_REF=") + (cfg_.llama() ? "0" : "1"),
+  };
+  jit_ = jit_get(opts, cfg_.device);
+  f_pre_ = jit_->fn("grt_preprocess");
+  f_sample_ = jit_->fn("grt_sample");
+  cuda_check(cudaDeviceSynchronize(), "model init");
+}
+
+Model::~Model() {
+  cudaSetDevice(cfg_.device);
+  cudaDeviceSynchronize();
+  if (h_out_tokens_) cudaFreeHost(const_cast<int*>(h_out_tokens_));
+  if (h_out_stamps_) cudaFreeHost(const_cast<unsigned long long*>(h_out_stamps_));
+}
+
+// init_model (model.cpp:30-76): U[-0.1, 0.1] for every tensor.
+void Model::init_weights() {
+  if (cfg_.init == GRT_INIT_NONE) return;
+  if (cfg_.init == GRT_INIT_PHILOX) {
+    for (const LogicalTensor& t : tensors_)
+      cuda_check(launch_map_init(t.map, t.dev, cfg_.seed, t.id, nullptr), "philox init");
+    cuda_check(cudaDeviceSynchronize(), "philox init");
+    return;
+  }
+  // mt19937_64 stream in draw order, generated on the host (serial by nature).
+  std::mt19937_64 eng(cfg_.seed);
+  size_t max_n = 0;
+  for (const LogicalTensor& t : tensors_) max_n = std::max<size_t>(max_n, t.rows * t.cols);
+  float* staging = nullptr;
+  cuda_check(cudaMalloc(&staging, max_n * 4), "cudaMalloc staging");
+  std::vector<float> buf;
+  for (const LogicalTensor& t : tensors_) {
+    const size_t n = t.rows * t.cols;
+    buf.resize(n);
+    for (size_t i = 0; i < n; ++i) buf[i] = uniform_symmetric(eng, 0.1f);
+    cuda_check(cudaMemcpy(staging, buf.data(), n * 4, cudaMemcpyHostToDevice), "upload");
+    cuda_check(launch_map_copy(t.map, t.dev, staging, static_cast<int>(Dt::F32), nullptr), "map copy");
+  }
+  cuda_check(cudaDeviceSynchronize(), "mt19937 init");
+  cudaFree(staging);
+}
+
+const LogicalTensor& Model::tensor(const std::string& name) const {
+  for (const LogicalTensor& t : tensors_)
+    if (t.name == name) return t;
+  raise(GRT_ShapeMismatch, "unknown tensor '" + name + "'");
+}
+
+void Model::upload(const std::string& name, const void* host, size_t bytes, int host_dtype) {
+  const LogicalTensor& t = tensor(name);
+  const size_t n = t.rows * t.cols;
+  const size_t eb = host_dtype == GRT_BF16 ? 2 : 4;
+  if (bytes != n * eb) raise(GRT_ShapeMismatch, "upload '" + name + "': byte count mismatch");
+  cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
+  void* staging = nullptr;
+  cuda_check(cudaMalloc(&staging, bytes), "cudaMalloc staging");
+  cuda_check(cudaMemcpy(staging, host, bytes, cudaMemcpyHostToDevice), "upload");
+  cuda_check(launch_map_copy(t.map, t.dev, staging, host_dtype, nullptr), "map copy");
+  cuda_check(cudaDeviceSynchronize(), "upload");
+  cudaFree(staging);
+}
+
+void Model::download(const std::string& name, float* host, size_t numel) {
+  const LogicalTensor& t = tensor(name);
+  const size_t n = t.rows * t.cols;
+  if (numel != n) raise(GRT_ShapeMismatch, "download '" + name + "': numel mismatch");
+  cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
+  float* staging = nullptr;
+  cuda_check(cudaMalloc(&staging, n * 4), "cudaMalloc staging");
+  cuda_check(launch_map_read(t.map, t.dev, staging, nullptr), "map read");
+  cuda_check(cudaMemcpy(host, staging, n * 4, cudaMemcpyDeviceToHost), "download");
+  cudaFree(staging);
+}
+
+uint64_t Model::decode_bytes(int length) const {
+  const uint64_t d = cfg_.d_model, L = cfg_.n_layers;
+  const uint64_t wb = cfg_.weight_dtype == GRT_BF16 ? 2 : 4;
+  const uint64_t kvb = kv_elem_bytes();
+  // weights streamed once (minus the embedding/pos tables: one row each)
+  const uint64_t V = cfg_.vocab_size;
+  uint64_t b = weight_bytes_ - (V * d + (cfg_.llama() ? 0 : cfg_.max_seq_len * d)) * wb;
+  b += d * wb * (cfg_.llama() ? 1 : 2);            // embedding (+pos) row
+  b += L * 2 * static_cast<uint64_t>(length) * d * kvb;  // K,V read over [0, length)
+  b += L * 2 * d * kvb;                              // K,V row write
+  return b;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+
+std::vector<KernelInvocation> Model::build_plan(int key, int B) {
+  const int d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
+  const int h = cfg_.n_heads, dh = cfg_.head_dim();
+  const Dt wdt = cfg_.weight_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
+  const Dt kvdt = cfg_.kv_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
+  const size_t wb = wdt == Dt::BF16 ? 2 : 4;
+  const size_t kvb = kv_elem_bytes();
+  const int max_len = std::min(key * B, S);
+  const int sms = num_sms(cfg_.device);
+  const int nsplit = std::min(max_nsplit_, attention_nsplit(max_len, h, sms));
+  int span_cap = (max_len + nsplit - 1) / nsplit;
+  span_cap = (span_cap + 3) / 4 * 4;
+  const bool llama = cfg_.llama();
+  const int norm = llama ? NORM_RMS : NORM_LN;
+  int* seq_len = &ctrl_->seq_len;
+  int* err = &ctrl_->err;
+
+  std::vector<KernelInvocation> plan;
+  auto gemv = [&](const char* name, int epi, int nrm, GemvParams p, size_t w_bytes) {
+    KernelInvocation inv;
+    inv.spec.name = name;
+    inv.spec.op_class = OpClass::Static;
+    inv.spec.flops = 2LL * p.n_rows * p.k;
+    inv.spec.bytes = static_cast<int64_t>(w_bytes);
+    inv.bindings = {{p.w, w_bytes}, {p.x, static_cast<size_t>(p.k) * 4}};
+    if (p.out) inv.bindings.push_back({p.out, 4});
+    inv.launch = [wdt, epi, nrm, p](cudaStream_t s) { return launch_gemv(wdt, nrm, epi, p, s, true, 0); };
+    plan.push_back(std::move(inv));
+  };
+  for (int l = 0; l < cfg_.n_layers; ++l) {
+    const LayerBuffers& L = layers_[l];
+    {  // ln1 + q,k,v + (RoPE) + kv_write
+      GemvParams p;
+      p.w = L.w_qkv;
+      p.n_rows = 3 * d;
+      p.k = d;
+      p.x = x_;
+      p.gamma = L.ln1_g;
+      p.beta = L.ln1_b;
+      p.eps = cfg_.norm_eps;
+      p.q_out = q_;
+      p.k_cache = L.k;
+      p.v_cache = L.v;
+      p.seq_len = seq_len;
+      p.rope_cos = rope_cos_;
+      p.rope_sin = rope_sin_;
+      p.n_heads = h;
+      p.head_dim = dh;
+      p.max_seq = S;
+      p.d_model = d;
+      p.kv_bf16 = kvdt == Dt::BF16;
+      p.err = err;
+      gemv("qkv", llama ? EPI_QKV_ROPE : EPI_QKV, norm, p, 3ull * d * d * wb);
+    }
+    {  // attention over [0, seq_len)
+      AttnParams a;
+      a.q = q_;
+      a.k_cache = L.k;
+      a.v_cache = L.v;
+      a.out = attn_;
+      a.part = attn_part_;
+      a.counters = attn_counters_;
+      a.seq_len = seq_len;
+      a.n_heads = h;
+      a.head_dim = dh;
+      a.max_seq = S;
+      a.span_cap = span_cap;
+      a.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
+      a.err = err;
+      KernelInvocation inv;
+      inv.spec.name = "attention";
+      inv.spec.flops = static_cast<int64_t>(h) * max_len * (4 * dh + 5);  // kernels.hpp:51
+      inv.spec.bytes = 2LL * max_len * d * kvb;
+      inv.bindings = {{L.k, static_cast<size_t>(h) * S * dh * kvb}, {L.v, static_cast<size_t>(h) * S * dh * kvb},
+                      {q_, static_cast<size_t>(d) * 4}, {attn_, static_cast<size_t>(d) * 4}};
+      inv.launch = [kvdt, a, nsplit](cudaStream_t s) { return launch_attention(kvdt, a, nsplit, s, true); };
+      plan.push_back(std::move(inv));
+    }
+    {  // wo + residual
+      GemvParams p;
+      p.w = L.w_o;
+      p.n_rows = d;
+      p.k = d;
+      p.x = attn_;
+      p.out = x_;
+      gemv("wo_residual", EPI_RESID, NORM_NONE, p, 1ull * d * d * wb);
+    }
+    {  // ln2 + w1 + relu  |  rms + gate/up + SwiGLU
+      GemvParams p;
+      p.w = L.w_up;
+      p.n_rows = llama ? 2 * ff : ff;
+      p.k = d;
+      p.x = x_;
+      p.gamma = L.ln2_g;
+      p.beta = L.ln2_b;
+      p.eps = cfg_.norm_eps;
+      p.out = act_;
+      gemv(llama ? "gate_up_swiglu" : "w1_relu", llama ? EPI_SWIGLU : EPI_RELU, norm, p,
+           static_cast<size_t>(p.n_rows) * d * wb);
+    }
+    {  // w2/down + residual
+      GemvParams p;
+      p.w = L.w_down;
+      p.n_rows = d;
+      p.k = ff;
+      p.x = act_;
+      p.out = x_;
+      gemv("down_residual", EPI_RESID, NORM_NONE, p, 1ull * d * ff * wb);
+    }
+  }
+  {  // ln_f + head
+    GemvParams p;
+    p.w = head_;
+    p.n_rows = V;
+    p.k = d;
+    p.x = x_;
+    p.gamma = lnf_g_;
+    p.beta = lnf_b_;
+    p.eps = cfg_.norm_eps;
+    p.out = logits_;
+    gemv("lnf_head", EPI_STORE, norm, p, 1ull * V * d * wb);
+  }
+  return plan;
+}
+
+const std::vector<KernelInvocation>& Model::plan(int key, int B) {
+  if (B < 1) raise(GRT_InvalidConfig, "bucket_size must be >= 1");
+  if (key < 1 || key > max_key(B))
+    raise(GRT_LengthOutOfRange, "plan key " + std::to_string(key) + " outside [1, " + std::to_string(max_key(B)) + "]");
+  std::lock_guard<std::mutex> lk(plan_mu_);
+  auto it = plans_.find({key, B});
+  if (it == plans_.end()) it = plans_.emplace(std::make_pair(key, B), build_plan(key, B)).first;
+  return it->second;
+}
+
+KernelInvocation Model::make_preprocess_op() {
+  KernelInvocation inv;
+  inv.spec.name = "extend_position+slot_append";
+  inv.spec.op_class = OpClass::Dynamic;
+  inv.spec.flops = 2LL * cfg_.d_model;
+  const size_t wb = cfg_.weight_dtype == GRT_BF16 ? 2 : 4;
+  inv.spec.bytes = static_cast<int64_t>(cfg_.d_model) * (wb * (cfg_.llama() ? 1 : 2) + 4);
+  inv.bindings = {{ctrl_, sizeof(GrtCtrl)}, {x_, static_cast<size_t>(cfg_.d_model) * 4}};
+  CUfunction f = f_pre_;
+  GrtCtrl* ctrl = ctrl_;
+  const void* emb = emb_;
+  const void* pos = pos_ ? pos_ : emb_;
+  float* x = x_;
+  const int threads = std::min(1024, (cfg_.d_model + 31) / 32 * 32);
+  inv.launch = [f, ctrl, emb, pos, x, threads](cudaStream_t s) {
+    GrtCtrl* a0 = ctrl;
+    const void* a1 = emb;
+    const void* a2 = pos;
+    float* a3 = x;
+    void* args[] = {&a0, &a1, &a2, &a3};
+    return launch_jit(f, dim3(1), dim3(threads), args, s, true);
+  };
+  return inv;
+}
+
+KernelInvocation Model::make_sample_op() {
+  KernelInvocation inv;
+  inv.spec.name = "sample_token";
+  inv.spec.op_class = OpClass::Dynamic;
+  inv.spec.flops = cfg_.vocab_size;
+  inv.spec.bytes = static_cast<int64_t>(cfg_.vocab_size) * 4;
+  inv.bindings = {{ctrl_, sizeof(GrtCtrl)}, {logits_, static_cast<size_t>(cfg_.vocab_size) * 4}};
+  CUfunction f = f_sample_;
+  GrtCtrl* ctrl = ctrl_;
+  const float* logits = logits_;
+  inv.launch = [f, ctrl, logits](cudaStream_t s) {
+    GrtCtrl* a0 = ctrl;
+    const float* a1 = logits;
+    void* args[] = {&a0, &a1};
+    return launch_jit(f, dim3(1), dim3(1024), args, s, true);
+  };
+  return inv;
+}
+
+}  // namespace grt

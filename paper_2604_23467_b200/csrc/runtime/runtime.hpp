@@ -1,0 +1,478 @@
+// runtime.hpp -- B200-native host runtime behind the C ABI (include/grt/c_api.h).
+//
+// Class names and semantics mirror the reference runtime (graphrt):
+//   Errc / Error              error.hpp:10-54
+//   ModelConfig / Model       model.hpp:17-132
+//   OpClass / KernelSpec / KernelInvocation   kernels.hpp:14-45
+//   Workspace -> Arena        exec_graph.hpp:20-40   (one device allocation)
+//   ExecGraph / CaptureEngine / CaptureSession  exec_graph.hpp:45-141 (cudaGraphExec_t)
+//   GraphCache                graph_cache.hpp:29-81  (same eviction policy)
+//   VirtualDevice -> CudaDevice  virtual_device.hpp:125-192 (real streams/events)
+//   RunMode / ModePolicy / Channel / ContextGenerator / GraphGenerator / Session
+//                             pipeline.hpp:18-189
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <random>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../jit/ctrl.h"
+#include "../kernels/kernels.h"
+#include "grt/c_api.h"
+
+namespace grt {
+
+// ---------------------------------------------------------------------------
+// errors (error.hpp:10-54): codes are grt_status values.
+using Errc = grt_status;
+
+class Error : public std::runtime_error {
+ public:
+  Error(Errc code, const std::string& what) : std::runtime_error(what), code_(code) {}
+  Errc code() const noexcept { return code_; }
+
+ private:
+  Errc code_;
+};
+
+[[noreturn]] void raise(Errc code, const std::string& what);
+const char* errc_name(Errc c) noexcept;
+void cuda_check(cudaError_t e, const char* what);
+void cu_check(CUresult e, const char* what);
+const char* cu_error_string(CUresult e);
+
+// ---------------------------------------------------------------------------
+// config (model.hpp:17-29)
+struct ModelConfig {
+  int arch = GRT_ARCH_REF;
+  int n_layers = 4;
+  int d_model = 64;
+  int n_heads = 4;
+  int vocab_size = 256;
+  int max_seq_len = 600;
+  int d_ff_ = 0;
+  float norm_eps = 1e-5f;
+  uint64_t seed = 1234;
+  int init = GRT_INIT_MT19937;
+  int weight_dtype = GRT_F32;
+  int kv_dtype = GRT_F32;
+  float rope_theta = 10000.0f;
+  int device = 0;
+  int tp_size = 1;
+  int tp_rank = 0;
+
+  int d_ff() const noexcept { return d_ff_ > 0 ? d_ff_ : 4 * d_model; }
+  int head_dim() const noexcept { return d_model / n_heads; }
+  bool llama() const noexcept { return arch == GRT_ARCH_LLAMA; }
+  void validate() const;  // raises InvalidConfig
+  static ModelConfig from_c(const grt_model_config& c);
+};
+
+// ---------------------------------------------------------------------------
+// arena: the Workspace of the reference (exec_graph.hpp:20-40) on the device.
+// Allocated once; never grows per capture.  contains() is the ForeignBuffer check.
+class Arena {
+ public:
+  Arena() = default;
+  ~Arena();
+  Arena(const Arena&) = delete;
+  Arena& operator=(const Arena&) = delete;
+  void reserve(size_t bytes);
+  void* alloc(size_t bytes, size_t align = 256);
+  bool contains(const void* p, size_t n) const;
+  size_t used() const { return used_; }
+  size_t capacity() const { return cap_; }
+  size_t allocations() const { return count_; }
+
+ private:
+  char* base_ = nullptr;
+  size_t cap_ = 0, used_ = 0, count_ = 0;
+};
+
+// ---------------------------------------------------------------------------
+// operator API (kernels.hpp:14-45)
+enum class OpClass { Static, Dynamic };
+
+struct DevRange {
+  const void* ptr;
+  size_t bytes;
+};
+
+struct KernelSpec {
+  std::string name;
+  OpClass op_class = OpClass::Static;
+  int64_t flops = 0;
+  int64_t bytes = 0;  // algorithmic HBM bytes (roofline accounting)
+};
+
+// One kernel instance.  `launch` enqueues it on a stream: it binds device
+// buffers (never host values), so it is equally valid eagerly or under capture.
+struct KernelInvocation {
+  KernelSpec spec;
+  std::vector<DevRange> bindings;
+  std::function<cudaError_t(cudaStream_t)> launch;
+};
+
+// ---------------------------------------------------------------------------
+// NVRTC-compiled dynamic kernels
+class JitModule {
+ public:
+  JitModule(const std::string& defines_key, const std::vector<std::string>& opts, int device);
+  ~JitModule();
+  CUfunction fn(const char* name) const;
+  double compile_ms() const { return compile_ms_; }
+
+ private:
+  CUmodule mod_ = nullptr;
+  double compile_ms_ = 0;
+};
+std::string jit_compile(const std::vector<std::string>& opts);  // NVRTC -> sm_100a cubin (no GPU needed)
+std::shared_ptr<JitModule> jit_get(const std::vector<std::string>& opts, int device);
+cudaError_t launch_jit(CUfunction f, dim3 grid, dim3 block, void** args, cudaStream_t s, bool pdl);
+
+// ---------------------------------------------------------------------------
+// model (model.hpp:58-132)
+struct LogicalTensor {
+  std::string name;
+  int64_t rows = 0, cols = 0;
+  int dtype = GRT_F32;
+  void* dev = nullptr;  // base of the physical buffer holding it
+  MapDesc map;
+  uint32_t id = 0;      // draw-order index (Philox tensor id)
+};
+
+struct LayerBuffers {
+  void* w_qkv = nullptr;  // [3d, d]
+  void* w_o = nullptr;    // [d, d]
+  void* w_up = nullptr;   // ref: W1 [ff, d]; llama: gate/up interleaved [2ff, d]
+  void* w_down = nullptr; // [d, ff]
+  float *ln1_g = nullptr, *ln1_b = nullptr, *ln2_g = nullptr, *ln2_b = nullptr;
+  void* k = nullptr;      // [h][max_seq][dh]
+  void* v = nullptr;
+};
+
+class Model {
+ public:
+  explicit Model(const ModelConfig& cfg);
+  ~Model();
+
+  const ModelConfig& config() const noexcept { return cfg_; }
+  Arena& arena() noexcept { return arena_; }
+  int device() const noexcept { return cfg_.device; }
+
+  // Static plan for one bucket key (lengths ((key-1)*B, key*B]).  Memoized;
+  // the returned reference is stable for the model's lifetime.  Raises
+  // LengthOutOfRange outside [1, max_key].
+  const std::vector<KernelInvocation>& plan(int key, int bucket_size);
+  int max_key(int bucket_size) const { return (cfg_.max_seq_len + bucket_size - 1) / bucket_size; }
+  static int key_of(int length, int bucket_size) { return (length + bucket_size - 1) / bucket_size; }
+
+  // Dynamic ops (DYNAMIC, NVRTC kernels; every runtime value read from ctrl).
+  KernelInvocation make_preprocess_op();   // extend_position + slot append
+  KernelInvocation make_sample_op();       // sample_token
+
+  // Weight I/O in the reference layout.
+  void upload(const std::string& name, const void* host, size_t bytes, int host_dtype);
+  void download(const std::string& name, float* host, size_t numel);
+  const LogicalTensor& tensor(const std::string& name) const;
+  uint64_t weight_bytes() const { return weight_bytes_; }
+  uint64_t decode_bytes(int length) const;  // algorithmic bytes of one pass at `length`
+
+  // device state
+  GrtCtrl* ctrl_dev() const { return ctrl_; }
+  int* tokens_dev() const { return tokens_; }
+  double* uniforms_dev() const { return uniforms_; }
+  float* logits_dev() const { return logits_; }
+  float* scratch_dev() const { return scratch_; }
+  float* x_dev() const { return x_; }
+  const LayerBuffers& layer(int l) const { return layers_[l]; }
+  volatile int* host_tokens() const { return h_out_tokens_; }
+  volatile unsigned long long* host_stamps() const { return h_out_stamps_; }
+  int max_gen() const { return max_gen_; }
+  int kv_elem_bytes() const { return cfg_.kv_dtype == GRT_BF16 ? 2 : 4; }
+  const std::set<const void*>& buffer_set() const { return buffers_; }
+
+ private:
+  void declare_tensors();
+  void init_weights();
+  std::vector<KernelInvocation> build_plan(int key, int bucket_size);
+  void* arena_buf(size_t bytes, const char* what);
+
+  ModelConfig cfg_;
+  Arena arena_;
+  std::vector<LogicalTensor> tensors_;
+  std::vector<LayerBuffers> layers_;
+  void *emb_ = nullptr, *pos_ = nullptr, *head_ = nullptr;
+  float *lnf_g_ = nullptr, *lnf_b_ = nullptr;
+  float *x_ = nullptr, *q_ = nullptr, *attn_ = nullptr, *act_ = nullptr, *logits_ = nullptr;
+  float *attn_part_ = nullptr, *rope_cos_ = nullptr, *rope_sin_ = nullptr, *scratch_ = nullptr;
+  int* attn_counters_ = nullptr;
+  GrtCtrl* ctrl_ = nullptr;
+  int* tokens_ = nullptr;
+  double* uniforms_ = nullptr;
+  int max_gen_ = 0;
+  int max_nsplit_ = 1;
+  volatile int* h_out_tokens_ = nullptr;
+  volatile unsigned long long* h_out_stamps_ = nullptr;
+  uint64_t weight_bytes_ = 0;
+  std::shared_ptr<JitModule> jit_;
+  CUfunction f_pre_ = nullptr, f_sample_ = nullptr;
+  std::mutex plan_mu_;
+  std::map<std::pair<int, int>, std::vector<KernelInvocation>> plans_;
+  std::set<const void*> buffers_;
+};
+
+// ---------------------------------------------------------------------------
+// capture / replay (exec_graph.hpp:45-141)
+class ExecGraph {
+ public:
+  ExecGraph(int key, cudaGraphExec_t exec, size_t kernels, int64_t flops, uint64_t epoch, int device);
+  ~ExecGraph();
+  int length_key() const noexcept { return key_; }
+  size_t kernel_count() const noexcept { return kernels_; }
+  int64_t total_flops() const noexcept { return flops_; }
+  uint64_t capture_epoch() const noexcept { return epoch_; }
+  cudaGraphExec_t exec() const noexcept { return exec_; }
+  void launch(cudaStream_t s) const;
+  // Records an event after the latest launch; destruction waits for it, so an
+  // evicted graph is only destroyed after its last replay retired.
+  void mark_launched(cudaStream_t s);
+
+ private:
+  int key_;
+  cudaGraphExec_t exec_;
+  size_t kernels_;
+  int64_t flops_;
+  uint64_t epoch_;
+  int device_;
+  cudaEvent_t last_ = nullptr;
+};
+using ExecGraphPtr = std::shared_ptr<ExecGraph>;
+
+class CaptureEngine {
+ public:
+  CaptureEngine(const Arena& arena, int device) : arena_(&arena), device_(device) {}
+  // Captures `kernels` on `stream` (cudaStreamCaptureModeThreadLocal) and
+  // instantiates them.  Raises CaptureViolation / ForeignBuffer / EmptyCapture /
+  // CaptureInProgress like CaptureSession::record / end_capture.
+  ExecGraphPtr capture(int key, const std::vector<const KernelInvocation*>& kernels, cudaStream_t stream);
+  bool binding_allowed(const DevRange& r) const { return arena_->contains(r.ptr, r.bytes); }
+
+ private:
+  const Arena* arena_;
+  int device_;
+  std::mutex mu_;
+  std::set<int> open_keys_;
+  uint64_t epoch_ = 0;
+};
+
+// graph_cache.hpp:29-81, ported with the same policy and statistics.
+enum class EvictionPolicy { LeastUsed = GRT_EVICT_LEAST_USED, LeastRecentlyUsed = GRT_EVICT_LRU };
+
+class GraphCache {
+ public:
+  explicit GraphCache(size_t capacity, EvictionPolicy policy = EvictionPolicy::LeastUsed);
+  std::optional<ExecGraphPtr> lookup(int key);
+  std::optional<int> insert(int key, ExecGraphPtr graph);
+  int precapture_warmup(int lo, int hi, const std::function<ExecGraphPtr(int)>& capture_fn);
+  void begin_session();
+  size_t release_inactive();
+  size_t size() const noexcept { return entries_.size(); }
+  size_t capacity() const noexcept { return capacity_; }
+  bool contains(int key) const { return entries_.count(key) != 0; }
+  uint64_t use_count(int key) const;
+  const grt_cache_stats& stats() const noexcept { return stats_; }
+  // graphs dropped by eviction/release, kept alive until their last launch retires
+  std::vector<ExecGraphPtr> take_dropped();
+
+ private:
+  struct Entry {
+    ExecGraphPtr graph;
+    uint64_t use_count = 0, insert_seq = 0, last_use_seq = 0;
+    bool active = false;
+  };
+  int pick_victim() const;
+  size_t capacity_;
+  EvictionPolicy policy_;
+  std::map<int, Entry> entries_;
+  uint64_t seq_ = 0;
+  bool in_session_ = false;
+  grt_cache_stats stats_{};
+  std::vector<ExecGraphPtr> dropped_;
+};
+
+// ---------------------------------------------------------------------------
+// pipeline (pipeline.hpp)
+enum class RunMode { Eager = 0, Hybrid = 1, GraphOnly = 2, AblateAsync = 3, AblateFused = 4, AblateBoth = 5 };
+const char* mode_name(RunMode m) noexcept;
+
+struct ModePolicy {
+  bool use_cache = false;
+  bool capture_on_miss = false;
+  bool async_capture = true;  // Capture stream + capture thread (false = inline, serialised)
+  bool fuse_dynamic = false;  // dynamic ops inside the step graph
+};
+ModePolicy policy_for(RunMode m) noexcept;
+
+enum class StepPath { Replayed = GRT_PATH_REPLAYED, EagerFallback = GRT_PATH_EAGER_FALLBACK };
+
+struct StepRequest {
+  int step_index = 0;
+  int length_key = 0;  // bucket key
+  bool fused = false;
+};
+struct StepResponse {
+  int step_index = 0;
+  StepPath path = StepPath::EagerFallback;
+};
+
+// Single-slot rendezvous with strict alternation (pipeline.cpp:56-78).
+class Channel {
+ public:
+  void send_request(const StepRequest& r);
+  StepRequest take_request();
+  void send_response(const StepResponse& r);
+  StepResponse take_response();
+
+ private:
+  enum class State { Idle, Requested, Serving, Responded };
+  State state_ = State::Idle;
+  StepRequest req_;
+  StepResponse resp_;
+};
+
+struct CacheConfig {
+  size_t capacity = 600;
+  int warmup_lo = 1;
+  int warmup_hi = 50;
+  bool prefill_uses_graphs = true;
+  EvictionPolicy policy = EvictionPolicy::LeastUsed;
+  int bucket_size = 64;
+  bool batched_prefill = false;
+  static CacheConfig from_c(const grt_cache_config& c);
+};
+
+// Two real streams (Replay = compute, Capture = side stream) plus the
+// background capture thread (virtual_device.hpp:125-192 with real CUDA).
+class CudaDevice {
+ public:
+  explicit CudaDevice(int device);
+  ~CudaDevice();
+  cudaStream_t replay() const { return s_rep_; }
+  cudaStream_t capture_stream() const { return s_cap_; }
+  int device() const { return device_; }
+  grt_counters& counters() { return counters_; }
+  void submit_kernel(const KernelInvocation& inv);              // eager launch on Replay
+  void submit_fused_block(const std::vector<KernelInvocation>& block);  // dynamic-only
+  void submit_replay(const ExecGraphPtr& g);
+  // Background capture: job runs on the capture thread, result harvested later.
+  void submit_capture(int key, std::function<ExecGraphPtr(cudaStream_t)> job);
+  std::vector<std::pair<int, ExecGraphPtr>> take_ready_captures();
+  bool capture_pending(int key);
+  void drain_captures();  // waits for the capture thread to go idle
+  void sync_all();
+
+ private:
+  void capture_loop();
+  int device_;
+  cudaStream_t s_rep_ = nullptr, s_cap_ = nullptr;
+  grt_counters counters_{};
+  std::thread worker_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::pair<int, std::function<ExecGraphPtr(cudaStream_t)>>> jobs_;
+  std::vector<std::pair<int, ExecGraphPtr>> ready_;
+  std::set<int> pending_;
+  std::string worker_error_;
+  Errc worker_code_ = GRT_OK;
+  bool busy_ = false;
+  bool stop_ = false;
+};
+
+struct GenerationRequest {
+  RunMode mode = RunMode::Hybrid;
+  std::vector<int> prompt;
+  int gen_len = 1;
+  grt_sample_params sampling{GRT_SAMPLE_GREEDY, 1.0f, 0, 1.0f, 7};
+};
+
+struct GenerationResult {
+  std::vector<int> tokens;
+  double ttft_us = 0, total_us = 0, prefill_us = 0;
+  std::vector<double> per_token_us;
+  grt_counters counters{};
+  grt_cache_stats cache_delta{};
+  std::vector<StepPath> prefill_paths, decode_paths;
+  int captures_completed = 0;
+  size_t cache_released = 0;
+  std::vector<double> host_token_us;  // host time each token became visible (us from entry)
+};
+
+struct KernelProfile {
+  std::string name;
+  double avg_ms = 0;
+  int64_t bytes = 0;
+};
+
+class Session {
+ public:
+  Session(Model& model, const CacheConfig& cc);
+  ~Session();
+  GenerationResult run(const GenerationRequest& req);
+  std::vector<KernelProfile> profile_plan(int key, int iters);
+
+  // step-level API (Model::step_math / prefill_math / reset / sample)
+  void reset();
+  void step(int token);
+  void prefill(const std::vector<int>& ids);
+  int cur_len() const { return cur_len_; }
+  void logits(float* out, int n);
+  void kv_row(int layer, int slot, int row, float* out);
+  int sample(const grt_sample_params& p);
+  void sampler_reset(uint64_t seed) {
+    sampler_.seed(seed);
+    n_sampled_ = 0;
+  }
+
+  GraphCache& cache() { return *cache_; }
+  CudaDevice& device() { return *dev_; }
+  const CacheConfig& cache_config() const { return cc_; }
+
+ private:
+  void validate(const GenerationRequest& req) const;
+  void write_ctrl(int seq_len, int prompt_len, const grt_sample_params& sp, int max_gen);
+  StepResponse serve(const StepRequest& req, bool allow_cache, const ModePolicy& pol);
+  int harvest();
+  std::vector<const KernelInvocation*> step_kernels(int key, bool fused);
+  ExecGraphPtr capture_now(int key, bool fused, cudaStream_t s);
+  int cache_key(int key, bool fused) const { return fused ? key : -key; }
+  void check_device_errors();
+
+  Model* model_;
+  CacheConfig cc_;
+  std::unique_ptr<CudaDevice> dev_;
+  std::unique_ptr<CaptureEngine> engine_;
+  std::unique_ptr<GraphCache> cache_;
+  KernelInvocation pre_op_, sample_op_;
+  std::mt19937_64 sampler_{7};
+  int cur_len_ = 0;
+  int n_sampled_ = 0;  // step-level sampler draws since sampler_reset (Philox counter / uniform index)
+  int captures_completed_ = 0;
+  GrtCtrl* h_ctrl_ = nullptr;  // pinned staging for ctrl writes
+};
+
+}  // namespace grt
