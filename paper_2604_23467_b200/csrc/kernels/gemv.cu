@@ -354,7 +354,10 @@ static GemvFn pick_any(Dt wdt, int norm, int epi) {
   return wdt == Dt::BF16 ? pick<__nv_bfloat16>(norm, epi) : pick<float>(norm, epi);
 }
 
-cudaError_t gemv_prepare(int /*device*/) {
+cudaError_t gemv_prepare(int device) {
+  int optin = 0;
+  cudaError_t err = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (err != cudaSuccess) return err;
   const int norms[] = {NORM_NONE, NORM_LN, NORM_RMS};
   const int epis[] = {EPI_STORE, EPI_RESID, EPI_QKV, EPI_QKV_ROPE, EPI_SWIGLU, EPI_RELU};
   for (Dt dt : {Dt::F32, Dt::BF16})
@@ -362,8 +365,11 @@ cudaError_t gemv_prepare(int /*device*/) {
       for (int e : epis) {
         GemvFn f = pick_any(dt, n, e);
         if (!f) continue;
-        cudaError_t err =
-            cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncAttributes fa;
+        err = cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f));
+        if (err != cudaSuccess) return err;
+        err = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   optin - static_cast<int>(fa.sharedSizeBytes));
         if (err != cudaSuccess) return err;
       }
   return cudaSuccess;
