@@ -68,7 +68,53 @@ enum DevErr : int {
   DEVERR_WRONG_LENGTH = 1,  // live seq_len outside the graph bucket
   DEVERR_CACHE_FULL = 2,
   DEVERR_TOKEN_RANGE = 4,
+  DEVERR_TIMEOUT = 8,       // persistent pass watchdog (a CTA never arrived)
 };
+
+// ---- persistent decode pass (decode_pass.cu) --------------------------------
+struct PassLayer {
+  const void* w_qkv;
+  const void* w_o;
+  const void* w_up;
+  const void* w_down;
+  const float* ln1_g;
+  const float* ln1_b;
+  const float* ln2_g;
+  const float* ln2_b;
+  void* k;
+  void* v;
+};
+
+struct PassParams {
+  int n_layers = 0, d = 0, ff = 0, V = 0, h = 0, dh = 0, max_seq = 0;
+  float eps = 1e-5f;
+  const PassLayer* layers = nullptr;  // device array [n_layers]
+  const void* head = nullptr;
+  const float* lnf_g = nullptr;
+  const float* lnf_b = nullptr;
+  float* x = nullptr;      // residual stream [d]
+  float* q = nullptr;      // [d]
+  float* attn = nullptr;   // [d]
+  float* act = nullptr;    // [ff]
+  float* logits = nullptr; // [V]
+  float* part = nullptr;   // [h][nsplit][dh+2]
+  const float* rope_cos = nullptr;
+  const float* rope_sin = nullptr;
+  int* sync = nullptr;     // [n_layers][sync_stride] counters, zeroed by grt_preprocess each pass
+  int sync_stride = 0;
+  const int* seq_len = nullptr;
+  int* err = nullptr;
+  int nsplit = 1, span_cap = 0;
+  float scale = 1.0f;
+};
+
+// Static pass of one decode step as ONE persistent kernel (one CTA per SM):
+// every layer's QKV | attention | Wo | gate-up | down phases separated by
+// device-side dependency counters, with each warp's weight ring streaming
+// across phase boundaries.  arch_llama selects RMSNorm/RoPE/SwiGLU.
+cudaError_t launch_decode_pass(Dt wdt, Dt kvdt, bool arch_llama, const PassParams& p, cudaStream_t s, bool pdl);
+cudaError_t decode_pass_prepare(int device);
+int decode_pass_sync_stride(int n_heads);
 
 int num_sms(int device);
 

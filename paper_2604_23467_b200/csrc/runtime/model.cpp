@@ -239,6 +239,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
   cuda_check(gemv_prepare(cfg_.device), "gemv_prepare");
   cuda_check(attention_prepare(), "attention_prepare");
+  cuda_check(decode_pass_prepare(cfg_.device), "decode_pass_prepare");
 
   const int64_t d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
   const int64_t h = cfg_.n_heads, dh = cfg_.head_dim();
@@ -278,6 +279,9 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   acc(sizeof(GrtCtrl));
   acc(S * 4);
   acc(max_gen_ * 8);
+  sync_stride_ = decode_pass_sync_stride(static_cast<int>(h));
+  acc(cfg_.n_layers * sizeof(PassLayer));
+  acc((static_cast<size_t>(cfg_.n_layers) * sync_stride_ + 1) * 4);
   arena_.reserve(need);
 
   layers_.resize(cfg_.n_layers);
@@ -312,6 +316,17 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   ctrl_ = static_cast<GrtCtrl*>(arena_buf(sizeof(GrtCtrl), "ctrl"));
   tokens_ = static_cast<int*>(arena_buf(S * 4, "tokens"));
   uniforms_ = static_cast<double*>(arena_buf(max_gen_ * 8, "uniforms"));
+  pass_layers_ = static_cast<PassLayer*>(arena_buf(cfg_.n_layers * sizeof(PassLayer), "pass_layers"));
+  pass_sync_ = static_cast<int*>(arena_buf((static_cast<size_t>(cfg_.n_layers) * sync_stride_ + 1) * 4, "pass_sync"));
+  {
+    std::vector<PassLayer> pl(cfg_.n_layers);
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+      const LayerBuffers& L = layers_[l];
+      pl[l] = PassLayer{L.w_qkv, L.w_o, L.w_up, L.w_down, L.ln1_g, L.ln1_b, L.ln2_g, L.ln2_b, L.k, L.v};
+    }
+    cuda_check(cudaMemcpy(pass_layers_, pl.data(), pl.size() * sizeof(PassLayer), cudaMemcpyHostToDevice),
+               "pass layers");
+  }
 
   weight_bytes_ = (V * d + (cfg_.llama() ? 0 : S * d) + V * d) * wb +
                   static_cast<uint64_t>(cfg_.n_layers) * ((3 * d * d + d * d + up_rows * d + d * ff) * wb) +
@@ -440,7 +455,14 @@ uint64_t Model::decode_bytes(int length) const {
 // ---------------------------------------------------------------------------
 // plans
 
-std::vector<KernelInvocation> Model::build_plan(int key, int B) {
+void Model::attention_split(int key, int B, int* nsplit, int* span_cap) const {
+  const int max_len = std::min(key * B, cfg_.max_seq_len);
+  const int ns = std::min(max_nsplit_, attention_nsplit(max_len, cfg_.n_heads, num_sms(cfg_.device)));
+  *nsplit = ns;
+  *span_cap = ((max_len + ns - 1) / ns + 3) / 4 * 4;
+}
+
+std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   const int d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
   const int h = cfg_.n_heads, dh = cfg_.head_dim();
   const Dt wdt = cfg_.weight_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
@@ -448,16 +470,65 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B) {
   const size_t wb = wdt == Dt::BF16 ? 2 : 4;
   const size_t kvb = kv_elem_bytes();
   const int max_len = std::min(key * B, S);
-  const int sms = num_sms(cfg_.device);
-  const int nsplit = std::min(max_nsplit_, attention_nsplit(max_len, h, sms));
-  int span_cap = (max_len + nsplit - 1) / nsplit;
-  span_cap = (span_cap + 3) / 4 * 4;
+  int nsplit = 1, span_cap = 4;
+  attention_split(key, B, &nsplit, &span_cap);
   const bool llama = cfg_.llama();
   const int norm = llama ? NORM_RMS : NORM_LN;
   int* seq_len = &ctrl_->seq_len;
   int* err = &ctrl_->err;
 
   std::vector<KernelInvocation> plan;
+  if (impl == 0) {
+    // the whole static pass (model.cpp:118-143) as one persistent kernel
+    PassParams pp;
+    pp.n_layers = cfg_.n_layers;
+    pp.d = d;
+    pp.ff = ff;
+    pp.V = V;
+    pp.h = h;
+    pp.dh = dh;
+    pp.max_seq = S;
+    pp.eps = cfg_.norm_eps;
+    pp.layers = pass_layers_;
+    pp.head = head_;
+    pp.lnf_g = lnf_g_;
+    pp.lnf_b = lnf_b_;
+    pp.x = x_;
+    pp.q = q_;
+    pp.attn = attn_;
+    pp.act = act_;
+    pp.logits = logits_;
+    pp.part = attn_part_;
+    pp.rope_cos = rope_cos_;
+    pp.rope_sin = rope_sin_;
+    pp.sync = pass_sync_;
+    pp.sync_stride = sync_stride_;
+    pp.seq_len = seq_len;
+    pp.err = err;
+    pp.nsplit = nsplit;
+    pp.span_cap = span_cap;
+    pp.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
+    KernelInvocation inv;
+    inv.spec.name = "decode_pass";
+    inv.spec.op_class = OpClass::Static;
+    const int64_t up_rows = llama ? 2LL * ff : ff;
+    inv.spec.flops = 2LL * cfg_.n_layers * (3LL * d * d + 1LL * d * d + up_rows * d + 1LL * d * ff) + 2LL * V * d +
+                     static_cast<int64_t>(cfg_.n_layers) * h * max_len * (4 * dh + 5);
+    inv.spec.bytes = static_cast<int64_t>(decode_bytes(max_len));
+    inv.bindings = {{pass_layers_, cfg_.n_layers * sizeof(PassLayer)},
+                    {pass_sync_, (static_cast<size_t>(cfg_.n_layers) * sync_stride_ + 1) * 4},
+                    {head_, static_cast<size_t>(V) * d * wb},
+                    {x_, static_cast<size_t>(d) * 4},
+                    {logits_, static_cast<size_t>(V) * 4}};
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+      inv.bindings.push_back({layers_[l].w_qkv, 3ull * d * d * wb});
+      inv.bindings.push_back({layers_[l].k, static_cast<size_t>(h) * S * dh * kvb});
+      inv.bindings.push_back({layers_[l].v, static_cast<size_t>(h) * S * dh * kvb});
+    }
+    inv.launch = [wdt, kvdt, llama, pp](cudaStream_t s) { return launch_decode_pass(wdt, kvdt, llama, pp, s, true); };
+    plan.push_back(std::move(inv));
+    return plan;
+  }
   auto gemv = [&](const char* name, int epi, int nrm, GemvParams p, size_t w_bytes) {
     KernelInvocation inv;
     inv.spec.name = name;
@@ -565,13 +636,15 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B) {
   return plan;
 }
 
-const std::vector<KernelInvocation>& Model::plan(int key, int B) {
+const std::vector<KernelInvocation>& Model::plan(int key, int B, int impl) {
   if (B < 1) raise(GRT_InvalidConfig, "bucket_size must be >= 1");
+  if (impl != 0 && impl != 1) raise(GRT_InvalidConfig, "pass_impl must be 0 or 1");
   if (key < 1 || key > max_key(B))
     raise(GRT_LengthOutOfRange, "plan key " + std::to_string(key) + " outside [1, " + std::to_string(max_key(B)) + "]");
   std::lock_guard<std::mutex> lk(plan_mu_);
-  auto it = plans_.find({key, B});
-  if (it == plans_.end()) it = plans_.emplace(std::make_pair(key, B), build_plan(key, B)).first;
+  const auto mk = std::make_pair(key, B * 2 + impl);
+  auto it = plans_.find(mk);
+  if (it == plans_.end()) it = plans_.emplace(mk, build_plan(key, B, impl)).first;
   return it->second;
 }
 

@@ -90,6 +90,7 @@ CacheConfig CacheConfig::from_c(const grt_cache_config& c) {
   cc.policy = c.policy == GRT_EVICT_LRU ? EvictionPolicy::LeastRecentlyUsed : EvictionPolicy::LeastUsed;
   cc.bucket_size = c.bucket_size;
   cc.batched_prefill = c.batched_prefill != 0;
+  cc.pass_impl = c.pass_impl;
   return cc;
 }
 
@@ -290,7 +291,7 @@ void Session::write_ctrl(int seq_len, int prompt_len, const grt_sample_params& s
 }
 
 std::vector<const KernelInvocation*> Session::step_kernels(int key, bool fused) {
-  const auto& plan = model_->plan(key, cc_.bucket_size);
+  const auto& plan = model_->plan(key, cc_.bucket_size, cc_.pass_impl);
   std::vector<const KernelInvocation*> ks;
   ks.reserve(plan.size() + 2);
   if (fused) {
@@ -332,7 +333,7 @@ StepResponse Session::serve(const StepRequest& req, bool allow_cache, const Mode
   }
   // eager fallback: dynamic block, then every static kernel launched directly
   dev_->submit_fused_block({sample_op_, pre_op_});
-  for (const KernelInvocation& inv : model_->plan(key, cc_.bucket_size)) dev_->submit_kernel(inv);
+  for (const KernelInvocation& inv : model_->plan(key, cc_.bucket_size, cc_.pass_impl)) dev_->submit_kernel(inv);
   if (use_cache && pol.capture_on_miss && !cache_->contains(ck)) {
     ++dev_->counters().events_recorded;  // ordering point, as record_event/wait_event in the reference
     ++dev_->counters().events_waited;
@@ -368,6 +369,10 @@ void Session::validate(const GenerationRequest& req) const {
 void Session::check_device_errors() {
   int err = 0;
   cuda_check(cudaMemcpy(&err, &model_->ctrl_dev()->err, sizeof(int), cudaMemcpyDeviceToHost), "read err");
+  if (err & DEVERR_TIMEOUT) {
+    model_->reset_pass_sync();
+    raise(GRT_CudaError, "device: persistent pass watchdog expired (a CTA never arrived)");
+  }
   if (err & DEVERR_WRONG_LENGTH) raise(GRT_WrongLength, "device: live length outside the graph bucket");
   if (err & DEVERR_CACHE_FULL) raise(GRT_CacheFull, "device: kv cache at max_seq");
   if (err & DEVERR_TOKEN_RANGE) raise(GRT_TokenOutOfRange, "device: token id out of range");
@@ -506,7 +511,8 @@ void Session::step(int token) {
   cuda_check(cudaMemcpyAsync(model_->tokens_dev() + cur_len_, &token, sizeof(int), cudaMemcpyHostToDevice, s),
              "token");
   dev_->submit_kernel(pre_op_);
-  for (const KernelInvocation& inv : model_->plan(Model::key_of(cur_len_ + 1, cc_.bucket_size), cc_.bucket_size))
+  for (const KernelInvocation& inv :
+       model_->plan(Model::key_of(cur_len_ + 1, cc_.bucket_size), cc_.bucket_size, cc_.pass_impl))
     dev_->submit_kernel(inv);
   cuda_check(cudaStreamSynchronize(s), "step");
   ++cur_len_;
@@ -554,7 +560,7 @@ void Session::kv_row(int layer, int slot, int row, float* out) {
 
 std::vector<KernelProfile> Session::profile_plan(int key, int iters) {
   if (iters < 1) raise(GRT_InvalidConfig, "iters must be >= 1");
-  const auto& plan = model_->plan(key, cc_.bucket_size);
+  const auto& plan = model_->plan(key, cc_.bucket_size, cc_.pass_impl);
   cudaStream_t s = dev_->replay();
   // a valid live length inside the bucket for the attention kernels
   const int len = std::min(key * cc_.bucket_size, model_->config().max_seq_len);

@@ -177,7 +177,9 @@ class Model {
   // Static plan for one bucket key (lengths ((key-1)*B, key*B]).  Memoized;
   // the returned reference is stable for the model's lifetime.  Raises
   // LengthOutOfRange outside [1, max_key].
-  const std::vector<KernelInvocation>& plan(int key, int bucket_size);
+  // impl 0: the whole pass is ONE persistent kernel (decode_pass.cu);
+  // impl 1: 5 per-op kernels per layer + head (gemv.cu / attention.cu).
+  const std::vector<KernelInvocation>& plan(int key, int bucket_size, int impl = 0);
   int max_key(int bucket_size) const { return (cfg_.max_seq_len + bucket_size - 1) / bucket_size; }
   static int key_of(int length, int bucket_size) { return (length + bucket_size - 1) / bucket_size; }
 
@@ -205,11 +207,17 @@ class Model {
   int max_gen() const { return max_gen_; }
   int kv_elem_bytes() const { return cfg_.kv_dtype == GRT_BF16 ? 2 : 4; }
   const std::set<const void*>& buffer_set() const { return buffers_; }
+  void reset_pass_sync() {
+    cudaMemset(pass_sync_, 0, (static_cast<size_t>(cfg_.n_layers) * sync_stride_ + 1) * 4);
+    cudaMemset(&ctrl_->err, 0, sizeof(int));
+    cudaDeviceSynchronize();
+  }
 
  private:
   void declare_tensors();
   void init_weights();
-  std::vector<KernelInvocation> build_plan(int key, int bucket_size);
+  std::vector<KernelInvocation> build_plan(int key, int bucket_size, int impl);
+  void attention_split(int key, int bucket_size, int* nsplit, int* span_cap) const;
   void* arena_buf(size_t bytes, const char* what);
 
   ModelConfig cfg_;
@@ -226,6 +234,9 @@ class Model {
   double* uniforms_ = nullptr;
   int max_gen_ = 0;
   int max_nsplit_ = 1;
+  PassLayer* pass_layers_ = nullptr;  // device [n_layers]
+  int* pass_sync_ = nullptr;          // device [n_layers * sync_stride + 1]
+  int sync_stride_ = 0;
   volatile int* h_out_tokens_ = nullptr;
   volatile unsigned long long* h_out_stamps_ = nullptr;
   uint64_t weight_bytes_ = 0;
@@ -363,6 +374,7 @@ struct CacheConfig {
   EvictionPolicy policy = EvictionPolicy::LeastUsed;
   int bucket_size = 64;
   bool batched_prefill = false;
+  int pass_impl = 0;
   static CacheConfig from_c(const grt_cache_config& c);
 };
 

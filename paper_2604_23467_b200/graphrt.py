@@ -116,7 +116,7 @@ class _ModelConfig(C.Structure):
 class _CacheConfig(C.Structure):
     _fields_ = [("capacity", C.c_uint64), ("warmup_lo", C.c_int32), ("warmup_hi", C.c_int32),
                 ("prefill_uses_graphs", C.c_int32), ("policy", C.c_int32), ("bucket_size", C.c_int32),
-                ("batched_prefill", C.c_int32)]
+                ("batched_prefill", C.c_int32), ("pass_impl", C.c_int32)]
 
 
 class _SampleParams(C.Structure):
@@ -280,6 +280,7 @@ class CacheConfig:
     policy: EvictionPolicy = EvictionPolicy.LeastUsed
     bucket_size: int = 64
     batched_prefill: bool = False
+    pass_impl: int = 0  # 0 persistent single-kernel pass, 1 per-op kernels
 
     def _c(self) -> _CacheConfig:
         c = _CacheConfig()
@@ -287,6 +288,7 @@ class CacheConfig:
         c.prefill_uses_graphs = 1 if self.prefill_uses_graphs else 0
         c.policy, c.bucket_size = int(self.policy), self.bucket_size
         c.batched_prefill = 1 if self.batched_prefill else 0
+        c.pass_impl = int(self.pass_impl)
         return c
 
 

@@ -138,20 +138,22 @@ def test_sampler_greedy_and_temperature(vocab):
 
 # --------------------------------------------------------------------- models
 
-def test_tiny_ref_fp32_matches_reference_fixture(golden):
-    """Reference defaults (tiny-ref): SURVEY Appendix A tokens, logits <= 1e-4."""
+@pytest.mark.parametrize("impl", [0, 1])
+def test_tiny_ref_fp32_matches_reference_fixture(golden, impl):
+    """Reference defaults (tiny-ref): SURVEY Appendix A tokens, logits <= 1e-4,
+    for the persistent pass (impl 0) and the per-op kernels (impl 1)."""
     gd = golden("tiny_ref_greedy.json")
-    s = g.Session(g.ModelConfig(), cache(bucket=64))
+    s = g.Session(g.ModelConfig(), cache(bucket=64, pass_impl=impl))
     toks, worst = step_parity(s, gd["prompt"], len(gd["tokens"]), gd["tokens"], gd["logits"], 1e-4)
     assert worst <= 1e-4, worst
     assert toks == gd["tokens"]
 
 
-@pytest.mark.parametrize("bucket", [1, 64])
-def test_all_modes_reproduce_reference_tokens(golden, bucket):
+@pytest.mark.parametrize("bucket,impl", [(1, 0), (64, 0), (64, 1)])
+def test_all_modes_reproduce_reference_tokens(golden, bucket, impl):
     """c1/c2 (acceptance_main.cpp:77-113): every RunMode yields the reference tokens."""
     gd = golden("tiny_ref_greedy.json")
-    s = g.Session(g.ModelConfig(), cache(bucket=bucket, hi=20))
+    s = g.Session(g.ModelConfig(), cache(bucket=bucket, hi=20, pass_impl=impl))
     for mode in g.ALL_MODES:
         r = s.run(g.GenerationRequest(mode=mode, prompt=gd["prompt"], gen_len=32))
         assert r.tokens == gd["tokens"], g.mode_name(mode)
@@ -192,20 +194,22 @@ def test_wide_temperature(golden):
     assert r.tokens == gd["tokens"]
 
 
+@pytest.mark.parametrize("impl", [0, 1])
 @pytest.mark.parametrize("name,tol", [("llama_tiny_f32", 1e-4), ("llama_tiny_bf16", 2e-2),
                                       ("llama_tiny_philox_bf16", 2e-2)])
-def test_llama_tiny_vs_oracle(golden, name, tol):
+def test_llama_tiny_vs_oracle(golden, name, tol, impl):
     gd = golden(name + ".json")
     c = gd["config"]
     mc = g.ModelConfig(arch=g.ARCH_LLAMA, d_ff_=c["d_ff"], weight_dtype=c.get("weight_dtype", 0),
                        kv_dtype=c.get("kv_dtype", 0), init=c.get("init", 0))
-    s = g.Session(mc, cache())
+    s = g.Session(mc, cache(pass_impl=impl))
     toks, worst = step_parity(s, gd["prompt"], len(gd["tokens"]), gd["tokens"], gd["logits"], tol)
     assert worst <= tol, worst
     margin_ok_tokens(toks, gd["tokens"], gd["logits"], tol)
 
 
-def test_llama_7b_dims_two_layers_vs_oracle():
+@pytest.mark.parametrize("impl", [0, 1])
+def test_llama_7b_dims_two_layers_vs_oracle(impl):
     """LLaMA-2 7B layer shapes (d 4096, ff 11008, V 32000, bf16, Philox init) on
     2 layers against the C oracle: logits max-abs <= 2e-2 after the final norm."""
     kw = dict(arch=g.ARCH_LLAMA, n_layers=2, d_model=4096, n_heads=32, vocab_size=32000, max_seq_len=64,
@@ -215,7 +219,7 @@ def test_llama_7b_dims_two_layers_vs_oracle():
                        n_threads=0)
     prompt = po.make_prompt(42, 6, 32000)
     ref_toks, ref_logits = o.generate_greedy(prompt, 4)
-    s = g.Session(g.ModelConfig(**kw), cache())
+    s = g.Session(g.ModelConfig(**kw), cache(pass_impl=impl))
     toks, worst = step_parity(s, prompt, 4, ref_toks, ref_logits, 2e-2)
     assert worst <= 2e-2, worst
     margin_ok_tokens(toks, ref_toks, ref_logits, 2e-2)
@@ -256,6 +260,39 @@ def test_hybrid_replays_warm_keys_and_captures_the_rest():
     r3 = s.run(g.GenerationRequest(mode=g.RunMode.Hybrid, prompt=prompt[:2], gen_len=2))
     assert r3.cache_released == 4
     assert r1.tokens == r2.tokens
+
+
+def test_persistent_pass_matches_per_op_kernels():
+    """The single-kernel pass and the per-op plan compute the same pass (chunk
+    sizes differ, so fp32 summation order differs): logits agree to 1e-4."""
+    mc = g.ModelConfig(arch=g.ARCH_LLAMA, d_ff_=176, weight_dtype=g.BF16, kv_dtype=g.BF16, init=g.INIT_PHILOX,
+                       n_layers=3, max_seq_len=200, seed=11)
+    prompt = po.make_prompt(5, 40, 256)
+    outs = []
+    for impl in (0, 1):
+        s = g.Session(g.Model(mc), cache(bucket=32, pass_impl=impl))
+        r = s.run(g.GenerationRequest(prompt=prompt, gen_len=100))
+        assert len(r.tokens) == 100
+        s.reset()
+        s.prefill(prompt)
+        outs.append(s.logits())
+    assert np.abs(outs[0] - outs[1]).max() < 1e-4
+
+
+def test_long_context_attention_splits():
+    """Lengths that need many attention splits (up to max_seq) vs the oracle."""
+    kw = dict(n_layers=2, d_model=256, n_heads=2, vocab_size=512, max_seq_len=700, seed=21)
+    o = po.OracleModel(arch=po.ARCH_LLAMA, d_ff=512, weight_dtype=po.BF16, kv_dtype=po.BF16, init=po.INIT_PHILOX, **kw)
+    prompt = po.make_prompt(9, 650, 512)
+    o.prefill(prompt)
+    want = o.logits()
+    s = g.Session(g.ModelConfig(arch=g.ARCH_LLAMA, d_ff_=512, weight_dtype=g.BF16, kv_dtype=g.BF16,
+                                init=g.INIT_PHILOX, **kw), cache(bucket=64))
+    r = s.run(g.GenerationRequest(prompt=prompt, gen_len=20))
+    s.reset()
+    s.prefill(prompt)
+    assert np.abs(s.logits() - want).max() < 2e-2
+    assert len(r.tokens) == 20
 
 
 def test_request_validation():
