@@ -205,6 +205,10 @@ grt_status grt_cache_stats_get(grt_session* s, grt_cache_stats* st, uint64_t* si
  * and names (NUL-separated into `names`, `names_len` bytes); *n = plan size. */
 grt_status grt_profile_plan(grt_session* s, int32_t key, int32_t iters, double* avg_ms, int64_t* bytes,
                             char* names, int32_t names_len, int32_t cap, int32_t* n);
+/* Runs one persistent static pass for bucket `key` with per-CTA %globaltimer
+ * stamps at every phase boundary: out[cta * stride + layer * 10 + e] (ns),
+ * e = qkv start/end, attention start/end, wo, up, down start/end. */
+grt_status grt_trace_pass(grt_session* s, int32_t key, uint64_t* out, int64_t cap, int32_t* grid, int32_t* stride);
 grt_status grt_session_counters(grt_session* s, grt_counters* c);
 
 /* ---- step-level API (Model::step_math / prefill_math / reset, model.cpp:168-183) */

@@ -323,6 +323,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
     prod.advance(p, warp);
   }
   griddep_wait();
+  if (p.trace && threadIdx.x == 0)
+    p.trace[static_cast<int64_t>(blockIdx.x) * p.trace_stride + p.n_layers * PASS_TRACE_PER_LAYER + 2] = globaltimer();
 
   const int len = *p.seq_len;
   EpiArgs ea;
@@ -381,18 +383,27 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
     return;
   }
 
+  unsigned long long* trace = p.trace ? p.trace + static_cast<int64_t>(blockIdx.x) * p.trace_stride : nullptr;
+  auto stamp = [&](int ev) {
+    if (trace && threadIdx.x == 0) trace[ev] = globaltimer();
+  };
+
   for (int l = 0; l < p.n_layers; ++l) {
     const PassLayer L = p.layers[l];
     int* sy = p.sync + l * p.sync_stride;
+    const int tb = l * PASS_TRACE_PER_LAYER;
     // ---- QKV: norm1 + q,k,v (+RoPE) + KV row write
     if (l > 0 && !phase_wait(p.sync + (l - 1) * p.sync_stride + SY_DOWN, G, p.err, &s_ok)) return;
+    stamp(tb + 0);
     load_x<WT, NORM, true>(p.x, L.ln1_g, L.ln1_b, p.eps, p.d, xs, red);
     ea.k_cache = L.k;
     ea.v_cache = L.v;
     run_phase(4 * l + 0, QkvTag{});
     phase_arrive(sy + SY_QKV);
+    stamp(tb + 1);
     // ---- attention over [0, len)
     if (!phase_wait(sy + SY_QKV, G, p.err, &s_ok)) return;
+    stamp(tb + 2);
     const int items = p.h * p.nsplit;
     for (int it = blockIdx.x; it < items; it += G) {
       if (sizeof(KT) == 2)
@@ -400,30 +411,39 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
       else
         attention_item<float>(p, L, l, it / p.nsplit, it % p.nsplit, len, asm_, red, &s_last);
     }
+    stamp(tb + 3);
     // ---- Wo + residual
     if (!phase_wait(sy + SY_ATTN, p.h, p.err, &s_ok)) return;
+    stamp(tb + 4);
     load_x<WT, NORM_NONE, true>(p.attn, nullptr, nullptr, 0.f, p.d, xs, red);
     ea.out = p.x;
     run_phase(4 * l + 1, ResidTag{});
     phase_arrive(sy + SY_WO);
+    stamp(tb + 5);
     // ---- norm2 + gate/up (SwiGLU) | W1 (ReLU)
     if (!phase_wait(sy + SY_WO, G, p.err, &s_ok)) return;
+    stamp(tb + 6);
     load_x<WT, NORM, true>(p.x, L.ln2_g, L.ln2_b, p.eps, p.d, xs, red);
     ea.out = p.act;
     run_phase(4 * l + 2, UpTag{});
     phase_arrive(sy + SY_UP);
+    stamp(tb + 7);
     // ---- down + residual
     if (!phase_wait(sy + SY_UP, G, p.err, &s_ok)) return;
+    stamp(tb + 8);
     load_x<WT, NORM_NONE, true>(p.act, nullptr, nullptr, 0.f, p.ff, xs, red);
     ea.out = p.x;
     run_phase(4 * l + 3, ResidTag{});
     phase_arrive(sy + SY_DOWN);
+    stamp(tb + 9);
   }
   // ---- ln_f + head
   if (!phase_wait(p.sync + (p.n_layers - 1) * p.sync_stride + SY_DOWN, G, p.err, &s_ok)) return;
+  stamp(p.n_layers * PASS_TRACE_PER_LAYER + 0);
   load_x<WT, NORM, true>(p.x, p.lnf_g, p.lnf_b, p.eps, p.d, xs, red);
   ea.out = p.logits;
   run_phase(4 * p.n_layers, StoreTag{});
+  stamp(p.n_layers * PASS_TRACE_PER_LAYER + 1);
 
   // Self-reset: the last CTA out zeroes every counter for the next pass (all
   // other CTAs have passed their last wait when they arrive here).

@@ -106,7 +106,10 @@ struct PassParams {
   int* err = nullptr;
   int nsplit = 1, span_cap = 0;
   float scale = 1.0f;
+  unsigned long long* trace = nullptr;  // optional [grid][trace_stride] %globaltimer phase stamps
+  int trace_stride = 0;
 };
+constexpr int PASS_TRACE_PER_LAYER = 10;  // qkv start/end, attn, wo, up, down (start/end each)
 
 // Static pass of one decode step as ONE persistent kernel (one CTA per SM):
 // every layer's QKV | attention | Wo | gate-up | down phases separated by

@@ -175,6 +175,17 @@ grt_status grt_generate(grt_session* s, const grt_generation_request* req, grt_g
   });
 }
 
+grt_status grt_trace_pass(grt_session* s, int32_t key, uint64_t* out, int64_t cap, int32_t* grid, int32_t* stride) {
+  return guard([&] {
+    int gr = 0, st = 0;
+    s->s->device().sync_all();
+    auto v = s->owner->m->trace_pass(key, s->s->cache_config().bucket_size, s->s->device().replay(), &gr, &st);
+    *grid = gr;
+    *stride = st;
+    for (int64_t i = 0; i < cap && i < static_cast<int64_t>(v.size()); ++i) out[i] = v[i];
+  });
+}
+
 grt_status grt_profile_plan(grt_session* s, int32_t key, int32_t iters, double* avg_ms, int64_t* bytes, char* names,
                             int32_t names_len, int32_t cap, int32_t* n) {
   return guard([&] {

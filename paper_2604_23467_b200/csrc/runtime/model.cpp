@@ -462,6 +462,57 @@ void Model::attention_split(int key, int B, int* nsplit, int* span_cap) const {
   *span_cap = ((max_len + ns - 1) / ns + 3) / 4 * 4;
 }
 
+PassParams Model::pass_params(int key, int B) const {
+  PassParams pp;
+  pp.n_layers = cfg_.n_layers;
+  pp.d = cfg_.d_model;
+  pp.ff = cfg_.d_ff();
+  pp.V = cfg_.vocab_size;
+  pp.h = cfg_.n_heads;
+  pp.dh = cfg_.head_dim();
+  pp.max_seq = cfg_.max_seq_len;
+  pp.eps = cfg_.norm_eps;
+  pp.layers = pass_layers_;
+  pp.head = head_;
+  pp.lnf_g = lnf_g_;
+  pp.lnf_b = lnf_b_;
+  pp.x = x_;
+  pp.q = q_;
+  pp.attn = attn_;
+  pp.act = act_;
+  pp.logits = logits_;
+  pp.part = attn_part_;
+  pp.rope_cos = rope_cos_;
+  pp.rope_sin = rope_sin_;
+  pp.sync = pass_sync_;
+  pp.sync_stride = sync_stride_;
+  pp.seq_len = &ctrl_->seq_len;
+  pp.err = &ctrl_->err;
+  attention_split(key, B, &pp.nsplit, &pp.span_cap);
+  pp.scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim()));  // model.cpp:119
+  return pp;
+}
+
+std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* grid, int* stride) {
+  PassParams pp = pass_params(key, B);
+  *grid = num_sms(cfg_.device);
+  *stride = cfg_.n_layers * PASS_TRACE_PER_LAYER + 4;
+  pp.trace_stride = *stride;
+  const size_t n = static_cast<size_t>(*grid) * *stride;
+  unsigned long long* buf = nullptr;
+  cuda_check(cudaMalloc(&buf, n * 8), "cudaMalloc trace");
+  cuda_check(cudaMemsetAsync(buf, 0, n * 8, s), "memset trace");
+  pp.trace = buf;
+  const Dt wdt = cfg_.weight_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
+  const Dt kvdt = cfg_.kv_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
+  cuda_check(launch_decode_pass(wdt, kvdt, cfg_.llama(), pp, s, false), "trace pass");
+  cuda_check(cudaStreamSynchronize(s), "trace pass");
+  std::vector<uint64_t> out(n);
+  cuda_check(cudaMemcpy(out.data(), buf, n * 8, cudaMemcpyDeviceToHost), "trace copy");
+  cudaFree(buf);
+  return out;
+}
+
 std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   const int d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
   const int h = cfg_.n_heads, dh = cfg_.head_dim();
@@ -480,34 +531,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   std::vector<KernelInvocation> plan;
   if (impl == 0) {
     // the whole static pass (model.cpp:118-143) as one persistent kernel
-    PassParams pp;
-    pp.n_layers = cfg_.n_layers;
-    pp.d = d;
-    pp.ff = ff;
-    pp.V = V;
-    pp.h = h;
-    pp.dh = dh;
-    pp.max_seq = S;
-    pp.eps = cfg_.norm_eps;
-    pp.layers = pass_layers_;
-    pp.head = head_;
-    pp.lnf_g = lnf_g_;
-    pp.lnf_b = lnf_b_;
-    pp.x = x_;
-    pp.q = q_;
-    pp.attn = attn_;
-    pp.act = act_;
-    pp.logits = logits_;
-    pp.part = attn_part_;
-    pp.rope_cos = rope_cos_;
-    pp.rope_sin = rope_sin_;
-    pp.sync = pass_sync_;
-    pp.sync_stride = sync_stride_;
-    pp.seq_len = seq_len;
-    pp.err = err;
-    pp.nsplit = nsplit;
-    pp.span_cap = span_cap;
-    pp.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
+    const PassParams pp = pass_params(key, B);
     KernelInvocation inv;
     inv.spec.name = "decode_pass";
     inv.spec.op_class = OpClass::Static;

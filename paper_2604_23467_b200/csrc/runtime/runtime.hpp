@@ -218,6 +218,13 @@ class Model {
   void init_weights();
   std::vector<KernelInvocation> build_plan(int key, int bucket_size, int impl);
   void attention_split(int key, int bucket_size, int* nsplit, int* span_cap) const;
+
+ public:
+  PassParams pass_params(int key, int bucket_size) const;
+  // Runs one persistent pass with per-CTA %globaltimer phase stamps (profiling).
+  std::vector<uint64_t> trace_pass(int key, int bucket_size, cudaStream_t s, int* grid, int* stride);
+
+ private:
   void* arena_buf(size_t bytes, const char* what);
 
   ModelConfig cfg_;

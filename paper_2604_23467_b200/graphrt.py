@@ -157,7 +157,7 @@ EXPORTS = [
     "grt_sampler_reset", "grt_op_gemv", "grt_op_attention", "grt_op_sample",
     "grt_graph_cache_create", "grt_graph_cache_destroy", "grt_graph_cache_lookup", "grt_graph_cache_insert",
     "grt_graph_cache_warmup", "grt_graph_cache_begin_session", "grt_graph_cache_release_inactive",
-    "grt_graph_cache_query", "grt_profile_plan",
+    "grt_graph_cache_query", "grt_profile_plan", "grt_trace_pass",
 ]
 
 _lib = None
@@ -207,6 +207,8 @@ def lib():
         L.grt_op_sample.argtypes = [vp, C.c_int32, C.POINTER(_SampleParams), C.c_uint64, C.c_double, vp, vp]
         L.grt_profile_plan.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                        C.c_char_p, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
+        L.grt_trace_pass.argtypes = [vp, C.c_int32, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_int32)]
         L.grt_graph_cache_create.argtypes = [C.c_uint64, C.c_int32, C.POINTER(vp)]
         L.grt_graph_cache_destroy.argtypes = [vp]
         L.grt_graph_cache_lookup.argtypes = [vp, C.c_int32, C.POINTER(C.c_int32)]
@@ -478,6 +480,15 @@ class Session:
         _check(lib().grt_profile_plan(self._h, key, iters, ms, by, names, len(names), cap, C.byref(n)))
         nm = names.raw.split(b"\0")
         return [(nm[i].decode(), ms[i], by[i]) for i in range(min(n.value, cap))]
+
+    def trace_pass(self, key: int):
+        """Per-CTA %globaltimer stamps of one persistent pass: array [grid, stride] (ns)."""
+        import numpy as np
+        cap = 148 * (self.model.cfg.n_layers * 10 + 4) * 2
+        buf = (C.c_uint64 * cap)()
+        gr, st = C.c_int32(), C.c_int32()
+        _check(lib().grt_trace_pass(self._h, key, buf, cap, C.byref(gr), C.byref(st)))
+        return np.ctypeslib.as_array(buf)[: gr.value * st.value].reshape(gr.value, st.value).copy()
 
     # step-level API (Model::step_math / prefill_math / reset, model.cpp:168-183)
     def reset(self):
