@@ -2,24 +2,27 @@
 //
 // Reference: Model::build_plan (model.cpp:118-143) -- 14 kernels per layer, each
 // a separate closure.  Batch-1 decode is bandwidth bound (13.2 GB of weights per
-// token for LLaMA-2 7B), so what limits it on a B200 is not arithmetic but the
+// token for LLaMA-2 7B), so on a B200 what limits it is not arithmetic but the
 // bubbles between ~160 dependent kernels.  Here the whole pass is one launch:
 //
-//   * grid = one CTA per SM, 8 warps; every warp owns a ring of DP_STAGES
-//     shared-memory slots that its lane 0 fills with cp.async.bulk (TMA engine)
-//     copies of the weight-row chunks it will consume, in consumption order,
-//     ACROSS phase and layer boundaries -- weights never depend on activations,
-//     so the ring keeps HBM busy while the CTA waits for a dependency;
+//   * grid = one CTA per SM, 8 warps.  Every warp owns a ring of DP_STAGES
+//     8 KB shared-memory slots; its lane 0 CLAIMS the next row pair of the
+//     current GEMV phase from a global counter (dynamic load balance: fast SMs
+//     take more rows) and streams it with cp.async.bulk (TMA engine) in 8 KB
+//     stages.  Claims run ahead of consumption ACROSS phase and layer
+//     boundaries -- weights never depend on activations -- so HBM stays busy
+//     while the CTA waits for a dependency;
 //   * phases per layer: QKV(+norm, RoPE, KV write) | attention | Wo(+residual) |
-//     gate/up(+norm, SwiGLU) | down(+residual); the boundaries are device-side
+//     gate/up(+norm, SwiGLU) | down(+residual); boundaries are device-side
 //     dependency counters (release: __threadfence + atomicAdd; acquire: spin +
-//     __threadfence); the last CTA out resets them for the next pass;
+//     __threadfence); the last CTA out resets all counters for the next pass;
 //   * activations produced by other CTAs in the same launch are read with
 //     ld.global.cg (L2), never through a possibly stale L1 line;
 //   * a watchdog turns a missing arrival into DEVERR_TIMEOUT instead of a hang.
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <climits>
 #include <type_traits>
 
 #include "common.cuh"
@@ -30,20 +33,16 @@ namespace grt {
 
 constexpr int DP_WARPS = 8;
 constexpr int DP_THREADS = DP_WARPS * 32;
-constexpr int DP_STAGES = 5;
-constexpr int DP_CH_BF16 = 1024;  // elements per row chunk: 2 KB -> 4 KB stages (row pair)
-constexpr int DP_CH_F32 = 512;
-constexpr uint32_t DP_STAGE_BYTES = 4096;
+constexpr int DP_STAGES = 2;
+constexpr uint32_t DP_STAGE_BYTES = 8192;
 constexpr unsigned long long DP_WATCHDOG_NS = 2000000000ull;  // 2 s
 
 enum SyncSlot { SY_QKV = 0, SY_ATTN = 1, SY_WO = 2, SY_UP = 3, SY_DOWN = 4, SY_HEADS = 8 };
 
 int decode_pass_sync_stride(int n_heads) { return ((SY_HEADS + n_heads + 31) / 32) * 32; }
-
-template <typename WT>
-constexpr int dp_ch() {
-  return sizeof(WT) == 2 ? DP_CH_BF16 : DP_CH_F32;
-}
+// sync array: [n_layers][stride] phase counters | [4L+1] row-pair claim counters | exit counter
+static __host__ __device__ int sync_total(int n_layers, int stride) { return n_layers * stride + 4 * n_layers + 2; }
+int decode_pass_sync_ints(int n_layers, int n_heads) { return sync_total(n_layers, decode_pass_sync_stride(n_heads)); }
 
 struct GemvPhase {
   const void* w;
@@ -69,60 +68,134 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Per-warp producer state: walks (phase, pair, chunk) in consumption order.
+// Per-stage metadata (written by the producer lane, read by the warp).
+struct StageMeta {
+  int ph;    // phase of the stage; -1 = slot empty
+  int pair;  // row pair
+  int off;   // byte offset in the pair's contiguous 2-row stream
+  int len;   // bytes in this stage
+};
+
+// Per-warp producer: claims row pairs phase by phase and issues 8 KB stages.
+// All lanes keep identical state (claims are broadcast from lane 0).
 template <typename WT, bool LLAMA>
 struct Producer {
-  int ph = 0, pi = 0, c = 0;
-  int nch = 0, my_pairs = 0, pair_begin = 0, n_last = 0;
+  int ph = 0;        // phase being claimed; > 4L = done
+  int pair = -1;     // claimed pair (-1: claim next)
+  int off = 0;       // next byte offset in the pair stream
+  int pair_bytes = 0;
   GemvPhase g{};
+  int n_pairs = 0;
+  int t = 0;         // stages issued
   bool done = false;
-  int t = 0;  // tasks issued
 
-  __device__ void load_phase(const PassParams& p, int warp) {
-    const int n_ph = 4 * p.n_layers + 1;
-    for (; ph < n_ph; ++ph) {
-      g = phase_desc<LLAMA>(p, ph);
-      const int n_pairs = (g.n_rows + 1) >> 1;
-      pair_begin = static_cast<int>(static_cast<int64_t>(blockIdx.x) * n_pairs / gridDim.x);
-      const int pair_end = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * n_pairs / gridDim.x);
-      const int span = pair_end - pair_begin - warp;
-      my_pairs = span <= 0 ? 0 : (span + DP_WARPS - 1) / DP_WARPS;
-      nch = (g.k + dp_ch<WT>() - 1) / dp_ch<WT>();
-      if (my_pairs > 0) {
-        pi = 0;
-        c = 0;
-        return;
+  __device__ void set_phase(const PassParams& p, int new_ph) {
+    ph = new_ph;
+    if (ph > 4 * p.n_layers) {
+      done = true;
+      return;
+    }
+    g = phase_desc<LLAMA>(p, ph);
+    n_pairs = (g.n_rows + 1) >> 1;
+  }
+
+  // Issues the next stage into slot t % DP_STAGES; returns false when exhausted.
+  __device__ bool issue(const PassParams& p, int* claims, uint8_t* ring, uint64_t* bars, StageMeta* meta,
+                        uint64_t pol) {
+    const int lane = threadIdx.x & 31;
+    while (!done && pair < 0) {
+      int c = 0;
+      if (lane == 0) c = atomicAdd(claims + ph, 1);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c < n_pairs) {
+        pair = c;
+        off = 0;
+        const int rows = (2 * c + 1 < g.n_rows) ? 2 : 1;
+        pair_bytes = rows * g.k * static_cast<int>(sizeof(WT));
+      } else {
+        set_phase(p, ph + 1);
       }
     }
-    done = true;
-  }
-
-  // lane 0 only
-  __device__ void issue(uint8_t* ring, uint64_t* bars, int warp, uint64_t pol) {
-    constexpr int CH = dp_ch<WT>();
-    const int row0 = 2 * (pair_begin + warp + pi * DP_WARPS);
-    const int c0 = c * CH;
-    const int ce = min(CH, g.k - c0);
-    const uint32_t bytes = static_cast<uint32_t>(ce) * sizeof(WT);
-    const bool has_b = row0 + 1 < g.n_rows;
+    if (done) return false;
     const int slot = t % DP_STAGES;
-    uint64_t* bar = &bars[slot];
-    uint8_t* dst = ring + slot * DP_STAGE_BYTES;
-    mbar_arrive_expect_tx(bar, has_b ? 2 * bytes : bytes);
-    const WT* src = reinterpret_cast<const WT*>(g.w) + static_cast<int64_t>(row0) * g.k + c0;
-    bulk_g2s(dst, src, bytes, bar, pol);
-    if (has_b) bulk_g2s(dst + DP_STAGE_BYTES / 2, src + g.k, bytes, bar, pol);
-  }
-
-  __device__ void advance(const PassParams& p, int warp) {
+    const int len = min(static_cast<int>(DP_STAGE_BYTES), pair_bytes - off);
+    if (lane == 0) {
+      meta[slot] = StageMeta{ph, pair, off, len};
+      uint64_t* bar = &bars[slot];
+      mbar_arrive_expect_tx(bar, static_cast<uint32_t>(len));
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(g.w) +
+                           static_cast<int64_t>(2 * pair) * g.k * static_cast<int64_t>(sizeof(WT)) + off;
+      bulk_g2s(ring + slot * DP_STAGE_BYTES, src, static_cast<uint32_t>(len), bar, pol);
+    }
+    off += len;
+    if (off >= pair_bytes) pair = -1;
     ++t;
-    if (++c < nch) return;
-    c = 0;
-    if (++pi < my_pairs) return;
-    ++ph;
-    load_phase(p, warp);
+    return true;
   }
 };
+
+// Dot of one stage of a pair stream: elements [e0, e0 + len/sizeof) of the
+// concatenation row_a | row_b (each of length k).
+template <typename WT>
+__device__ __forceinline__ void dot_stage(const uint8_t* st, int e0, int len, int k, const float* xs, float& acc_a,
+                                          float& acc_b) {
+  const int lane = threadIdx.x & 31;
+  const int groups = len >> 4;  // 16-byte groups
+  float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+  if constexpr (sizeof(WT) == 2) {
+    const uint4* w = reinterpret_cast<const uint4*>(st);
+    const float4* xa = reinterpret_cast<const float4*>(xs);
+    const float4* xb = reinterpret_cast<const float4*>(xs + (k >> 1));
+#pragma unroll 4
+    for (int q = lane; q < groups; q += 32) {
+      const int e = e0 + q * 8;
+      const bool isb = e >= k;
+      const int gi = (isb ? e - k : e) >> 3;
+      const uint4 u = w[q];
+      const float4 x0 = xa[gi];
+      const float4 x1 = xb[gi];
+      float s0 = bf16lo(u.x) * x0.x;
+      float s1 = bf16hi(u.x) * x0.y;
+      s0 = fmaf(bf16lo(u.y), x0.z, s0);
+      s1 = fmaf(bf16hi(u.y), x0.w, s1);
+      s0 = fmaf(bf16lo(u.z), x1.x, s0);
+      s1 = fmaf(bf16hi(u.z), x1.y, s1);
+      s0 = fmaf(bf16lo(u.w), x1.z, s0);
+      s1 = fmaf(bf16hi(u.w), x1.w, s1);
+      if (isb) {
+        b0 += s0;
+        b1 += s1;
+      } else {
+        a0 += s0;
+        a1 += s1;
+      }
+    }
+  } else {
+    const float4* w = reinterpret_cast<const float4*>(st);
+    const float4* xv = reinterpret_cast<const float4*>(xs);
+#pragma unroll 4
+    for (int q = lane; q < groups; q += 32) {
+      const int e = e0 + q * 4;
+      const bool isb = e >= k;
+      const int gi = (isb ? e - k : e) >> 2;
+      const float4 u = w[q];
+      const float4 x = xv[gi];
+      float s0 = u.x * x.x;
+      float s1 = u.y * x.y;
+      s0 = fmaf(u.z, x.z, s0);
+      s1 = fmaf(u.w, x.w, s1);
+      if (isb) {
+        b0 += s0;
+        b1 += s1;
+      } else {
+        a0 += s0;
+        a1 += s1;
+      }
+    }
+  }
+  acc_a += a0 + a1;
+  acc_b += b0 + b1;
+}
 
 // ---- dependency counters ------------------------------------------------------
 
@@ -142,7 +215,6 @@ __device__ __forceinline__ bool phase_wait(int* ctr, int target, int* err, int* 
     if (*v < target) {
       const unsigned long long t0 = globaltimer();
       while (*v < target) {
-        __nanosleep(64);
         if (globaltimer() - t0 > DP_WATCHDOG_NS) {
           atomicOr(err, DEVERR_TIMEOUT);
           ok = 0;
@@ -171,7 +243,7 @@ __device__ __forceinline__ float4 kv_load4<__nv_bfloat16>(const __nv_bfloat16* p
   return make_float4(bf16lo(u.x), bf16hi(u.x), bf16lo(u.y), bf16hi(u.y));
 }
 
-__device__ __forceinline__ float block_max_256(float v, float* red) {
+__device__ __forceinline__ float block_max_all(float v, float* red) {
   v = warp_max(v);
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
@@ -189,8 +261,8 @@ template <typename KT>
 __device__ void attention_item(const PassParams& p, const PassLayer& L, int layer, int head, int split, int len,
                                float* sm, float* red, int* s_last) {
   const int dh = p.dh, ns = p.nsplit;
-  const int gs = dh >> 2;              // lanes per position
-  const int npg = DP_THREADS / gs;     // position groups
+  const int gs = dh >> 2;           // lanes per position
+  const int npg = DP_THREADS / gs;  // position groups
   const int span = (len + ns - 1) / ns;
   const int j0 = split * span;
   const int n = max(0, min(len, j0 + span) - j0);
@@ -216,7 +288,7 @@ __device__ void attention_item(const PassParams& p, const PassLayer& L, int laye
   __syncthreads();
   float m = -INFINITY;
   for (int jj = threadIdx.x; jj < n; jj += DP_THREADS) m = fmaxf(m, sc[jj]);
-  m = block_max_256(m, red);
+  m = block_max_all(m, red);
   float l = 0.0f;
   for (int jj = threadIdx.x; jj < n; jj += DP_THREADS) {
     const float e = expf(sc[jj] - m);
@@ -296,9 +368,9 @@ template <typename WT, typename KT, bool LLAMA>
 __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[DP_WARPS][DP_STAGES];
+  __shared__ StageMeta metas[DP_WARPS][DP_STAGES];
   __shared__ float red[32];
   __shared__ int s_ok, s_last;
-  constexpr int CH = dp_ch<WT>();
   constexpr int NORM = LLAMA ? NORM_RMS : NORM_LN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -307,21 +379,25 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   float* xs = reinterpret_cast<float*>(smem + static_cast<size_t>(DP_WARPS) * DP_STAGES * DP_STAGE_BYTES);
   float* asm_ = xs + max(p.d, p.ff);  // attention scratch
   uint64_t* mybar = bars[warp];
+  StageMeta* meta = metas[warp];
   const uint64_t pol = l2_evict_first_policy();
+  int* claims = p.sync + p.n_layers * p.sync_stride;
 
   Producer<WT, LLAMA> prod;
   if (lane == 0) {
 #pragma unroll
-    for (int s = 0; s < DP_STAGES; ++s) mbar_init(&mybar[s], 1);
+    for (int s = 0; s < DP_STAGES; ++s) {
+      mbar_init(&mybar[s], 1);
+      meta[s].ph = -1;
+    }
     mbar_fence_init();
   }
   __syncwarp();
-  prod.load_phase(p, warp);
+  prod.set_phase(p, 0);
   // Weights do not depend on the previous kernel: fill the ring before waiting.
-  for (int s = 0; s < DP_STAGES && !prod.done; ++s) {
-    if (lane == 0) prod.issue(ring, mybar, warp, pol);
-    prod.advance(p, warp);
-  }
+  for (int s = 0; s < DP_STAGES; ++s)
+    if (!prod.issue(p, claims, ring, mybar, meta, pol)) break;
+  __syncwarp();
   griddep_wait();
   if (p.trace && threadIdx.x == 0)
     p.trace[static_cast<int64_t>(blockIdx.x) * p.trace_stride + p.n_layers * PASS_TRACE_PER_LAYER + 2] = globaltimer();
@@ -337,38 +413,36 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   ea.kv_bf16 = sizeof(KT) == 2;
   ea.q_out = p.q;
 
-  int t = 0;  // tasks consumed by this warp
-  // Consume every task of GEMV phase `ph` with epilogue EPI.
+  int t = 0;  // stages consumed by this warp
+  // Consume every stage this warp claimed in GEMV phase `ph`.
   auto run_phase = [&](int ph, auto epi_tag) {
     constexpr int EPI = decltype(epi_tag)::value;
     const GemvPhase g = phase_desc<LLAMA>(p, ph);
-    const int n_pairs = (g.n_rows + 1) >> 1;
-    const int pb = static_cast<int>(static_cast<int64_t>(blockIdx.x) * n_pairs / G);
-    const int pe = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * n_pairs / G);
-    const int span = pe - pb - warp;
-    const int my_pairs = span <= 0 ? 0 : (span + DP_WARPS - 1) / DP_WARPS;
-    const int nch = (g.k + CH - 1) / CH;
-    for (int pi = 0; pi < my_pairs; ++pi) {
-      const int pair = pb + warp + pi * DP_WARPS;
-      float acc_a = 0.0f, acc_b = 0.0f;
-      for (int c = 0; c < nch; ++c, ++t) {
-        const int slot = t % DP_STAGES;
-        mbar_wait(&mybar[slot], static_cast<uint32_t>((t / DP_STAGES) & 1));
-        const int c0 = c * CH;
-        const uint8_t* st = ring + slot * DP_STAGE_BYTES;
-        dot_chunk<WT>(st, st + DP_STAGE_BYTES / 2, xs, g.k, c0, min(CH, g.k - c0), acc_a, acc_b);
-        __syncwarp();
-        if (!prod.done) {
-          if (lane == 0) {
-            fence_proxy_async_smem();
-            prod.issue(ring, mybar, warp, pol);
-          }
-          prod.advance(p, warp);
-        }
+    float acc_a = 0.0f, acc_b = 0.0f;
+    for (;;) {
+      const int slot = t % DP_STAGES;
+      const StageMeta m = meta[slot];
+      if (m.ph != ph) break;  // ring moved on to a later phase (or ran dry)
+      mbar_wait(&mybar[slot], static_cast<uint32_t>((t / DP_STAGES) & 1));
+      dot_stage<WT>(ring + slot * DP_STAGE_BYTES, m.off / static_cast<int>(sizeof(WT)), m.len, g.k, xs, acc_a,
+                    acc_b);
+      __syncwarp();
+      if (lane == 0) {
+        meta[slot].ph = -1;
+        fence_proxy_async_smem();
       }
-      const float va = warp_sum(acc_a);
-      const float vb = warp_sum(acc_b);
-      if (lane == 0) epilogue<EPI>(ea, pair, va, vb, 2 * pair + 1 < g.n_rows);
+      __syncwarp();
+      prod.issue(p, claims, ring, mybar, meta, pol);
+      __syncwarp();
+      ++t;
+      const int rows = (2 * m.pair + 1 < g.n_rows) ? 2 : 1;
+      if (m.off + m.len >= rows * g.k * static_cast<int>(sizeof(WT))) {
+        const float va = warp_sum(acc_a);
+        const float vb = warp_sum(acc_b);
+        if (lane == 0) epilogue<EPI>(ea, m.pair, va, vb, rows == 2);
+        acc_a = 0.0f;
+        acc_b = 0.0f;
+      }
     }
   };
   using QkvTag = std::integral_constant<int, LLAMA ? EPI_QKV_ROPE : EPI_QKV>;
@@ -376,17 +450,17 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   using UpTag = std::integral_constant<int, LLAMA ? EPI_SWIGLU : EPI_RELU>;
   using StoreTag = std::integral_constant<int, EPI_STORE>;
 
+  unsigned long long* trace = p.trace ? p.trace + static_cast<int64_t>(blockIdx.x) * p.trace_stride : nullptr;
+  auto stamp = [&](int ev) {
+    if (trace && threadIdx.x == 0) trace[ev] = globaltimer();
+  };
+
   if (len < 1 || len > p.max_seq || (len + p.nsplit - 1) / p.nsplit > p.span_cap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(p.err, DEVERR_WRONG_LENGTH);
     // drain the prefetched stages so no bulk copy is outstanding at exit
     for (int s = 0; s < min(DP_STAGES, prod.t); ++s) mbar_wait(&mybar[s], 0);
     return;
   }
-
-  unsigned long long* trace = p.trace ? p.trace + static_cast<int64_t>(blockIdx.x) * p.trace_stride : nullptr;
-  auto stamp = [&](int ev) {
-    if (trace && threadIdx.x == 0) trace[ev] = globaltimer();
-  };
 
   for (int l = 0; l < p.n_layers; ++l) {
     const PassLayer L = p.layers[l];
@@ -445,17 +519,17 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   run_phase(4 * p.n_layers, StoreTag{});
   stamp(p.n_layers * PASS_TRACE_PER_LAYER + 1);
 
-  // Self-reset: the last CTA out zeroes every counter for the next pass (all
-  // other CTAs have passed their last wait when they arrive here).
+  // Self-reset: the last CTA out zeroes every counter (phase, head, claim) for
+  // the next pass; all other CTAs have passed their last wait and claim.
   __syncthreads();
-  int* exit_ctr = p.sync + p.n_layers * p.sync_stride;
+  const int total = sync_total(p.n_layers, p.sync_stride);
+  int* exit_ctr = p.sync + total - 1;
   if (threadIdx.x == 0) {
     __threadfence();
     s_last = atomicAdd(exit_ctr, 1) == G - 1;
   }
   __syncthreads();
   if (s_last) {
-    const int total = p.n_layers * p.sync_stride + 1;
     for (int i = threadIdx.x; i < total; i += DP_THREADS) p.sync[i] = 0;
     __threadfence();
   }

@@ -118,6 +118,7 @@ constexpr int PASS_TRACE_PER_LAYER = 10;  // qkv start/end, attn, wo, up, down (
 cudaError_t launch_decode_pass(Dt wdt, Dt kvdt, bool arch_llama, const PassParams& p, cudaStream_t s, bool pdl);
 cudaError_t decode_pass_prepare(int device);
 int decode_pass_sync_stride(int n_heads);
+int decode_pass_sync_ints(int n_layers, int n_heads);  // size of PassParams::sync
 
 int num_sms(int device);
 

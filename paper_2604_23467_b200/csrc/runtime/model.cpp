@@ -281,7 +281,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   acc(max_gen_ * 8);
   sync_stride_ = decode_pass_sync_stride(static_cast<int>(h));
   acc(cfg_.n_layers * sizeof(PassLayer));
-  acc((static_cast<size_t>(cfg_.n_layers) * sync_stride_ + 1) * 4);
+  acc(static_cast<size_t>(sync_ints()) * 4);
   arena_.reserve(need);
 
   layers_.resize(cfg_.n_layers);
@@ -317,7 +317,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   tokens_ = static_cast<int*>(arena_buf(S * 4, "tokens"));
   uniforms_ = static_cast<double*>(arena_buf(max_gen_ * 8, "uniforms"));
   pass_layers_ = static_cast<PassLayer*>(arena_buf(cfg_.n_layers * sizeof(PassLayer), "pass_layers"));
-  pass_sync_ = static_cast<int*>(arena_buf((static_cast<size_t>(cfg_.n_layers) * sync_stride_ + 1) * 4, "pass_sync"));
+  pass_sync_ = static_cast<int*>(arena_buf(static_cast<size_t>(sync_ints()) * 4, "pass_sync"));
   {
     std::vector<PassLayer> pl(cfg_.n_layers);
     for (int l = 0; l < cfg_.n_layers; ++l) {
@@ -540,7 +540,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
                      static_cast<int64_t>(cfg_.n_layers) * h * max_len * (4 * dh + 5);
     inv.spec.bytes = static_cast<int64_t>(decode_bytes(max_len));
     inv.bindings = {{pass_layers_, cfg_.n_layers * sizeof(PassLayer)},
-                    {pass_sync_, (static_cast<size_t>(cfg_.n_layers) * sync_stride_ + 1) * 4},
+                    {pass_sync_, static_cast<size_t>(sync_ints()) * 4},
                     {head_, static_cast<size_t>(V) * d * wb},
                     {x_, static_cast<size_t>(d) * 4},
                     {logits_, static_cast<size_t>(V) * 4}};

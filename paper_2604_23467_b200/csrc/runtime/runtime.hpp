@@ -207,8 +207,9 @@ class Model {
   int max_gen() const { return max_gen_; }
   int kv_elem_bytes() const { return cfg_.kv_dtype == GRT_BF16 ? 2 : 4; }
   const std::set<const void*>& buffer_set() const { return buffers_; }
+  int sync_ints() const { return decode_pass_sync_ints(cfg_.n_layers, cfg_.n_heads); }
   void reset_pass_sync() {
-    cudaMemset(pass_sync_, 0, (static_cast<size_t>(cfg_.n_layers) * sync_stride_ + 1) * 4);
+    cudaMemset(pass_sync_, 0, static_cast<size_t>(sync_ints()) * 4);
     cudaMemset(&ctrl_->err, 0, sizeof(int));
     cudaDeviceSynchronize();
   }
