@@ -67,12 +67,94 @@ __device__ __forceinline__ float act_ld(const float* p) {
   return *p;
 }
 
-// Activation prologue: xs = norm(x) (or x).  Loop shapes follow the reference
-// layernorm (kernels.cpp:66-83): sum -> mean, sum of squares -> variance,
-// inv = 1/sqrt(var + eps); RMSNorm drops the mean and beta.
+template <typename WT, int NORM, bool CG>
+__device__ __noinline__ void load_x_slow(const float* x, const float* gamma, const float* beta, float eps, int k,
+                                         float* xs, float* red);
+
+template <bool CG>
+__device__ __forceinline__ float4 act_ld4(const float* p) {
+  if constexpr (CG) return __ldcg(reinterpret_cast<const float4*>(p));
+  return *reinterpret_cast<const float4*>(p);
+}
+
+// Writes float4 #j4 of the activation into the shared-memory layout (for bf16
+// weights an aligned float4 of x is exactly one float4 of plane j4&1).
+template <typename WT>
+__device__ __forceinline__ void xs_store4(float* xs, int j4, int k, float4 v) {
+  if constexpr (WTraits<WT>::VEC == 8)
+    reinterpret_cast<float4*>(xs + (j4 & 1) * (k >> 1))[j4 >> 1] = v;
+  else
+    reinterpret_cast<float4*>(xs)[j4] = v;
+}
+
+constexpr int LOADX_MAXV = 12;  // float4 per thread kept in registers (k <= 12*4*blockDim)
+
+// Activation prologue: xs = norm(x) (or x).  The whole activation row is pulled
+// into registers with independent 16-byte loads first (latency paid once, not
+// per element), then reduced, normalised and stored.  Norm arithmetic follows
+// the reference layernorm (kernels.cpp:66-83): sum -> mean, sum of squared
+// deviations -> variance, inv = 1/sqrt(var + eps); RMSNorm drops mean and beta.
 template <typename WT, int NORM, bool CG>
 __device__ __forceinline__ void load_x(const float* x, const float* gamma, const float* beta, float eps, int k,
                                        float* xs, float* red) {
+  const int n4 = k >> 2;
+  if (n4 <= LOADX_MAXV * static_cast<int>(blockDim.x)) {
+    float4 v[LOADX_MAXV];
+#pragma unroll
+    for (int i = 0; i < LOADX_MAXV; ++i) {
+      const int j4 = threadIdx.x + i * blockDim.x;
+      v[i] = j4 < n4 ? act_ld4<CG>(x + 4 * j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float mean = 0.0f, inv = 1.0f;
+    if constexpr (NORM == NORM_RMS) {
+      float ss = 0.0f;
+#pragma unroll
+      for (int i = 0; i < LOADX_MAXV; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+      ss = block_sum(ss, red);
+      inv = 1.0f / sqrtf(ss / static_cast<float>(k) + eps);
+    } else if constexpr (NORM == NORM_LN) {
+      float s = 0.0f;
+#pragma unroll
+      for (int i = 0; i < LOADX_MAXV; ++i) s += v[i].x + v[i].y + v[i].z + v[i].w;
+      mean = block_sum(s, red) / static_cast<float>(k);
+      float var = 0.0f;
+#pragma unroll
+      for (int i = 0; i < LOADX_MAXV; ++i) {
+        const int j4 = threadIdx.x + i * blockDim.x;
+        if (j4 < n4) {
+          const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+          var += a * a + b * b + c * c + d * d;
+        }
+      }
+      var = block_sum(var, red) / static_cast<float>(k);
+      inv = 1.0f / sqrtf(var + eps);
+    }
+#pragma unroll
+    for (int i = 0; i < LOADX_MAXV; ++i) {
+      const int j4 = threadIdx.x + i * blockDim.x;
+      if (j4 >= n4) continue;
+      float4 o = v[i];
+      if constexpr (NORM == NORM_RMS) {
+        const float4 g = *reinterpret_cast<const float4*>(gamma + 4 * j4);
+        o = make_float4(o.x * inv * g.x, o.y * inv * g.y, o.z * inv * g.z, o.w * inv * g.w);
+      } else if constexpr (NORM == NORM_LN) {
+        const float4 g = *reinterpret_cast<const float4*>(gamma + 4 * j4);
+        const float4 b = *reinterpret_cast<const float4*>(beta + 4 * j4);
+        o = make_float4((o.x - mean) * inv * g.x + b.x, (o.y - mean) * inv * g.y + b.y,
+                        (o.z - mean) * inv * g.z + b.z, (o.w - mean) * inv * g.w + b.w);
+      }
+      xs_store4<WT>(xs, j4, k, o);
+    }
+    __syncthreads();
+    return;
+  }
+  load_x_slow<WT, NORM, CG>(x, gamma, beta, eps, k, xs, red);
+}
+
+// Generic fallback for very wide activations (k > 12*4*blockDim).
+template <typename WT, int NORM, bool CG>
+__device__ __noinline__ void load_x_slow(const float* x, const float* gamma, const float* beta, float eps, int k,
+                                         float* xs, float* red) {
   if constexpr (NORM == NORM_NONE) {
     for (int j = threadIdx.x; j < k; j += blockDim.x) xs[xs_index<WT>(j, k)] = act_ld<CG>(x + j);
   } else if constexpr (NORM == NORM_RMS) {
