@@ -3,22 +3,25 @@
 // Reference: Model::build_plan (model.cpp:118-143) -- 14 kernels per layer, each
 // a separate closure.  Batch-1 decode is bandwidth bound (13.2 GB of weights per
 // token for LLaMA-2 7B), so on a B200 what limits it is not arithmetic but the
-// bubbles between ~160 dependent kernels.  Here the whole pass is one launch:
+// bubbles between ~160 dependent kernels.  Here the whole pass is one launch,
+// warp-specialised:
 //
-//   * grid = one CTA per SM, 8 warps.  Every warp owns a ring of DP_STAGES
-//     8 KB shared-memory slots; its lane 0 CLAIMS the next row pair of the
-//     current GEMV phase from a global counter (dynamic load balance: fast SMs
-//     take more rows) and streams it with cp.async.bulk (TMA engine) in 8 KB
-//     stages.  Claims run ahead of consumption ACROSS phase and layer
-//     boundaries -- weights never depend on activations -- so HBM stays busy
-//     while the CTA waits for a dependency;
+//   * grid = one CTA per SM.  Warp 8 is the PRODUCER: one lane walks every GEMV
+//     phase of the pass (QKV, Wo, gate/up, down per layer, then the LM head),
+//     takes its CTA's row pairs (a static share plus dynamically claimed tail
+//     pairs for load balance) and streams them into a 16-slot x 8 KB ring with
+//     cp.async.bulk (TMA engine) under an evict-first L2 policy.  Weights never
+//     depend on activations, so it runs ahead ACROSS phase and layer boundaries,
+//     throttled only by free slots -- HBM stays busy while the CTA waits.
+//   * warps 0-7 are CONSUMERS: each stage is split across the 8 warps (1 KB
+//     each); per row pair the warp partials are reduced in a fixed order, so
+//     results are deterministic.  Between phases the consumers wait on
+//     device-side dependency counters (release: __threadfence + atomicAdd;
+//     acquire: spin + __threadfence); the last CTA out resets every counter.
 //   * phases per layer: QKV(+norm, RoPE, KV write) | attention | Wo(+residual) |
-//     gate/up(+norm, SwiGLU) | down(+residual); boundaries are device-side
-//     dependency counters (release: __threadfence + atomicAdd; acquire: spin +
-//     __threadfence); the last CTA out resets all counters for the next pass;
-//   * activations produced by other CTAs in the same launch are read with
-//     ld.global.cg (L2), never through a possibly stale L1 line;
-//   * a watchdog turns a missing arrival into DEVERR_TIMEOUT instead of a hang.
+//     gate/up(+norm, SwiGLU) | down(+residual); activations written by other
+//     CTAs in this launch are read with ld.global.cg (L2), never a stale L1 line;
+//   * watchdogs turn a missing arrival into DEVERR_TIMEOUT instead of a hang.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -31,11 +34,13 @@
 
 namespace grt {
 
-constexpr int DP_WARPS = 8;
-constexpr int DP_THREADS = DP_WARPS * 32;
-constexpr int DP_STAGES = 2;
+constexpr int DP_CWARPS = 8;                       // consumer warps
+constexpr int DP_THREADS = (DP_CWARPS + 1) * 32;   // + producer warp
+constexpr int DP_STAGES = 16;
 constexpr uint32_t DP_STAGE_BYTES = 8192;
+constexpr uint32_t DP_SLICE = DP_STAGE_BYTES / DP_CWARPS;  // bytes of a stage per consumer warp
 constexpr unsigned long long DP_WATCHDOG_NS = 2000000000ull;  // 2 s
+constexpr int DP_END = INT_MAX;
 
 enum SyncSlot { SY_QKV = 0, SY_ATTN = 1, SY_WO = 2, SY_UP = 3, SY_DOWN = 4, SY_HEADS = 8 };
 
@@ -68,146 +73,135 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Per-stage metadata (written by the producer lane, read by the warp).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// wait with a watchdog; returns false on expiry
+__device__ __forceinline__ bool mbar_wait_wd(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return true;
+  const unsigned long long t0 = globaltimer();
+  while (!mbar_try_wait(bar, parity))
+    if (globaltimer() - t0 > DP_WATCHDOG_NS) return false;
+  return true;
+}
+
 struct StageMeta {
-  int ph;    // phase of the stage; -1 = slot empty
+  int ph;    // phase of the stage; DP_END after the last one
   int pair;  // row pair
   int off;   // byte offset in the pair's contiguous 2-row stream
   int len;   // bytes in this stage
 };
 
-// Per-warp producer: claims row pairs phase by phase and issues 8 KB stages.
-// All lanes keep identical state (claims are broadcast from lane 0).
+// Static share: 4/5 of the pairs in contiguous blocks per CTA; the rest are
+// claimed one pair at a time by whichever CTA is ready first.
+__device__ __forceinline__ int static_share(int n_pairs, int G) { return (n_pairs * 4 / 5) / G; }
+
+// ---- producer (warp 8, lane 0) ---------------------------------------------------
+
 template <typename WT, bool LLAMA>
-struct Producer {
-  int ph = 0;        // phase being claimed; > 4L = done
-  int pair = -1;     // claimed pair (-1: claim next)
-  int off = 0;       // next byte offset in the pair stream
-  int pair_bytes = 0;
-  GemvPhase g{};
-  int n_pairs = 0;
-  int t = 0;         // stages issued
-  bool done = false;
-
-  __device__ void set_phase(const PassParams& p, int new_ph) {
-    ph = new_ph;
-    if (ph > 4 * p.n_layers) {
-      done = true;
-      return;
-    }
-    g = phase_desc<LLAMA>(p, ph);
-    n_pairs = (g.n_rows + 1) >> 1;
-  }
-
-  // Issues the next stage into slot t % DP_STAGES; returns false when exhausted.
-  __device__ bool issue(const PassParams& p, int* claims, uint8_t* ring, uint64_t* bars, StageMeta* meta,
-                        uint64_t pol) {
-    const int lane = threadIdx.x & 31;
-    while (!done && pair < 0) {
-      int c = 0;
-      if (lane == 0) c = atomicAdd(claims + ph, 1);
-      c = __shfl_sync(0xffffffffu, c, 0);
-      if (c < n_pairs) {
-        pair = c;
-        off = 0;
-        const int rows = (2 * c + 1 < g.n_rows) ? 2 : 1;
-        pair_bytes = rows * g.k * static_cast<int>(sizeof(WT));
-      } else {
-        set_phase(p, ph + 1);
-      }
-    }
-    if (done) return false;
-    const int slot = t % DP_STAGES;
-    const int len = min(static_cast<int>(DP_STAGE_BYTES), pair_bytes - off);
-    if (lane == 0) {
+__device__ void producer(const PassParams& p, uint8_t* ring, uint64_t* full, uint64_t* empty, StageMeta* meta) {
+  const uint64_t pol = l2_evict_first_policy();
+  int* claims = p.sync + p.n_layers * p.sync_stride;
+  const int G = gridDim.x;
+  uint32_t t = 0;
+  auto next_slot = [&](int& slot) -> bool {
+    slot = t % DP_STAGES;
+    // the first pass over the ring finds every slot free
+    return mbar_wait_wd(&empty[slot], ((t / DP_STAGES) & 1) ^ 1);
+  };
+  auto stream_pair = [&](int ph, const GemvPhase& g, int pair) -> bool {
+    const int rows = (2 * pair + 1 < g.n_rows) ? 2 : 1;
+    const int bytes = rows * g.k * static_cast<int>(sizeof(WT));
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(g.w) +
+                         static_cast<int64_t>(2 * pair) * g.k * static_cast<int64_t>(sizeof(WT));
+    for (int off = 0; off < bytes; off += DP_STAGE_BYTES) {
+      int slot;
+      if (!next_slot(slot)) return false;
+      const int len = min(static_cast<int>(DP_STAGE_BYTES), bytes - off);
       meta[slot] = StageMeta{ph, pair, off, len};
-      uint64_t* bar = &bars[slot];
-      mbar_arrive_expect_tx(bar, static_cast<uint32_t>(len));
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(g.w) +
-                           static_cast<int64_t>(2 * pair) * g.k * static_cast<int64_t>(sizeof(WT)) + off;
-      bulk_g2s(ring + slot * DP_STAGE_BYTES, src, static_cast<uint32_t>(len), bar, pol);
+      mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(len));
+      bulk_g2s(ring + slot * DP_STAGE_BYTES, src + off, static_cast<uint32_t>(len), &full[slot], pol);
+      ++t;
     }
-    off += len;
-    if (off >= pair_bytes) pair = -1;
-    ++t;
     return true;
+  };
+  const int n_ph = 4 * p.n_layers + 1;
+  for (int ph = 0; ph < n_ph; ++ph) {
+    const GemvPhase g = phase_desc<LLAMA>(p, ph);
+    const int n_pairs = (g.n_rows + 1) >> 1;
+    const int s0 = static_share(n_pairs, G);
+    for (int pr = blockIdx.x * s0; pr < (blockIdx.x + 1) * s0; ++pr)
+      if (!stream_pair(ph, g, pr)) return;
+    for (;;) {
+      const int pr = G * s0 + atomicAdd(claims + ph, 1);
+      if (pr >= n_pairs) break;
+      if (!stream_pair(ph, g, pr)) return;
+    }
   }
-};
+  int slot;
+  if (!next_slot(slot)) return;
+  meta[slot] = StageMeta{DP_END, 0, 0, 0};
+  mbar_arrive(&full[slot]);
+}
 
-// Dot of one stage of a pair stream: elements [e0, e0 + len/sizeof) of the
-// concatenation row_a | row_b (each of length k).
+// ---- consumer-side helpers ------------------------------------------------------
+
+// This warp's slice of one stage: bytes [w*SLICE, (w+1)*SLICE) of the stage,
+// i.e. elements e0 + ... of the concatenation row_a | row_b (length k each).
 template <typename WT>
-__device__ __forceinline__ void dot_stage(const uint8_t* st, int e0, int len, int k, const float* xs, float& acc_a,
-                                          float& acc_b) {
+__device__ __forceinline__ void dot_slice(const uint8_t* st, int stage_e0, int len, int k, const float* xs, int warp,
+                                          float& acc_a, float& acc_b) {
   const int lane = threadIdx.x & 31;
-  const int groups = len >> 4;  // 16-byte groups
-  float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
-  if constexpr (sizeof(WT) == 2) {
-    const uint4* w = reinterpret_cast<const uint4*>(st);
-    const float4* xa = reinterpret_cast<const float4*>(xs);
-    const float4* xb = reinterpret_cast<const float4*>(xs + (k >> 1));
-#pragma unroll 4
-    for (int q = lane; q < groups; q += 32) {
-      const int e = e0 + q * 8;
-      const bool isb = e >= k;
-      const int gi = (isb ? e - k : e) >> 3;
-      const uint4 u = w[q];
-      const float4 x0 = xa[gi];
-      const float4 x1 = xb[gi];
-      float s0 = bf16lo(u.x) * x0.x;
-      float s1 = bf16hi(u.x) * x0.y;
+  const int b0 = warp * static_cast<int>(DP_SLICE);
+  const int b1 = min(len, b0 + static_cast<int>(DP_SLICE));
+  float a0 = 0.f, a1 = 0.f, c0 = 0.f, c1 = 0.f;
+  for (int b = b0 + lane * 16; b < b1; b += 32 * 16) {
+    const int e = stage_e0 + b / static_cast<int>(sizeof(WT));
+    const bool isb = e >= k;
+    const int col = isb ? e - k : e;
+    float s0, s1;
+    if constexpr (sizeof(WT) == 2) {
+      const uint4 u = *reinterpret_cast<const uint4*>(st + b);
+      const float4 x0 = reinterpret_cast<const float4*>(xs)[col >> 3];
+      const float4 x1 = reinterpret_cast<const float4*>(xs + (k >> 1))[col >> 3];
+      s0 = bf16lo(u.x) * x0.x;
+      s1 = bf16hi(u.x) * x0.y;
       s0 = fmaf(bf16lo(u.y), x0.z, s0);
       s1 = fmaf(bf16hi(u.y), x0.w, s1);
       s0 = fmaf(bf16lo(u.z), x1.x, s0);
       s1 = fmaf(bf16hi(u.z), x1.y, s1);
       s0 = fmaf(bf16lo(u.w), x1.z, s0);
       s1 = fmaf(bf16hi(u.w), x1.w, s1);
-      if (isb) {
-        b0 += s0;
-        b1 += s1;
-      } else {
-        a0 += s0;
-        a1 += s1;
-      }
-    }
-  } else {
-    const float4* w = reinterpret_cast<const float4*>(st);
-    const float4* xv = reinterpret_cast<const float4*>(xs);
-#pragma unroll 4
-    for (int q = lane; q < groups; q += 32) {
-      const int e = e0 + q * 4;
-      const bool isb = e >= k;
-      const int gi = (isb ? e - k : e) >> 2;
-      const float4 u = w[q];
-      const float4 x = xv[gi];
-      float s0 = u.x * x.x;
-      float s1 = u.y * x.y;
+    } else {
+      const float4 u = *reinterpret_cast<const float4*>(st + b);
+      const float4 x = reinterpret_cast<const float4*>(xs)[col >> 2];
+      s0 = u.x * x.x;
+      s1 = u.y * x.y;
       s0 = fmaf(u.z, x.z, s0);
       s1 = fmaf(u.w, x.w, s1);
-      if (isb) {
-        b0 += s0;
-        b1 += s1;
-      } else {
-        a0 += s0;
-        a1 += s1;
-      }
+    }
+    if (isb) {
+      c0 += s0;
+      c1 += s1;
+    } else {
+      a0 += s0;
+      a1 += s1;
     }
   }
   acc_a += a0 + a1;
-  acc_b += b0 + b1;
+  acc_b += c0 + c1;
 }
 
-// ---- dependency counters ------------------------------------------------------
-
 __device__ __forceinline__ void phase_arrive(int* ctr) {
-  __syncthreads();
+  consumer_sync();
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(ctr, 1);
   }
 }
 
-// returns false on watchdog expiry (uniform across the CTA)
+// returns false on watchdog expiry (uniform across the consumer warps)
 __device__ __forceinline__ bool phase_wait(int* ctr, int target, int* err, int* s_ok) {
   if (threadIdx.x == 0) {
     int ok = 1;
@@ -225,7 +219,7 @@ __device__ __forceinline__ bool phase_wait(int* ctr, int target, int* err, int* 
     __threadfence();
     *s_ok = ok;
   }
-  __syncthreads();
+  consumer_sync();
   return *s_ok != 0;
 }
 
@@ -245,32 +239,33 @@ __device__ __forceinline__ float4 kv_load4<__nv_bfloat16>(const __nv_bfloat16* p
 
 __device__ __forceinline__ float block_max_all(float v, float* red) {
   v = warp_max(v);
-  __syncthreads();
+  consumer_sync();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
+  consumer_sync();
   if (threadIdx.x < 32) {
-    float t = threadIdx.x < DP_WARPS ? red[threadIdx.x] : -INFINITY;
+    float t = threadIdx.x < DP_CWARPS ? red[threadIdx.x] : -INFINITY;
     t = warp_max(t);
     if (threadIdx.x == 0) red[0] = t;
   }
-  __syncthreads();
+  consumer_sync();
   return red[0];
 }
 
 template <typename KT>
 __device__ void attention_item(const PassParams& p, const PassLayer& L, int layer, int head, int split, int len,
                                float* sm, float* red, int* s_last) {
+  constexpr int NT = CONSUMER_THREADS;
   const int dh = p.dh, ns = p.nsplit;
-  const int gs = dh >> 2;           // lanes per position
-  const int npg = DP_THREADS / gs;  // position groups
+  const int gs = dh >> 2;   // lanes per position
+  const int npg = NT / gs;  // position groups
   const int span = (len + ns - 1) / ns;
   const int j0 = split * span;
   const int n = max(0, min(len, j0 + span) - j0);
   float* qs = sm;
   float* sc = qs + dh;
   float* op = sc + p.span_cap;
-  for (int d = threadIdx.x; d < dh; d += DP_THREADS) qs[d] = __ldcg(p.q + head * dh + d);
-  __syncthreads();
+  for (int d = threadIdx.x; d < dh; d += NT) qs[d] = __ldcg(p.q + head * dh + d);
+  consumer_sync();
   const KT* K = reinterpret_cast<const KT*>(L.k) + static_cast<int64_t>(head) * p.max_seq * dh;
   const KT* V = reinterpret_cast<const KT*>(L.v) + static_cast<int64_t>(head) * p.max_seq * dh;
   const int grp = threadIdx.x / gs, gl = threadIdx.x - grp * gs;
@@ -285,12 +280,12 @@ __device__ void attention_item(const PassParams& p, const PassLayer& L, int laye
     for (int o = gs >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (jj < n && gl == 0) sc[jj] = s * p.scale;
   }
-  __syncthreads();
+  consumer_sync();
   float m = -INFINITY;
-  for (int jj = threadIdx.x; jj < n; jj += DP_THREADS) m = fmaxf(m, sc[jj]);
+  for (int jj = threadIdx.x; jj < n; jj += NT) m = fmaxf(m, sc[jj]);
   m = block_max_all(m, red);
   float l = 0.0f;
-  for (int jj = threadIdx.x; jj < n; jj += DP_THREADS) {
+  for (int jj = threadIdx.x; jj < n; jj += NT) {
     const float e = expf(sc[jj] - m);
     sc[jj] = e;
     l += e;
@@ -306,23 +301,23 @@ __device__ void attention_item(const PassParams& p, const PassLayer& L, int laye
     acc.w = fmaf(e, v4.w, acc.w);
   }
   reinterpret_cast<float4*>(op + grp * dh)[gl] = acc;
-  __syncthreads();
+  consumer_sync();
   int* head_ctr = p.sync + layer * p.sync_stride + SY_HEADS + head;
   int* attn_ctr = p.sync + layer * p.sync_stride + SY_ATTN;
   if (ns == 1) {
     const float inv = 1.0f / l;
-    for (int d = threadIdx.x; d < dh; d += DP_THREADS) {
+    for (int d = threadIdx.x; d < dh; d += NT) {
       float o = 0.0f;
       for (int g = 0; g < npg; ++g) o += op[g * dh + d];
       p.attn[head * dh + d] = o * inv;
     }
     phase_arrive(attn_ctr);
-    __syncthreads();
+    consumer_sync();
     return;
   }
   const int stride = dh + 2;
   float* mine = p.part + (static_cast<int64_t>(head) * ns + split) * stride;
-  for (int d = threadIdx.x; d < dh; d += DP_THREADS) {
+  for (int d = threadIdx.x; d < dh; d += NT) {
     float o = 0.0f;
     for (int g = 0; g < npg; ++g) o += op[g * dh + d];
     mine[d] = o;
@@ -331,13 +326,13 @@ __device__ void attention_item(const PassParams& p, const PassLayer& L, int laye
     mine[dh] = n > 0 ? m : -INFINITY;
     mine[dh + 1] = n > 0 ? l : 0.0f;
   }
-  __syncthreads();
+  consumer_sync();
   if (threadIdx.x == 0) {
     __threadfence();
     *s_last = (atomicAdd(head_ctr, 1) == ns - 1);
     if (*s_last) __threadfence();
   }
-  __syncthreads();
+  consumer_sync();
   if (!*s_last) return;
   // merge the splits in order (deterministic)
   const float* base = p.part + static_cast<int64_t>(head) * ns * stride;
@@ -350,7 +345,7 @@ __device__ void attention_item(const PassParams& p, const PassLayer& L, int laye
     if (ls > 0.0f) Lsum += ls * expf(__ldcg(base + s * stride + dh) - M);
   }
   const float invL = 1.0f / Lsum;
-  for (int d = threadIdx.x; d < dh; d += DP_THREADS) {
+  for (int d = threadIdx.x; d < dh; d += NT) {
     float o = 0.0f;
     for (int s = 0; s < ns; ++s) {
       const float ls = __ldcg(base + s * stride + dh + 1);
@@ -359,45 +354,42 @@ __device__ void attention_item(const PassParams& p, const PassLayer& L, int laye
     p.attn[head * dh + d] = o * invL;
   }
   phase_arrive(attn_ctr);
-  __syncthreads();
+  consumer_sync();
 }
 
 // ---- the kernel -------------------------------------------------------------------
 
 template <typename WT, typename KT, bool LLAMA>
 __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bars[DP_WARPS][DP_STAGES];
-  __shared__ StageMeta metas[DP_WARPS][DP_STAGES];
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[DP_STAGES], empty[DP_STAGES];
+  __shared__ StageMeta meta[DP_STAGES];
   __shared__ float red[32];
+  __shared__ float pair_red[2][DP_CWARPS][2];
   __shared__ int s_ok, s_last;
   constexpr int NORM = LLAMA ? NORM_RMS : NORM_LN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
-  uint8_t* ring = smem + static_cast<size_t>(warp) * DP_STAGES * DP_STAGE_BYTES;
-  float* xs = reinterpret_cast<float*>(smem + static_cast<size_t>(DP_WARPS) * DP_STAGES * DP_STAGE_BYTES);
+  uint8_t* ring = smem;
+  float* xs = reinterpret_cast<float*>(smem + static_cast<size_t>(DP_STAGES) * DP_STAGE_BYTES);
   float* asm_ = xs + max(p.d, p.ff);  // attention scratch
-  uint64_t* mybar = bars[warp];
-  StageMeta* meta = metas[warp];
-  const uint64_t pol = l2_evict_first_policy();
-  int* claims = p.sync + p.n_layers * p.sync_stride;
 
-  Producer<WT, LLAMA> prod;
-  if (lane == 0) {
-#pragma unroll
+  if (threadIdx.x == 0) {
     for (int s = 0; s < DP_STAGES; ++s) {
-      mbar_init(&mybar[s], 1);
-      meta[s].ph = -1;
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], DP_CWARPS);
     }
     mbar_fence_init();
   }
-  __syncwarp();
-  prod.set_phase(p, 0);
-  // Weights do not depend on the previous kernel: fill the ring before waiting.
-  for (int s = 0; s < DP_STAGES; ++s)
-    if (!prod.issue(p, claims, ring, mybar, meta, pol)) break;
-  __syncwarp();
+  __syncthreads();  // all 9 warps: barriers initialised
+
+  if (warp == DP_CWARPS) {  // ---------------- producer warp
+    if (lane == 0) producer<WT, LLAMA>(p, ring, full, empty, meta);
+    return;
+  }
+
+  // ---------------- consumer warps 0..7
   griddep_wait();
   if (p.trace && threadIdx.x == 0)
     p.trace[static_cast<int64_t>(blockIdx.x) * p.trace_stride + p.n_layers * PASS_TRACE_PER_LAYER + 2] = globaltimer();
@@ -413,33 +405,47 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   ea.kv_bf16 = sizeof(KT) == 2;
   ea.q_out = p.q;
 
-  int t = 0;  // stages consumed by this warp
-  // Consume every stage this warp claimed in GEMV phase `ph`.
+  uint32_t t = 0;    // stages consumed
+  int npairs_done = 0;
+  bool alive = true;
+  // Consume every stage of GEMV phase `ph` (the producer streams them in order).
   auto run_phase = [&](int ph, auto epi_tag) {
     constexpr int EPI = decltype(epi_tag)::value;
     const GemvPhase g = phase_desc<LLAMA>(p, ph);
     float acc_a = 0.0f, acc_b = 0.0f;
     for (;;) {
       const int slot = t % DP_STAGES;
-      const StageMeta m = meta[slot];
-      if (m.ph != ph) break;  // ring moved on to a later phase (or ran dry)
-      mbar_wait(&mybar[slot], static_cast<uint32_t>((t / DP_STAGES) & 1));
-      dot_stage<WT>(ring + slot * DP_STAGE_BYTES, m.off / static_cast<int>(sizeof(WT)), m.len, g.k, xs, acc_a,
-                    acc_b);
-      __syncwarp();
-      if (lane == 0) {
-        meta[slot].ph = -1;
-        fence_proxy_async_smem();
+      if (!mbar_wait_wd(&full[slot], (t / DP_STAGES) & 1)) {
+        if (threadIdx.x == 0) atomicOr(p.err, DEVERR_TIMEOUT);
+        alive = false;
+        return;
       }
+      const StageMeta m = meta[slot];
+      if (m.ph != ph) return;  // stage of a later phase (or the end marker): leave it
+      dot_slice<WT>(ring + slot * DP_STAGE_BYTES, m.off / static_cast<int>(sizeof(WT)), m.len, g.k, xs, warp,
+                    acc_a, acc_b);
       __syncwarp();
-      prod.issue(p, claims, ring, mybar, meta, pol);
-      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
       ++t;
       const int rows = (2 * m.pair + 1 < g.n_rows) ? 2 : 1;
       if (m.off + m.len >= rows * g.k * static_cast<int>(sizeof(WT))) {
         const float va = warp_sum(acc_a);
         const float vb = warp_sum(acc_b);
-        if (lane == 0) epilogue<EPI>(ea, m.pair, va, vb, rows == 2);
+        float* pr = &pair_red[npairs_done & 1][0][0];
+        if (lane == 0) {
+          pr[warp * 2] = va;
+          pr[warp * 2 + 1] = vb;
+        }
+        consumer_sync();
+        if (threadIdx.x == 0) {
+          float sa = 0.0f, sb = 0.0f;
+          for (int w = 0; w < DP_CWARPS; ++w) {
+            sa += pr[w * 2];
+            sb += pr[w * 2 + 1];
+          }
+          epilogue<EPI>(ea, m.pair, sa, sb, rows == 2);
+        }
+        ++npairs_done;
         acc_a = 0.0f;
         acc_b = 0.0f;
       }
@@ -456,13 +462,20 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   };
 
   if (len < 1 || len > p.max_seq || (len + p.nsplit - 1) / p.nsplit > p.span_cap) {
+    // Invalid live length for this bucket: flag it and drain the stream so the
+    // producer finishes and no bulk copy is outstanding at exit.
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(p.err, DEVERR_WRONG_LENGTH);
-    // drain the prefetched stages so no bulk copy is outstanding at exit
-    for (int s = 0; s < min(DP_STAGES, prod.t); ++s) mbar_wait(&mybar[s], 0);
-    return;
+    for (;;) {
+      const int slot = t % DP_STAGES;
+      if (!mbar_wait_wd(&full[slot], (t / DP_STAGES) & 1)) return;
+      if (meta[slot].ph == DP_END) return;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      ++t;
+    }
   }
 
-  for (int l = 0; l < p.n_layers; ++l) {
+  for (int l = 0; l < p.n_layers && alive; ++l) {
     const PassLayer L = p.layers[l];
     int* sy = p.sync + l * p.sync_stride;
     const int tb = l * PASS_TRACE_PER_LAYER;
@@ -511,6 +524,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
     phase_arrive(sy + SY_DOWN);
     stamp(tb + 9);
   }
+  if (!alive) return;
   // ---- ln_f + head
   if (!phase_wait(p.sync + (p.n_layers - 1) * p.sync_stride + SY_DOWN, G, p.err, &s_ok)) return;
   stamp(p.n_layers * PASS_TRACE_PER_LAYER + 0);
@@ -521,16 +535,16 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
 
   // Self-reset: the last CTA out zeroes every counter (phase, head, claim) for
   // the next pass; all other CTAs have passed their last wait and claim.
-  __syncthreads();
+  consumer_sync();
   const int total = sync_total(p.n_layers, p.sync_stride);
   int* exit_ctr = p.sync + total - 1;
   if (threadIdx.x == 0) {
     __threadfence();
     s_last = atomicAdd(exit_ctr, 1) == G - 1;
   }
-  __syncthreads();
+  consumer_sync();
   if (s_last) {
-    for (int i = threadIdx.x; i < total; i += DP_THREADS) p.sync[i] = 0;
+    for (int i = threadIdx.x; i < total; i += CONSUMER_THREADS) p.sync[i] = 0;
     __threadfence();
   }
 }
@@ -551,9 +565,9 @@ static PassFn pick_pass(Dt wdt, Dt kvdt, bool llama) {
 }
 
 static size_t pass_smem(const PassParams& p) {
-  const int npg = DP_THREADS / std::max(1, p.dh / 4);
-  return static_cast<size_t>(DP_WARPS) * DP_STAGES * DP_STAGE_BYTES +
-         static_cast<size_t>(std::max(p.d, p.ff)) * 4 + (static_cast<size_t>(p.dh) + p.span_cap + npg * p.dh) * 4;
+  const int npg = CONSUMER_THREADS / std::max(1, p.dh / 4);
+  return static_cast<size_t>(DP_STAGES) * DP_STAGE_BYTES + static_cast<size_t>(std::max(p.d, p.ff)) * 4 +
+         (static_cast<size_t>(p.dh) + p.span_cap + npg * p.dh) * 4;
 }
 
 cudaError_t decode_pass_prepare(int device) {

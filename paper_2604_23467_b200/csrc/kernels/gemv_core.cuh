@@ -44,18 +44,23 @@ __device__ __forceinline__ int xs_index(int j, int k) {
   }
 }
 
+// The compute ("consumer") warps of a CTA: 8 warps.  They synchronise on named
+// barrier 1 so a dedicated producer warp (decode_pass.cu) never has to join.
+constexpr int CONSUMER_THREADS = 256;
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
 __device__ __forceinline__ float block_sum(float v, float* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   v = warp_sum(v);
-  __syncthreads();  // red reuse
+  consumer_sync();  // red reuse
   if (lane == 0) red[warp] = v;
-  __syncthreads();
+  consumer_sync();
   if (threadIdx.x < 32) {
-    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+    float t = threadIdx.x < (CONSUMER_THREADS >> 5) ? red[threadIdx.x] : 0.0f;
     t = warp_sum(t);
     if (threadIdx.x == 0) red[0] = t;
   }
-  __syncthreads();
+  consumer_sync();
   return red[0];
 }
 
@@ -98,11 +103,11 @@ template <typename WT, int NORM, bool CG>
 __device__ __forceinline__ void load_x(const float* x, const float* gamma, const float* beta, float eps, int k,
                                        float* xs, float* red) {
   const int n4 = k >> 2;
-  if (n4 <= LOADX_MAXV * static_cast<int>(blockDim.x)) {
+  if (n4 <= LOADX_MAXV * static_cast<int>(CONSUMER_THREADS)) {
     float4 v[LOADX_MAXV];
 #pragma unroll
     for (int i = 0; i < LOADX_MAXV; ++i) {
-      const int j4 = threadIdx.x + i * blockDim.x;
+      const int j4 = threadIdx.x + i * CONSUMER_THREADS;
       v[i] = j4 < n4 ? act_ld4<CG>(x + 4 * j4) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     float mean = 0.0f, inv = 1.0f;
@@ -120,7 +125,7 @@ __device__ __forceinline__ void load_x(const float* x, const float* gamma, const
       float var = 0.0f;
 #pragma unroll
       for (int i = 0; i < LOADX_MAXV; ++i) {
-        const int j4 = threadIdx.x + i * blockDim.x;
+        const int j4 = threadIdx.x + i * CONSUMER_THREADS;
         if (j4 < n4) {
           const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
           var += a * a + b * b + c * c + d * d;
@@ -131,7 +136,7 @@ __device__ __forceinline__ void load_x(const float* x, const float* gamma, const
     }
 #pragma unroll
     for (int i = 0; i < LOADX_MAXV; ++i) {
-      const int j4 = threadIdx.x + i * blockDim.x;
+      const int j4 = threadIdx.x + i * CONSUMER_THREADS;
       if (j4 >= n4) continue;
       float4 o = v[i];
       if constexpr (NORM == NORM_RMS) {
@@ -145,7 +150,7 @@ __device__ __forceinline__ void load_x(const float* x, const float* gamma, const
       }
       xs_store4<WT>(xs, j4, k, o);
     }
-    __syncthreads();
+    consumer_sync();
     return;
   }
   load_x_slow<WT, NORM, CG>(x, gamma, beta, eps, k, xs, red);
@@ -156,41 +161,41 @@ template <typename WT, int NORM, bool CG>
 __device__ __noinline__ void load_x_slow(const float* x, const float* gamma, const float* beta, float eps, int k,
                                          float* xs, float* red) {
   if constexpr (NORM == NORM_NONE) {
-    for (int j = threadIdx.x; j < k; j += blockDim.x) xs[xs_index<WT>(j, k)] = act_ld<CG>(x + j);
+    for (int j = threadIdx.x; j < k; j += CONSUMER_THREADS) xs[xs_index<WT>(j, k)] = act_ld<CG>(x + j);
   } else if constexpr (NORM == NORM_RMS) {
     float ss = 0.0f;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    for (int j = threadIdx.x; j < k; j += CONSUMER_THREADS) {
       const float v = act_ld<CG>(x + j);
       xs[xs_index<WT>(j, k)] = v;
       ss += v * v;
     }
     ss = block_sum(ss, red);  // also orders the xs writes above
     const float inv = 1.0f / sqrtf(ss / static_cast<float>(k) + eps);
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    for (int j = threadIdx.x; j < k; j += CONSUMER_THREADS) {
       const int i = xs_index<WT>(j, k);
       xs[i] = xs[i] * inv * gamma[j];
     }
   } else {
     float s = 0.0f;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    for (int j = threadIdx.x; j < k; j += CONSUMER_THREADS) {
       const float v = act_ld<CG>(x + j);
       xs[xs_index<WT>(j, k)] = v;
       s += v;
     }
     const float mean = block_sum(s, red) / static_cast<float>(k);
     float var = 0.0f;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    for (int j = threadIdx.x; j < k; j += CONSUMER_THREADS) {
       const float c = xs[xs_index<WT>(j, k)] - mean;
       var += c * c;
     }
     var = block_sum(var, red) / static_cast<float>(k);
     const float inv = 1.0f / sqrtf(var + eps);
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    for (int j = threadIdx.x; j < k; j += CONSUMER_THREADS) {
       const int i = xs_index<WT>(j, k);
       xs[i] = (xs[i] - mean) * inv * gamma[j] + beta[j];
     }
   }
-  __syncthreads();
+  consumer_sync();
 }
 
 // Partial dot products of one row pair over one chunk [c0, c0+ce).
