@@ -38,7 +38,7 @@ constexpr int DP_CWARPS = 8;                       // consumer warps
 constexpr int DP_THREADS = (DP_CWARPS + 1) * 32;   // + producer warp
 constexpr int DP_STAGES = 16;
 constexpr uint32_t DP_STAGE_BYTES = 8192;
-constexpr uint32_t DP_SLICE = DP_STAGE_BYTES / DP_CWARPS;  // bytes of a stage per consumer warp
+constexpr int DP_PARTS = 64;  // per-stage partial-sum slots (> DP_STAGES + max stages per pair)
 constexpr unsigned long long DP_WATCHDOG_NS = 2000000000ull;  // 2 s
 constexpr int DP_END = INT_MAX;
 
@@ -139,24 +139,27 @@ __device__ void producer(const PassParams& p, uint8_t* ring, uint64_t* full, uin
       if (!stream_pair(ph, g, pr)) return;
     }
   }
-  int slot;
-  if (!next_slot(slot)) return;
-  meta[slot] = StageMeta{DP_END, 0, 0, 0};
-  mbar_arrive(&full[slot]);
+  // one end marker per consumer warp (warp w owns stages w, w+8, ...)
+  for (int w = 0; w < DP_CWARPS; ++w) {
+    int slot;
+    if (!next_slot(slot)) return;
+    meta[slot] = StageMeta{DP_END, 0, 0, 0};
+    mbar_arrive(&full[slot]);
+    ++t;
+  }
 }
 
 // ---- consumer-side helpers ------------------------------------------------------
 
-// This warp's slice of one stage: bytes [w*SLICE, (w+1)*SLICE) of the stage,
-// i.e. elements e0 + ... of the concatenation row_a | row_b (length k each).
+// Dot of one whole stage (one warp): bytes [0, len) of the stage are elements
+// stage_e0 + ... of the concatenation row_a | row_b (length k each).
 template <typename WT>
-__device__ __forceinline__ void dot_slice(const uint8_t* st, int stage_e0, int len, int k, const float* xs, int warp,
+__device__ __forceinline__ void dot_stage(const uint8_t* st, int stage_e0, int len, int k, const float* xs,
                                           float& acc_a, float& acc_b) {
   const int lane = threadIdx.x & 31;
-  const int b0 = warp * static_cast<int>(DP_SLICE);
-  const int b1 = min(len, b0 + static_cast<int>(DP_SLICE));
   float a0 = 0.f, a1 = 0.f, c0 = 0.f, c1 = 0.f;
-  for (int b = b0 + lane * 16; b < b1; b += 32 * 16) {
+#pragma unroll 4
+  for (int b = lane * 16; b < len; b += 32 * 16) {
     const int e = stage_e0 + b / static_cast<int>(sizeof(WT));
     const bool isb = e >= k;
     const int col = isb ? e - k : e;
@@ -365,7 +368,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   __shared__ uint64_t full[DP_STAGES], empty[DP_STAGES];
   __shared__ StageMeta meta[DP_STAGES];
   __shared__ float red[32];
-  __shared__ float pair_red[2][DP_CWARPS][2];
+  __shared__ float2 part_sum[DP_PARTS];
+  __shared__ int part_seq[DP_PARTS];
   __shared__ int s_ok, s_last;
   constexpr int NORM = LLAMA ? NORM_RMS : NORM_LN;
 
@@ -378,8 +382,9 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   if (threadIdx.x == 0) {
     for (int s = 0; s < DP_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], DP_CWARPS);
+      mbar_init(&empty[s], 1);
     }
+    for (int s = 0; s < DP_PARTS; ++s) part_seq[s] = -1;
     mbar_fence_init();
   }
   __syncthreads();  // all 9 warps: barriers initialised
@@ -405,14 +410,19 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   ea.kv_bf16 = sizeof(KT) == 2;
   ea.q_out = p.q;
 
-  uint32_t t = 0;    // stages consumed
-  int npairs_done = 0;
+  // Warp w consumes the CTA's stages w, w+8, w+16, ... (whole 8 KB stages).  A
+  // row pair spans 1..6 consecutive stages, so its partial sums come from
+  // several warps: each warp posts its stage partial in part_sum[t % 64] with
+  // the stage number in part_seq; the warp holding the pair's LAST stage waits
+  // for the others, adds them in stage order (deterministic) and runs the
+  // epilogue.  It releases its own ring slot only afterwards, which bounds how
+  // far the producer can run ahead and keeps the 64 partial slots from wrapping.
+  int t = warp;  // next stage of this warp
   bool alive = true;
-  // Consume every stage of GEMV phase `ph` (the producer streams them in order).
   auto run_phase = [&](int ph, auto epi_tag) {
     constexpr int EPI = decltype(epi_tag)::value;
     const GemvPhase g = phase_desc<LLAMA>(p, ph);
-    float acc_a = 0.0f, acc_b = 0.0f;
+    const int sz = static_cast<int>(sizeof(WT));
     for (;;) {
       const int slot = t % DP_STAGES;
       if (!mbar_wait_wd(&full[slot], (t / DP_STAGES) & 1)) {
@@ -422,33 +432,39 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
       }
       const StageMeta m = meta[slot];
       if (m.ph != ph) return;  // stage of a later phase (or the end marker): leave it
-      dot_slice<WT>(ring + slot * DP_STAGE_BYTES, m.off / static_cast<int>(sizeof(WT)), m.len, g.k, xs, warp,
-                    acc_a, acc_b);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      ++t;
+      float acc_a = 0.0f, acc_b = 0.0f;
+      dot_stage<WT>(ring + slot * DP_STAGE_BYTES, m.off / sz, m.len, g.k, xs, acc_a, acc_b);
+      const float va = warp_sum(acc_a);
+      const float vb = warp_sum(acc_b);
       const int rows = (2 * m.pair + 1 < g.n_rows) ? 2 : 1;
-      if (m.off + m.len >= rows * g.k * static_cast<int>(sizeof(WT))) {
-        const float va = warp_sum(acc_a);
-        const float vb = warp_sum(acc_b);
-        float* pr = &pair_red[npairs_done & 1][0][0];
+      const int pair_bytes = rows * g.k * sz;
+      if (m.off + m.len < pair_bytes) {  // not the pair's last stage: post the partial
         if (lane == 0) {
-          pr[warp * 2] = va;
-          pr[warp * 2 + 1] = vb;
+          part_sum[t % DP_PARTS] = make_float2(va, vb);
+          __threadfence_block();
+          reinterpret_cast<volatile int*>(part_seq)[t % DP_PARTS] = t;
+          mbar_arrive(&empty[slot]);
         }
-        consumer_sync();
-        if (threadIdx.x == 0) {
+      } else {
+        if (lane == 0) {
+          const int n_prev = m.off / static_cast<int>(DP_STAGE_BYTES);  // earlier stages of this pair
           float sa = 0.0f, sb = 0.0f;
-          for (int w = 0; w < DP_CWARPS; ++w) {
-            sa += pr[w * 2];
-            sb += pr[w * 2 + 1];
+          for (int j = n_prev; j >= 1; --j) {
+            const int ts = t - j;
+            volatile int* seq = reinterpret_cast<volatile int*>(part_seq);
+            while (seq[ts % DP_PARTS] != ts) {
+            }
+            __threadfence_block();
+            const float2 ps = part_sum[ts % DP_PARTS];
+            sa += ps.x;
+            sb += ps.y;
           }
-          epilogue<EPI>(ea, m.pair, sa, sb, rows == 2);
+          epilogue<EPI>(ea, m.pair, sa + va, sb + vb, rows == 2);
+          mbar_arrive(&empty[slot]);
         }
-        ++npairs_done;
-        acc_a = 0.0f;
-        acc_b = 0.0f;
       }
+      __syncwarp();
+      t += DP_CWARPS;
     }
   };
   using QkvTag = std::integral_constant<int, LLAMA ? EPI_QKV_ROPE : EPI_QKV>;
@@ -471,7 +487,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
       if (meta[slot].ph == DP_END) return;
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
-      ++t;
+      t += DP_CWARPS;
     }
   }
 
