@@ -36,7 +36,7 @@ namespace grt {
 
 constexpr int DP_CWARPS = 8;                       // consumer warps
 constexpr int DP_THREADS = (DP_CWARPS + 1) * 32;   // + producer warp
-constexpr int DP_STAGES = 16;
+constexpr int DP_STAGES = 20;
 constexpr uint32_t DP_STAGE_BYTES = 8192;
 constexpr int DP_PARTS = 64;  // per-stage partial-sum slots (> DP_STAGES + max stages per pair)
 constexpr unsigned long long DP_WATCHDOG_NS = 2000000000ull;  // 2 s
@@ -131,11 +131,16 @@ __device__ void producer(const PassParams& p, uint8_t* ring, uint64_t* full, uin
     const GemvPhase g = phase_desc<LLAMA>(p, ph);
     const int n_pairs = (g.n_rows + 1) >> 1;
     const int s0 = static_share(n_pairs, G);
+    // The first tail claim is put in flight before the static share is
+    // streamed, and every later one before the pair it follows: the atomic's
+    // round trip overlaps the copies instead of stalling the producer.
+    int nxt = atomicAdd(claims + ph, 1);
     for (int pr = blockIdx.x * s0; pr < (blockIdx.x + 1) * s0; ++pr)
       if (!stream_pair(ph, g, pr)) return;
     for (;;) {
-      const int pr = G * s0 + atomicAdd(claims + ph, 1);
+      const int pr = G * s0 + nxt;
       if (pr >= n_pairs) break;
+      nxt = atomicAdd(claims + ph, 1);
       if (!stream_pair(ph, g, pr)) return;
     }
   }
@@ -264,46 +269,78 @@ __device__ void attention_item(const PassParams& p, const PassLayer& L, int laye
   const int span = (len + ns - 1) / ns;
   const int j0 = split * span;
   const int n = max(0, min(len, j0 + span) - j0);
-  float* qs = sm;
-  float* sc = qs + dh;
-  float* op = sc + p.span_cap;
-  for (int d = threadIdx.x; d < dh; d += NT) qs[d] = __ldcg(p.q + head * dh + d);
-  consumer_sync();
+  // Latency-oriented: q comes straight from L2, and each thread issues the K and
+  // V loads of a batch of positions together before using any of them; an
+  // online softmax per position group avoids a scores round trip through smem.
+  float* op = sm;                 // [npg][dh] group partial outputs
+  float* gmax = op + npg * dh;    // [npg]
+  float* gsum = gmax + npg;       // [npg]
   const KT* K = reinterpret_cast<const KT*>(L.k) + static_cast<int64_t>(head) * p.max_seq * dh;
   const KT* V = reinterpret_cast<const KT*>(L.v) + static_cast<int64_t>(head) * p.max_seq * dh;
   const int grp = threadIdx.x / gs, gl = threadIdx.x - grp * gs;
-  const float4 q4 = reinterpret_cast<const float4*>(qs)[gl];
-  for (int jb = 0; jb < n; jb += npg) {
-    const int jj = jb + grp;
-    float s = 0.0f;
-    if (jj < n) {
-      const float4 k4 = kv_load4<KT>(K + static_cast<int64_t>(j0 + jj) * dh + 4 * gl);
-      s = q4.x * k4.x + q4.y * k4.y + q4.z * k4.z + q4.w * k4.w;
+  const float4 q4 = __ldcg(reinterpret_cast<const float4*>(p.q + head * dh) + gl);
+  constexpr int BATCH = 4;
+  float mt = -INFINITY, lt = 0.0f;
+  float4 ot = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int jb = 0; jb < n; jb += BATCH * npg) {  // trip count uniform across the CTA
+    float4 kk[BATCH], vv[BATCH];
+#pragma unroll
+    for (int i = 0; i < BATCH; ++i) {
+      const int jj = jb + grp + i * npg;
+      if (jj < n) {
+        kk[i] = kv_load4<KT>(K + static_cast<int64_t>(j0 + jj) * dh + 4 * gl);
+        vv[i] = kv_load4<KT>(V + static_cast<int64_t>(j0 + jj) * dh + 4 * gl);
+      } else {
+        kk[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        vv[i] = kk[i];
+      }
     }
-    for (int o = gs >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (jj < n && gl == 0) sc[jj] = s * p.scale;
+    float s[BATCH];
+    float bmax = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < BATCH; ++i) {
+      float v = q4.x * kk[i].x + q4.y * kk[i].y + q4.z * kk[i].z + q4.w * kk[i].w;
+      for (int o = gs >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      s[i] = (jb + grp + i * npg < n) ? v * p.scale : -INFINITY;
+      bmax = fmaxf(bmax, s[i]);
+    }
+    if (bmax > -INFINITY) {
+      const float mnew = fmaxf(mt, bmax);
+      const float c = mt > -INFINITY ? expf(mt - mnew) : 0.0f;
+      lt *= c;
+      ot.x *= c;
+      ot.y *= c;
+      ot.z *= c;
+      ot.w *= c;
+#pragma unroll
+      for (int i = 0; i < BATCH; ++i) {
+        const float e = s[i] > -INFINITY ? expf(s[i] - mnew) : 0.0f;
+        lt += e;
+        ot.x = fmaf(e, vv[i].x, ot.x);
+        ot.y = fmaf(e, vv[i].y, ot.y);
+        ot.z = fmaf(e, vv[i].z, ot.z);
+        ot.w = fmaf(e, vv[i].w, ot.w);
+      }
+      mt = mnew;
+    }
   }
+  if (gl == 0) {
+    gmax[grp] = mt;
+    gsum[grp] = lt;
+  }
+  reinterpret_cast<float4*>(op + grp * dh)[gl] = ot;
   consumer_sync();
   float m = -INFINITY;
-  for (int jj = threadIdx.x; jj < n; jj += NT) m = fmaxf(m, sc[jj]);
-  m = block_max_all(m, red);
+  for (int g = 0; g < npg; ++g) m = fmaxf(m, gmax[g]);
   float l = 0.0f;
-  for (int jj = threadIdx.x; jj < n; jj += NT) {
-    const float e = expf(sc[jj] - m);
-    sc[jj] = e;
-    l += e;
+  for (int g = 0; g < npg; ++g)
+    if (gmax[g] > -INFINITY) l += gsum[g] * expf(gmax[g] - m);
+  {  // rescale this thread's own group partial to the CTA max
+    const float c = mt > -INFINITY ? expf(mt - m) : 0.0f;
+    float4* mine4 = reinterpret_cast<float4*>(op + grp * dh) + gl;
+    float4 v = *mine4;
+    *mine4 = make_float4(v.x * c, v.y * c, v.z * c, v.w * c);
   }
-  l = block_sum(l, red);
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int jj = grp; jj < n; jj += npg) {
-    const float e = sc[jj];
-    const float4 v4 = kv_load4<KT>(V + static_cast<int64_t>(j0 + jj) * dh + 4 * gl);
-    acc.x = fmaf(e, v4.x, acc.x);
-    acc.y = fmaf(e, v4.y, acc.y);
-    acc.z = fmaf(e, v4.z, acc.z);
-    acc.w = fmaf(e, v4.w, acc.w);
-  }
-  reinterpret_cast<float4*>(op + grp * dh)[gl] = acc;
   consumer_sync();
   int* head_ctr = p.sync + layer * p.sync_stride + SY_HEADS + head;
   int* attn_ctr = p.sync + layer * p.sync_stride + SY_ATTN;
@@ -583,7 +620,7 @@ static PassFn pick_pass(Dt wdt, Dt kvdt, bool llama) {
 static size_t pass_smem(const PassParams& p) {
   const int npg = CONSUMER_THREADS / std::max(1, p.dh / 4);
   return static_cast<size_t>(DP_STAGES) * DP_STAGE_BYTES + static_cast<size_t>(std::max(p.d, p.ff)) * 4 +
-         (static_cast<size_t>(p.dh) + p.span_cap + npg * p.dh) * 4;
+         (static_cast<size_t>(npg) * p.dh + 2 * npg + 32) * 4;
 }
 
 cudaError_t decode_pass_prepare(int device) {
