@@ -36,8 +36,14 @@ namespace grt {
 
 constexpr int DP_CWARPS = 8;                       // consumer warps
 constexpr int DP_THREADS = (DP_CWARPS + 1) * 32;   // + producer warp
-constexpr int DP_STAGES = 20;
-constexpr uint32_t DP_STAGE_BYTES = 8192;
+#ifndef GRT_DP_STAGES
+#define GRT_DP_STAGES 10
+#endif
+#ifndef GRT_DP_STAGE_KB
+#define GRT_DP_STAGE_KB 16
+#endif
+constexpr int DP_STAGES = GRT_DP_STAGES;
+constexpr uint32_t DP_STAGE_BYTES = GRT_DP_STAGE_KB * 1024;  // 16 KB = one LLaMA-7B row pair (k=4096)
 constexpr int DP_PARTS = 64;  // per-stage partial-sum slots (> DP_STAGES + max stages per pair)
 constexpr unsigned long long DP_WATCHDOG_NS = 2000000000ull;  // 2 s
 constexpr int DP_END = INT_MAX;
