@@ -37,10 +37,10 @@ namespace grt {
 constexpr int DP_CWARPS = 8;                       // consumer warps
 constexpr int DP_THREADS = (DP_CWARPS + 1) * 32;   // + producer warp
 #ifndef GRT_DP_STAGES
-#define GRT_DP_STAGES 10
+#define GRT_DP_STAGES 20
 #endif
 #ifndef GRT_DP_STAGE_KB
-#define GRT_DP_STAGE_KB 16
+#define GRT_DP_STAGE_KB 8
 #endif
 constexpr int DP_STAGES = GRT_DP_STAGES;
 constexpr uint32_t DP_STAGE_BYTES = GRT_DP_STAGE_KB * 1024;  // 16 KB = one LLaMA-7B row pair (k=4096)
