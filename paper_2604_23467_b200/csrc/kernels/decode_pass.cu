@@ -28,13 +28,14 @@
 #include <climits>
 #include <type_traits>
 
+#define GRT_CONSUMER_THREADS 384  // 12 consumer warps (3 per SM sub-partition)
 #include "common.cuh"
 #include "gemv_core.cuh"
 #include "kernels.h"
 
 namespace grt {
 
-constexpr int DP_CWARPS = 8;                       // consumer warps
+constexpr int DP_CWARPS = CONSUMER_THREADS / 32;   // consumer warps
 constexpr int DP_THREADS = (DP_CWARPS + 1) * 32;   // + producer warp
 #ifndef GRT_DP_STAGES
 #define GRT_DP_STAGES 20
@@ -164,47 +165,65 @@ __device__ void producer(const PassParams& p, uint8_t* ring, uint64_t* full, uin
 
 // Dot of one whole stage (one warp): bytes [0, len) of the stage are elements
 // stage_e0 + ... of the concatenation row_a | row_b (length k each).
+// Dot of bytes [b_lo, b_hi) of a stage that all belong to ONE row, whose first
+// byte b_lo corresponds to column col0; 16-byte groups, lane-strided.
+template <typename WT>
+__device__ __forceinline__ float dot_run(const uint8_t* st, int b_lo, int b_hi, int col0, int k, const float* xs) {
+  const int lane = threadIdx.x & 31;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if constexpr (sizeof(WT) == 2) {
+    // group q covers columns col0 + 8q .. +7 -> float4 #(col0/8 + q) of each x plane
+    const uint4* w = reinterpret_cast<const uint4*>(st + b_lo);
+    const float4* xa = reinterpret_cast<const float4*>(xs) + (col0 >> 3);
+    const float4* xb = reinterpret_cast<const float4*>(xs + (k >> 1)) + (col0 >> 3);
+    const int groups = (b_hi - b_lo) >> 4;
+#pragma unroll 4
+    for (int q = lane; q < groups; q += 32) {
+      const uint4 u = w[q];
+      const float4 x0 = xa[q];
+      const float4 x1 = xb[q];
+      a0 = fmaf(bf16lo(u.x), x0.x, a0);
+      a1 = fmaf(bf16hi(u.x), x0.y, a1);
+      a2 = fmaf(bf16lo(u.y), x0.z, a2);
+      a3 = fmaf(bf16hi(u.y), x0.w, a3);
+      a0 = fmaf(bf16lo(u.z), x1.x, a0);
+      a1 = fmaf(bf16hi(u.z), x1.y, a1);
+      a2 = fmaf(bf16lo(u.w), x1.z, a2);
+      a3 = fmaf(bf16hi(u.w), x1.w, a3);
+    }
+  } else {
+    const float4* w = reinterpret_cast<const float4*>(st + b_lo);
+    const float4* xv = reinterpret_cast<const float4*>(xs) + (col0 >> 2);
+    const int groups = (b_hi - b_lo) >> 4;
+#pragma unroll 4
+    for (int q = lane; q < groups; q += 32) {
+      const float4 u = w[q];
+      const float4 x = xv[q];
+      a0 = fmaf(u.x, x.x, a0);
+      a1 = fmaf(u.y, x.y, a1);
+      a2 = fmaf(u.z, x.z, a2);
+      a3 = fmaf(u.w, x.w, a3);
+    }
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+// Dot of one whole stage (one warp): bytes [0, len) of the stage are elements
+// stage_e0 + ... of the concatenation row_a | row_b (length k each).  The row
+// boundary is crossed at most once, so the stage splits into <= 2 linear runs.
 template <typename WT>
 __device__ __forceinline__ void dot_stage(const uint8_t* st, int stage_e0, int len, int k, const float* xs,
                                           float& acc_a, float& acc_b) {
-  const int lane = threadIdx.x & 31;
-  float a0 = 0.f, a1 = 0.f, c0 = 0.f, c1 = 0.f;
-#pragma unroll 4
-  for (int b = lane * 16; b < len; b += 32 * 16) {
-    const int e = stage_e0 + b / static_cast<int>(sizeof(WT));
-    const bool isb = e >= k;
-    const int col = isb ? e - k : e;
-    float s0, s1;
-    if constexpr (sizeof(WT) == 2) {
-      const uint4 u = *reinterpret_cast<const uint4*>(st + b);
-      const float4 x0 = reinterpret_cast<const float4*>(xs)[col >> 3];
-      const float4 x1 = reinterpret_cast<const float4*>(xs + (k >> 1))[col >> 3];
-      s0 = bf16lo(u.x) * x0.x;
-      s1 = bf16hi(u.x) * x0.y;
-      s0 = fmaf(bf16lo(u.y), x0.z, s0);
-      s1 = fmaf(bf16hi(u.y), x0.w, s1);
-      s0 = fmaf(bf16lo(u.z), x1.x, s0);
-      s1 = fmaf(bf16hi(u.z), x1.y, s1);
-      s0 = fmaf(bf16lo(u.w), x1.z, s0);
-      s1 = fmaf(bf16hi(u.w), x1.w, s1);
-    } else {
-      const float4 u = *reinterpret_cast<const float4*>(st + b);
-      const float4 x = reinterpret_cast<const float4*>(xs)[col >> 2];
-      s0 = u.x * x.x;
-      s1 = u.y * x.y;
-      s0 = fmaf(u.z, x.z, s0);
-      s1 = fmaf(u.w, x.w, s1);
-    }
-    if (isb) {
-      c0 += s0;
-      c1 += s1;
-    } else {
-      a0 += s0;
-      a1 += s1;
-    }
+  const int sz = static_cast<int>(sizeof(WT));
+  const int e_end = stage_e0 + len / sz;
+  if (stage_e0 < k) {
+    const int hi = min(e_end, k);
+    acc_a += dot_run<WT>(st, 0, (hi - stage_e0) * sz, stage_e0, k, xs);
   }
-  acc_a += a0 + a1;
-  acc_b += c0 + c1;
+  if (e_end > k) {
+    const int lo = max(stage_e0, k);
+    acc_b += dot_run<WT>(st, (lo - stage_e0) * sz, len, lo - k, k, xs);
+  }
 }
 
 __device__ __forceinline__ void phase_arrive(int* ctr) {

@@ -46,8 +46,11 @@ __device__ __forceinline__ int xs_index(int j, int k) {
 
 // The compute ("consumer") warps of a CTA: 8 warps.  They synchronise on named
 // barrier 1 so a dedicated producer warp (decode_pass.cu) never has to join.
-constexpr int CONSUMER_THREADS = 256;
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+#ifndef GRT_CONSUMER_THREADS
+#define GRT_CONSUMER_THREADS 256
+#endif
+constexpr int CONSUMER_THREADS = GRT_CONSUMER_THREADS;
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONSUMER_THREADS) : "memory"); }
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -92,7 +95,8 @@ __device__ __forceinline__ void xs_store4(float* xs, int j4, int k, float4 v) {
     reinterpret_cast<float4*>(xs)[j4] = v;
 }
 
-constexpr int LOADX_MAXV = 12;  // float4 per thread kept in registers (k <= 12*4*blockDim)
+// float4 per thread kept in registers: covers k <= 12288 (LLaMA-2 7B d_ff = 11008)
+constexpr int LOADX_MAXV = (12288 / 4 + CONSUMER_THREADS - 1) / CONSUMER_THREADS;
 
 // Activation prologue: xs = norm(x) (or x).  The whole activation row is pulled
 // into registers with independent 16-byte loads first (latency paid once, not
