@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   __shared__ float2 part_sum[DP_PARTS];
   __shared__ int part_seq[DP_PARTS];
   __shared__ int s_ok, s_last;
+  __shared__ int s_ready, s_waited;  // trace only: stages already landed when a consumer arrived vs not
   constexpr int NORM = LLAMA ? NORM_RMS : NORM_LN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -447,6 +448,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < DP_PARTS; ++s) part_seq[s] = -1;
+    s_ready = 0;
+    s_waited = 0;
     mbar_fence_init();
   }
   __syncthreads();  // all 9 warps: barriers initialised
@@ -487,6 +490,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
     const int sz = static_cast<int>(sizeof(WT));
     for (;;) {
       const int slot = t % DP_STAGES;
+      if (p.trace && lane == 0) atomicAdd(mbar_try_wait(&full[slot], (t / DP_STAGES) & 1) ? &s_ready : &s_waited, 1);
       if (!mbar_wait_wd(&full[slot], (t / DP_STAGES) & 1)) {
         if (threadIdx.x == 0) atomicOr(p.err, DEVERR_TIMEOUT);
         alive = false;
@@ -610,6 +614,11 @@ __global__ void __launch_bounds__(DP_THREADS, 1) decode_pass_kernel(const PassPa
   ea.out = p.logits;
   run_phase(4 * p.n_layers, StoreTag{});
   stamp(p.n_layers * PASS_TRACE_PER_LAYER + 1);
+  consumer_sync();
+  if (trace && threadIdx.x == 0) {
+    trace[p.n_layers * PASS_TRACE_PER_LAYER + 3] = static_cast<unsigned long long>(s_ready);
+    trace[p.n_layers * PASS_TRACE_PER_LAYER + 4] = static_cast<unsigned long long>(s_waited);
+  }
 
   // Self-reset: the last CTA out zeroes every counter (phase, head, claim) for
   // the next pass; all other CTAs have passed their last wait and claim.

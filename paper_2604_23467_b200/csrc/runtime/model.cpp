@@ -496,7 +496,7 @@ PassParams Model::pass_params(int key, int B) const {
 std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* grid, int* stride) {
   PassParams pp = pass_params(key, B);
   *grid = num_sms(cfg_.device);
-  *stride = cfg_.n_layers * PASS_TRACE_PER_LAYER + 4;
+  *stride = cfg_.n_layers * PASS_TRACE_PER_LAYER + 8;  // + head start/end, kernel start, ready/waited counts
   pp.trace_stride = *stride;
   const size_t n = static_cast<size_t>(*grid) * *stride;
   unsigned long long* buf = nullptr;

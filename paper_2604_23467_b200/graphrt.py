@@ -484,7 +484,7 @@ class Session:
     def trace_pass(self, key: int):
         """Per-CTA %globaltimer stamps of one persistent pass: array [grid, stride] (ns)."""
         import numpy as np
-        cap = 148 * (self.model.cfg.n_layers * 10 + 4) * 2
+        cap = 160 * (self.model.cfg.n_layers * 10 + 8)
         buf = (C.c_uint64 * cap)()
         gr, st = C.c_int32(), C.c_int32()
         _check(lib().grt_trace_pass(self._h, key, buf, cap, C.byref(gr), C.byref(st)))

@@ -49,3 +49,7 @@ for rep in range(3):
     out["head_us"] = float((tr[:, L * 10 + 1].max() - tr[:, L * 10 + 0].min()) / 1e3)
     res.append(out)
 print(json.dumps(res[-1], indent=1))
+ready = tr[:, L * 10 + 3].sum()
+waited = tr[:, L * 10 + 4].sum()
+print(json.dumps({"stages_ready_on_arrival": int(ready), "stages_waited": int(waited),
+                  "ready_frac": float(ready / max(1, ready + waited))}))

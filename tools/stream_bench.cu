@@ -72,6 +72,70 @@ __global__ void __launch_bounds__(512, 1) bulk_stream(const uint8_t* __restrict_
   if (acc == 12345.f) out[0] = acc;
 }
 
+// One producer thread (last warp) feeds a CTA ring of `depth` stages; consumer
+// warp w takes stages w, w+nc, ...  (the decode_pass v4 structure).
+__global__ void __launch_bounds__(544, 1) central_stream(const uint8_t* __restrict__ src, size_t bytes,
+                                                          int stage_bytes, int depth, int nc, int compute,
+                                                          float* out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[32], empty[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t n_stages = bytes / stage_bytes;
+  // this CTA's contiguous share of stages
+  const size_t s0 = n_stages * blockIdx.x / gridDim.x, s1 = n_stages * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < depth; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  auto wait = [&](uint64_t* b, uint32_t par) {
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                   : "=r"(ok)
+                   : "r"(smem_u32(b)), "r"(par)
+                   : "memory");
+  };
+  if (warp == nc) {
+    if (lane != 0) return;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    for (size_t i = s0; i < s1; ++i) {
+      const uint32_t t = static_cast<uint32_t>(i - s0);
+      const int slot = t % depth;
+      wait(&empty[slot], ((t / depth) & 1) ^ 1);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[slot])),
+                   "r"(stage_bytes));
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+          "%4;" ::"r"(smem_u32(smem + slot * stage_bytes)),
+          "l"(src + i * stage_bytes), "r"(stage_bytes), "r"(smem_u32(&full[slot])), "l"(pol)
+          : "memory");
+    }
+    return;
+  }
+  float acc = 0.f;
+  for (size_t i = s0 + warp; i < s1; i += nc) {
+    const uint32_t t = static_cast<uint32_t>(i - s0);
+    const int slot = t % depth;
+    wait(&full[slot], (t / depth) & 1);
+    if (compute) {
+      const uint4* w = reinterpret_cast<const uint4*>(smem + slot * stage_bytes);
+      for (int g = lane; g < stage_bytes / 16; g += 32) {
+        const uint4 u = w[g];
+        acc += __uint_as_float(u.x << 16) + __uint_as_float(u.y & 0xffff0000u) + __uint_as_float(u.z << 16) +
+               __uint_as_float(u.w & 0xffff0000u);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[slot])) : "memory");
+  }
+  if (acc == 12345.f) out[0] = acc;
+}
+
 template <int UNROLL>
 __global__ void __launch_bounds__(512) ldg_stream(const int4* __restrict__ src, size_t n16, float* out) {
   const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -129,6 +193,17 @@ int main() {
       double gbs = timeit([&] { bulk_stream<<<sms, nw * 32, smem>>>(buf, bytes, sb, depth, compute, out); });
       printf("bulk stage=%6d depth=%2d warps=%2d ring=%3zu KB compute=%d : %7.1f GB/s\n", sb, depth, nw, smem / 1024,
              compute, gbs);
+    }
+  cudaFuncSetAttribute(central_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  const int ccfgs[][3] = {{8192, 20, 12}, {8192, 20, 8}, {16384, 10, 8}, {16384, 12, 12}, {32768, 6, 8},
+                          {4096, 32, 8},  {8192, 26, 12}};
+  for (int compute = 0; compute < 2; ++compute)
+    for (auto& c : ccfgs) {
+      const int sb = c[0], depth = c[1], nc = c[2];
+      const size_t smem = static_cast<size_t>(sb) * depth;
+      double gbs = timeit([&] { central_stream<<<sms, (nc + 1) * 32, smem>>>(buf, bytes, sb, depth, nc, compute, out); });
+      printf("central stage=%6d depth=%2d consumers=%2d ring=%3zu KB compute=%d : %7.1f GB/s\n", sb, depth, nc,
+             smem / 1024, compute, gbs);
     }
   for (int blocks_per_sm : {1, 2, 4, 8}) {
     double g4 = timeit([&] { ldg_stream<4><<<sms * blocks_per_sm, 512>>>((const int4*)buf, bytes / 16, out); });
