@@ -184,6 +184,7 @@ def main():
     ap.add_argument("--mode", default="hybrid")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--bucket", type=int, default=64)
+    ap.add_argument("--pass-impl", type=int, default=0, help="0 persistent single-kernel pass, 1 per-op kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--sweep", default="", help="comma list of prompt lengths for a TTFT sweep (extra key)")
@@ -204,7 +205,7 @@ def main():
     cfg = g.ModelConfig.llama2_7b(n_layers=args.layers, max_seq_len=max_seq, device=local)
     t_init = time.time()
     sess = g.Session(cfg, g.CacheConfig(bucket_size=args.bucket, warmup_lo=1, warmup_hi=10 ** 6 // args.bucket,
-                                        capacity=4096))
+                                        capacity=4096, pass_impl=args.pass_impl))
     init_s = time.time() - t_init
     model = sess.model
     prompt = [(i * 7919 + 17) % 32000 for i in range(P)]

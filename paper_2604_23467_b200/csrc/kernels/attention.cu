@@ -5,11 +5,8 @@
 // read from device memory (seq_len) instead of being baked into the plan
 // (model.cpp:118-131), so one captured graph serves every length in its bucket.
 //
-// Grid = (n_heads, nsplit).  Each CTA scores its span of positions (a group of
-// head_dim/4 lanes per position, coalesced row reads of the [h][max_seq][dh]
-// cache), does a local softmax, accumulates P.V and, when nsplit > 1, publishes
-// (m, l, o) partials; the LAST CTA of a head (arrival counter) merges the
-// partials in split order, so results are deterministic run to run.
+// One thread-block cluster per head, sized for the graph's length bucket; see
+// attn_decode_kernel.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -19,7 +16,7 @@
 
 namespace grt {
 
-constexpr int ATTN_THREADS = 128;
+constexpr int ATTN_THREADS = 256;
 
 template <typename KT>
 __device__ __forceinline__ float4 load4(const KT* p);
@@ -38,175 +35,230 @@ __device__ __forceinline__ float group_sum(float v, int gs) {
   return v;
 }
 
-__device__ __forceinline__ float block_reduce(float v, float* red, bool is_max) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  v = is_max ? warp_max(v) : warp_sum(v);
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = threadIdx.x < (ATTN_THREADS / 32) ? red[threadIdx.x] : (is_max ? -INFINITY : 0.0f);
-    t = is_max ? warp_max(t) : warp_sum(t);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
-  return red[0];
+// Decode attention for one head = one thread-block CLUSTER of `ns` CTAs
+// (ns = 1..16, sized for the graph's bucket); CTA r of the cluster owns
+// positions [r*span, (r+1)*span) in `rounds` passes of ATTN_WARPS warps x
+// ATTN_UNROLL row groups.  A row of dh elements is read by G = dh/4 lanes
+// (4 elements each), so one warp load covers RPW = 32/G positions.
+//  * every K and V row of a pass is requested at once, right after the
+//    dependency wait and in parallel with the seq_len / q loads (the rows are
+//    addressed by bucket position, masked by the live length afterwards): one
+//    memory round trip instead of three -- the kernel is latency bound;
+//  * scores, max-subtracted softmax and P.V per warp (online across passes),
+//    merged across warps in shared memory in warp order;
+//  * the cluster's CTAs merge their partials {o[dh], m, l} through distributed
+//    shared memory in rank order (deterministic, no global fences/atomics) and
+//    rank 0 writes out[head] -- Wo reads a plain activation row.
+constexpr int ATTN_UNROLL = 8;
+constexpr int ATTN_WARPS = ATTN_THREADS / 32;
+constexpr int ATTN_MAX_CLUSTER = 16;
+__host__ __device__ constexpr int attn_pass_span(int dh) { return ATTN_WARPS * ATTN_UNROLL * (32 / (dh / 4)); }
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// generic address of `p` (this CTA's shared memory) in CTA `rank` of the cluster
+template <typename T>
+__device__ __forceinline__ const T* dsmem_map(const T* p, uint32_t rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<const T*>(out);
 }
 
 template <typename KT>
 __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(const AttnParams p) {
-  extern __shared__ __align__(16) float sm[];
-  __shared__ float red[32];
-  __shared__ int s_last;
-  griddep_launch_dependents();
+  __shared__ float s_m[ATTN_WARPS], s_l[ATTN_WARPS];
+  __shared__ __align__(16) float s_o[ATTN_WARPS][256];
+  __shared__ __align__(16) float c_o[256];  // this CTA's partial, read by rank 0 over DSMEM
+  __shared__ float c_ml[2];
+  op_stamp(p.trace, 0);
+  const int dh = p.head_dim;
+  const int G = dh >> 2, RPW = 32 / G;
+  const int ns = static_cast<int>(cluster_nctarank());
+  const int rank = static_cast<int>(cluster_ctarank());
+  const int head = blockIdx.x / ns;
+  const int pass = ATTN_WARPS * ATTN_UNROLL * RPW;
+  const int rounds = p.rounds;
+  const int span = pass * rounds;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / G, c = lane - g * G;
+  const KT* K = reinterpret_cast<const KT*>(p.k_cache) + static_cast<int64_t>(head) * p.max_seq * dh + 4 * c;
+  const KT* V = reinterpret_cast<const KT*>(p.v_cache) + static_cast<int64_t>(head) * p.max_seq * dh + 4 * c;
   griddep_wait();
+  op_stamp(p.trace, 1);
 
   const int len = p.seq_len ? *p.seq_len : p.len_fixed;
-  const int head = blockIdx.x, split = blockIdx.y, ns = gridDim.y;
-  const int dh = p.head_dim;
-  const int gs = dh >> 2;                  // lanes per position (4 dims per lane)
-  const int npg = ATTN_THREADS / gs;       // position groups per CTA
-  const int span = (len + ns - 1) / ns;
-  if (len < 1 || span > p.span_cap) {
-    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && p.err) atomicOr(p.err, DEVERR_WRONG_LENGTH);
-    return;  // uniform across the grid: every CTA sees the same len
-  }
-  const int j0 = split * span;
-  const int j1 = min(len, j0 + span);
-  const int n = max(0, j1 - j0);
-
-  float* qs = sm;                  // [dh]
-  float* sc = qs + dh;             // [span_cap]
-  float* op = sc + p.span_cap;     // [npg][dh]
-  for (int d = threadIdx.x; d < dh; d += ATTN_THREADS) qs[d] = p.q[head * dh + d];
-  __syncthreads();
-
-  const KT* K = reinterpret_cast<const KT*>(p.k_cache) + static_cast<int64_t>(head) * p.max_seq * dh;
-  const KT* V = reinterpret_cast<const KT*>(p.v_cache) + static_cast<int64_t>(head) * p.max_seq * dh;
-  const int grp = threadIdx.x / gs, gl = threadIdx.x - grp * gs;
-  const float4 q4 = reinterpret_cast<const float4*>(qs)[gl];
-
-  // scores
-  for (int jb = 0; jb < n; jb += npg) {  // warp-uniform trip count (shuffles below)
-    const int jj = jb + grp;
-    float s = 0.0f;
-    if (jj < n) {
-      const float4 k4 = load4<KT>(K + static_cast<int64_t>(j0 + jj) * dh + 4 * gl);
-      s = q4.x * k4.x + q4.y * k4.y + q4.z * k4.z + q4.w * k4.w;
-    }
-    s = group_sum(s, gs);
-    if (jj < n && gl == 0) sc[jj] = s * p.scale;
-  }
-  __syncthreads();
-  float m = -INFINITY;
-  for (int jj = threadIdx.x; jj < n; jj += ATTN_THREADS) m = fmaxf(m, sc[jj]);
-  m = block_reduce(m, red, true);
-  float l = 0.0f;
-  for (int jj = threadIdx.x; jj < n; jj += ATTN_THREADS) {
-    const float e = expf(sc[jj] - m);
-    sc[jj] = e;
-    l += e;
-  }
-  l = block_reduce(l, red, false);  // ends with __syncthreads: sc visible
-
-  // o = sum_j e_j V_j
+  const float4 q4 = __ldcg(reinterpret_cast<const float4*>(p.q + head * dh) + c);
+  float m = -INFINITY, l = 0.0f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int jj = grp; jj < n; jj += npg) {
-    const float e = sc[jj];
-    const float4 v4 = load4<KT>(V + static_cast<int64_t>(j0 + jj) * dh + 4 * gl);
-    acc.x = fmaf(e, v4.x, acc.x);
-    acc.y = fmaf(e, v4.y, acc.y);
-    acc.z = fmaf(e, v4.z, acc.z);
-    acc.w = fmaf(e, v4.w, acc.w);
+  for (int r = 0; r < rounds; ++r) {
+    const int jw = rank * span + r * pass + warp * ATTN_UNROLL * RPW;  // first position of this warp
+    float4 kv[ATTN_UNROLL], vv[ATTN_UNROLL];
+#pragma unroll
+    for (int u = 0; u < ATTN_UNROLL; ++u) {
+      const int j = min(jw + u * RPW + g, p.max_seq - 1);  // bucket position (masked below)
+      kv[u] = load4<KT>(K + static_cast<int64_t>(j) * dh);
+      vv[u] = load4<KT>(V + static_cast<int64_t>(j) * dh);
+    }
+    float sc[ATTN_UNROLL];
+    float mr = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < ATTN_UNROLL; ++u) {
+      float sv = q4.x * kv[u].x + q4.y * kv[u].y + q4.z * kv[u].z + q4.w * kv[u].w;
+      sv = group_sum(sv, G);  // lanes of one row share the score
+      sc[u] = jw + u * RPW + g < len ? sv * p.scale : -INFINITY;
+      mr = fmaxf(mr, sc[u]);
+    }
+    for (int o = G; o < 32; o <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));  // across row groups
+    if (r == 0 && p.trace && warp == 0) op_stamp(p.trace, 2);
+    if (mr != -INFINITY) {
+      const float mn = fmaxf(m, mr);
+      const float f = m == -INFINITY ? 0.0f : __expf(m - mn);
+      l *= f;
+      acc = make_float4(acc.x * f, acc.y * f, acc.z * f, acc.w * f);
+      m = mn;
+#pragma unroll
+      for (int u = 0; u < ATTN_UNROLL; ++u) {
+        if (sc[u] == -INFINITY) continue;  // masked rows never touch V (it may be stale)
+        const float e = __expf(sc[u] - m);
+        l += e;
+        acc.x = fmaf(e, vv[u].x, acc.x);
+        acc.y = fmaf(e, vv[u].y, acc.y);
+        acc.z = fmaf(e, vv[u].z, acc.z);
+        acc.w = fmaf(e, vv[u].w, acc.w);
+      }
+    }
   }
-  reinterpret_cast<float4*>(op + grp * dh)[gl] = acc;
+  griddep_launch_dependents();
+  // the warp's m is uniform; l and acc are per row group: reduce over groups
+  for (int o = G; o < 32; o <<= 1) {
+    l += __shfl_xor_sync(0xffffffffu, l, o);
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+  }
+  if (lane < G) reinterpret_cast<float4*>(s_o[warp])[c] = acc;
+  if (lane == 0) {
+    s_m[warp] = m;
+    s_l[warp] = l;
+  }
   __syncthreads();
 
-  if (ns == 1) {
-    const float inv = 1.0f / l;
-    for (int d = threadIdx.x; d < dh; d += ATTN_THREADS) {
-      float o = 0.0f;
-      for (int g = 0; g < npg; ++g) o += op[g * dh + d];
-      p.out[head * dh + d] = o * inv;
-    }
-    return;
+  // CTA merge (fixed warp order) -> this CTA's partial {o, m, l}
+  float M = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < ATTN_WARPS; ++w) M = fmaxf(M, s_m[w]);
+  float L = 0.0f, f[ATTN_WARPS];
+#pragma unroll
+  for (int w = 0; w < ATTN_WARPS; ++w) {
+    f[w] = s_m[w] == -INFINITY ? 0.0f : __expf(s_m[w] - M);
+    L += s_l[w] * f[w];
   }
-
-  // publish this split's partial
-  const int stride = dh + 2;
-  float* mine = p.part + (static_cast<int64_t>(head) * ns + split) * stride;
   for (int d = threadIdx.x; d < dh; d += ATTN_THREADS) {
     float o = 0.0f;
-    for (int g = 0; g < npg; ++g) o += op[g * dh + d];
-    mine[d] = o;
+#pragma unroll
+    for (int w = 0; w < ATTN_WARPS; ++w) o += s_o[w][d] * f[w];
+    c_o[d] = o;
   }
   if (threadIdx.x == 0) {
-    mine[dh] = n > 0 ? m : -INFINITY;
-    mine[dh + 1] = n > 0 ? l : 0.0f;
+    c_ml[0] = M;
+    c_ml[1] = L;
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&p.counters[head], 1) == ns - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
-  // merge in split order (deterministic)
-  const float* base = p.part + static_cast<int64_t>(head) * ns * stride;
-  float M = -INFINITY;
-  for (int s = 0; s < ns; ++s) {
-    const float ls = __ldcg(base + s * stride + dh + 1);
-    if (ls > 0.0f) M = fmaxf(M, __ldcg(base + s * stride + dh));
+  if (len < 1 || len > ns * span) {  // live length outside the bucket this graph was built for
+    if (threadIdx.x == 0 && rank == 0 && head == 0 && p.err) atomicOr(p.err, DEVERR_WRONG_LENGTH);
   }
-  float L = 0.0f;
-  for (int s = 0; s < ns; ++s) {
-    const float ls = __ldcg(base + s * stride + dh + 1);
-    if (ls > 0.0f) L += ls * expf(__ldcg(base + s * stride + dh) - M);
-  }
-  const float invL = 1.0f / L;
-  for (int d = threadIdx.x; d < dh; d += ATTN_THREADS) {
-    float o = 0.0f;
-    for (int s = 0; s < ns; ++s) {
-      const float ls = __ldcg(base + s * stride + dh + 1);
-      if (ls > 0.0f) o += __ldcg(base + s * stride + d) * expf(__ldcg(base + s * stride + dh) - M);
+  cluster_sync_all();  // partials visible cluster-wide
+  if (rank == 0) {
+    float MM = -INFINITY;
+    for (int r = 0; r < ns; ++r) MM = fmaxf(MM, *dsmem_map(&c_ml[0], r));
+    float LL = 0.0f;
+    for (int r = 0; r < ns; ++r) {
+      const float mr = *dsmem_map(&c_ml[0], r);
+      if (mr != -INFINITY) LL += *dsmem_map(&c_ml[1], r) * __expf(mr - MM);
     }
-    p.out[head * dh + d] = o * invL;
+    const float inv = 1.0f / LL;
+    for (int d = threadIdx.x; d < dh; d += ATTN_THREADS) {
+      float o = 0.0f;
+      for (int r = 0; r < ns; ++r) {
+        const float mr = *dsmem_map(&c_ml[0], r);
+        if (mr != -INFINITY) o += *dsmem_map(&c_o[d], r) * __expf(mr - MM);
+      }
+      p.out[head * dh + d] = o * inv;
+    }
   }
-  if (threadIdx.x == 0) p.counters[head] = 0;  // self-reset for the next replay
+  cluster_sync_all();  // keep every CTA's shared memory alive until rank 0 has read it
+  op_stamp(p.trace, 3);
+}
+
+// Cluster size and passes for a bucket of max_len positions.
+static void attn_shape(int max_len, int head_dim, int* ns, int* rounds) {
+  const int pass = attn_pass_span(head_dim);
+  const int need = std::max(1, (max_len + pass - 1) / pass);  // passes over the whole bucket
+  int c = 1;
+  while (c < need && c < ATTN_MAX_CLUSTER) c <<= 1;
+  *ns = c;
+  *rounds = (need + c - 1) / c;
+}
+
+int attention_splits(int max_len, int head_dim) {
+  int ns, rounds;
+  attn_shape(max_len, head_dim, &ns, &rounds);
+  return ns;
 }
 
 int attention_nsplit(int max_len, int n_heads, int sms) {
-  // Aim for ~one wave of CTAs and >= 32 positions per CTA.
+  // persistent pass: aim for ~one wave of CTAs and >= 32 positions per CTA.
   int ns = std::max(1, std::min((max_len + 31) / 32, std::max(1, (2 * sms) / std::max(1, n_heads))));
   return std::min(ns, 64);
 }
 
-cudaError_t launch_attention(Dt kvdt, AttnParams p, int nsplit, cudaStream_t s, bool pdl) {
+cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s, bool pdl) {
   const int gs = p.head_dim / 4;
-  if (p.head_dim % 4 != 0 || gs < 1 || gs > 32 || (gs & (gs - 1)) != 0) return cudaErrorInvalidValue;
-  const int npg = ATTN_THREADS / gs;
-  const size_t smem = (static_cast<size_t>(p.head_dim) + p.span_cap + static_cast<size_t>(npg) * p.head_dim) * 4;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (p.head_dim % 4 != 0 || gs < 1 || gs > 32 || (gs & (gs - 1)) != 0 || p.head_dim > 256)
+    return cudaErrorInvalidValue;
+  int ns, rounds;
+  attn_shape(max_len, p.head_dim, &ns, &rounds);
+  p.rounds = rounds;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_heads, nsplit);
+  cfg.gridDim = dim3(p.n_heads * ns);
   cfg.blockDim = dim3(ATTN_THREADS);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ns;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = pdl ? 2 : 1;
   if (kvdt == Dt::BF16) return cudaLaunchKernelEx(&cfg, attn_decode_kernel<__nv_bfloat16>, p);
   return cudaLaunchKernelEx(&cfg, attn_decode_kernel<float>, p);
 }
 
 cudaError_t attention_prepare() {
-  cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<__nv_bfloat16>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(attn_decode_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (const void* f : {reinterpret_cast<const void*>(attn_decode_kernel<__nv_bfloat16>),
+                        reinterpret_cast<const void*>(attn_decode_kernel<float>)}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    // same L1/shared carveout as the GEMVs, so the next GEMV's CTAs can become
+    // resident next to attention CTAs (PDL) without an SM reconfiguration
+    e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
-// (200 KB + the 132 B of static shared memory stays below the 227 KB opt-in limit)
 
 }  // namespace grt

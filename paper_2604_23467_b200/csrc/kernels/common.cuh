@@ -74,6 +74,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Bulk L2 prefetch (TMA engine, fire and forget): pulls [src, src+bytes) into L2
+// without occupying shared memory.  src 16-B aligned, bytes a multiple of 16.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// one stamp per CTA (thread 0), only when tracing is on
+__device__ __forceinline__ void op_stamp(unsigned long long* tr, int i) {
+  if (tr && threadIdx.x == 0) {
+    const int cta = blockIdx.x + blockIdx.y * gridDim.x;
+    tr[cta * 4 + i] = gtimer();
+  }
+}
+
 // ---- numerics -----------------------------------------------------------------
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }

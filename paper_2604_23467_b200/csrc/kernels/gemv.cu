@@ -1,17 +1,24 @@
 // gemv.cu -- per-op fused GEMV kernels (K1 QKV, K4 Wo, K5 gate/up, K6 down,
-// K7 LM head) for sm_100a.  Used by the per-op plan (eager-launch ablation and
-// op-level tests); the default static pass is the persistent decode_pass.cu,
-// built from the same device functions (gemv_core.cuh).
+// K7 LM head) for sm_100a: the default static decode pass (pass_impl 1) is a
+// graph of these plus the split-K attention kernel.
 //
 // Memory-bound design (decode is ~1 flop/byte; tensor cores stay idle):
-//  * each warp owns a private ring of GEMV_STAGES shared-memory slots; lane 0
-//    streams weight row chunks with cp.async.bulk (TMA engine, SASS UBLKCP)
-//    under an evict-first L2 policy, completion tracked by an mbarrier per slot;
-//  * the first ring fill is issued BEFORE griddepcontrol.wait, so weight
-//    streaming overlaps the previous kernel (Programmatic Dependent Launch).
+//  * each warp owns a private ring of `stages` shared-memory slots (as deep as
+//    the 227 KB opt-in budget allows after the activation row, up to
+//    GEMV_MAX_STAGES); lane 0 streams weight row chunks with cp.async.bulk (TMA
+//    engine, SASS UBLKCP) under an evict-first L2 policy, completion tracked by
+//    one mbarrier per slot;
+//  * the whole first ring fill -- and the norm weights -- are loaded BEFORE
+//    griddepcontrol.wait, so with Programmatic Dependent Launch the kernel
+//    streams its weights while the previous kernel drains;
+//  * a CTA owns a contiguous range of row PAIRS (2p, 2p+1), dealt round-robin
+//    to its warps; pairs let RoPE (rotate-half) and SwiGLU finish in-warp;
+//  * the QKV kernel prefetches this layer's K/V rows [0, seq_len) into L2 (and
+//    warms their TLB entries) for the attention kernel that follows.
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemv_core.cuh"
@@ -20,63 +27,153 @@
 namespace grt {
 
 constexpr int GEMV_WARPS = 8;
-constexpr int GEMV_STAGES = 2;
+constexpr int GEMV_MAX_STAGES = 4;
 constexpr int GEMV_THREADS = GEMV_WARPS * 32;
+
+// Activation prologue with the norm weights already in registers (they are
+// weights, so they are loaded before griddepcontrol.wait): x is pulled into
+// registers with independent 16-byte loads, reduced, normalised (reference
+// layernorm kernels.cpp:66-83; RMSNorm drops mean and beta) and stored in the
+// shared-memory layout dot_chunk expects.
+template <typename WT, int NORM>
+__device__ __forceinline__ void load_x_pre(const float* x, const float4* gv, const float4* bv, float eps, int k,
+                                           float* xs, float* red) {
+  const int n4 = k >> 2;
+  float4 v[LOADX_MAXV];
+#pragma unroll
+  for (int i = 0; i < LOADX_MAXV; ++i) {
+    const int j4 = threadIdx.x + i * CONSUMER_THREADS;
+    v[i] = j4 < n4 ? *reinterpret_cast<const float4*>(x + 4 * j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float mean = 0.0f, inv = 1.0f;
+  if constexpr (NORM == NORM_RMS) {
+    float ss = 0.0f;
+#pragma unroll
+    for (int i = 0; i < LOADX_MAXV; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    ss = block_sum(ss, red);
+    inv = 1.0f / sqrtf(ss / static_cast<float>(k) + eps);
+  } else if constexpr (NORM == NORM_LN) {
+    float sm = 0.0f;
+#pragma unroll
+    for (int i = 0; i < LOADX_MAXV; ++i) sm += v[i].x + v[i].y + v[i].z + v[i].w;
+    mean = block_sum(sm, red) / static_cast<float>(k);
+    float var = 0.0f;
+#pragma unroll
+    for (int i = 0; i < LOADX_MAXV; ++i) {
+      const int j4 = threadIdx.x + i * CONSUMER_THREADS;
+      if (j4 < n4) {
+        const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+        var += a * a + b * b + c * c + d * d;
+      }
+    }
+    var = block_sum(var, red) / static_cast<float>(k);
+    inv = 1.0f / sqrtf(var + eps);
+  }
+#pragma unroll
+  for (int i = 0; i < LOADX_MAXV; ++i) {
+    const int j4 = threadIdx.x + i * CONSUMER_THREADS;
+    if (j4 >= n4) continue;
+    float4 o = v[i];
+    if constexpr (NORM == NORM_RMS) {
+      const float4 g = gv[i];
+      o = make_float4(o.x * inv * g.x, o.y * inv * g.y, o.z * inv * g.z, o.w * inv * g.w);
+    } else if constexpr (NORM == NORM_LN) {
+      const float4 g = gv[i], b = bv[i];
+      o = make_float4((o.x - mean) * inv * g.x + b.x, (o.y - mean) * inv * g.y + b.y, (o.z - mean) * inv * g.z + b.z,
+                      (o.w - mean) * inv * g.w + b.w);
+    }
+    xs_store4<WT>(xs, j4, k, o);
+  }
+  consumer_sync();
+}
 
 template <typename WT, int NORM, int EPI>
 __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bars[GEMV_WARPS][GEMV_STAGES];
+  __shared__ uint64_t bars[GEMV_WARPS][GEMV_MAX_STAGES];
   __shared__ float red[32];
-  constexpr int CH = WTraits<WT>::CH;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = p.stages;
   const uint32_t rowb = static_cast<uint32_t>(p.rowb);
   const uint32_t stageb = 2 * rowb;
-  uint8_t* mystage = smem + static_cast<size_t>(warp) * GEMV_STAGES * stageb;
-  float* xs = reinterpret_cast<float*>(smem + static_cast<size_t>(GEMV_WARPS) * GEMV_STAGES * stageb);
+  uint8_t* mystage = smem + static_cast<size_t>(warp) * S * stageb;
+  float* xs = reinterpret_cast<float*>(smem + static_cast<size_t>(GEMV_WARPS) * S * stageb);
 
+  const int CH = p.ch, nch = p.nch;
   const int n_pairs = (p.n_rows + 1) >> 1;
   const int pair_begin = static_cast<int>(static_cast<int64_t>(blockIdx.x) * n_pairs / gridDim.x);
   const int pair_end = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * n_pairs / gridDim.x);
-  const int nch = (p.k + CH - 1) / CH;
   const int span = pair_end - pair_begin - warp;
-  const int my_pairs = span <= 0 ? 0 : (span + GEMV_WARPS - 1) / GEMV_WARPS;
-  const int n_tasks = my_pairs * nch;
+  const int n_tasks = span <= 0 ? 0 : (span + GEMV_WARPS - 1) / GEMV_WARPS * nch;
   uint64_t* mybar = bars[warp];
   const uint64_t pol = l2_evict_first_policy();
-  const WT* W = reinterpret_cast<const WT*>(p.w);
+  const WT* Wt = reinterpret_cast<const WT*>(p.w);
 
-  auto issue = [&](int t) {
-    const int pi = t / nch, c = t - pi * nch;
+  auto issue = [&](int i) {
+    const int pi = i / nch, c = i - pi * nch;
     const int row0 = 2 * (pair_begin + warp + pi * GEMV_WARPS);
     const int c0 = c * CH;
     const int ce = min(CH, p.k - c0);
     const uint32_t bytes = static_cast<uint32_t>(ce) * sizeof(WT);
     const bool has_b = row0 + 1 < p.n_rows;
-    const int slot = t % GEMV_STAGES;
+    const int slot = i % S;
     uint64_t* bar = &mybar[slot];
     uint8_t* dst = mystage + slot * stageb;
     mbar_arrive_expect_tx(bar, has_b ? 2 * bytes : bytes);
-    const WT* src = W + static_cast<int64_t>(row0) * p.k + c0;
+    const WT* src = Wt + static_cast<int64_t>(row0) * p.k + c0;
     bulk_g2s(dst, src, bytes, bar, pol);
     if (has_b) bulk_g2s(dst + rowb, src + p.k, bytes, bar, pol);
   };
 
+  op_stamp(p.trace, 0);
   if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < GEMV_STAGES; ++s) mbar_init(&mybar[s], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&mybar[s], 1);
     mbar_fence_init();
   }
   __syncwarp();
   griddep_launch_dependents();
-  // Weights never depend on the previous kernel: start streaming now.
+  // Weights never depend on the previous kernel: fill the whole ring now.
   if (lane == 0) {
-    const int pre = min(GEMV_STAGES, n_tasks);
-    for (int t = 0; t < pre; ++t) issue(t);
+    const int pre = min(S, n_tasks);
+    for (int i = 0; i < pre; ++i) issue(i);
+  }
+  // norm weights are weights too: in registers before the dependency wait
+  constexpr bool HAS_G = NORM == NORM_RMS || NORM == NORM_LN;
+  float4 gv[HAS_G ? LOADX_MAXV : 1], bv[NORM == NORM_LN ? LOADX_MAXV : 1];
+  const bool pre_norm = p.k <= LOADX_MAXV * 4 * CONSUMER_THREADS;
+  if constexpr (HAS_G) {
+    if (pre_norm) {
+      const int n4 = p.k >> 2;
+#pragma unroll
+      for (int i = 0; i < LOADX_MAXV; ++i) {
+        const int j4 = threadIdx.x + i * CONSUMER_THREADS;
+        gv[i] = j4 < n4 ? __ldg(reinterpret_cast<const float4*>(p.gamma) + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (NORM == NORM_LN)
+          bv[i] = j4 < n4 ? __ldg(reinterpret_cast<const float4*>(p.beta) + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
   }
   griddep_wait();
-  load_x<WT, NORM, false>(p.x, p.gamma, p.beta, p.eps, p.k, xs, red);
+  op_stamp(p.trace, 1);
+  if constexpr (EPI == EPI_QKV || EPI == EPI_QKV_ROPE) {
+    // L2 prefetch (and TLB warm-up) of this layer's K/V rows [0, seq_len-1) for
+    // the attention kernel: one contiguous [len, dh] run per (head, K|V).
+    if (threadIdx.x == 0 && p.seq_len && static_cast<int>(blockIdx.x) < 2 * p.n_heads) {
+      const int hh = blockIdx.x >> 1;
+      const size_t eb = p.kv_bf16 ? 2 : 4;
+      const uint8_t* base = static_cast<const uint8_t*>((blockIdx.x & 1) ? p.v_cache : p.k_cache) +
+                            static_cast<size_t>(hh) * p.max_seq * p.head_dim * eb;
+      const uint64_t bytes = static_cast<uint64_t>(max(0, *p.seq_len - 1)) * p.head_dim * eb;
+      for (uint64_t o = 0; o < bytes; o += 65536)
+        prefetch_l2_bulk(base + o, static_cast<uint32_t>(bytes - o < 65536 ? bytes - o : 65536));
+    }
+  }
+  if (HAS_G && pre_norm)
+    load_x_pre<WT, (HAS_G ? NORM : NORM_RMS)>(p.x, gv, bv, p.eps, p.k, xs, red);
+  else
+    load_x<WT, NORM, false>(p.x, p.gamma, p.beta, p.eps, p.k, xs, red);
+  op_stamp(p.trace, 2);
 
   EpiArgs ea;
   ea.out = p.out;
@@ -91,28 +188,48 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
   ea.d_model = p.d_model;
   ea.kv_bf16 = p.kv_bf16;
 
+  // Epilogues are deferred and run lane-parallel: lane j keeps the results of
+  // the warp's j-th pair (mod 32) and all lanes finish together, so the
+  // epilogue's own memory round trips (residual read, RoPE table) are paid
+  // once per 32 pairs instead of once per pair inside the streaming loop.
   float acc_a = 0.0f, acc_b = 0.0f;
-  for (int t = 0; t < n_tasks; ++t) {
-    const int slot = t % GEMV_STAGES;
-    mbar_wait(&mybar[slot], static_cast<uint32_t>((t / GEMV_STAGES) & 1));
-    const int pi = t / nch, c = t - pi * nch;
+  float my_a = 0.0f, my_b = 0.0f;
+  int my_pair = -1;
+  auto flush = [&]() {
+    if (my_pair >= 0) epilogue<EPI>(ea, my_pair, my_a, my_b, 2 * my_pair + 1 < p.n_rows);
+    my_pair = -1;
+  };
+  for (int i = 0; i < n_tasks; ++i) {
+    const int slot = i % S;
+    mbar_wait(&mybar[slot], static_cast<uint32_t>((i / S) & 1));
+    const int pi = i / nch, c = i - pi * nch;
     const int pair = pair_begin + warp + pi * GEMV_WARPS;
     const int c0 = c * CH;
     const int ce = min(CH, p.k - c0);
     const uint8_t* st = mystage + slot * stageb;
     dot_chunk<WT>(st, st + rowb, xs, p.k, c0, ce, acc_a, acc_b);
     __syncwarp();
-    if (lane == 0 && t + GEMV_STAGES < n_tasks) {
+    if (lane == 0 && i + S < n_tasks) {
       fence_proxy_async_smem();
-      issue(t + GEMV_STAGES);
+      issue(i + S);
     }
     if (c == nch - 1) {
       const float va = warp_sum(acc_a);
       const float vb = warp_sum(acc_b);
-      if (lane == 0) epilogue<EPI>(ea, pair, va, vb, 2 * pair + 1 < p.n_rows);
+      if (lane == (pi & 31)) {
+        my_a = va;
+        my_b = vb;
+        my_pair = pair;
+      }
       acc_a = 0.0f;
       acc_b = 0.0f;
+      if ((pi & 31) == 31) flush();
     }
+  }
+  flush();
+  if (p.trace) {
+    consumer_sync();
+    op_stamp(p.trace, 3);
   }
 }
 
@@ -130,15 +247,47 @@ int num_sms(int device) {
   return cached[device];
 }
 
-template <typename WT>
-static int rowb_for(int k) {
-  const int ce = std::min(WTraits<WT>::CH, k);
-  return ((ce * static_cast<int>(sizeof(WT)) + 15) / 16) * 16;
+static int smem_optin(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) return 227 * 1024;
+  if (!cached[device]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cached[device] = n > 0 ? n : 227 * 1024;
+  }
+  return cached[device];
+}
+
+// chunking of a k-long row: near-equal chunks of <= CH elements, multiple of 8
+static void chunking(Dt wdt, int k, int* ch, int* nch, int* rowb) {
+  const int chmax = wdt == Dt::BF16 ? WTraits<__nv_bfloat16>::CH : WTraits<float>::CH;
+  *nch = (k + chmax - 1) / chmax;
+  *ch = ((k + *nch - 1) / *nch + 7) / 8 * 8;
+  *rowb = ((*ch * (wdt == Dt::BF16 ? 2 : 4) + 15) / 16) * 16;
+}
+
+static constexpr int kStaticSmemReserve = 1024;  // bars + red + alignment
+
+int gemv_max_stages() {
+  static const int v = [] {
+    const char* e = getenv("GRT_GEMV_STAGES");
+    const int s = e ? atoi(e) : GEMV_MAX_STAGES;
+    return std::max(1, std::min(GEMV_MAX_STAGES, s));
+  }();
+  return v;
+}
+
+static int stages_for(int device, int rowb, int k) {
+  const int budget = smem_optin(device) - kStaticSmemReserve - k * 4;
+  const int s = budget / (GEMV_WARPS * 2 * rowb);
+  return std::max(1, std::min(gemv_max_stages(), s));
 }
 
 size_t gemv_smem_bytes(Dt wdt, int k) {
-  const int rowb = wdt == Dt::BF16 ? rowb_for<__nv_bfloat16>(k) : rowb_for<float>(k);
-  return static_cast<size_t>(GEMV_WARPS) * GEMV_STAGES * 2 * rowb + static_cast<size_t>(k) * sizeof(float);
+  int ch, nch, rowb, dev = 0;
+  chunking(wdt, k, &ch, &nch, &rowb);
+  cudaGetDevice(&dev);
+  return static_cast<size_t>(GEMV_WARPS) * stages_for(dev, rowb, k) * 2 * rowb + static_cast<size_t>(k) * sizeof(float);
 }
 
 using GemvFn = void (*)(const GemvParams);
@@ -165,9 +314,7 @@ static GemvFn pick_any(Dt wdt, int norm, int epi) {
 }
 
 cudaError_t gemv_prepare(int device) {
-  int optin = 0;
-  cudaError_t err = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  if (err != cudaSuccess) return err;
+  const int optin = smem_optin(device);
   const int norms[] = {NORM_NONE, NORM_LN, NORM_RMS};
   const int epis[] = {EPI_STORE, EPI_RESID, EPI_QKV, EPI_QKV_ROPE, EPI_SWIGLU, EPI_RELU};
   for (Dt dt : {Dt::F32, Dt::BF16})
@@ -176,7 +323,7 @@ cudaError_t gemv_prepare(int device) {
         GemvFn f = pick_any(dt, n, e);
         if (!f) continue;
         cudaFuncAttributes fa;
-        err = cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f));
+        cudaError_t err = cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f));
         if (err != cudaSuccess) return err;
         err = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    optin - static_cast<int>(fa.sharedSizeBytes));
@@ -189,16 +336,17 @@ cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s,
   GemvFn f = pick_any(wdt, norm, epi);
   if (!f) return cudaErrorInvalidValue;
   if (p.k % 8 != 0 || p.n_rows < 1) return cudaErrorInvalidValue;
-  p.rowb = wdt == Dt::BF16 ? rowb_for<__nv_bfloat16>(p.k) : rowb_for<float>(p.k);
   int dev = 0;
   cudaGetDevice(&dev);
+  chunking(wdt, p.k, &p.ch, &p.nch, &p.rowb);
+  p.stages = stages_for(dev, p.rowb, p.k);
   const int n_pairs = (p.n_rows + 1) / 2;
   int grid = grid_ctas > 0 ? grid_ctas : num_sms(dev);
   grid = std::max(1, std::min(grid, (n_pairs + GEMV_WARPS - 1) / GEMV_WARPS));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(GEMV_THREADS);
-  cfg.dynamicSmemBytes = gemv_smem_bytes(wdt, p.k);
+  cfg.dynamicSmemBytes = static_cast<size_t>(GEMV_WARPS) * p.stages * 2 * p.rowb + static_cast<size_t>(p.k) * 4;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

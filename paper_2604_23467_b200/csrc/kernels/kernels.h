@@ -31,6 +31,8 @@ struct GemvParams {
   int n_rows = 0;
   int k = 0;
   int rowb = 0;             // bytes of one row chunk slot in shared memory (set by the launcher)
+  int ch = 0, nch = 0;      // k-chunk elements and chunks per row (set by the launcher)
+  int stages = 0;           // ring slots per warp (set by the launcher from the smem budget)
   const float* x = nullptr; // input activation [k] fp32
   const float* gamma = nullptr;
   const float* beta = nullptr;
@@ -46,6 +48,7 @@ struct GemvParams {
   int n_heads = 0, head_dim = 0, max_seq = 0, d_model = 0;
   int kv_bf16 = 0;
   int* err = nullptr;       // device error word (WrongLength / CacheFull flags)
+  unsigned long long* trace = nullptr;  // optional [cta][4] %globaltimer stamps (profiling)
 };
 
 struct AttnParams {
@@ -61,7 +64,12 @@ struct AttnParams {
   int span_cap = 0;              // max positions per split CTA (smem sizing)
   float scale = 1.0f;
   int* err = nullptr;
+  unsigned long long* trace = nullptr;  // optional [cta][4] %globaltimer stamps (profiling)
+  int rounds = 1;                // passes per CTA (set by the launcher)
 };
+// Per-op trace stamps: 0 CTA start, 1 dependency released (griddepcontrol.wait),
+// 2 operands ready (activation loaded / KV rows loaded), 3 CTA done.
+constexpr int OP_TRACE_CTAS = 1024;  // stamp slots per kernel in a traced plan
 
 // Device error flags (bit set by kernels, read by the host after a run).
 enum DevErr : int {
@@ -127,9 +135,12 @@ cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s,
 size_t gemv_smem_bytes(Dt wdt, int k);
 cudaError_t gemv_prepare(int device);  // raises the dynamic smem limit once per process
 
-// Split-K flash-decode over the KV cache.
-cudaError_t launch_attention(Dt kvdt, AttnParams p, int nsplit, cudaStream_t s, bool pdl);
-int attention_nsplit(int max_len, int n_heads, int sms);
+// Split-K flash-decode over the KV cache for live lengths up to max_len (the
+// graph bucket's end): one thread-block cluster per head, partials merged over
+// distributed shared memory.  Writes out[h*dh].
+cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s, bool pdl);
+int attention_nsplit(int max_len, int n_heads, int sms);  // persistent pass split count
+int attention_splits(int max_len, int head_dim);         // cluster size of attn_decode_kernel for a bucket
 cudaError_t attention_prepare();
 
 // Weight materialisation: writes a logical reference-layout tensor into its

@@ -179,7 +179,8 @@ grt_status grt_trace_pass(grt_session* s, int32_t key, uint64_t* out, int64_t ca
   return guard([&] {
     int gr = 0, st = 0;
     s->s->device().sync_all();
-    auto v = s->owner->m->trace_pass(key, s->s->cache_config().bucket_size, s->s->device().replay(), &gr, &st);
+    auto v = s->owner->m->trace_pass(key, s->s->cache_config().bucket_size, s->s->device().replay(), &gr, &st,
+                                     s->s->cache_config().pass_impl);
     *grid = gr;
     *stride = st;
     for (int64_t i = 0; i < cap && i < static_cast<int64_t>(v.size()); ++i) out[i] = v[i];
@@ -323,8 +324,8 @@ grt_status grt_op_gemv(const void* w, int32_t w_dtype, const float* x, float* ou
     int dev = 0;
     grt::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     grt::cuda_check(grt::gemv_prepare(dev), "gemv_prepare");
-    grt::cuda_check(grt::launch_gemv(w_dtype == GRT_BF16 ? grt::Dt::BF16 : grt::Dt::F32, grt::NORM_NONE, grt::EPI_STORE, p,
-                                     static_cast<cudaStream_t>(stream), false, 0),
+    grt::cuda_check(grt::launch_gemv(w_dtype == GRT_BF16 ? grt::Dt::BF16 : grt::Dt::F32, grt::NORM_NONE,
+                                     grt::EPI_STORE, p, static_cast<cudaStream_t>(stream), false, 0),
                     "launch_gemv");
   });
 }
@@ -335,31 +336,20 @@ grt_status grt_op_attention(const float* q, const void* k, const void* v, int32_
     int dev = 0;
     grt::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     grt::cuda_check(grt::attention_prepare(), "attention_prepare");
-    const int nsplit = grt::attention_nsplit(len, n_heads, grt::num_sms(dev));
-    float* part = nullptr;
-    int* counters = nullptr;
-    grt::cuda_check(cudaMalloc(&part, static_cast<size_t>(n_heads) * nsplit * (head_dim + 2) * 4), "cudaMalloc");
-    grt::cuda_check(cudaMalloc(&counters, n_heads * 4), "cudaMalloc");
-    cudaMemset(counters, 0, n_heads * 4);
     grt::AttnParams a;
     a.q = q;
     a.k_cache = k;
     a.v_cache = v;
     a.out = out;
-    a.part = part;
-    a.counters = counters;
     a.len_fixed = len;
     a.n_heads = n_heads;
     a.head_dim = head_dim;
     a.max_seq = max_seq;
-    a.span_cap = ((len + nsplit - 1) / nsplit + 3) / 4 * 4;
     a.scale = scale;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    grt::cuda_check(grt::launch_attention(kv_dtype == GRT_BF16 ? grt::Dt::BF16 : grt::Dt::F32, a, nsplit, st, false),
+    grt::cuda_check(grt::launch_attention(kv_dtype == GRT_BF16 ? grt::Dt::BF16 : grt::Dt::F32, a, len, st, false),
                     "launch_attention");
     grt::cuda_check(cudaStreamSynchronize(st), "attention");
-    cudaFree(part);
-    cudaFree(counters);
   });
 }
 

@@ -43,6 +43,7 @@ struct DriverApi {
   CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
   CUresult (*LaunchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;
   CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
 };
 
 template <typename F>
@@ -67,6 +68,7 @@ const DriverApi& drv() {
       resolve("cuModuleGetFunction", api.ModuleGetFunction);
       resolve("cuLaunchKernelEx", api.LaunchKernelEx);
       resolve("cuGetErrorString", api.GetErrorString);
+      resolve("cuFuncSetAttribute", api.FuncSetAttribute);
     } catch (const Error& e) {
       err = e.what();
     }
@@ -121,6 +123,9 @@ JitModule::~JitModule() {
 CUfunction JitModule::fn(const char* name) const {
   CUfunction f = nullptr;
   cu_check(drv().ModuleGetFunction(&f, mod_, name), name);
+  // same L1/shared carveout as the GEMVs: PDL successors can co-reside without
+  // an SM reconfiguration
+  cu_check(drv().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100), name);
   return f;
 }
 

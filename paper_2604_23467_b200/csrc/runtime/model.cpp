@@ -311,6 +311,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   scratch_ = static_cast<float*>(arena_buf(V * 4, "scratch"));
   attn_part_ = static_cast<float*>(arena_buf(h * max_nsplit_ * (dh + 2) * 4, "attn_part"));
   attn_counters_ = static_cast<int*>(arena_buf(h * 4, "attn_counters"));
+
   rope_cos_ = static_cast<float*>(arena_buf(S * (dh / 2) * 4, "rope_cos"));
   rope_sin_ = static_cast<float*>(arena_buf(S * (dh / 2) * 4, "rope_sin"));
   ctrl_ = static_cast<GrtCtrl*>(arena_buf(sizeof(GrtCtrl), "ctrl"));
@@ -493,7 +494,41 @@ PassParams Model::pass_params(int key, int B) const {
   return pp;
 }
 
-std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* grid, int* stride) {
+std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* grid, int* stride, int impl) {
+  if (impl == 1) {
+    const int n_k = 5 * cfg_.n_layers + 1;
+    const size_t n = static_cast<size_t>(n_k) * OP_TRACE_CTAS * 4;
+    unsigned long long* buf = nullptr;
+    cuda_check(cudaMalloc(&buf, n * 8), "cudaMalloc trace");
+    op_trace_ = buf;
+    std::vector<KernelInvocation> plan;
+    try {
+      plan = build_plan(key, B, 1);
+    } catch (...) {
+      op_trace_ = nullptr;
+      cudaFree(buf);
+      throw;
+    }
+    op_trace_ = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "trace capture");
+    for (const KernelInvocation& inv : plan) cuda_check(inv.launch(s), inv.spec.name.c_str());
+    cuda_check(cudaStreamEndCapture(s, &g), "trace capture");
+    cuda_check(cudaGraphInstantiate(&ge, g, 0), "trace instantiate");
+    cuda_check(cudaGraphLaunch(ge, s), "trace launch");  // warm
+    cuda_check(cudaMemsetAsync(buf, 0, n * 8, s), "memset trace");
+    cuda_check(cudaGraphLaunch(ge, s), "trace launch");
+    cuda_check(cudaStreamSynchronize(s), "trace");
+    std::vector<uint64_t> out(n);
+    cuda_check(cudaMemcpy(out.data(), buf, n * 8, cudaMemcpyDeviceToHost), "trace copy");
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaFree(buf);
+    *grid = n_k;
+    *stride = OP_TRACE_CTAS * 4;
+    return out;
+  }
   PassParams pp = pass_params(key, B);
   *grid = num_sms(cfg_.device);
   *stride = cfg_.n_layers * PASS_TRACE_PER_LAYER + 8;  // + head start/end, kernel start, ready/waited counts
@@ -553,7 +588,11 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
     plan.push_back(std::move(inv));
     return plan;
   }
+  auto next_trace = [&]() -> unsigned long long* {
+    return op_trace_ ? op_trace_ + plan.size() * OP_TRACE_CTAS * 4 : nullptr;
+  };
   auto gemv = [&](const char* name, int epi, int nrm, GemvParams p, size_t w_bytes) {
+    p.trace = next_trace();
     KernelInvocation inv;
     inv.spec.name = name;
     inv.spec.op_class = OpClass::Static;
@@ -604,16 +643,17 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       a.span_cap = span_cap;
       a.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
       a.err = err;
+      a.trace = next_trace();
       KernelInvocation inv;
       inv.spec.name = "attention";
       inv.spec.flops = static_cast<int64_t>(h) * max_len * (4 * dh + 5);  // kernels.hpp:51
       inv.spec.bytes = 2LL * max_len * d * kvb;
       inv.bindings = {{L.k, static_cast<size_t>(h) * S * dh * kvb}, {L.v, static_cast<size_t>(h) * S * dh * kvb},
                       {q_, static_cast<size_t>(d) * 4}, {attn_, static_cast<size_t>(d) * 4}};
-      inv.launch = [kvdt, a, nsplit](cudaStream_t s) { return launch_attention(kvdt, a, nsplit, s, true); };
+      inv.launch = [kvdt, a, max_len](cudaStream_t s) { return launch_attention(kvdt, a, max_len, s, true); };
       plan.push_back(std::move(inv));
     }
-    {  // wo + residual
+    {  // (merge attention splits) + wo + residual
       GemvParams p;
       p.w = L.w_o;
       p.n_rows = d;

@@ -218,12 +218,17 @@ class Model {
   void declare_tensors();
   void init_weights();
   std::vector<KernelInvocation> build_plan(int key, int bucket_size, int impl);
+  unsigned long long* op_trace_ = nullptr;
+  // set only while building a traced per-op plan
   void attention_split(int key, int bucket_size, int* nsplit, int* span_cap) const;
 
  public:
   PassParams pass_params(int key, int bucket_size) const;
   // Runs one persistent pass with per-CTA %globaltimer phase stamps (profiling).
-  std::vector<uint64_t> trace_pass(int key, int bucket_size, cudaStream_t s, int* grid, int* stride);
+  // impl 0: per-CTA phase stamps of the persistent pass ([grid][stride]);
+  // impl 1: the per-op plan captured as a graph, [n_kernels][OP_TRACE_CTAS*4]
+  // stamps (start, released, operands ready, done) per CTA.
+  std::vector<uint64_t> trace_pass(int key, int bucket_size, cudaStream_t s, int* grid, int* stride, int impl = 0);
 
  private:
   void* arena_buf(size_t bytes, const char* what);

@@ -484,7 +484,10 @@ class Session:
     def trace_pass(self, key: int):
         """Per-CTA %globaltimer stamps of one persistent pass: array [grid, stride] (ns)."""
         import numpy as np
-        cap = 160 * (self.model.cfg.n_layers * 10 + 8)
+        if self.cache_cfg.pass_impl == 1:
+            cap = (5 * self.model.cfg.n_layers + 1) * 4096
+        else:
+            cap = 160 * (self.model.cfg.n_layers * 10 + 8)
         buf = (C.c_uint64 * cap)()
         gr, st = C.c_int32(), C.c_int32()
         _check(lib().grt_trace_pass(self._h, key, buf, cap, C.byref(gr), C.byref(st)))
