@@ -184,7 +184,7 @@ def main():
     ap.add_argument("--mode", default="hybrid")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--bucket", type=int, default=64)
-    ap.add_argument("--pass-impl", type=int, default=0, help="0 persistent single-kernel pass, 1 per-op kernels")
+    ap.add_argument("--pass-impl", type=int, default=1, help="1 per-op kernel graph (default), 0 persistent single-kernel pass")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--sweep", default="", help="comma list of prompt lengths for a TTFT sweep (extra key)")

@@ -113,7 +113,7 @@ typedef struct grt_cache_config {
   int32_t policy;      /* grt_eviction */
   int32_t bucket_size; /* KV positions per graph key; 1 = the reference's exact-length keys */
   int32_t batched_prefill; /* 1 = one batched prefill pass (TTFT path); 0 = token-by-token like the reference */
-  int32_t pass_impl;   /* 0 = persistent single-kernel static pass; 1 = per-op kernels (5 per layer) */
+  int32_t pass_impl;   /* 1 = per-op kernels, 5 per layer (default); 0 = persistent single-kernel static pass */
 } grt_cache_config;
 
 typedef struct grt_sample_params {

@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(const AttnPar
   const KT* V = reinterpret_cast<const KT*>(p.v_cache) + static_cast<int64_t>(head) * p.max_seq * dh + 4 * c;
   griddep_wait();
   op_stamp(p.trace, 1);
+  if (p.trigger == 0) griddep_launch_dependents();
 
   const int len = p.seq_len ? *p.seq_len : p.len_fixed;
   const float4 q4 = __ldcg(reinterpret_cast<const float4*>(p.q + head * dh) + c);
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(const AttnPar
       }
     }
   }
-  griddep_launch_dependents();
+  if (p.trigger == 1) griddep_launch_dependents();
   // the warp's m is uniform; l and acc are per row group: reduce over groups
   for (int o = G; o < 32; o <<= 1) {
     l += __shfl_xor_sync(0xffffffffu, l, o);
@@ -199,6 +201,7 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(const AttnPar
   }
   cluster_sync_all();  // keep every CTA's shared memory alive until rank 0 has read it
   op_stamp(p.trace, 3);
+  // (trigger 2: the successor launches when this CTA exits)
 }
 
 // Cluster size and passes for a bucket of max_len positions.
@@ -230,6 +233,11 @@ cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s,
   int ns, rounds;
   attn_shape(max_len, p.head_dim, &ns, &rounds);
   p.rounds = rounds;
+  static const int trig = [] {
+    const char* e = getenv("GRT_ATTN_TRIGGER");
+    return e ? atoi(e) : 1;
+  }();
+  p.trigger = trig;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_heads * ns);
   cfg.blockDim = dim3(ATTN_THREADS);

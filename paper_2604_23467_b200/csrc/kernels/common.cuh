@@ -86,10 +86,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 // one stamp per CTA (thread 0), only when tracing is on
+constexpr int OP_TRACE_STRIDE = 8;
 __device__ __forceinline__ void op_stamp(unsigned long long* tr, int i) {
   if (tr && threadIdx.x == 0) {
     const int cta = blockIdx.x + blockIdx.y * gridDim.x;
-    tr[cta * 4 + i] = gtimer();
+    tr[cta * OP_TRACE_STRIDE + i] = gtimer();
   }
 }
 

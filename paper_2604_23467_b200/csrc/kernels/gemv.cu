@@ -11,8 +11,11 @@
 //  * the whole first ring fill -- and the norm weights -- are loaded BEFORE
 //    griddepcontrol.wait, so with Programmatic Dependent Launch the kernel
 //    streams its weights while the previous kernel drains;
-//  * a CTA owns a contiguous range of row PAIRS (2p, 2p+1), dealt round-robin
-//    to its warps; pairs let RoPE (rotate-half) and SwiGLU finish in-warp;
+//  * a CTA owns a contiguous range of row PAIRS (2p, 2p+1); its (pair, k-chunk)
+//    tasks are dealt round-robin to the warps (equal bytes per warp), partial
+//    dot products are summed per pair in shared memory, and the epilogues run
+//    thread-parallel at the end; pairs let RoPE (rotate-half) and SwiGLU
+//    finish in one epilogue;
 //  * the QKV kernel prefetches this layer's K/V rows [0, seq_len) into L2 (and
 //    warms their TLB entries) for the attention kernel that follows.
 #include <cuda_bf16.h>
@@ -104,15 +107,21 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
   const int n_pairs = (p.n_rows + 1) >> 1;
   const int pair_begin = static_cast<int>(static_cast<int64_t>(blockIdx.x) * n_pairs / gridDim.x);
   const int pair_end = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * n_pairs / gridDim.x);
-  const int span = pair_end - pair_begin - warp;
-  const int n_tasks = span <= 0 ? 0 : (span + GEMV_WARPS - 1) / GEMV_WARPS * nch;
+  // The CTA's (pair, chunk) tasks are dealt round-robin to its warps: every
+  // warp streams the same bytes (+-1 chunk) and at any moment the 8 warps read
+  // 8 adjacent chunks.  Per-task dot products go to shared memory and are
+  // summed per pair in chunk order at the end (deterministic).
+  const int Tc = (pair_end - pair_begin) * nch;
+  const int n_tasks = Tc > warp ? (Tc - warp + GEMV_WARPS - 1) / GEMV_WARPS : 0;
+  float* part = xs + p.k;  // [pairs of this CTA][nch][2]
   uint64_t* mybar = bars[warp];
   const uint64_t pol = l2_evict_first_policy();
   const WT* Wt = reinterpret_cast<const WT*>(p.w);
 
   auto issue = [&](int i) {
-    const int pi = i / nch, c = i - pi * nch;
-    const int row0 = 2 * (pair_begin + warp + pi * GEMV_WARPS);
+    const int t = warp + i * GEMV_WARPS;
+    const int pl = t / nch, c = t - pl * nch;
+    const int row0 = 2 * (pair_begin + pl);
     const int c0 = c * CH;
     const int ce = min(CH, p.k - c0);
     const uint32_t bytes = static_cast<uint32_t>(ce) * sizeof(WT);
@@ -188,50 +197,50 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
   ea.d_model = p.d_model;
   ea.kv_bf16 = p.kv_bf16;
 
-  // Epilogues are deferred and run lane-parallel: lane j keeps the results of
-  // the warp's j-th pair (mod 32) and all lanes finish together, so the
-  // epilogue's own memory round trips (residual read, RoPE table) are paid
-  // once per 32 pairs instead of once per pair inside the streaming loop.
-  float acc_a = 0.0f, acc_b = 0.0f;
-  float my_a = 0.0f, my_b = 0.0f;
-  int my_pair = -1;
-  auto flush = [&]() {
-    if (my_pair >= 0) epilogue<EPI>(ea, my_pair, my_a, my_b, 2 * my_pair + 1 < p.n_rows);
-    my_pair = -1;
-  };
   for (int i = 0; i < n_tasks; ++i) {
     const int slot = i % S;
     mbar_wait(&mybar[slot], static_cast<uint32_t>((i / S) & 1));
-    const int pi = i / nch, c = i - pi * nch;
-    const int pair = pair_begin + warp + pi * GEMV_WARPS;
+    if (i == 0 && warp == 0) op_stamp(p.trace, 4);
+    const int t = warp + i * GEMV_WARPS;
+    const int c = t % nch;
     const int c0 = c * CH;
     const int ce = min(CH, p.k - c0);
     const uint8_t* st = mystage + slot * stageb;
+    float acc_a = 0.0f, acc_b = 0.0f;
     dot_chunk<WT>(st, st + rowb, xs, p.k, c0, ce, acc_a, acc_b);
     __syncwarp();
     if (lane == 0 && i + S < n_tasks) {
       fence_proxy_async_smem();
       issue(i + S);
     }
-    if (c == nch - 1) {
-      const float va = warp_sum(acc_a);
-      const float vb = warp_sum(acc_b);
-      if (lane == (pi & 31)) {
-        my_a = va;
-        my_b = vb;
-        my_pair = pair;
-      }
-      acc_a = 0.0f;
-      acc_b = 0.0f;
-      if ((pi & 31) == 31) flush();
+    acc_a = warp_sum(acc_a);
+    acc_b = warp_sum(acc_b);
+    if (lane == 0) {
+      part[2 * t] = acc_a;
+      part[2 * t + 1] = acc_b;
     }
   }
-  flush();
+  if (warp == 0) op_stamp(p.trace, 5);
+  consumer_sync();
+  // Epilogues run thread-parallel (one pair per thread): their own memory
+  // round trips (residual read, RoPE table) are paid once per CTA.
+  for (int pl = threadIdx.x; pl < pair_end - pair_begin; pl += CONSUMER_THREADS) {
+    float va = 0.0f, vb = 0.0f;
+    for (int c = 0; c < nch; ++c) {
+      va += part[2 * (pl * nch + c)];
+      vb += part[2 * (pl * nch + c) + 1];
+    }
+    const int pair = pair_begin + pl;
+    epilogue<EPI>(ea, pair, va, vb, 2 * pair + 1 < p.n_rows);
+  }
   if (p.trace) {
     consumer_sync();
     op_stamp(p.trace, 3);
   }
 }
+
+// pairs a CTA owns at most (sizes the per-task partial sums in shared memory)
+static int max_pairs_per_cta(int n_pairs, int grid) { return (n_pairs + grid - 1) / grid; }
 
 // ---------------------------------------------------------------------------
 // Host side
@@ -277,8 +286,8 @@ int gemv_max_stages() {
   return v;
 }
 
-static int stages_for(int device, int rowb, int k) {
-  const int budget = smem_optin(device) - kStaticSmemReserve - k * 4;
+static int stages_for(int device, int rowb, int k, int part_bytes) {
+  const int budget = smem_optin(device) - kStaticSmemReserve - k * 4 - part_bytes;
   const int s = budget / (GEMV_WARPS * 2 * rowb);
   return std::max(1, std::min(gemv_max_stages(), s));
 }
@@ -287,7 +296,7 @@ size_t gemv_smem_bytes(Dt wdt, int k) {
   int ch, nch, rowb, dev = 0;
   chunking(wdt, k, &ch, &nch, &rowb);
   cudaGetDevice(&dev);
-  return static_cast<size_t>(GEMV_WARPS) * stages_for(dev, rowb, k) * 2 * rowb + static_cast<size_t>(k) * sizeof(float);
+  return static_cast<size_t>(GEMV_WARPS) * stages_for(dev, rowb, k, 0) * 2 * rowb + static_cast<size_t>(k) * sizeof(float);
 }
 
 using GemvFn = void (*)(const GemvParams);
@@ -339,14 +348,18 @@ cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s,
   int dev = 0;
   cudaGetDevice(&dev);
   chunking(wdt, p.k, &p.ch, &p.nch, &p.rowb);
-  p.stages = stages_for(dev, p.rowb, p.k);
   const int n_pairs = (p.n_rows + 1) / 2;
   int grid = grid_ctas > 0 ? grid_ctas : num_sms(dev);
-  grid = std::max(1, std::min(grid, (n_pairs + GEMV_WARPS - 1) / GEMV_WARPS));
+  grid = std::max(1, std::min(grid, (n_pairs * p.nch + GEMV_WARPS - 1) / GEMV_WARPS));
+  const int part_bytes = max_pairs_per_cta(n_pairs, grid) * p.nch * 2 * 4;
+  p.stages = stages_for(dev, p.rowb, p.k, part_bytes);
+  if (static_cast<int64_t>(GEMV_WARPS) * p.stages * 2 * p.rowb + p.k * 4 + part_bytes >
+      smem_optin(dev) - kStaticSmemReserve)
+    return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(GEMV_THREADS);
-  cfg.dynamicSmemBytes = static_cast<size_t>(GEMV_WARPS) * p.stages * 2 * p.rowb + static_cast<size_t>(p.k) * 4;
+  cfg.dynamicSmemBytes = static_cast<size_t>(GEMV_WARPS) * p.stages * 2 * p.rowb + static_cast<size_t>(p.k) * 4 + part_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

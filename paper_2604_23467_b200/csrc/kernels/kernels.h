@@ -66,9 +66,11 @@ struct AttnParams {
   int* err = nullptr;
   unsigned long long* trace = nullptr;  // optional [cta][4] %globaltimer stamps (profiling)
   int rounds = 1;                // passes per CTA (set by the launcher)
+  int trigger = 1;               // when the successor may launch: 0 start, 1 after KV loads, 2 at exit
 };
-// Per-op trace stamps: 0 CTA start, 1 dependency released (griddepcontrol.wait),
-// 2 operands ready (activation loaded / KV rows loaded), 3 CTA done.
+// Per-op trace stamps (8 slots per CTA): 0 CTA start, 1 dependency released
+// (griddepcontrol.wait), 2 operands ready (activation loaded / KV rows loaded),
+// 3 CTA done, 4 first weight stage landed, 5 streaming loop done.
 constexpr int OP_TRACE_CTAS = 1024;  // stamp slots per kernel in a traced plan
 
 // Device error flags (bit set by kernels, read by the host after a run).

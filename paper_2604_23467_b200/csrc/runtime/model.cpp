@@ -497,7 +497,7 @@ PassParams Model::pass_params(int key, int B) const {
 std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* grid, int* stride, int impl) {
   if (impl == 1) {
     const int n_k = 5 * cfg_.n_layers + 1;
-    const size_t n = static_cast<size_t>(n_k) * OP_TRACE_CTAS * 4;
+    const size_t n = static_cast<size_t>(n_k) * OP_TRACE_CTAS * 8;
     unsigned long long* buf = nullptr;
     cuda_check(cudaMalloc(&buf, n * 8), "cudaMalloc trace");
     op_trace_ = buf;
@@ -526,7 +526,7 @@ std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* gri
     cudaGraphDestroy(g);
     cudaFree(buf);
     *grid = n_k;
-    *stride = OP_TRACE_CTAS * 4;
+    *stride = OP_TRACE_CTAS * 8;
     return out;
   }
   PassParams pp = pass_params(key, B);
@@ -589,7 +589,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
     return plan;
   }
   auto next_trace = [&]() -> unsigned long long* {
-    return op_trace_ ? op_trace_ + plan.size() * OP_TRACE_CTAS * 4 : nullptr;
+    return op_trace_ ? op_trace_ + plan.size() * OP_TRACE_CTAS * 8 : nullptr;
   };
   auto gemv = [&](const char* name, int epi, int nrm, GemvParams p, size_t w_bytes) {
     p.trace = next_trace();

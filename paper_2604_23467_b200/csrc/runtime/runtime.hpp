@@ -387,7 +387,7 @@ struct CacheConfig {
   EvictionPolicy policy = EvictionPolicy::LeastUsed;
   int bucket_size = 64;
   bool batched_prefill = false;
-  int pass_impl = 0;
+  int pass_impl = 1;  // 1: per-op kernel graph (default, fastest); 0: persistent single-kernel pass
   static CacheConfig from_c(const grt_cache_config& c);
 };
 

@@ -282,7 +282,7 @@ class CacheConfig:
     policy: EvictionPolicy = EvictionPolicy.LeastUsed
     bucket_size: int = 64
     batched_prefill: bool = False
-    pass_impl: int = 0  # 0 persistent single-kernel pass, 1 per-op kernels
+    pass_impl: int = 1  # 1 per-op kernel graph (default), 0 persistent single-kernel pass
 
     def _c(self) -> _CacheConfig:
         c = _CacheConfig()
@@ -485,7 +485,7 @@ class Session:
         """Per-CTA %globaltimer stamps of one persistent pass: array [grid, stride] (ns)."""
         import numpy as np
         if self.cache_cfg.pass_impl == 1:
-            cap = (5 * self.model.cfg.n_layers + 1) * 4096
+            cap = (5 * self.model.cfg.n_layers + 1) * 8192
         else:
             cap = 160 * (self.model.cfg.n_layers * 10 + 8)
         buf = (C.c_uint64 * cap)()

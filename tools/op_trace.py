@@ -24,7 +24,7 @@ s.run(g.GenerationRequest(prompt=list(range(1, 11)), gen_len=T - 10))
 key = (T + 63) // 64
 names = ["qkv", "attn", "wo", "gate_up", "down"] * layers + ["head"]
 for rep in range(2):
-    tr = s.trace_pass(key).astype(np.int64).reshape(len(names), -1, 4)
+    tr = s.trace_pass(key).astype(np.int64).reshape(len(names), -1, 8)
     rows = {}
     prev_end = None
     t0 = None
@@ -37,7 +37,12 @@ for rep in range(2):
         done = st[:, 3][st[:, 3] > 0]
         rdy = st[:, 2][st[:, 2] > 0]
         end = done.max()
-        r = rows.setdefault(nm, {k: [] for k in ("dep", "ready", "body", "tail", "eff", "ctas", "start_spread", "early")})
+        r = rows.setdefault(nm, {k: [] for k in ("dep", "ready", "body", "tail", "eff", "ctas", "start_spread", "early",
+                                                 "first", "loop", "epi")})
+        if (st[:, 4] > 0).any():
+            r["first"].append(np.median(st[:, 4] - st[:, 1]))  # first stage landed, relative to release
+            r["loop"].append(np.median(st[:, 5] - st[:, 2]))   # streaming loop after operands ready
+            r["epi"].append(np.median(st[:, 3] - st[:, 5]))    # deferred epilogue + CTA sync
         if prev_end is not None:
             r["dep"].append(rel - prev_end)
             r["early"].append(prev_end - np.median(st[:, 0]))
@@ -54,7 +59,7 @@ for rep in range(2):
         f = {k: (np.mean(v) / 1e3 if v else float('nan')) for k, v in r.items() if k != "ctas"}
         print(f"  {nm:8s} ctas={int(np.mean(r['ctas'])):4d} dep={f['dep']:6.2f} ready={f['ready']:6.2f} "
               f"body={f['body']:6.2f} tail={f['tail']:6.2f} eff={f['eff']:6.2f} start_spread={f['start_spread']:6.2f} "
-              f"early={f['early']:6.2f} us")
+              f"early={f['early']:6.2f} first={f['first']:6.2f} loop={f['loop']:6.2f} epi={f['epi']:6.2f} us")
 # per-CTA operand latency distribution of the attention kernels (last rep)
 i_att = [i for i, n in enumerate(names) if n == "attn"]
 lat = []
