@@ -184,6 +184,7 @@ def main():
     ap.add_argument("--mode", default="hybrid")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--bucket", type=int, default=64)
+    ap.add_argument("--batched-prefill", type=int, default=1, help="1: tcgen05 batched prefill (TTFT path); 0: token-by-token")
     ap.add_argument("--pass-impl", type=int, default=1, help="1 per-op kernel graph (default), 0 persistent single-kernel pass")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -205,7 +206,8 @@ def main():
     cfg = g.ModelConfig.llama2_7b(n_layers=args.layers, max_seq_len=max_seq, device=local)
     t_init = time.time()
     sess = g.Session(cfg, g.CacheConfig(bucket_size=args.bucket, warmup_lo=1, warmup_hi=10 ** 6 // args.bucket,
-                                        capacity=4096, pass_impl=args.pass_impl))
+                                        capacity=4096, pass_impl=args.pass_impl,
+                                        batched_prefill=bool(args.batched_prefill)))
     init_s = time.time() - t_init
     model = sess.model
     prompt = [(i * 7919 + 17) % 32000 for i in range(P)]

@@ -75,7 +75,11 @@ typedef enum grt_run_mode {
 typedef enum grt_eviction { GRT_EVICT_LEAST_USED = 0, GRT_EVICT_LRU = 1 } grt_eviction;
 
 /* Replaces graphrt::StepPath (pipeline.hpp:43). */
-typedef enum grt_step_path { GRT_PATH_REPLAYED = 0, GRT_PATH_EAGER_FALLBACK = 1 } grt_step_path;
+typedef enum grt_step_path {
+  GRT_PATH_REPLAYED = 0,
+  GRT_PATH_EAGER_FALLBACK = 1,
+  GRT_PATH_BATCHED = 2 /* extension: prompt token served by the batched (tcgen05) prefill */
+} grt_step_path;
 
 /* Replaces graphrt::SampleStrategy (kernels.hpp:105-115), extended with top-k/top-p. */
 typedef enum grt_sample_kind {
@@ -244,6 +248,11 @@ grt_status grt_op_gemv(const void* w, int32_t w_dtype, const float* x, float* ou
 grt_status grt_op_attention(const float* q, const void* k, const void* v, int32_t kv_dtype, float* out,
                             int32_t n_heads, int32_t head_dim, int32_t max_seq, int32_t len, float scale,
                             void* stream);
+/* Batched-prefill projection on the tensor cores (tcgen05/TMEM): out[p, m] =
+ * x[p, :] . W[m, :] for W bf16 [m_rows, k] and x bf16 [n_tok, k] (row-major,
+ * k % 64 == 0, n_tok <= 512); out fp32 [n_tok, m_rows]. */
+grt_status grt_op_prefill_gemm(const void* w, const void* x, float* out, int32_t m_rows, int32_t k, int32_t n_tok,
+                               void* stream);
 /* Samples from device logits; writes the token to *token_dev (device int32). */
 grt_status grt_op_sample(const float* logits, int32_t vocab, const grt_sample_params* p, uint64_t step,
                          double uniform, int32_t* token_dev, void* stream);

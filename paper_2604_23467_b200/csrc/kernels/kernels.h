@@ -145,6 +145,44 @@ int attention_nsplit(int max_len, int n_heads, int sms);  // persistent pass spl
 int attention_splits(int max_len, int head_dim);         // cluster size of attn_decode_kernel for a bucket
 cudaError_t attention_prepare();
 
+// ---- batched prefill (prefill_gemm.cu, prefill.cu) ------------------------------
+enum PgEpi : int {
+  PG_EPI_STORE = 0,     // out[n][m] = v
+  PG_EPI_RESID = 1,     // out[n][m] += v          (Wo, down: residual stream X)
+  PG_EPI_SWIGLU = 2,    // out_bf16[n][m/2] = silu(gate) * up   (rows 2j, 2j+1)
+  PG_EPI_QKV = 3,       // q -> q_out[n], k/v -> KV rows start_pos + n
+  PG_EPI_QKV_ROPE = 4,  // as QKV with rotate-half RoPE at position start_pos + n
+};
+struct PrefillGemmParams {
+  int M = 0, K = 0, P = 0;  // Y[P, M] = X[P, K] . W[M, K]^T  (bf16 operands, fp32 accumulate)
+  int ntile = 0, n_ntiles = 0, ksplit = 1, stages = 0;  // set by the launcher
+  int epi = PG_EPI_STORE;
+  float* out = nullptr;
+  void* out_bf16 = nullptr;
+  float* q_out = nullptr;  // [P][d_model]
+  void* k_cache = nullptr;
+  void* v_cache = nullptr;
+  const float* rope_cos = nullptr;
+  const float* rope_sin = nullptr;
+  int head_dim = 0, max_seq = 0, d_model = 0, start_pos = 0, kv_bf16 = 0;
+  float* part = nullptr;   // split-K scratch, prefill_gemm_part_floats()
+  int* counters = nullptr; // [m_tiles], zero-initialised, self-resetting
+};
+// tcgen05/TMEM GEMM; w: bf16 [M, K] row-major (the device weight layout), x:
+// bf16 [P, K] row-major (P <= 512), both K % 64 == 0.
+cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams p, cudaStream_t s, bool pdl);
+cudaError_t prefill_gemm_prepare();
+int prefill_gemm_ksplit(int M, int K, int sms);
+size_t prefill_gemm_part_floats(int M, int K, int P, int sms);
+constexpr int PREFILL_CHUNK = 512;  // tokens per batched pass (two 256-token TMEM accumulators)
+cudaError_t launch_prefill_embed(Dt wdt, const int* tokens, int start, int P, const void* emb, int d, float* X,
+                                 int vocab, int* err, cudaStream_t s);
+cudaError_t launch_prefill_rmsnorm(const float* X, int P, const float* gamma, float eps, int d, void* Xn,
+                                   cudaStream_t s);
+cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, const void* v, int start, int P, int d,
+                                     int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s);
+cudaError_t launch_prefill_handoff(const float* X_last, int d, float* x, int* seq_len, int len, cudaStream_t s);
+
 // Weight materialisation: writes a logical reference-layout tensor into its
 // device layout.  `src` (host-copied, fp32 or bf16 on device) or Philox init.
 struct MapDesc {

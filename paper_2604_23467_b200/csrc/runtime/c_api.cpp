@@ -330,6 +330,34 @@ grt_status grt_op_gemv(const void* w, int32_t w_dtype, const float* x, float* ou
   });
 }
 
+grt_status grt_op_prefill_gemm(const void* w, const void* x, float* out, int32_t m_rows, int32_t k, int32_t n_tok,
+                               void* stream) {
+  return guard([&] {
+    int dev = 0;
+    grt::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    grt::cuda_check(grt::prefill_gemm_prepare(), "prefill_gemm_prepare");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    grt::PrefillGemmParams p;
+    p.M = m_rows;
+    p.K = k;
+    p.P = n_tok;
+    p.epi = grt::PG_EPI_STORE;
+    p.out = out;
+    const size_t nf = grt::prefill_gemm_part_floats(m_rows, k, n_tok, grt::num_sms(dev));
+    if (nf) {
+      grt::cuda_check(cudaMalloc(&p.part, nf * sizeof(float)), "cudaMalloc");
+      grt::cuda_check(cudaMalloc(&p.counters, 4096 * sizeof(int)), "cudaMalloc");
+      grt::cuda_check(cudaMemsetAsync(p.counters, 0, 4096 * sizeof(int), st), "cudaMemset");
+    }
+    const cudaError_t e = grt::launch_prefill_gemm(w, x, p, st, false);
+    const cudaError_t e2 = cudaStreamSynchronize(st);
+    if (p.part) cudaFree(p.part);
+    if (p.counters) cudaFree(p.counters);
+    grt::cuda_check(e, "launch_prefill_gemm");
+    grt::cuda_check(e2, "prefill_gemm");
+  });
+}
+
 grt_status grt_op_attention(const float* q, const void* k, const void* v, int32_t kv_dtype, float* out, int32_t n_heads,
                             int32_t head_dim, int32_t max_seq, int32_t len, float scale, void* stream) {
   return guard([&] {

@@ -240,6 +240,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   cuda_check(gemv_prepare(cfg_.device), "gemv_prepare");
   cuda_check(attention_prepare(), "attention_prepare");
   cuda_check(decode_pass_prepare(cfg_.device), "decode_pass_prepare");
+  cuda_check(prefill_gemm_prepare(), "prefill_gemm_prepare");
 
   const int64_t d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
   const int64_t h = cfg_.n_heads, dh = cfg_.head_dim();
@@ -279,6 +280,23 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   acc(sizeof(GrtCtrl));
   acc(S * 4);
   acc(max_gen_ * 8);
+  const bool pf = supports_batched_prefill();
+  size_t pf_part = 0;
+  if (pf) {
+    const int64_t C = PREFILL_CHUNK;
+    const int64_t kmax = std::max(d, ff);
+    pf_part = std::max({prefill_gemm_part_floats(static_cast<int>(3 * d), static_cast<int>(d), PREFILL_CHUNK, sms),
+                        prefill_gemm_part_floats(static_cast<int>(d), static_cast<int>(d), PREFILL_CHUNK, sms),
+                        prefill_gemm_part_floats(static_cast<int>(up_rows), static_cast<int>(d), PREFILL_CHUNK, sms),
+                        prefill_gemm_part_floats(static_cast<int>(d), static_cast<int>(ff), PREFILL_CHUNK, sms)});
+    acc(C * d * 4);          // X
+    acc(C * d * 4);          // Q
+    acc(C * kmax * 2);       // Xn (bf16)
+    acc(C * d * 2);          // attention out (bf16)
+    acc(C * ff * 2);         // SwiGLU act (bf16)
+    acc(std::max<size_t>(pf_part, 1) * 4);
+    acc(4096 * 4);           // split-K tile counters
+  }
   sync_stride_ = decode_pass_sync_stride(static_cast<int>(h));
   acc(cfg_.n_layers * sizeof(PassLayer));
   acc(static_cast<size_t>(sync_ints()) * 4);
@@ -311,6 +329,16 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   scratch_ = static_cast<float*>(arena_buf(V * 4, "scratch"));
   attn_part_ = static_cast<float*>(arena_buf(h * max_nsplit_ * (dh + 2) * 4, "attn_part"));
   attn_counters_ = static_cast<int*>(arena_buf(h * 4, "attn_counters"));
+  if (pf) {
+    const int64_t C = PREFILL_CHUNK;
+    pf_X_ = static_cast<float*>(arena_buf(C * d * 4, "prefill_x"));
+    pf_Q_ = static_cast<float*>(arena_buf(C * d * 4, "prefill_q"));
+    pf_Xn_ = arena_buf(C * std::max(d, ff) * 2, "prefill_xn");
+    pf_A_ = arena_buf(C * d * 2, "prefill_attn");
+    pf_act_ = arena_buf(C * ff * 2, "prefill_act");
+    pf_part_ = static_cast<float*>(arena_buf(std::max<size_t>(pf_part, 1) * 4, "prefill_splitk"));
+    pf_cnt_ = static_cast<int*>(arena_buf(4096 * 4, "prefill_counters"));
+  }
 
   rope_cos_ = static_cast<float*>(arena_buf(S * (dh / 2) * 4, "rope_cos"));
   rope_sin_ = static_cast<float*>(arena_buf(S * (dh / 2) * 4, "rope_sin"));
@@ -451,6 +479,95 @@ uint64_t Model::decode_bytes(int length) const {
   b += L * 2 * static_cast<uint64_t>(length) * d * kvb;  // K,V read over [0, length)
   b += L * 2 * d * kvb;                              // K,V row write
   return b;
+}
+
+// ---------------------------------------------------------------------------
+// batched prefill
+
+bool Model::supports_batched_prefill() const {
+  return cfg_.llama() && cfg_.weight_dtype == GRT_BF16 && cfg_.d_model % 64 == 0 && cfg_.d_ff() % 64 == 0 &&
+         cfg_.head_dim() % 4 == 0 && (cfg_.head_dim() / 4) <= 32;
+}
+
+void Model::prefill_batched(int p, cudaStream_t s) {
+  if (!supports_batched_prefill()) raise(GRT_Unsupported, "batched prefill needs the LLaMA arch with bf16 weights");
+  if (p < 1 || p > cfg_.max_seq_len) raise(GRT_PromptTooLong, "batched prefill length out of range");
+  const int d = cfg_.d_model, ff = cfg_.d_ff(), h = cfg_.n_heads, dh = cfg_.head_dim(), S = cfg_.max_seq_len;
+  const Dt kvdt = cfg_.kv_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
+  const float scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
+  int last_P = 0;
+  for (int start = 0; start < p; start += PREFILL_CHUNK) {
+    const int P = std::min(PREFILL_CHUNK, p - start);
+    last_P = P;
+    cuda_check(launch_prefill_embed(Dt::BF16, tokens_, start, P, emb_, d, pf_X_, cfg_.vocab_size, &ctrl_->err, s),
+               "prefill embed");
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+      const LayerBuffers& L = layers_[l];
+      cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln1_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm1");
+      PrefillGemmParams q;
+      q.M = 3 * d;
+      q.K = d;
+      q.P = P;
+      q.epi = PG_EPI_QKV_ROPE;
+      q.q_out = pf_Q_;
+      q.k_cache = L.k;
+      q.v_cache = L.v;
+      q.rope_cos = rope_cos_;
+      q.rope_sin = rope_sin_;
+      q.head_dim = dh;
+      q.max_seq = S;
+      q.d_model = d;
+      q.start_pos = start;
+      q.kv_bf16 = kvdt == Dt::BF16;
+      q.part = pf_part_;
+      q.counters = pf_cnt_;
+      cuda_check(launch_prefill_gemm(L.w_qkv, pf_Xn_, q, s, false), "prefill qkv");
+      cuda_check(launch_prefill_attention(kvdt, pf_Q_, L.k, L.v, start, P, d, h, dh, S, scale, pf_A_, s),
+                 "prefill attention");
+      PrefillGemmParams o;
+      o.M = d;
+      o.K = d;
+      o.P = P;
+      o.epi = PG_EPI_RESID;
+      o.out = pf_X_;
+      o.part = pf_part_;
+      o.counters = pf_cnt_;
+      cuda_check(launch_prefill_gemm(L.w_o, pf_A_, o, s, false), "prefill wo");
+      cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln2_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm2");
+      PrefillGemmParams u;
+      u.M = 2 * ff;
+      u.K = d;
+      u.P = P;
+      u.epi = PG_EPI_SWIGLU;
+      u.out_bf16 = pf_act_;
+      u.part = pf_part_;
+      u.counters = pf_cnt_;
+      cuda_check(launch_prefill_gemm(L.w_up, pf_Xn_, u, s, false), "prefill gate_up");
+      PrefillGemmParams w2;
+      w2.M = d;
+      w2.K = ff;
+      w2.P = P;
+      w2.epi = PG_EPI_RESID;
+      w2.out = pf_X_;
+      w2.part = pf_part_;
+      w2.counters = pf_cnt_;
+      cuda_check(launch_prefill_gemm(L.w_down, pf_act_, w2, s, false), "prefill down");
+    }
+  }
+  // hand off to the decode state: last token's residual row, seq_len = p; then
+  // ln_f + LM head for that row only (the only logits the sampler consumes)
+  cuda_check(launch_prefill_handoff(pf_X_ + static_cast<int64_t>(last_P - 1) * d, d, x_, &ctrl_->seq_len, p, s),
+             "prefill handoff");
+  GemvParams hp;
+  hp.w = head_;
+  hp.n_rows = cfg_.vocab_size;
+  hp.k = d;
+  hp.x = x_;
+  hp.gamma = lnf_g_;
+  hp.beta = lnf_b_;
+  hp.eps = cfg_.norm_eps;
+  hp.out = logits_;
+  cuda_check(launch_gemv(Dt::BF16, NORM_RMS, EPI_STORE, hp, s, false, 0), "prefill head");
 }
 
 // ---------------------------------------------------------------------------

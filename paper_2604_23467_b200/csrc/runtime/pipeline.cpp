@@ -421,10 +421,17 @@ GenerationResult Session::run(const GenerationRequest& req) {
 
   const double t0 = now_us();
   cuda_check(cudaEventRecord(ev0, s), "event");
-  for (int j = 1; j <= p; ++j) {
-    channel.send_request({j, Model::key_of(j, B), pol.fuse_dynamic});
-    channel.send_response(serve(channel.take_request(), cc_.prefill_uses_graphs, pol));
-    res.prefill_paths.push_back(channel.take_response().path);
+  if (cc_.batched_prefill && model_->supports_batched_prefill()) {
+    // all p prompt tokens through each layer at once (tcgen05 GEMMs); leaves
+    // the device exactly where p single-token passes would
+    model_->prefill_batched(p, s);
+    res.prefill_paths.assign(p, StepPath::Batched);
+  } else {
+    for (int j = 1; j <= p; ++j) {
+      channel.send_request({j, Model::key_of(j, B), pol.fuse_dynamic});
+      channel.send_response(serve(channel.take_request(), cc_.prefill_uses_graphs, pol));
+      res.prefill_paths.push_back(channel.take_response().path);
+    }
   }
   cuda_check(cudaEventRecord(ev1, s), "event");
 
@@ -523,6 +530,18 @@ void Session::prefill(const std::vector<int>& ids) {
   if (ids.empty()) raise(GRT_EmptyPrompt, "prefill: prompt is empty");
   if (static_cast<int>(ids.size()) > model_->config().max_seq_len)
     raise(GRT_PromptTooLong, "prefill: prompt length " + std::to_string(ids.size()) + " exceeds max_seq_len");
+  if (cc_.batched_prefill && cur_len_ == 0 && model_->supports_batched_prefill()) {
+    for (int t : ids)
+      if (t < 0 || t >= model_->config().vocab_size) raise(GRT_TokenOutOfRange, "token id " + std::to_string(t));
+    cudaStream_t s = dev_->replay();
+    cuda_check(cudaMemcpyAsync(model_->tokens_dev(), ids.data(), ids.size() * sizeof(int), cudaMemcpyHostToDevice, s),
+               "prompt");
+    model_->prefill_batched(static_cast<int>(ids.size()), s);
+    cuda_check(cudaStreamSynchronize(s), "prefill");
+    cur_len_ = static_cast<int>(ids.size());
+    check_device_errors();
+    return;
+  }
   for (int t : ids) step(t);
 }
 

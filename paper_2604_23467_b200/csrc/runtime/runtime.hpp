@@ -208,6 +208,14 @@ class Model {
   int kv_elem_bytes() const { return cfg_.kv_dtype == GRT_BF16 ? 2 : 4; }
   const std::set<const void*>& buffer_set() const { return buffers_; }
   int sync_ints() const { return decode_pass_sync_ints(cfg_.n_layers, cfg_.n_heads); }
+
+  // Batched prefill (LLaMA arch, bf16 weights): tokens_dev()[0, p) pass through
+  // each layer together -- tcgen05 GEMMs for the projections, one causal
+  // attention launch -- in chunks of PREFILL_CHUNK tokens; leaves the device in
+  // the state p token-by-token passes would (KV rows [0, p), seq_len = p,
+  // residual/logits of the last token).  Enqueued on `s`, no host sync.
+  bool supports_batched_prefill() const;
+  void prefill_batched(int p, cudaStream_t s);
   void reset_pass_sync() {
     cudaMemset(pass_sync_, 0, static_cast<size_t>(sync_ints()) * 4);
     cudaMemset(&ctrl_->err, 0, sizeof(int));
@@ -242,6 +250,10 @@ class Model {
   float *x_ = nullptr, *q_ = nullptr, *attn_ = nullptr, *act_ = nullptr, *logits_ = nullptr;
   float *attn_part_ = nullptr, *rope_cos_ = nullptr, *rope_sin_ = nullptr, *scratch_ = nullptr;
   int* attn_counters_ = nullptr;
+  // batched-prefill workspace (allocated only when supported)
+  float *pf_X_ = nullptr, *pf_Q_ = nullptr, *pf_part_ = nullptr;
+  void *pf_Xn_ = nullptr, *pf_A_ = nullptr, *pf_act_ = nullptr;
+  int* pf_cnt_ = nullptr;
   GrtCtrl* ctrl_ = nullptr;
   int* tokens_ = nullptr;
   double* uniforms_ = nullptr;
@@ -352,7 +364,7 @@ struct ModePolicy {
 };
 ModePolicy policy_for(RunMode m) noexcept;
 
-enum class StepPath { Replayed = GRT_PATH_REPLAYED, EagerFallback = GRT_PATH_EAGER_FALLBACK };
+enum class StepPath { Replayed = GRT_PATH_REPLAYED, EagerFallback = GRT_PATH_EAGER_FALLBACK, Batched = GRT_PATH_BATCHED };
 
 struct StepRequest {
   int step_index = 0;

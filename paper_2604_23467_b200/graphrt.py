@@ -90,6 +90,7 @@ def mode_from_name(name: str) -> RunMode:
 class StepPath(enum.IntEnum):
     Replayed = 0
     EagerFallback = 1
+    Batched = 2  # prompt token served by the batched (tcgen05) prefill
 
 
 class EvictionPolicy(enum.IntEnum):
@@ -154,7 +155,7 @@ EXPORTS = [
     "grt_model_upload", "grt_model_download", "grt_model_weight_bytes", "grt_model_decode_bytes",
     "grt_session_create", "grt_session_destroy", "grt_generate", "grt_cache_stats_get", "grt_session_counters",
     "grt_reset", "grt_step", "grt_prefill", "grt_cur_len", "grt_get_logits", "grt_get_kv_row", "grt_sample",
-    "grt_sampler_reset", "grt_op_gemv", "grt_op_attention", "grt_op_sample",
+    "grt_sampler_reset", "grt_op_gemv", "grt_op_attention", "grt_op_sample", "grt_op_prefill_gemm",
     "grt_graph_cache_create", "grt_graph_cache_destroy", "grt_graph_cache_lookup", "grt_graph_cache_insert",
     "grt_graph_cache_warmup", "grt_graph_cache_begin_session", "grt_graph_cache_release_inactive",
     "grt_graph_cache_query", "grt_profile_plan", "grt_trace_pass",
@@ -202,6 +203,7 @@ def lib():
         L.grt_sample.argtypes = [vp, C.POINTER(_SampleParams), C.POINTER(C.c_int32)]
         L.grt_sampler_reset.argtypes = [vp, C.c_uint64]
         L.grt_op_gemv.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, C.c_int32, vp]
+        L.grt_op_prefill_gemm.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp]
         L.grt_op_attention.argtypes = [vp, vp, vp, C.c_int32, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                        C.c_float, vp]
         L.grt_op_sample.argtypes = [vp, C.c_int32, C.POINTER(_SampleParams), C.c_uint64, C.c_double, vp, vp]
@@ -603,6 +605,11 @@ def run_inference(model_cfg: ModelConfig, cache_cfg: CacheConfig, req: Generatio
 
 def op_gemv(w_ptr: int, w_dtype: int, x_ptr: int, out_ptr: int, n: int, k: int, stream: int = 0):
     _check(lib().grt_op_gemv(w_ptr, w_dtype, x_ptr, out_ptr, n, k, stream or None))
+
+
+def op_prefill_gemm(w_ptr: int, x_ptr: int, out_ptr: int, m_rows: int, k: int, n_tok: int, stream: int = 0):
+    """tcgen05 prefill GEMM: out[n_tok, m_rows] = x[n_tok, k] . W[m_rows, k]^T (bf16 in, fp32 out)."""
+    _check(lib().grt_op_prefill_gemm(w_ptr, x_ptr, out_ptr, m_rows, k, n_tok, stream or None))
 
 
 def op_attention(q_ptr, k_ptr, v_ptr, kv_dtype, out_ptr, n_heads, head_dim, max_seq, length, scale, stream=0):

@@ -319,3 +319,75 @@ def test_step_api_errors():
     with pytest.raises(g.Error) as e:
         s.step(1)
     assert e.value.code == g.Errc.ShapeMismatch  # position outside the learned table
+
+
+# ------------------------------------------------------------ batched prefill
+
+@pytest.mark.parametrize("m,k,p", [(128, 64, 16), (256, 128, 10), (12288, 4096, 10), (4096, 4096, 200),
+                                   (22016, 4096, 500), (4096, 11008, 37), (192, 64, 300), (4096, 4096, 512)])
+def test_prefill_gemm_tcgen05_matches_fp64(m, k, p):
+    """tcgen05/TMEM GEMM (bf16 operands, fp32 accumulate) vs an fp64 product of
+    the same bf16 values; covers split-K (small m), two N tiles (p > 256),
+    ragged token counts and partial M tiles."""
+    rs = np.random.RandomState(m + k + p)
+    w = bf16_round(rs.uniform(-0.1, 0.1, (m, k)).astype(np.float32))
+    x = bf16_round(rs.randn(p, k).astype(np.float32))
+    wd = torch.from_numpy(bf16_bits(w).view(np.int16)).cuda()
+    xd = torch.from_numpy(bf16_bits(x).view(np.int16)).cuda()
+    out = torch.full((p, m), float("nan"), dtype=torch.float32, device="cuda")
+    g.op_prefill_gemm(wd.data_ptr(), xd.data_ptr(), out.data_ptr(), m, k, p)
+    torch.cuda.synchronize()
+    want = x.astype(np.float64) @ w.astype(np.float64).T
+    scale = np.abs(x).astype(np.float64) @ np.abs(w).astype(np.float64).T
+    err = np.abs(out.cpu().numpy() - want) / np.maximum(scale, 1e-30)
+    assert np.isfinite(out.cpu().numpy()).all()
+    assert err.max() < 1e-5, err.max()
+
+
+def _llama_pair(kw, prompt_len, batched):
+    import pyoracle as po
+    o = po.OracleModel(arch=po.ARCH_LLAMA, weight_dtype=po.BF16, kv_dtype=po.BF16, init=po.INIT_PHILOX,
+                       d_ff=kw.pop("d_ff"), **kw)
+    s = g.Session(g.ModelConfig(arch=g.ARCH_LLAMA, weight_dtype=g.BF16, kv_dtype=g.BF16, init=g.INIT_PHILOX,
+                                d_ff_=o.cfg.d_ff, **kw), g.CacheConfig(bucket_size=64, batched_prefill=batched))
+    return o, s
+
+
+@pytest.mark.parametrize("kw,plen", [
+    (dict(n_layers=2, d_model=64, n_heads=4, vocab_size=256, max_seq_len=640, seed=3, d_ff=192), 6),
+    (dict(n_layers=2, d_model=128, n_heads=2, vocab_size=512, max_seq_len=640, seed=5, d_ff=320), 300),
+    (dict(n_layers=2, d_model=128, n_heads=2, vocab_size=512, max_seq_len=640, seed=5, d_ff=320), 600),
+])
+def test_batched_prefill_matches_oracle(kw, plen):
+    """Batched (tcgen05) prefill: last-token logits vs the oracle's token-by-token
+    prefill (bf16 activations into the GEMMs; tolerance 2e-2), then decoding
+    continues from the handed-off state (incremental == restart, model_test.cpp:129-146)."""
+    import pyoracle as po
+    o, s = _llama_pair(dict(kw), plen, True)
+    prompt = po.make_prompt(42, plen, kw["vocab_size"])
+    o.prefill(prompt)
+    s.prefill(prompt)
+    err = float(np.abs(s.logits() - o.logits()).max())
+    assert err <= 2e-2, err
+    # two more single-token steps on top of the batched state
+    for t in (5, 7):
+        o.step(t)
+        s.step(t)
+        err = float(np.abs(s.logits() - o.logits()).max())
+        assert err <= 2e-2, err
+
+
+def test_batched_prefill_run_tokens_match_token_by_token():
+    """Session.run with batched prefill reproduces the token-by-token run's greedy
+    stream wherever the logit margins allow (same weights, same prompt)."""
+    kw = dict(arch=g.ARCH_LLAMA, n_layers=2, d_model=128, n_heads=2, vocab_size=512, max_seq_len=256, seed=9,
+              d_ff_=320, weight_dtype=g.BF16, kv_dtype=g.BF16, init=g.INIT_PHILOX)
+    import pyoracle as po
+    prompt = po.make_prompt(42, 40, 512)
+    ra = g.Session(g.ModelConfig(**kw), g.CacheConfig(bucket_size=32, batched_prefill=True)).run(
+        g.GenerationRequest(prompt=prompt, gen_len=16))
+    rb = g.Session(g.ModelConfig(**kw), g.CacheConfig(bucket_size=32, batched_prefill=False)).run(
+        g.GenerationRequest(prompt=prompt, gen_len=16))
+    assert ra.prefill_paths == [g.StepPath.Batched] * 40
+    agree = sum(1 for a, b in zip(ra.tokens, rb.tokens) if a == b)
+    assert ra.tokens[:4] == rb.tokens[:4] and agree >= 12, (ra.tokens, rb.tokens)
