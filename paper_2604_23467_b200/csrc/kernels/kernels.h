@@ -155,7 +155,7 @@ enum PgEpi : int {
 };
 struct PrefillGemmParams {
   int M = 0, K = 0, P = 0;  // Y[P, M] = X[P, K] . W[M, K]^T  (bf16 operands, fp32 accumulate)
-  int ntile = 0, n_ntiles = 0, ksplit = 1, stages = 0;  // set by the launcher
+  int ntile = 0, n_ntiles = 0, ksplit = 1, stages = 0, kbox = 1;  // set by the launcher
   int epi = PG_EPI_STORE;
   float* out = nullptr;
   void* out_bf16 = nullptr;

@@ -32,25 +32,43 @@ __global__ void prefill_embed_kernel(const int* tokens, int start, int P, const 
   for (int j = threadIdx.x; j < d; j += blockDim.x) X[static_cast<int64_t>(i) * d + j] = to_f32(row[j]);
 }
 
-// Xn[i] = bf16(rmsnorm(X[i]) * gamma): ss = sum x^2 ; inv = 1/sqrt(ss/d + eps)
-__global__ void prefill_rmsnorm_kernel(const float* X, const float* gamma, float eps, int d, __nv_bfloat16* Xn) {
+// Xn[i] = bf16(rmsnorm(X[i]) * gamma): ss = sum x^2 ; inv = 1/sqrt(ss/d + eps).
+// The row is pulled into registers with independent 16-byte loads (d <= 16 KB).
+constexpr int PN_THREADS = 256, PN_MAXV = 16;  // d <= 16384
+__global__ void __launch_bounds__(PN_THREADS) prefill_rmsnorm_kernel(const float* X, const float* gamma, float eps, int d,
+                                                                     __nv_bfloat16* Xn) {
   __shared__ float red[32];
   const int i = blockIdx.x;
-  const float* x = X + static_cast<int64_t>(i) * d;
+  const float4* x = reinterpret_cast<const float4*>(X + static_cast<int64_t>(i) * d);
+  const int n4 = d >> 2;
+  float4 v[PN_MAXV], g[PN_MAXV];
   float ss = 0.0f;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) ss += x[j] * x[j];
+#pragma unroll
+  for (int u = 0; u < PN_MAXV; ++u) {
+    const int j = threadIdx.x + u * PN_THREADS;
+    v[u] = j < n4 ? x[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    g[u] = j < n4 ? reinterpret_cast<const float4*>(gamma)[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < PN_MAXV; ++u) ss += v[u].x * v[u].x + v[u].y * v[u].y + v[u].z * v[u].z + v[u].w * v[u].w;
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   if (threadIdx.x < 32) {
-    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+    float t = threadIdx.x < (PN_THREADS >> 5) ? red[threadIdx.x] : 0.0f;
     t = warp_sum(t);
     if (threadIdx.x == 0) red[0] = t;
   }
   __syncthreads();
   const float inv = 1.0f / sqrtf(red[0] / static_cast<float>(d) + eps);
-  for (int j = threadIdx.x; j < d; j += blockDim.x)
-    Xn[static_cast<int64_t>(i) * d + j] = __float2bfloat16_rn(x[j] * inv * gamma[j]);
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(Xn + static_cast<int64_t>(i) * d);
+#pragma unroll
+  for (int u = 0; u < PN_MAXV; ++u) {
+    const int j = threadIdx.x + u * PN_THREADS;
+    if (j >= n4) continue;
+    o[2 * j] = __floats2bfloat162_rn(v[u].x * inv * g[u].x, v[u].y * inv * g[u].y);
+    o[2 * j + 1] = __floats2bfloat162_rn(v[u].z * inv * g[u].z, v[u].w * inv * g[u].w);
+  }
 }
 
 template <typename KT>
@@ -65,74 +83,124 @@ __device__ __forceinline__ float4 ld4<__nv_bfloat16>(const __nv_bfloat16* p) {
   return make_float4(bf16lo(u.x), bf16hi(u.x), bf16lo(u.y), bf16hi(u.y));
 }
 
-// One warp per (query, head); G = dh/4 lanes per key row, RPW = 32/G rows per
-// load, 8 row groups in flight, online softmax.  Output bf16 (Wo GEMM operand).
-constexpr int PA_WARPS = 4;
-constexpr int PA_UNROLL = 8;
-template <typename KT>
-__global__ void __launch_bounds__(PA_WARPS * 32)
-    prefill_attn_kernel(const float* Q, const void* k_cache, const void* v_cache, int start, int P, int d, int dh,
+// Causal prefill attention, flash style on CUDA cores: one CTA = one head x a
+// block of PA_QB queries; key/value tiles of PA_KB rows are staged in shared
+// memory once and reused by all PA_QB queries (instead of every query reading
+// every key row from L2).  256 threads; thread (tq, tk) owns queries 4tq..4tq+3
+// and keys tk + 16r (scores) / dims tk*DH/16.. (output), so every shared-memory
+// load feeds 2-4 FMAs.  Online softmax per query row across key tiles.
+constexpr int PA_QB = 64, PA_KB = 64, PA_THREADS = 256;
+
+template <typename KT, int DH>
+__global__ void __launch_bounds__(PA_THREADS)
+    prefill_attn_kernel(const float* Q, const void* k_cache, const void* v_cache, int start, int P, int d,
                         int max_seq, float scale, __nv_bfloat16* out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * PA_WARPS + warp;
-  const int head = blockIdx.y;
-  if (i >= P) return;
-  const int G = dh >> 2, RPW = 32 / G;
-  const int g = lane / G, c = lane - g * G;
-  const int last = start + i;  // keys [0, last]
-  const KT* K = reinterpret_cast<const KT*>(k_cache) + static_cast<int64_t>(head) * max_seq * dh + 4 * c;
-  const KT* V = reinterpret_cast<const KT*>(v_cache) + static_cast<int64_t>(head) * max_seq * dh + 4 * c;
-  const float4 q4 = *reinterpret_cast<const float4*>(Q + static_cast<int64_t>(i) * d + head * dh + 4 * c);
-  float m = -INFINITY, l = 0.0f;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int jb = 0; jb <= last; jb += RPW * PA_UNROLL) {
-    float4 kv[PA_UNROLL], vv[PA_UNROLL];
+  extern __shared__ __align__(16) float sm[];
+  constexpr int KS = DH + 1;   // odd row stride: conflict-free column reads of K
+  constexpr int DPT = DH / 16; // output dims per thread
+  float* Qs = sm;                       // [QB][DH]
+  float* Ks = Qs + PA_QB * DH;          // [KB][DH+1]
+  float* Vs = Ks + PA_KB * KS;          // [KB][DH]
+  float* Ps = Vs + PA_KB * DH;          // [QB][KB+1]
+  const int head = blockIdx.y, q0 = blockIdx.x * PA_QB;
+  const int t = threadIdx.x, tq = t >> 4, tk = t & 15;
+  const int nq = min(PA_QB, P - q0);
+  const KT* Kh = reinterpret_cast<const KT*>(k_cache) + static_cast<int64_t>(head) * max_seq * DH;
+  const KT* Vh = reinterpret_cast<const KT*>(v_cache) + static_cast<int64_t>(head) * max_seq * DH;
+
+  for (int e = t; e < PA_QB * DH; e += PA_THREADS) {
+    const int qi = e / DH, dd = e - qi * DH;
+    Qs[e] = qi < nq ? Q[static_cast<int64_t>(q0 + qi) * d + head * DH + dd] : 0.0f;
+  }
+  float m[4], l[4], o[4][DPT];
 #pragma unroll
-    for (int u = 0; u < PA_UNROLL; ++u) {
-      const int j = min(jb + u * RPW + g, last);
-      kv[u] = ld4<KT>(K + static_cast<int64_t>(j) * dh);
-      vv[u] = ld4<KT>(V + static_cast<int64_t>(j) * dh);
+  for (int r = 0; r < 4; ++r) {
+    m[r] = -INFINITY;
+    l[r] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) o[r][j] = 0.0f;
+  }
+  const int last_pos = start + q0 + nq - 1;
+  for (int kb = 0; kb <= last_pos; kb += PA_KB) {
+    __syncthreads();  // previous tile fully consumed (and Qs written, first time)
+    for (int e = t; e < PA_KB * DH; e += PA_THREADS) {
+      const int kk = e / DH, dd = e - kk * DH;
+      const int pos = min(kb + kk, last_pos);
+      Ks[kk * KS + dd] = to_f32(Kh[static_cast<int64_t>(pos) * DH + dd]);
+      Vs[kk * DH + dd] = to_f32(Vh[static_cast<int64_t>(pos) * DH + dd]);
     }
-    float sc[PA_UNROLL];
-    float mr = -INFINITY;
+    __syncthreads();
+    // scores S[4 queries][4 keys]
+    float sc[4][4];
 #pragma unroll
-    for (int u = 0; u < PA_UNROLL; ++u) {
-      float sv = q4.x * kv[u].x + q4.y * kv[u].y + q4.z * kv[u].z + q4.w * kv[u].w;
-      for (int o = G >> 1; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
-      sc[u] = jb + u * RPW + g <= last ? sv * scale : -INFINITY;
-      mr = fmaxf(mr, sc[u]);
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sc[r][c] = 0.0f;
+#pragma unroll 8
+    for (int dd = 0; dd < DH; ++dd) {
+      float qv[4], kv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) qv[r] = Qs[(4 * tq + r) * DH + dd];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) kv[c] = Ks[(tk + 16 * c) * KS + dd];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sc[r][c] = fmaf(qv[r], kv[c], sc[r][c]);
     }
-    for (int o = G; o < 32; o <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
-    const float mn = fmaxf(m, mr);
-    const float f = m == -INFINITY ? 0.0f : __expf(m - mn);
-    l *= f;
-    acc = make_float4(acc.x * f, acc.y * f, acc.z * f, acc.w * f);
-    m = mn;
+    // scale, causal mask, online softmax (a query row lives in 16 lanes)
 #pragma unroll
-    for (int u = 0; u < PA_UNROLL; ++u) {
-      if (sc[u] == -INFINITY) continue;
-      const float e = __expf(sc[u] - m);
-      l += e;
-      acc.x = fmaf(e, vv[u].x, acc.x);
-      acc.y = fmaf(e, vv[u].y, acc.y);
-      acc.z = fmaf(e, vv[u].z, acc.z);
-      acc.w = fmaf(e, vv[u].w, acc.w);
+    for (int r = 0; r < 4; ++r) {
+      const int qpos = start + q0 + 4 * tq + r;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int kpos = kb + tk + 16 * c;
+        sc[r][c] = (kpos <= qpos) ? sc[r][c] * scale : -INFINITY;
+        mx = fmaxf(mx, sc[r][c]);
+      }
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const float mn = fmaxf(m[r], mx);
+      const float f = (m[r] == -INFINITY || mn == -INFINITY) ? 0.0f : __expf(m[r] - mn);
+      float rs = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float pv = sc[r][c] == -INFINITY ? 0.0f : __expf(sc[r][c] - mn);
+        Ps[(4 * tq + r) * (PA_KB + 1) + tk + 16 * c] = pv;
+        rs += pv;
+      }
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, off);
+      l[r] = l[r] * f + rs;
+      m[r] = mn;
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) o[r][j] *= f;
+    }
+    __syncwarp();  // Ps rows of this thread's queries are written by its own half-warp
+    // O += P V
+#pragma unroll 4
+    for (int kk = 0; kk < PA_KB; ++kk) {
+      float pv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) pv[r] = Ps[(4 * tq + r) * (PA_KB + 1) + kk];
+      float vv[DPT];
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) vv[j] = Vs[kk * DH + tk * DPT + j];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) o[r][j] = fmaf(pv[r], vv[j], o[r][j]);
     }
   }
-  for (int o = G; o < 32; o <<= 1) {
-    l += __shfl_xor_sync(0xffffffffu, l, o);
-    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
-    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
-  }
-  if (lane < G) {
-    const float inv = 1.0f / l;
-    __nv_bfloat16* o = out + static_cast<int64_t>(i) * d + head * dh + 4 * c;
-    o[0] = __float2bfloat16_rn(acc.x * inv);
-    o[1] = __float2bfloat16_rn(acc.y * inv);
-    o[2] = __float2bfloat16_rn(acc.z * inv);
-    o[3] = __float2bfloat16_rn(acc.w * inv);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int qi = 4 * tq + r;
+    if (qi >= nq) continue;
+    const float inv = 1.0f / l[r];
+    __nv_bfloat16* op = out + static_cast<int64_t>(q0 + qi) * d + head * DH + tk * DPT;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) op[j] = __float2bfloat16_rn(o[r][j] * inv);
   }
 }
 
@@ -155,22 +223,44 @@ cudaError_t launch_prefill_embed(Dt wdt, const int* tokens, int start, int P, co
 
 cudaError_t launch_prefill_rmsnorm(const float* X, int P, const float* gamma, float eps, int d, void* Xn,
                                    cudaStream_t s) {
-  prefill_rmsnorm_kernel<<<P, 256, 0, s>>>(X, gamma, eps, d, static_cast<__nv_bfloat16*>(Xn));
+  if (d % 4 != 0 || d > 4 * PN_MAXV * PN_THREADS) return cudaErrorInvalidValue;
+  prefill_rmsnorm_kernel<<<P, PN_THREADS, 0, s>>>(X, gamma, eps, d, static_cast<__nv_bfloat16*>(Xn));
   return cudaGetLastError();
+}
+
+template <typename KT, int DH>
+static cudaError_t attn_launch(const float* Q, const void* k, const void* v, int start, int P, int d, int n_heads,
+                               int max_seq, float scale, void* out, cudaStream_t s) {
+  const size_t smem = (static_cast<size_t>(PA_QB) * DH + PA_KB * (DH + 1) + PA_KB * DH + PA_QB * (PA_KB + 1)) * 4;
+  static bool attr_set = false;  // idempotent
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_attn_kernel<KT, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((P + PA_QB - 1) / PA_QB, n_heads);
+  prefill_attn_kernel<KT, DH><<<grid, PA_THREADS, smem, s>>>(Q, k, v, start, P, d, max_seq, scale,
+                                                               static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError();
+}
+
+template <typename KT>
+static cudaError_t attn_dispatch(int dh, const float* Q, const void* k, const void* v, int start, int P, int d,
+                                 int n_heads, int max_seq, float scale, void* out, cudaStream_t s) {
+  switch (dh) {
+    case 16: return attn_launch<KT, 16>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+    case 32: return attn_launch<KT, 32>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+    case 64: return attn_launch<KT, 64>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+    case 128: return attn_launch<KT, 128>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, const void* v, int start, int P, int d,
                                      int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s) {
-  const int gs = dh / 4;
-  if (dh % 4 != 0 || gs < 1 || gs > 32 || (gs & (gs - 1)) != 0) return cudaErrorInvalidValue;
-  dim3 grid((P + PA_WARPS - 1) / PA_WARPS, n_heads);
-  if (kvdt == Dt::BF16)
-    prefill_attn_kernel<__nv_bfloat16><<<grid, PA_WARPS * 32, 0, s>>>(Q, k, v, start, P, d, dh, max_seq, scale,
-                                                                      static_cast<__nv_bfloat16*>(out));
-  else
-    prefill_attn_kernel<float><<<grid, PA_WARPS * 32, 0, s>>>(Q, k, v, start, P, d, dh, max_seq, scale,
-                                                              static_cast<__nv_bfloat16*>(out));
-  return cudaGetLastError();
+  if (kvdt == Dt::BF16) return attn_dispatch<__nv_bfloat16>(dh, Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+  return attn_dispatch<float>(dh, Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
 }
 
 cudaError_t launch_prefill_handoff(const float* X_last, int d, float* x, int* seq_len, int len, cudaStream_t s) {

@@ -7,9 +7,9 @@
 // once, turning every projection into a GEMM  Y[P, N] = X[P, K] . W[N, K]^T.
 //
 // Shape: the weight is the MMA's A operand (M = 128 weight rows per CTA, K-major
-// as stored), the P tokens are B (N = up to 256 tokens per MMA, K-major bf16
-// activations) -- weights are streamed from HBM exactly once per GEMM however
-// many tokens there are (two N tiles / TMEM accumulators cover P <= 512).
+// as stored), the tokens are B (N = one tile of <= 128 tokens per CTA, K-major
+// bf16 activations).  CTAs of the same weight tile run concurrently, so the
+// weights stream from HBM about once per GEMM (token tiles re-hit L2).
 //   * warp 0: TMA producer (cp.async.bulk.tensor.2d, SWIZZLE_128B, 64-wide K
 //     blocks) into a `stages`-deep ring, mbarrier full/empty handshakes;
 //   * warp 1: allocates TMEM and issues tcgen05.mma.cta_group::1.kind::f16
@@ -17,7 +17,7 @@
 //     elected lane; tcgen05.commit frees ring slots and signals the epilogue;
 //   * warps 2-5: epilogue -- tcgen05.ld 32x32b (one weight row per thread, 16
 //     tokens per load) -> fused RoPE/KV-cache write, SwiGLU, residual add;
-//   * small-M GEMMs (Wo, down) split K over several CTAs; partials go to a
+//   * short prompts (memory-bound) split K over several CTAs; partials go to a
 //     global scratch and the last CTA of a tile sums them in split order
 //     (deterministic).
 #include <cuda.h>
@@ -96,42 +96,53 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
 }
 
 // ---- epilogue -------------------------------------------------------------------
+// One thread = one weight row m, 16 tokens at a time (the 16 TMEM columns of
+// one tcgen05.ld); every global load the epilogue needs for those tokens (RoPE
+// table entries, residual values) is issued before any is used, so the memory
+// latency is paid once per 16 tokens, not once per token.
 
-// Value v of weight row m (global) for token n; vp is row m^1's value (the
-// RoPE / SwiGLU partner, adjacent TMEM lane).
-__device__ __forceinline__ void pg_epilogue(const PrefillGemmParams& p, int m, int n, float v, float vp) {
-  if (m >= p.M || n >= p.P) return;
+__device__ __forceinline__ void pg_epilogue16(const PrefillGemmParams& p, int m, int n0, int nv, const float (&v)[16]) {
+  float vp[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) vp[j] = __shfl_xor_sync(0xffffffffu, v[j], 1);  // row m^1 (RoPE / SwiGLU partner)
+  if (m >= p.M) return;
   switch (p.epi) {
-    case PG_EPI_STORE:
-      p.out[static_cast<int64_t>(n) * p.M + m] = v;
-      break;
-    case PG_EPI_RESID: {
-      float* o = p.out + static_cast<int64_t>(n) * p.M + m;
-      *o = *o + v;
+    case PG_EPI_STORE: {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nv) p.out[static_cast<int64_t>(n0 + j) * p.M + m] = v[j];
       break;
     }
-    case PG_EPI_SWIGLU:
-      if ((m & 1) == 0) {
-        const float s = v / (1.0f + expf(-v));
-        static_cast<__nv_bfloat16*>(p.out_bf16)[static_cast<int64_t>(n) * (p.M >> 1) + (m >> 1)] = __float2bfloat16_rn(s * vp);
+    case PG_EPI_RESID: {
+      float old[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) old[j] = j < nv ? p.out[static_cast<int64_t>(n0 + j) * p.M + m] : 0.0f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nv) p.out[static_cast<int64_t>(n0 + j) * p.M + m] = old[j] + v[j];
+      break;
+    }
+    case PG_EPI_SWIGLU: {
+      if (m & 1) return;
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out_bf16) + (m >> 1);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j >= nv) continue;
+        const float sg = v[j] / (1.0f + expf(-v[j]));
+        o[static_cast<int64_t>(n0 + j) * (p.M >> 1)] = __float2bfloat16_rn(sg * vp[j]);
       }
       break;
+    }
     default: {  // PG_EPI_QKV / PG_EPI_QKV_ROPE: same index math as the decode epilogue (gemv_core.cuh)
       if (m & 1) return;
       const int d = p.d_model, dh = p.head_dim;
-      const int pos = p.start_pos + n;
       const int sec = m / d;
       const int lp = (m >> 1) - sec * (d >> 1);
-      float ra = v, rb = vp;
-      int e0, e1, head;
-      if (p.epi == PG_EPI_QKV_ROPE && sec < 2) {
-        const int half = dh >> 1;
+      const bool rope = p.epi == PG_EPI_QKV_ROPE && sec < 2;
+      int e0, e1, head, i = 0, half = dh >> 1;
+      if (rope) {
         head = lp / half;
-        const int i = lp - head * half;
-        const float c = p.rope_cos[static_cast<int64_t>(pos) * half + i];
-        const float s = p.rope_sin[static_cast<int64_t>(pos) * half + i];
-        ra = v * c - vp * s;
-        rb = vp * c + v * s;
+        i = lp - head * half;
         e0 = i;
         e1 = i + half;
       } else {
@@ -140,28 +151,56 @@ __device__ __forceinline__ void pg_epilogue(const PrefillGemmParams& p, int m, i
         e0 = e - head * dh;
         e1 = e0 + 1;
       }
-      if (sec == 0) {
-        float* q = p.q_out + static_cast<int64_t>(n) * d + head * dh;
-        q[e0] = ra;
-        q[e1] = rb;
-      } else {
-        void* cache = sec == 1 ? p.k_cache : p.v_cache;
-        const int64_t base = (static_cast<int64_t>(head) * p.max_seq + pos) * dh;
-        if (p.kv_bf16) {
-          __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(cache) + base;
-          c[e0] = __float2bfloat16_rn(ra);
-          c[e1] = __float2bfloat16_rn(rb);
+      float cs[16], sn[16];
+      if (rope) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int64_t t = static_cast<int64_t>(p.start_pos + n0 + (j < nv ? j : 0)) * half + i;
+          cs[j] = p.rope_cos[t];
+          sn[j] = p.rope_sin[t];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j >= nv) continue;
+        float ra = v[j], rb = vp[j];
+        if (rope) {
+          ra = v[j] * cs[j] - vp[j] * sn[j];
+          rb = vp[j] * cs[j] + v[j] * sn[j];
+        }
+        const int n = n0 + j;
+        if (sec == 0) {
+          float* q = p.q_out + static_cast<int64_t>(n) * d + head * dh;
+          q[e0] = ra;
+          q[e1] = rb;
         } else {
-          float* c = reinterpret_cast<float*>(cache) + base;
-          c[e0] = ra;
-          c[e1] = rb;
+          void* cache = sec == 1 ? p.k_cache : p.v_cache;
+          const int64_t base = (static_cast<int64_t>(head) * p.max_seq + p.start_pos + n) * dh;
+          if (p.kv_bf16) {
+            __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(cache) + base;
+            c[e0] = __float2bfloat16_rn(ra);
+            c[e1] = __float2bfloat16_rn(rb);
+          } else {
+            float* c = reinterpret_cast<float*>(cache) + base;
+            c[e0] = ra;
+            c[e1] = rb;
+          }
         }
       }
     }
   }
 }
 
+// mbarrier wait for threads that idle through the main loop: back off so they
+// do not steal issue slots from the TMA / MMA threads on their SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(256);
+}
+
 // ---- the kernel -----------------------------------------------------------------
+// grid = m_tiles x n_tiles x ksplit.  A CTA owns one 128-row weight tile, one
+// tile of `ntile` tokens and one K range; each pipeline stage carries `kbox`
+// 64-wide K boxes (kbox * 128 contiguous bytes per weight row).
 
 __global__ void __launch_bounds__(PG_THREADS, 1)
     prefill_gemm_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
@@ -173,15 +212,20 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m_tile = blockIdx.x / p.ksplit, split = blockIdx.x - m_tile * p.ksplit;
-  const int m0 = m_tile * PG_BM;
-  const int nkb = p.K / PG_BK;
+  const int split = blockIdx.x % p.ksplit;
+  const int mn = blockIdx.x / p.ksplit;
+  const int n_tile = mn % p.n_ntiles, m_tile = mn / p.n_ntiles;
+  const int m0 = m_tile * PG_BM, n0 = n_tile * p.ntile;
+  const int kstep = PG_BK * p.kbox;
+  const int nkb = p.K / kstep;
   const int kb0 = static_cast<int>(static_cast<int64_t>(split) * nkb / p.ksplit);
   const int kb1 = static_cast<int>(static_cast<int64_t>(split + 1) * nkb / p.ksplit);
   const int S = p.stages;
-  const uint32_t a_bytes = PG_BM * PG_BK * 2;
-  const uint32_t b_tile_bytes = static_cast<uint32_t>(p.ntile) * PG_BK * 2;
-  const uint32_t stage_bytes = a_bytes + p.n_ntiles * b_tile_bytes;
+  const uint32_t a_box = PG_BM * PG_BK * 2;
+  const uint32_t b_box = static_cast<uint32_t>(p.ntile) * PG_BK * 2;
+  const uint32_t stage_bytes = p.kbox * (a_box + b_box);
+  uint32_t cols = 32;
+  while (cols < static_cast<uint32_t>(p.ntile)) cols <<= 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -191,9 +235,7 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
     mbar_init(&acc_bar, 1);
     mbar_fence_init();
   }
-  if (warp == 1) {  // TMEM: one fp32 column per token, n_ntiles accumulators of ntile columns
-    uint32_t cols = 32;
-    while (cols < static_cast<uint32_t>(p.n_ntiles * p.ntile)) cols <<= 1;
+  if (warp == 1) {  // TMEM accumulator: 128 lanes (weight rows) x ntile fp32 columns (tokens)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "r"(cols)
                  : "memory");
@@ -207,18 +249,17 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // weights do not depend on the previous kernel: the first ring fill of W
-      // could start before the wait, but the activation tile shares the stage
-      // barrier, so wait first (prefill is not latency critical per kernel).
       griddep_wait();
       for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
         const int s = i % S;
         mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
         uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
         mbar_arrive_expect_tx(&full[s], stage_bytes);
-        tma_load_2d(st, &map_w, kb * PG_BK, m0, &full[s]);
-        for (int t = 0; t < p.n_ntiles; ++t)
-          tma_load_2d(st + a_bytes + t * b_tile_bytes, &map_x, kb * PG_BK, t * p.ntile, &full[s]);
+        for (int j = 0; j < p.kbox; ++j) {
+          const int k0 = kb * kstep + j * PG_BK;
+          tma_load_2d(st + j * a_box, &map_w, k0, m0, &full[s]);
+          tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, k0, n0, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -229,72 +270,69 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
         mbar_wait(&full[s], (i / S) & 1);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
+        const uint32_t sb = sa + p.kbox * a_box;
+        for (int j = 0; j < p.kbox; ++j) {
 #pragma unroll
-        for (int k = 0; k < PG_BK / PG_UK; ++k) {
-          const uint64_t ad = sw128_desc(sa + k * PG_UK * 2);
-          for (int t = 0; t < p.n_ntiles; ++t) {
-            const uint64_t bd = sw128_desc(sa + a_bytes + t * b_tile_bytes + k * PG_UK * 2);
-            tc_mma_bf16(tmem + t * p.ntile, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < PG_BK / PG_UK; ++k) {
+            const uint64_t ad = sw128_desc(sa + j * a_box + k * PG_UK * 2);
+            const uint64_t bd = sw128_desc(sb + j * b_box + k * PG_UK * 2);
+            tc_mma_bf16(tmem, ad, bd, idesc, (i > 0 || j > 0 || k > 0) ? 1u : 0u);
           }
         }
         tc_commit(&empty[s]);  // frees the slot once these MMAs have read it
       }
-      tc_commit(&acc_bar);  // accumulators complete
+      tc_commit(&acc_bar);  // accumulator complete
     }
     __syncwarp();
   } else {
     // epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31 = weight rows
     const int lane_base = 32 * (warp & 3);
     const int m = m0 + lane_base + lane;
-    mbar_wait(&acc_bar, 0);
+    mbar_wait_sleep(&acc_bar, 0);
     tc_fence_after();
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(lane_base) << 16);
     const bool split_k = p.ksplit > 1;
-    const int P_pad = p.n_ntiles * p.ntile;
-    float* mypart = split_k ? p.part + (static_cast<int64_t>(m_tile) * p.ksplit + split) * P_pad * PG_BM : nullptr;
-    for (int t = 0; t < p.n_ntiles; ++t) {
-      for (int c0 = 0; c0 < p.ntile; c0 += 16) {
-        float v[16];
-        tc_ld16(t_lane + t * p.ntile + c0, v);
-        const int nb = t * p.ntile + c0;
-        if (split_k) {
+    const int tile_id = m_tile * p.n_ntiles + n_tile;
+    float* mypart = split_k ? p.part + (static_cast<int64_t>(tile_id) * p.ksplit + split) * p.ntile * PG_BM : nullptr;
+    const int n_valid = min(p.ntile, p.P - n0);
+    for (int c0 = 0; c0 < n_valid; c0 += 16) {
+      float v[16];
+      tc_ld16(t_lane + c0, v);
+      if (split_k) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) mypart[static_cast<int64_t>(nb + j) * PG_BM + lane_base + lane] = v[j];
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float vp = __shfl_xor_sync(0xffffffffu, v[j], 1);
-            pg_epilogue(p, m, nb + j, v[j], vp);
-          }
-        }
+        for (int j = 0; j < 16; ++j) mypart[static_cast<int64_t>(c0 + j) * PG_BM + lane_base + lane] = v[j];
+      } else {
+        pg_epilogue16(p, m, n0 + c0, min(16, n_valid - c0), v);
       }
     }
     if (split_k) {
-      // last CTA of this M tile sums the partials in split order
+      // the last CTA of this output tile sums the partials in split order
       __threadfence();
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (warp == 2 && lane == 0) s_last = atomicAdd(p.counters + m_tile, 1) == p.ksplit - 1;
+      if (warp == 2 && lane == 0) s_last = atomicAdd(p.counters + tile_id, 1) == p.ksplit - 1;
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (s_last) {
         __threadfence();
-        const float* base = p.part + static_cast<int64_t>(m_tile) * p.ksplit * P_pad * PG_BM;
-        for (int n = 0; n < p.P; ++n) {
-          float v = 0.0f;
-          for (int s = 0; s < p.ksplit; ++s) v += __ldcg(base + (static_cast<int64_t>(s) * P_pad + n) * PG_BM + lane_base + lane);
-          const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
-          pg_epilogue(p, m, n, v, vp);
+        const float* base = p.part + static_cast<int64_t>(tile_id) * p.ksplit * p.ntile * PG_BM + lane_base + lane;
+        for (int n = 0; n < n_valid; n += 16) {
+          float v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = 0.0f;
+          for (int s = 0; s < p.ksplit; ++s) {
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+              if (n + u < n_valid) v[u] += __ldcg(base + (static_cast<int64_t>(s) * p.ntile + n + u) * PG_BM);
+          }
+          pg_epilogue16(p, m, n0 + n, min(16, n_valid - n), v);
         }
-        if (warp == 2 && lane == 0) p.counters[m_tile] = 0;  // self-reset
+        if (warp == 2 && lane == 0) p.counters[tile_id] = 0;  // self-reset
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
-    uint32_t cols = 32;
-    while (cols < static_cast<uint32_t>(p.n_ntiles * p.ntile)) cols <<= 1;
+  if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols) : "memory");
-  }
 }
 
 // ---- host side --------------------------------------------------------------------
@@ -331,21 +369,55 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int 
 }
 }  // namespace
 
-int prefill_gemm_ksplit(int M, int K, int sms) {
+// Tiling policy: tokens are split into N tiles of <= 128 (P > 128) so large
+// prompts spread over the SMs without any reduction; K is split only for short
+// prompts (P <= 64: memory-bound, N cannot supply the parallelism), and then
+// each stage carries 4 K boxes (512 contiguous bytes per weight row).
+struct PgShape {
+  int ntile, n_ntiles, ksplit, kbox;
+};
+static PgShape pg_shape(int M, int K, int P, int sms) {
+  PgShape sh;
   const int m_tiles = (M + PG_BM - 1) / PG_BM;
-  const int nkb = K / PG_BK;
-  int ks = std::max(1, (sms + m_tiles - 1) / m_tiles);
-  if (m_tiles * 2 > sms) ks = 1;  // already >= half a wave: no split
-  return std::max(1, std::min(ks, std::min(nkb, 8)));
+  sh.kbox = 1;
+  sh.ksplit = 1;
+  if (P <= 64) {
+    // memory-bound: one N tile; split K so the tiles fill (but do not overflow) one wave
+    sh.ntile = (P + 15) / 16 * 16;
+    sh.n_ntiles = 1;
+    sh.kbox = (K % (4 * PG_BK) == 0) ? 4 : ((K % (2 * PG_BK) == 0) ? 2 : 1);
+    const int nkb = K / (PG_BK * sh.kbox);
+    sh.ksplit = std::max(1, std::min({sms / m_tiles, nkb, 8}));
+    return sh;
+  }
+  // compute-bound: pick the token tile (16..256) minimising waves x per-tile time
+  double best = 1e30;
+  for (int nt = 64; nt <= PG_MAX_NT; nt += 16) {
+    const int n_tiles = (P + nt - 1) / nt;
+    const int nt_used = ((P + n_tiles - 1) / n_tiles + 15) / 16 * 16;
+    const int ctas = m_tiles * n_tiles;
+    const double waves = static_cast<double>((ctas + sms - 1) / sms);
+    const double cost = waves * (nt_used + 48);  // 48 ~ fixed per-tile cost (fill, epilogue) in token units
+    if (cost < best) {
+      best = cost;
+      sh.ntile = nt_used;
+      sh.n_ntiles = n_tiles;
+    }
+  }
+  return sh;
 }
 
+int prefill_gemm_ksplit(int M, int K, int sms) { return pg_shape(M, K, 16, sms).ksplit; }
+
 size_t prefill_gemm_part_floats(int M, int K, int P, int sms) {
-  const int m_tiles = (M + PG_BM - 1) / PG_BM;
-  const int ks = prefill_gemm_ksplit(M, K, sms);
-  if (ks == 1) return 0;
-  const int nt = P > PG_MAX_NT ? 2 : 1;
-  const int ntile = ((P + nt - 1) / nt + 15) / 16 * 16;
-  return static_cast<size_t>(m_tiles) * ks * nt * ntile * PG_BM;
+  size_t worst = 0;
+  for (int q = 16; q <= std::max(16, std::min(P, 64)); q += 16) {  // split-K only happens for P <= 64
+    const PgShape sh = pg_shape(M, K, q, sms);
+    if (sh.ksplit == 1) continue;
+    const int m_tiles = (M + PG_BM - 1) / PG_BM;
+    worst = std::max(worst, static_cast<size_t>(m_tiles) * sh.n_ntiles * sh.ksplit * sh.ntile * PG_BM);
+  }
+  return worst;
 }
 
 cudaError_t prefill_gemm_prepare() {
@@ -353,23 +425,26 @@ cudaError_t prefill_gemm_prepare() {
 }
 
 cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams p, cudaStream_t s, bool pdl) {
-  if (p.K % PG_BK != 0 || p.P < 1 || p.P > 2 * PG_MAX_NT || p.M < 1) return cudaErrorInvalidValue;
+  if (p.K % PG_BK != 0 || p.P < 1 || p.P > PREFILL_CHUNK || p.M < 1) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int sms = num_sms(dev);
-  p.n_ntiles = p.P > PG_MAX_NT ? 2 : 1;
-  p.ntile = ((p.P + p.n_ntiles - 1) / p.n_ntiles + 15) / 16 * 16;
-  p.ksplit = prefill_gemm_ksplit(p.M, p.K, sms);
+  const PgShape sh = pg_shape(p.M, p.K, p.P, num_sms(dev));
+  p.ntile = sh.ntile;
+  p.n_ntiles = sh.n_ntiles;
+  p.ksplit = sh.ksplit;
+  p.kbox = sh.kbox;
   if (p.ksplit > 1 && (!p.part || !p.counters)) return cudaErrorInvalidValue;
-  const int stage_bytes = PG_BM * PG_BK * 2 + p.n_ntiles * p.ntile * PG_BK * 2;
+  const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
+  if (p.ksplit > 1 && m_tiles * p.n_ntiles > 4096) return cudaErrorInvalidValue;
+  const int stage_bytes = p.kbox * (PG_BM * PG_BK * 2 + p.ntile * PG_BK * 2);
   const int budget = 220 * 1024 - 1024;
-  p.stages = std::max(2, std::min(8, budget / stage_bytes));
+  p.stages = std::min(8, budget / stage_bytes);
+  if (p.stages < 2) return cudaErrorInvalidValue;
   CUtensorMap mw, mx;
   if (!make_map(&mw, w, p.M, p.K, PG_BM)) return cudaErrorInvalidValue;
   if (!make_map(&mx, x, p.P, p.K, p.ntile)) return cudaErrorInvalidValue;
-  const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(m_tiles * p.ksplit);
+  cfg.gridDim = dim3(m_tiles * p.n_ntiles * p.ksplit);
   cfg.blockDim = dim3(PG_THREADS);
   cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + 1024;
   cfg.stream = s;

@@ -485,8 +485,9 @@ uint64_t Model::decode_bytes(int length) const {
 // batched prefill
 
 bool Model::supports_batched_prefill() const {
+  const int dh = cfg_.head_dim();
   return cfg_.llama() && cfg_.weight_dtype == GRT_BF16 && cfg_.d_model % 64 == 0 && cfg_.d_ff() % 64 == 0 &&
-         cfg_.head_dim() % 4 == 0 && (cfg_.head_dim() / 4) <= 32;
+         (dh == 16 || dh == 32 || dh == 64 || dh == 128);
 }
 
 void Model::prefill_batched(int p, cudaStream_t s) {
