@@ -240,6 +240,26 @@ grt_status grt_graph_cache_release_inactive(grt_graph_cache* c, uint64_t* droppe
 grt_status grt_graph_cache_query(grt_graph_cache* c, int32_t key, int32_t* contains, uint64_t* use_count,
                                  uint64_t* size, grt_cache_stats* stats);
 
+/* ---- tensor parallelism ----------------------------------------
+ * One process per GPU: rank 0 calls grt_tp_unique_id and shares the bytes with
+ * the other ranks (e.g. torch.distributed broadcast); every rank creates its
+ * model with tp_size/tp_rank set, then grt_model_attach_nccl before creating
+ * its session.  The allreduce (after Wo and down) and the logits allgather are
+ * NCCL collectives enqueued on the step stream, i.e. captured into the bucket
+ * graphs.  No reference interface exists for this (the reference is
+ * single-device). */
+#define GRT_TP_UNIQUE_ID_BYTES 128
+grt_status grt_tp_unique_id(uint8_t* out, int32_t len);
+grt_status grt_model_attach_nccl(grt_model* m, const uint8_t* unique_id, int32_t len);
+/* Single-device validation of the sharded model: tp_size ranks in one process
+ * stepped in lockstep, collectives emulated in-process (rank-order sums). */
+typedef struct grt_tp_emu grt_tp_emu;
+grt_status grt_tp_emu_create(const grt_model_config* cfg, grt_tp_emu** out); /* cfg->tp_size ranks */
+grt_status grt_tp_emu_destroy(grt_tp_emu* e);
+grt_status grt_tp_emu_reset(grt_tp_emu* e);
+grt_status grt_tp_emu_step(grt_tp_emu* e, int32_t token);
+grt_status grt_tp_emu_logits(grt_tp_emu* e, float* out, int32_t n);
+
 /* ---- op-level API on device pointers (kernel parity tests) ----------------- */
 /* out[n] = W[n,k] . x[k] with W in the device ([n,k], row-major) layout. */
 grt_status grt_op_gemv(const void* w, int32_t w_dtype, const float* x, float* out, int32_t n, int32_t k,

@@ -40,9 +40,15 @@ __device__ __forceinline__ float philox_weight(uint64_t seed, uint32_t tid, uint
   return static_cast<float>((2.0 * u - 1.0) * static_cast<double>(0.1f));
 }
 
-// Physical element index of logical (p, j) of a [rows=k, cols=n] tensor.
+__host__ __device__ __forceinline__ int64_t win_p1(const MapDesc& d) { return d.p1 > 0 ? d.p1 : d.rows; }
+__host__ __device__ __forceinline__ int64_t win_j1(const MapDesc& d) { return d.j1 > 0 ? d.j1 : d.cols; }
+
+// Physical element index of logical (p, j) of a [rows=k, cols=n] tensor
+// (inside the shard window).
 __device__ __forceinline__ int64_t phys_index(const MapDesc& d, int64_t p, int64_t j) {
-  if (!d.transpose) return p * d.cols + j;
+  p -= d.p0;
+  j -= d.j0;
+  if (!d.transpose) return p * (win_j1(d) - d.j0) + j;
   int64_t jj = j;
   if (d.rope_pair) {
     const int64_t dh = d.head_dim, half = dh >> 1;
@@ -67,44 +73,47 @@ __device__ __forceinline__ float load_dt(const void* src, int64_t i, int dt) {
 
 // Iterate the logical tensor with p (the reduction index) fastest, so writes of
 // a transposed matrix stay coalesced along the physical row.
+__device__ __forceinline__ void window_coords(const MapDesc& d, int64_t t, int64_t& p, int64_t& j) {
+  const int64_t wr = win_p1(d) - d.p0, wc = win_j1(d) - d.j0;
+  if (d.transpose) {
+    j = t / wr;
+    p = t - j * wr;
+  } else {
+    p = t / wc;
+    j = t - p * wc;
+  }
+  p += d.p0;
+  j += d.j0;
+}
+
 __global__ void map_init_kernel(MapDesc d, void* dst, uint64_t seed, uint32_t tid) {
-  const int64_t n = d.rows * d.cols;
+  const int64_t n = (win_p1(d) - d.p0) * (win_j1(d) - d.j0);
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int64_t p, j;
-    if (d.transpose) {
-      j = t / d.rows;
-      p = t - j * d.rows;
-    } else {
-      p = t / d.cols;
-      j = t - p * d.cols;
-    }
+    window_coords(d, t, p, j);
     store_dt(dst, phys_index(d, p, j), philox_weight(seed, tid, p * d.cols + j), d.dst_dtype);
   }
 }
 
 __global__ void map_copy_kernel(MapDesc d, void* dst, const void* src, int src_dt) {
-  const int64_t n = d.rows * d.cols;
+  const int64_t n = (win_p1(d) - d.p0) * (win_j1(d) - d.j0);
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int64_t p, j;
-    if (d.transpose) {
-      j = t / d.rows;
-      p = t - j * d.rows;
-    } else {
-      p = t / d.cols;
-      j = t - p * d.cols;
-    }
+    window_coords(d, t, p, j);
     store_dt(dst, phys_index(d, p, j), load_dt(src, p * d.cols + j, src_dt), d.dst_dtype);
   }
 }
 
+// writes the shard window into `out` at its logical positions (full [rows, cols])
 __global__ void map_read_kernel(MapDesc d, const void* dst, float* out) {
-  const int64_t n = d.rows * d.cols;
+  const int64_t wc = win_j1(d) - d.j0;
+  const int64_t n = (win_p1(d) - d.p0) * wc;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t p = t / d.cols, j = t - p * d.cols;
-    out[t] = load_dt(dst, phys_index(d, p, j), d.dst_dtype);
+    const int64_t p = d.p0 + t / wc, j = d.j0 + (t - (t / wc) * wc);
+    out[p * d.cols + j] = load_dt(dst, phys_index(d, p, j), d.dst_dtype);
   }
 }
 
@@ -116,7 +125,7 @@ static dim3 grid_for(int64_t n) {
 }
 
 cudaError_t launch_map_init(const MapDesc& d, void* dst, uint64_t seed, uint32_t tensor_id, cudaStream_t s) {
-  map_init_kernel<<<grid_for(d.rows * d.cols), 256, 0, s>>>(d, dst, seed, tensor_id);
+  map_init_kernel<<<grid_for((win_p1(d) - d.p0) * (win_j1(d) - d.j0)), 256, 0, s>>>(d, dst, seed, tensor_id);
   return cudaGetLastError();
 }
 

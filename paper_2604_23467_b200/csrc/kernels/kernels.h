@@ -183,6 +183,14 @@ cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, con
                                      int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s);
 cudaError_t launch_prefill_handoff(const float* X_last, int d, float* x, int* seq_len, int len, cudaStream_t s);
 
+// ---- tensor-parallel exchange, in-process emulation (tp_emu.cu) ----------------
+constexpr int TP_MAX = 8;
+struct TpPtrs {
+  float* p[TP_MAX];
+};
+cudaError_t launch_emu_allreduce(const TpPtrs& bufs, int T, size_t n, cudaStream_t s);
+cudaError_t launch_emu_allgather(const TpPtrs& in, const TpPtrs& out, int T, size_t n, cudaStream_t s);
+
 // Weight materialisation: writes a logical reference-layout tensor into its
 // device layout.  `src` (host-copied, fp32 or bf16 on device) or Philox init.
 struct MapDesc {
@@ -195,6 +203,12 @@ struct MapDesc {
   int rope_pair = 0;            // permute j within heads: (i, i+half) -> (2i, 2i+1)
   int head_dim = 0;
   int dst_dtype = 0;            // Dt
+  // Tensor-parallel shard window of the logical tensor: logical rows [p0, p1)
+  // (row-parallel: input dims) x columns [j0, j1) (column-parallel: outputs).
+  // Values are drawn at their LOGICAL index, so a shard holds exactly the
+  // entries of the full model; physical positions are window-relative.
+  // p1 == 0 / j1 == 0 mean "to the end".
+  int64_t p0 = 0, p1 = 0, j0 = 0, j1 = 0;
 };
 cudaError_t launch_map_init(const MapDesc& d, void* dst, uint64_t seed, uint32_t tensor_id, cudaStream_t s);
 cudaError_t launch_map_copy(const MapDesc& d, void* dst, const void* src, int src_dtype, cudaStream_t s);

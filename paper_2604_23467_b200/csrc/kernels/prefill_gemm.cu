@@ -411,7 +411,8 @@ int prefill_gemm_ksplit(int M, int K, int sms) { return pg_shape(M, K, 16, sms).
 
 size_t prefill_gemm_part_floats(int M, int K, int P, int sms) {
   size_t worst = 0;
-  for (int q = 16; q <= std::max(16, std::min(P, 64)); q += 16) {  // split-K only happens for P <= 64
+  (void)P;
+  for (int q = 16; q <= 64; q += 16) {  // split-K only happens for P <= 64: size for the worst case
     const PgShape sh = pg_shape(M, K, q, sms);
     if (sh.ksplit == 1) continue;
     const int m_tiles = (M + PG_BM - 1) / PG_BM;

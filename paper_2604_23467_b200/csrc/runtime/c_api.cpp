@@ -6,7 +6,11 @@
 #include "runtime.hpp"
 
 struct grt_model {
+  std::unique_ptr<grt::NcclComm> comm;  // destroyed after the model's sessions (declared first)
   std::unique_ptr<grt::Model> m;
+};
+struct grt_tp_emu {
+  std::unique_ptr<grt::TpEmu> e;
 };
 struct grt_session {
   grt_model* owner;
@@ -109,6 +113,45 @@ grt_status grt_model_create(const grt_model_config* cfg, grt_model** out) {
     h->m = std::make_unique<grt::Model>(grt::ModelConfig::from_c(*cfg));
     *out = h.release();
   });
+}
+
+grt_status grt_tp_unique_id(uint8_t* out, int32_t len) {
+  return guard([&] {
+    const std::vector<uint8_t> id = grt::nccl_unique_id();
+    if (!out || len < static_cast<int32_t>(id.size())) grt::raise(GRT_InvalidConfig, "unique id buffer too small");
+    std::memcpy(out, id.data(), id.size());
+  });
+}
+
+grt_status grt_model_attach_nccl(grt_model* m, const uint8_t* unique_id, int32_t len) {
+  return guard([&] {
+    if (!m || !unique_id || len < GRT_TP_UNIQUE_ID_BYTES) grt::raise(GRT_InvalidConfig, "bad arguments");
+    const grt::ModelConfig& c = m->m->config();
+    if (c.tp_size < 2) grt::raise(GRT_InvalidConfig, "model is not tensor parallel (tp_size < 2)");
+    m->comm = std::make_unique<grt::NcclComm>(unique_id, c.tp_size, c.tp_rank, c.device);
+    m->m->attach_comm(m->comm.get());
+  });
+}
+
+grt_status grt_tp_emu_create(const grt_model_config* cfg, grt_tp_emu** out) {
+  return guard([&] {
+    if (!cfg || !out) grt::raise(GRT_InvalidConfig, "null argument");
+    auto h = std::make_unique<grt_tp_emu>();
+    h->e = std::make_unique<grt::TpEmu>(grt::ModelConfig::from_c(*cfg));
+    *out = h.release();
+  });
+}
+grt_status grt_tp_emu_destroy(grt_tp_emu* e) {
+  return guard([&] { delete e; });
+}
+grt_status grt_tp_emu_reset(grt_tp_emu* e) {
+  return guard([&] { e->e->reset(); });
+}
+grt_status grt_tp_emu_step(grt_tp_emu* e, int32_t token) {
+  return guard([&] { e->e->step(token); });
+}
+grt_status grt_tp_emu_logits(grt_tp_emu* e, float* out, int32_t n) {
+  return guard([&] { e->e->logits(out, n); });
 }
 
 grt_status grt_model_destroy(grt_model* m) {

@@ -93,7 +93,15 @@ void ModelConfig::validate() const {
   if (weight_dtype != GRT_F32 && weight_dtype != GRT_BF16) raise(GRT_InvalidConfig, "weight_dtype");
   if (kv_dtype != GRT_F32 && kv_dtype != GRT_BF16) raise(GRT_InvalidConfig, "kv_dtype");
   if (init != GRT_INIT_MT19937 && init != GRT_INIT_PHILOX && init != GRT_INIT_NONE) raise(GRT_InvalidConfig, "init");
-  if (tp_size != 1) raise(GRT_Unsupported, "tensor parallel sessions are created through grt_tp_* (tp_size must be 1 here)");
+  if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size) raise(GRT_InvalidConfig, "tp_rank must be in [0, tp_size)");
+  if (tp_size > 1) {
+    if (arch != GRT_ARCH_LLAMA) raise(GRT_Unsupported, "tensor parallelism is implemented for the LLaMA arch");
+    if (n_heads % tp_size != 0) raise(GRT_InvalidConfig, "n_heads must be divisible by tp_size");
+    if (d_ff() % tp_size != 0 || (d_ff() / tp_size) % 8 != 0)
+      raise(GRT_InvalidConfig, "d_ff / tp_size must be a multiple of 8");
+    if (vocab_size % tp_size != 0) raise(GRT_InvalidConfig, "vocab_size must be divisible by tp_size");
+    if ((d_model / tp_size) % 8 != 0) raise(GRT_InvalidConfig, "d_model / tp_size must be a multiple of 8");
+  }
 }
 
 ModelConfig ModelConfig::from_c(const grt_model_config& c) {
@@ -197,6 +205,20 @@ void Model::declare_tensors() {
     m.rope_pair = rope;
     return m;
   };
+  // tensor-parallel windows: column-parallel keeps outputs [r*w, (r+1)*w),
+  // row-parallel keeps inputs [r*w, (r+1)*w) (ld = w)
+  const int64_t r = cfg_.tp_rank;
+  auto cols = [&](MapDesc m, int64_t w) {
+    m.j0 = r * w;
+    m.j1 = (r + 1) * w;
+    return m;
+  };
+  auto rows = [&](MapDesc m, int64_t w) {
+    m.p0 = r * w;
+    m.p1 = (r + 1) * w;
+    return m;
+  };
+  const int64_t dq = dq_, ffl = ffl_, Vl = vl_;
   MapDesc plain;
   add("embedding", V, d, wdt, emb_, plain);
   if (!cfg_.llama()) add("pos_table", cfg_.max_seq_len, d, wdt, pos_, plain);
@@ -204,10 +226,10 @@ void Model::declare_tensors() {
   for (int l = 0; l < cfg_.n_layers; ++l) {
     const std::string p = "layers." + std::to_string(l) + ".";
     LayerBuffers& L = layers_[l];
-    add(p + "wq", d, d, wdt, L.w_qkv, mat(d, 0, 1, 0, rope));
-    add(p + "wk", d, d, wdt, L.w_qkv, mat(d, d, 1, 0, rope));
-    add(p + "wv", d, d, wdt, L.w_qkv, mat(d, 2 * d, 1, 0, 0));
-    add(p + "wo", d, d, wdt, L.w_o, mat(d, 0, 1, 0, 0));
+    add(p + "wq", d, d, wdt, L.w_qkv, cols(mat(d, 0, 1, 0, rope), dq));
+    add(p + "wk", d, d, wdt, L.w_qkv, cols(mat(d, dq, 1, 0, rope), dq));
+    add(p + "wv", d, d, wdt, L.w_qkv, cols(mat(d, 2 * dq, 1, 0, 0), dq));
+    add(p + "wo", d, d, wdt, L.w_o, rows(mat(dq, 0, 1, 0, 0), dq));
     if (!cfg_.llama()) {
       add(p + "w1", d, ff, wdt, L.w_up, mat(d, 0, 1, 0, 0));
       add(p + "w2", ff, d, wdt, L.w_down, mat(ff, 0, 1, 0, 0));
@@ -216,16 +238,16 @@ void Model::declare_tensors() {
       add(p + "ln2_gamma", 1, d, GRT_F32, L.ln2_g, plain);
       add(p + "ln2_beta", 1, d, GRT_F32, L.ln2_b, plain);
     } else {
-      add(p + "w_gate", d, ff, wdt, L.w_up, mat(d, 0, 2, 0, 0));
-      add(p + "w_up", d, ff, wdt, L.w_up, mat(d, 0, 2, 1, 0));
-      add(p + "w_down", ff, d, wdt, L.w_down, mat(ff, 0, 1, 0, 0));
+      add(p + "w_gate", d, ff, wdt, L.w_up, cols(mat(d, 0, 2, 0, 0), ffl));
+      add(p + "w_up", d, ff, wdt, L.w_up, cols(mat(d, 0, 2, 1, 0), ffl));
+      add(p + "w_down", ff, d, wdt, L.w_down, rows(mat(ffl, 0, 1, 0, 0), ffl));
       add(p + "ln1_gamma", 1, d, GRT_F32, L.ln1_g, plain);
       add(p + "ln2_gamma", 1, d, GRT_F32, L.ln2_g, plain);
     }
   }
   add("lnf_gamma", 1, d, GRT_F32, lnf_g_, plain);
   if (!cfg_.llama()) add("lnf_beta", 1, d, GRT_F32, lnf_b_, plain);
-  add("head", d, V, wdt, head_, mat(d, 0, 1, 0, 0));
+  add("head", d, V, wdt, head_, cols(mat(d, 0, 1, 0, 0), Vl));
 }
 
 Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
@@ -250,6 +272,14 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   max_nsplit_ = attention_nsplit(static_cast<int>(S), static_cast<int>(h), sms);
   max_gen_ = static_cast<int>(S);
   const int64_t up_rows = cfg_.llama() ? 2 * ff : ff;
+  // this rank's shard (the whole model when tp_size == 1)
+  const int64_t T = cfg_.tp_size;
+  hl_ = static_cast<int>(h / T);
+  dq_ = static_cast<int>(d / T);
+  ffl_ = static_cast<int>(ff / T);
+  vl_ = static_cast<int>(V / T);
+  const int64_t dq = dq_, ffl = ffl_, Vl = vl_, hl = hl_;
+  const int64_t upl = cfg_.llama() ? 2 * ffl : ffl;
 
   // size the arena: weights, KV, workspace, control
   size_t need = 0;
@@ -257,17 +287,18 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   acc(V * d * wb);
   if (!cfg_.llama()) acc(S * d * wb);
   for (int l = 0; l < cfg_.n_layers; ++l) {
-    acc(3 * d * d * wb);
-    acc(d * d * wb);
-    acc(up_rows * d * wb);
-    acc(d * ff * wb);
+    acc(3 * dq * d * wb);
+    acc(d * dq * wb);
+    acc(upl * d * wb);
+    acc(d * ffl * wb);
     for (int i = 0; i < 4; ++i) acc(d * 4);
-    acc(h * S * dh * kvb);
-    acc(h * S * dh * kvb);
+    acc(hl * S * dh * kvb);
+    acc(hl * S * dh * kvb);
   }
   acc(d * 4);
   acc(d * 4);
-  acc(V * d * wb);
+  acc(Vl * d * wb);
+  acc(Vl * 4);              // local logits (tp)
   acc(d * 4);               // x
   acc(d * 4);               // q
   acc(d * 4);               // attn
@@ -285,10 +316,10 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   if (pf) {
     const int64_t C = PREFILL_CHUNK;
     const int64_t kmax = std::max(d, ff);
-    pf_part = std::max({prefill_gemm_part_floats(static_cast<int>(3 * d), static_cast<int>(d), PREFILL_CHUNK, sms),
-                        prefill_gemm_part_floats(static_cast<int>(d), static_cast<int>(d), PREFILL_CHUNK, sms),
-                        prefill_gemm_part_floats(static_cast<int>(up_rows), static_cast<int>(d), PREFILL_CHUNK, sms),
-                        prefill_gemm_part_floats(static_cast<int>(d), static_cast<int>(ff), PREFILL_CHUNK, sms)});
+    pf_part = std::max({prefill_gemm_part_floats(static_cast<int>(3 * dq), static_cast<int>(d), PREFILL_CHUNK, sms),
+                        prefill_gemm_part_floats(static_cast<int>(d), static_cast<int>(dq), PREFILL_CHUNK, sms),
+                        prefill_gemm_part_floats(static_cast<int>(upl), static_cast<int>(d), PREFILL_CHUNK, sms),
+                        prefill_gemm_part_floats(static_cast<int>(d), static_cast<int>(ffl), PREFILL_CHUNK, sms)});
     acc(C * d * 4);          // X
     acc(C * d * 4);          // Q
     acc(C * kmax * 2);       // Xn (bf16)
@@ -307,25 +338,26 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   if (!cfg_.llama()) pos_ = arena_buf(S * d * wb, "pos_table");
   for (int l = 0; l < cfg_.n_layers; ++l) {
     LayerBuffers& L = layers_[l];
-    L.w_qkv = arena_buf(3 * d * d * wb, "w_qkv");
-    L.w_o = arena_buf(d * d * wb, "w_o");
-    L.w_up = arena_buf(up_rows * d * wb, "w_up");
-    L.w_down = arena_buf(d * ff * wb, "w_down");
+    L.w_qkv = arena_buf(3 * dq * d * wb, "w_qkv");
+    L.w_o = arena_buf(d * dq * wb, "w_o");
+    L.w_up = arena_buf(upl * d * wb, "w_up");
+    L.w_down = arena_buf(d * ffl * wb, "w_down");
     L.ln1_g = static_cast<float*>(arena_buf(d * 4, "ln1_g"));
     L.ln1_b = static_cast<float*>(arena_buf(d * 4, "ln1_b"));
     L.ln2_g = static_cast<float*>(arena_buf(d * 4, "ln2_g"));
     L.ln2_b = static_cast<float*>(arena_buf(d * 4, "ln2_b"));
-    L.k = arena_buf(h * S * dh * kvb, "k");
-    L.v = arena_buf(h * S * dh * kvb, "v");
+    L.k = arena_buf(hl * S * dh * kvb, "k");
+    L.v = arena_buf(hl * S * dh * kvb, "v");
   }
   lnf_g_ = static_cast<float*>(arena_buf(d * 4, "lnf_g"));
   lnf_b_ = static_cast<float*>(arena_buf(d * 4, "lnf_b"));
-  head_ = arena_buf(V * d * wb, "head");
+  head_ = arena_buf(Vl * d * wb, "head");
   x_ = static_cast<float*>(arena_buf(d * 4, "x"));
   q_ = static_cast<float*>(arena_buf(d * 4, "q"));
   attn_ = static_cast<float*>(arena_buf(d * 4, "attn"));
   act_ = static_cast<float*>(arena_buf(up_rows * 4, "act"));
   logits_ = static_cast<float*>(arena_buf(V * 4, "logits"));
+  logits_local_ = T > 1 ? static_cast<float*>(arena_buf(Vl * 4, "logits_local")) : logits_;
   scratch_ = static_cast<float*>(arena_buf(V * 4, "scratch"));
   attn_part_ = static_cast<float*>(arena_buf(h * max_nsplit_ * (dh + 2) * 4, "attn_part"));
   attn_counters_ = static_cast<int*>(arena_buf(h * 4, "attn_counters"));
@@ -357,8 +389,9 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
                "pass layers");
   }
 
-  weight_bytes_ = (V * d + (cfg_.llama() ? 0 : S * d) + V * d) * wb +
-                  static_cast<uint64_t>(cfg_.n_layers) * ((3 * d * d + d * d + up_rows * d + d * ff) * wb) +
+  (void)up_rows;
+  weight_bytes_ = (V * d + (cfg_.llama() ? 0 : S * d) + Vl * d) * wb +
+                  static_cast<uint64_t>(cfg_.n_layers) * ((3 * dq * d + d * dq + upl * d + d * ffl) * wb) +
                   static_cast<uint64_t>(cfg_.n_layers) * 4 * d * 4 + 2 * d * 4;
 
   declare_tensors();
@@ -463,6 +496,7 @@ void Model::download(const std::string& name, float* host, size_t numel) {
   cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
   float* staging = nullptr;
   cuda_check(cudaMalloc(&staging, n * 4), "cudaMalloc staging");
+  cuda_check(cudaMemset(staging, 0, n * 4), "cudaMemset staging");  // outside this rank's shard: 0
   cuda_check(launch_map_read(t.map, t.dev, staging, nullptr), "map read");
   cuda_check(cudaMemcpy(host, staging, n * 4, cudaMemcpyDeviceToHost), "download");
   cudaFree(staging);
@@ -476,8 +510,9 @@ uint64_t Model::decode_bytes(int length) const {
   const uint64_t V = cfg_.vocab_size;
   uint64_t b = weight_bytes_ - (V * d + (cfg_.llama() ? 0 : cfg_.max_seq_len * d)) * wb;
   b += d * wb * (cfg_.llama() ? 1 : 2);            // embedding (+pos) row
-  b += L * 2 * static_cast<uint64_t>(length) * d * kvb;  // K,V read over [0, length)
-  b += L * 2 * d * kvb;                              // K,V row write
+  const uint64_t dq = static_cast<uint64_t>(dq_);  // this rank's heads
+  b += L * 2 * static_cast<uint64_t>(length) * dq * kvb;  // K,V read over [0, length)
+  b += L * 2 * dq * kvb;                                   // K,V row write
   return b;
 }
 
@@ -493,7 +528,10 @@ bool Model::supports_batched_prefill() const {
 void Model::prefill_batched(int p, cudaStream_t s) {
   if (!supports_batched_prefill()) raise(GRT_Unsupported, "batched prefill needs the LLaMA arch with bf16 weights");
   if (p < 1 || p > cfg_.max_seq_len) raise(GRT_PromptTooLong, "batched prefill length out of range");
-  const int d = cfg_.d_model, ff = cfg_.d_ff(), h = cfg_.n_heads, dh = cfg_.head_dim(), S = cfg_.max_seq_len;
+  const int d = cfg_.d_model, dh = cfg_.head_dim(), S = cfg_.max_seq_len;
+  const int T = cfg_.tp_size, dq = dq_, ffl = ffl_, hl = hl_;  // this rank's shard
+  if (T > 1 && !comm_) raise(GRT_InvalidConfig, "tensor-parallel prefill needs an attached communicator");
+  const int resid_epi = (T == 1 || cfg_.tp_rank == 0) ? PG_EPI_RESID : PG_EPI_STORE;
   const Dt kvdt = cfg_.kv_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
   const float scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
   int last_P = 0;
@@ -506,7 +544,7 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       const LayerBuffers& L = layers_[l];
       cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln1_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm1");
       PrefillGemmParams q;
-      q.M = 3 * d;
+      q.M = 3 * dq;
       q.K = d;
       q.P = P;
       q.epi = PG_EPI_QKV_ROPE;
@@ -517,26 +555,27 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       q.rope_sin = rope_sin_;
       q.head_dim = dh;
       q.max_seq = S;
-      q.d_model = d;
+      q.d_model = dq;
       q.start_pos = start;
       q.kv_bf16 = kvdt == Dt::BF16;
       q.part = pf_part_;
       q.counters = pf_cnt_;
       cuda_check(launch_prefill_gemm(L.w_qkv, pf_Xn_, q, s, false), "prefill qkv");
-      cuda_check(launch_prefill_attention(kvdt, pf_Q_, L.k, L.v, start, P, d, h, dh, S, scale, pf_A_, s),
+      cuda_check(launch_prefill_attention(kvdt, pf_Q_, L.k, L.v, start, P, dq, hl, dh, S, scale, pf_A_, s),
                  "prefill attention");
       PrefillGemmParams o;
       o.M = d;
-      o.K = d;
+      o.K = dq;
       o.P = P;
-      o.epi = PG_EPI_RESID;
+      o.epi = resid_epi;
       o.out = pf_X_;
       o.part = pf_part_;
       o.counters = pf_cnt_;
       cuda_check(launch_prefill_gemm(L.w_o, pf_A_, o, s, false), "prefill wo");
+      if (T > 1) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce wo");
       cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln2_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm2");
       PrefillGemmParams u;
-      u.M = 2 * ff;
+      u.M = 2 * ffl;
       u.K = d;
       u.P = P;
       u.epi = PG_EPI_SWIGLU;
@@ -546,13 +585,14 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       cuda_check(launch_prefill_gemm(L.w_up, pf_Xn_, u, s, false), "prefill gate_up");
       PrefillGemmParams w2;
       w2.M = d;
-      w2.K = ff;
+      w2.K = ffl;
       w2.P = P;
-      w2.epi = PG_EPI_RESID;
+      w2.epi = resid_epi;
       w2.out = pf_X_;
       w2.part = pf_part_;
       w2.counters = pf_cnt_;
       cuda_check(launch_prefill_gemm(L.w_down, pf_act_, w2, s, false), "prefill down");
+      if (T > 1) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce down");
     }
   }
   // hand off to the decode state: last token's residual row, seq_len = p; then
@@ -561,14 +601,15 @@ void Model::prefill_batched(int p, cudaStream_t s) {
              "prefill handoff");
   GemvParams hp;
   hp.w = head_;
-  hp.n_rows = cfg_.vocab_size;
+  hp.n_rows = vl_;
   hp.k = d;
   hp.x = x_;
   hp.gamma = lnf_g_;
   hp.beta = lnf_b_;
   hp.eps = cfg_.norm_eps;
-  hp.out = logits_;
+  hp.out = logits_local_;
   cuda_check(launch_gemv(Dt::BF16, NORM_RMS, EPI_STORE, hp, s, false, 0), "prefill head");
+  if (T > 1) cuda_check(comm_->allgather(logits_local_, logits_, static_cast<size_t>(vl_), s), "prefill allgather");
 }
 
 // ---------------------------------------------------------------------------
@@ -721,12 +762,38 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
     inv.launch = [wdt, epi, nrm, p](cudaStream_t s) { return launch_gemv(wdt, nrm, epi, p, s, true, 0); };
     plan.push_back(std::move(inv));
   };
+  // Tensor parallelism: this rank's shard has hl heads (dq = hl*dh
+  // attention dims), ffl d_ff columns and vl vocab rows.  Row-parallel Wo/down
+  // produce partial residual updates: rank 0 adds its partial to x, the other
+  // ranks overwrite x with theirs, and an in-place allreduce (sum) leaves
+  // x + sum_r partial_r on every rank.  The LM head is vocab-parallel; an
+  // allgather assembles the full logits (rank order) for the sampler.
+  const int T = cfg_.tp_size, hl = hl_, dq = dq_, ffl = ffl_, vl = vl_;
+  const int resid_epi = (T == 1 || cfg_.tp_rank == 0) ? EPI_RESID : EPI_STORE;
+  TpComm** commp = &comm_;
+  auto allreduce_x = [&](const char* name) {
+    KernelInvocation inv;
+    inv.spec.name = name;
+    inv.spec.op_class = OpClass::Static;
+    inv.spec.bytes = static_cast<int64_t>(d) * 4;
+    inv.bindings = {{x_, static_cast<size_t>(d) * 4}};
+    inv.collective = COLL_ALLREDUCE;
+    inv.coll_in = x_;
+    inv.coll_out = x_;
+    inv.coll_n = static_cast<size_t>(d);
+    float* x = x_;
+    inv.launch = [commp, x, d](cudaStream_t s) {
+      if (!*commp) return cudaErrorInvalidValue;  // no communicator attached
+      return (*commp)->allreduce_sum(x, static_cast<size_t>(d), s);
+    };
+    plan.push_back(std::move(inv));
+  };
   for (int l = 0; l < cfg_.n_layers; ++l) {
     const LayerBuffers& L = layers_[l];
-    {  // ln1 + q,k,v + (RoPE) + kv_write
+    {  // ln1 + q,k,v + (RoPE) + kv_write   (column-parallel: this rank's heads)
       GemvParams p;
       p.w = L.w_qkv;
-      p.n_rows = 3 * d;
+      p.n_rows = 3 * dq;
       p.k = d;
       p.x = x_;
       p.gamma = L.ln1_g;
@@ -738,15 +805,15 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       p.seq_len = seq_len;
       p.rope_cos = rope_cos_;
       p.rope_sin = rope_sin_;
-      p.n_heads = h;
+      p.n_heads = hl;
       p.head_dim = dh;
       p.max_seq = S;
-      p.d_model = d;
+      p.d_model = dq;  // q | k | v sections of the shard are dq rows each
       p.kv_bf16 = kvdt == Dt::BF16;
       p.err = err;
-      gemv("qkv", llama ? EPI_QKV_ROPE : EPI_QKV, norm, p, 3ull * d * d * wb);
+      gemv("qkv", llama ? EPI_QKV_ROPE : EPI_QKV, norm, p, 3ull * dq * d * wb);
     }
-    {  // attention over [0, seq_len)
+    {  // attention over [0, seq_len) for this rank's heads
       AttnParams a;
       a.q = q_;
       a.k_cache = L.k;
@@ -755,7 +822,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       a.part = attn_part_;
       a.counters = attn_counters_;
       a.seq_len = seq_len;
-      a.n_heads = h;
+      a.n_heads = hl;
       a.head_dim = dh;
       a.max_seq = S;
       a.span_cap = span_cap;
@@ -764,26 +831,27 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       a.trace = next_trace();
       KernelInvocation inv;
       inv.spec.name = "attention";
-      inv.spec.flops = static_cast<int64_t>(h) * max_len * (4 * dh + 5);  // kernels.hpp:51
-      inv.spec.bytes = 2LL * max_len * d * kvb;
-      inv.bindings = {{L.k, static_cast<size_t>(h) * S * dh * kvb}, {L.v, static_cast<size_t>(h) * S * dh * kvb},
-                      {q_, static_cast<size_t>(d) * 4}, {attn_, static_cast<size_t>(d) * 4}};
+      inv.spec.flops = static_cast<int64_t>(hl) * max_len * (4 * dh + 5);  // kernels.hpp:51
+      inv.spec.bytes = 2LL * max_len * dq * kvb;
+      inv.bindings = {{L.k, static_cast<size_t>(hl) * S * dh * kvb}, {L.v, static_cast<size_t>(hl) * S * dh * kvb},
+                      {q_, static_cast<size_t>(dq) * 4}, {attn_, static_cast<size_t>(dq) * 4}};
       inv.launch = [kvdt, a, max_len](cudaStream_t s) { return launch_attention(kvdt, a, max_len, s, true); };
       plan.push_back(std::move(inv));
     }
-    {  // (merge attention splits) + wo + residual
+    {  // wo + residual (row-parallel under TP)
       GemvParams p;
       p.w = L.w_o;
       p.n_rows = d;
-      p.k = d;
+      p.k = dq;
       p.x = attn_;
       p.out = x_;
-      gemv("wo_residual", EPI_RESID, NORM_NONE, p, 1ull * d * d * wb);
+      gemv("wo_residual", resid_epi, NORM_NONE, p, 1ull * d * dq * wb);
+      if (T > 1) allreduce_x("allreduce_wo");
     }
-    {  // ln2 + w1 + relu  |  rms + gate/up + SwiGLU
+    {  // ln2 + w1 + relu  |  rms + gate/up + SwiGLU   (column-parallel)
       GemvParams p;
       p.w = L.w_up;
-      p.n_rows = llama ? 2 * ff : ff;
+      p.n_rows = llama ? 2 * ffl : ffl;
       p.k = d;
       p.x = x_;
       p.gamma = L.ln2_g;
@@ -793,34 +861,55 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       gemv(llama ? "gate_up_swiglu" : "w1_relu", llama ? EPI_SWIGLU : EPI_RELU, norm, p,
            static_cast<size_t>(p.n_rows) * d * wb);
     }
-    {  // w2/down + residual
+    {  // w2/down + residual (row-parallel)
       GemvParams p;
       p.w = L.w_down;
       p.n_rows = d;
-      p.k = ff;
+      p.k = ffl;
       p.x = act_;
       p.out = x_;
-      gemv("down_residual", EPI_RESID, NORM_NONE, p, 1ull * d * ff * wb);
+      gemv("down_residual", resid_epi, NORM_NONE, p, 1ull * d * ffl * wb);
+      if (T > 1) allreduce_x("allreduce_down");
     }
   }
-  {  // ln_f + head
+  {  // ln_f + head (vocab-parallel)
     GemvParams p;
     p.w = head_;
-    p.n_rows = V;
+    p.n_rows = vl;
     p.k = d;
     p.x = x_;
     p.gamma = lnf_g_;
     p.beta = lnf_b_;
     p.eps = cfg_.norm_eps;
-    p.out = logits_;
-    gemv("lnf_head", EPI_STORE, norm, p, 1ull * V * d * wb);
+    p.out = logits_local_;
+    gemv("lnf_head", EPI_STORE, norm, p, 1ull * vl * d * wb);
   }
+  if (T > 1) {
+    KernelInvocation inv;
+    inv.spec.name = "allgather_logits";
+    inv.spec.op_class = OpClass::Static;
+    inv.spec.bytes = static_cast<int64_t>(V) * 4;
+    inv.bindings = {{logits_local_, static_cast<size_t>(vl) * 4}, {logits_, static_cast<size_t>(V) * 4}};
+    inv.collective = COLL_ALLGATHER;
+    inv.coll_in = logits_local_;
+    inv.coll_out = logits_;
+    inv.coll_n = static_cast<size_t>(vl);
+    float* in = logits_local_;
+    float* out = logits_;
+    inv.launch = [commp, in, out, vl](cudaStream_t s) {
+      if (!*commp) return cudaErrorInvalidValue;
+      return (*commp)->allgather(in, out, static_cast<size_t>(vl), s);
+    };
+    plan.push_back(std::move(inv));
+  }
+  (void)ff;
   return plan;
 }
 
 const std::vector<KernelInvocation>& Model::plan(int key, int B, int impl) {
   if (B < 1) raise(GRT_InvalidConfig, "bucket_size must be >= 1");
   if (impl != 0 && impl != 1) raise(GRT_InvalidConfig, "pass_impl must be 0 or 1");
+  if (impl == 0 && cfg_.tp_size > 1) raise(GRT_Unsupported, "the persistent pass (pass_impl 0) is single-GPU only");
   if (key < 1 || key > max_key(B))
     raise(GRT_LengthOutOfRange, "plan key " + std::to_string(key) + " outside [1, " + std::to_string(max_key(B)) + "]");
   std::lock_guard<std::mutex> lk(plan_mu_);

@@ -227,6 +227,13 @@ void CudaDevice::sync_all() {
 // Session
 
 Session::Session(Model& model, const CacheConfig& cc) : model_(&model), cc_(cc) {
+  if (model.tp_size() > 1) {
+    // tensor parallel: per-op plan with in-graph NCCL collectives; captures run
+    // on the submitting thread (one NCCL communicator must not be driven from
+    // two host threads), so every rank captures/launches in the same order
+    if (!model.comm()) raise(GRT_InvalidConfig, "tensor-parallel model has no communicator (grt_model_attach_nccl)");
+    cc_.pass_impl = 1;
+  }
   if (cc_.bucket_size < 1) raise(GRT_InvalidConfig, "bucket_size must be >= 1");
   cuda_check(cudaSetDevice(model.device()), "cudaSetDevice");
   dev_ = std::make_unique<CudaDevice>(model.device());
@@ -337,7 +344,7 @@ StepResponse Session::serve(const StepRequest& req, bool allow_cache, const Mode
   if (use_cache && pol.capture_on_miss && !cache_->contains(ck)) {
     ++dev_->counters().events_recorded;  // ordering point, as record_event/wait_event in the reference
     ++dev_->counters().events_waited;
-    if (pol.async_capture) {
+    if (pol.async_capture && model_->tp_size() == 1) {
       if (!dev_->capture_pending(ck))
         dev_->submit_capture(ck, [this, key, fused](cudaStream_t s) { return capture_now(key, fused, s); });
     } else {

@@ -121,10 +121,27 @@ struct KernelSpec {
 
 // One kernel instance.  `launch` enqueues it on a stream: it binds device
 // buffers (never host values), so it is equally valid eagerly or under capture.
+// Tensor-parallel collective on the step path: an in-graph NCCL
+// allreduce / allgather for one-rank-per-GPU sessions, or the in-process
+// emulation used to validate the sharding on a single GPU.
+class TpComm {
+ public:
+  virtual ~TpComm() = default;
+  virtual cudaError_t allreduce_sum(float* buf, size_t n, cudaStream_t s) = 0;                   // in place
+  virtual cudaError_t allgather(const float* in, float* out, size_t n_per_rank, cudaStream_t s) = 0;  // rank order
+};
+enum CollectiveKind : int { COLL_NONE = 0, COLL_ALLREDUCE = 1, COLL_ALLGATHER = 2 };
+
 struct KernelInvocation {
   KernelSpec spec;
   std::vector<DevRange> bindings;
   std::function<cudaError_t(cudaStream_t)> launch;
+  // collectives (TP): `launch` calls the attached TpComm; the fields let an
+  // emulation driver run the same exchange across in-process ranks
+  int collective = COLL_NONE;
+  float* coll_in = nullptr;
+  float* coll_out = nullptr;
+  size_t coll_n = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -216,6 +233,16 @@ class Model {
   // residual/logits of the last token).  Enqueued on `s`, no host sync.
   bool supports_batched_prefill() const;
   void prefill_batched(int p, cudaStream_t s);
+
+  // Tensor parallelism (tp_size > 1): this model holds rank tp_rank's shard --
+  // QKV/gate/up/head column-parallel (heads, d_ff and vocab split), Wo/down
+  // row-parallel, KV cache by head.  Collectives go through `comm`, which the
+  // caller owns and must attach before any plan is built.
+  int tp_size() const { return cfg_.tp_size; }
+  int tp_rank() const { return cfg_.tp_rank; }
+  void attach_comm(TpComm* c) { comm_ = c; }
+  TpComm* comm() const { return comm_; }
+  float* logits_local_dev() const { return logits_local_; }
   void reset_pass_sync() {
     cudaMemset(pass_sync_, 0, static_cast<size_t>(sync_ints()) * 4);
     cudaMemset(&ctrl_->err, 0, sizeof(int));
@@ -254,6 +281,10 @@ class Model {
   float *pf_X_ = nullptr, *pf_Q_ = nullptr, *pf_part_ = nullptr;
   void *pf_Xn_ = nullptr, *pf_A_ = nullptr, *pf_act_ = nullptr;
   int* pf_cnt_ = nullptr;
+  // tensor-parallel shard dims: heads, attention width, d_ff, vocab per rank
+  int hl_ = 0, dq_ = 0, ffl_ = 0, vl_ = 0;
+  float* logits_local_ = nullptr;  // [vl_] before the allgather (== logits_ when tp_size == 1)
+  TpComm* comm_ = nullptr;
   GrtCtrl* ctrl_ = nullptr;
   int* tokens_ = nullptr;
   double* uniforms_ = nullptr;
@@ -510,6 +541,46 @@ class Session {
   int n_sampled_ = 0;  // step-level sampler draws since sampler_reset (Philox counter / uniform index)
   int captures_completed_ = 0;
   GrtCtrl* h_ctrl_ = nullptr;  // pinned staging for ctrl writes
+};
+
+// ---------------------------------------------------------------------------
+// tensor parallelism (tp.cpp)
+
+// One rank per GPU: NCCL communicator over NVLink/NVSwitch; the collectives
+// are enqueued on the step stream, so they are captured into the bucket graphs
+// like every kernel (in the same order on every rank).
+class NcclComm : public TpComm {
+ public:
+  NcclComm(const void* unique_id, int nranks, int rank, int device);
+  ~NcclComm() override;
+  cudaError_t allreduce_sum(float* buf, size_t n, cudaStream_t s) override;
+  cudaError_t allgather(const float* in, float* out, size_t n_per_rank, cudaStream_t s) override;
+
+ private:
+  void* comm_ = nullptr;  // ncclComm_t
+};
+std::vector<uint8_t> nccl_unique_id();
+
+// T ranks of a tensor-parallel model in ONE process on one device, stepped in
+// lockstep on one stream: every kernel of every rank in plan order, each
+// collective replaced by the in-process exchange (tp_emu.cu).  Validates the
+// sharding (column/row/vocab splits, head-sharded KV, rank-0 residual rule)
+// against the tp_size == 1 model on a single GPU.
+class TpEmu {
+ public:
+  explicit TpEmu(const ModelConfig& cfg);
+  ~TpEmu();
+  void reset();
+  void step(int token);
+  void logits(float* out, int n);
+  int tp_size() const { return static_cast<int>(ranks_.size()); }
+
+ private:
+  std::vector<std::unique_ptr<Model>> ranks_;
+  std::vector<KernelInvocation> pre_;
+  cudaStream_t s_ = nullptr;
+  int cur_len_ = 0;
+  GrtCtrl* h_ctrl_ = nullptr;
 };
 
 }  // namespace grt

@@ -159,6 +159,8 @@ EXPORTS = [
     "grt_graph_cache_create", "grt_graph_cache_destroy", "grt_graph_cache_lookup", "grt_graph_cache_insert",
     "grt_graph_cache_warmup", "grt_graph_cache_begin_session", "grt_graph_cache_release_inactive",
     "grt_graph_cache_query", "grt_profile_plan", "grt_trace_pass",
+    "grt_tp_unique_id", "grt_model_attach_nccl", "grt_tp_emu_create", "grt_tp_emu_destroy", "grt_tp_emu_reset",
+    "grt_tp_emu_step", "grt_tp_emu_logits",
 ]
 
 _lib = None
@@ -190,6 +192,13 @@ def lib():
         L.grt_model_weight_bytes.argtypes = [vp, C.POINTER(C.c_uint64)]
         L.grt_model_decode_bytes.argtypes = [vp, C.c_int32, C.POINTER(C.c_uint64)]
         L.grt_session_create.argtypes = [vp, C.POINTER(_CacheConfig), C.POINTER(vp)]
+        L.grt_tp_unique_id.argtypes = [C.c_char_p, C.c_int32]
+        L.grt_model_attach_nccl.argtypes = [vp, C.c_char_p, C.c_int32]
+        L.grt_tp_emu_create.argtypes = [C.POINTER(_ModelConfig), C.POINTER(vp)]
+        L.grt_tp_emu_destroy.argtypes = [vp]
+        L.grt_tp_emu_reset.argtypes = [vp]
+        L.grt_tp_emu_step.argtypes = [vp, C.c_int32]
+        L.grt_tp_emu_logits.argtypes = [vp, C.POINTER(C.c_float), C.c_int32]
         L.grt_session_destroy.argtypes = [vp]
         L.grt_generate.argtypes = [vp, C.POINTER(_Request), C.POINTER(_Result)]
         L.grt_cache_stats_get.argtypes = [vp, C.POINTER(_CacheStats), C.POINTER(C.c_uint64)]
@@ -250,6 +259,8 @@ class ModelConfig:
     kv_dtype: int = F32
     rope_theta: float = 10000.0
     device: int = 0
+    tp_size: int = 1   # tensor parallel ranks; this model holds rank tp_rank's shard
+    tp_rank: int = 0
 
     def d_ff(self) -> int:
         return self.d_ff_ if self.d_ff_ > 0 else 4 * self.d_model
@@ -263,7 +274,7 @@ class ModelConfig:
         c.vocab_size, c.max_seq_len, c.d_ff = self.vocab_size, self.max_seq_len, self.d_ff_
         c.norm_eps, c.seed, c.init = self.ln_eps, self.seed, self.init
         c.weight_dtype, c.kv_dtype, c.rope_theta = self.weight_dtype, self.kv_dtype, self.rope_theta
-        c.device, c.tp_size, c.tp_rank = self.device, 1, 0
+        c.device, c.tp_size, c.tp_rank = self.device, self.tp_size, self.tp_rank
         return c
 
     @staticmethod
@@ -408,6 +419,10 @@ class Model:
         _check(lib().grt_model_download(self._h, name.encode(), out.ctypes.data_as(C.POINTER(C.c_float)), numel))
         return out
 
+    def attach_nccl(self, unique_id: bytes) -> None:
+        """Joins this rank's model to the NCCL tensor-parallel group (all ranks call it)."""
+        _check(lib().grt_model_attach_nccl(self._h, bytes(unique_id), len(unique_id)))
+
     def weight_bytes(self) -> int:
         v = C.c_uint64()
         _check(lib().grt_model_weight_bytes(self._h, C.byref(v)))
@@ -417,6 +432,52 @@ class Model:
         v = C.c_uint64()
         _check(lib().grt_model_decode_bytes(self._h, length, C.byref(v)))
         return v.value
+
+
+def tp_unique_id() -> bytes:
+    """NCCL unique id for a tensor-parallel group (rank 0 creates, every rank attaches)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().grt_tp_unique_id(buf, 128))
+    return buf.raw
+
+
+class TPEmu:
+    """Single-device validation of a tensor-parallel model: cfg.tp_size ranks in
+    one process, stepped in lockstep with the collectives emulated in-process."""
+
+    def __init__(self, cfg: "ModelConfig"):
+        h = C.c_void_p()
+        c = cfg._c()
+        _check(lib().grt_tp_emu_create(C.byref(c), C.byref(h)))
+        self._h = h
+        self.vocab = cfg.vocab_size
+
+    def reset(self):
+        _check(lib().grt_tp_emu_reset(self._h))
+
+    def step(self, token: int):
+        _check(lib().grt_tp_emu_step(self._h, int(token)))
+
+    def prefill(self, tokens):
+        for t in tokens:
+            self.step(t)
+
+    def logits(self):
+        import numpy as np
+        out = np.zeros(self.vocab, np.float32)
+        _check(lib().grt_tp_emu_logits(self._h, out.ctypes.data_as(C.POINTER(C.c_float)), self.vocab))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().grt_tp_emu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Session:

@@ -391,3 +391,29 @@ def test_batched_prefill_run_tokens_match_token_by_token():
     assert ra.prefill_paths == [g.StepPath.Batched] * 40
     agree = sum(1 for a, b in zip(ra.tokens, rb.tokens) if a == b)
     assert ra.tokens[:4] == rb.tokens[:4] and agree >= 12, (ra.tokens, rb.tokens)
+
+
+# ---------------------------------------------------------- tensor parallelism
+
+@pytest.mark.parametrize("tp,kw,tol", [
+    (2, dict(n_layers=2, d_model=64, n_heads=4, vocab_size=256, max_seq_len=128, d_ff_=192, seed=3), 1e-4),
+    (4, dict(n_layers=2, d_model=64, n_heads=4, vocab_size=256, max_seq_len=128, d_ff_=192, seed=3), 1e-4),
+    (8, dict(n_layers=2, d_model=4096, n_heads=32, vocab_size=32000, max_seq_len=128, d_ff_=11008, seed=11), 2e-3),
+])
+def test_tp_sharded_decode_matches_single_gpu(tp, kw, tol):
+    """The TP-sharded model (column-parallel QKV/gate-up/head, row-parallel
+    Wo/down, head-sharded KV, rank-0 residual rule, allreduce + logits
+    allgather) reproduces the tp_size=1 model's logits step by step; ranks run
+    in lockstep on one device with the collectives emulated in-process (the
+    only difference is the summation order of the row-parallel partials)."""
+    base = dict(arch=g.ARCH_LLAMA, init=g.INIT_PHILOX, weight_dtype=g.BF16, kv_dtype=g.BF16, **kw)
+    ref = g.Session(g.ModelConfig(**base), g.CacheConfig(bucket_size=64, warmup_hi=0))
+    emu = g.TPEmu(g.ModelConfig(tp_size=tp, **base))
+    import pyoracle as po
+    prompt = po.make_prompt(42, 12, kw["vocab_size"])
+    worst = 0.0
+    for t in prompt:
+        ref.step(t)
+        emu.step(t)
+        worst = max(worst, float(np.abs(ref.logits() - emu.logits()).max()))
+    assert worst <= tol, worst
