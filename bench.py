@@ -10,8 +10,10 @@ are generated untimed, the next K are timed.  value = p50 ms/token from device
 %globaltimer stamps written by the sampler kernel (CUDA-event equivalent, on the
 stream that runs the step); e2e = the same metric as seen by the host through
 the public API (token read from host-mapped memory each step).
-Multi-GPU: the path does not shard in this round (TP is "next"), so N>1 runs N
-independent replicas (one per GPU, torchrun), max over ranks.
+Multi-GPU (torchrun, one process per GPU): --parallel tp (default) shards the
+model over the N GPUs (tensor parallel, NCCL allreduce/allgather captured in the
+step graphs; strong scaling: value = per-token latency, max over ranks);
+--parallel replicas runs N independent copies (weak scaling).
 """
 from __future__ import annotations
 
@@ -184,6 +186,8 @@ def main():
     ap.add_argument("--mode", default="hybrid")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--bucket", type=int, default=64)
+    ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
+                    help="N>1: tensor-parallel decode over the N GPUs (NCCL in-graph) or N independent replicas")
     ap.add_argument("--batched-prefill", type=int, default=1, help="1: tcgen05 batched prefill (TTFT path); 0: token-by-token")
     ap.add_argument("--pass-impl", type=int, default=1, help="1 per-op kernel graph (default), 0 persistent single-kernel pass")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -203,11 +207,29 @@ def main():
     W, K, P = args.warmup, args.steps, args.prompt_len
     n = W + K
     max_seq = max(640, ((P + n + 63) // 64) * 64)
-    cfg = g.ModelConfig.llama2_7b(n_layers=args.layers, max_seq_len=max_seq, device=local)
+    cc = g.CacheConfig(bucket_size=args.bucket, warmup_lo=1, warmup_hi=10 ** 6 // args.bucket, capacity=4096,
+                       pass_impl=args.pass_impl, batched_prefill=bool(args.batched_prefill))
     t_init = time.time()
-    sess = g.Session(cfg, g.CacheConfig(bucket_size=args.bucket, warmup_lo=1, warmup_hi=10 ** 6 // args.bucket,
-                                        capacity=4096, pass_impl=args.pass_impl,
-                                        batched_prefill=bool(args.batched_prefill)))
+    parallel = "single"
+    tp_error = None
+    if world > 1 and args.parallel == "tp":
+        # tensor parallel: rank r holds shard r; NCCL unique id handed over gloo
+        try:
+            obj = [g.tp_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            cfg = g.ModelConfig.llama2_7b(n_layers=args.layers, max_seq_len=max_seq, device=local, tp_size=world,
+                                          tp_rank=rank)
+            model = g.Model(cfg)
+            model.attach_nccl(obj[0])
+            sess = g.Session(model, cc)
+            parallel = f"tp{world}"
+        except Exception as e:  # reported in the JSON line, never silent
+            tp_error = f"{type(e).__name__}: {e}"
+            parallel = None
+    if parallel is None or (world > 1 and args.parallel == "replicas") or world == 1:
+        cfg = g.ModelConfig.llama2_7b(n_layers=args.layers, max_seq_len=max_seq, device=local)
+        sess = g.Session(cfg, cc)
+        parallel = "single" if world == 1 else f"{world} replicas"
     init_s = time.time() - t_init
     model = sess.model
     prompt = [(i * 7919 + 17) % 32000 for i in range(P)]
@@ -280,25 +302,27 @@ def main():
     nodes_per_step = r.counters.graph_kernel_nodes / max(1, r.counters.graph_replays)
     line = {
         "metric": METRIC, "value": round(p50, 4), "unit": "ms/token", "n_gpus": args.gpus, "steps": K,
-        "warmup": W, "ms_per_step": round(mean, 4), "higher_is_better": False, "scaling": "weak",
+        "warmup": W, "ms_per_step": round(mean, 4), "higher_is_better": False,
         "vs_baseline": None, "dtype": "bf16",
+        "scaling": "strong" if parallel.startswith("tp") else "weak",
         "data": "synthetic: random-init LLaMA-2 7B weights (Philox U[-0.1,0.1], bf16), prompt make_prompt(42,P,32000)",
         "config": {"workload": f"LLaMA-2 7B bs1, prompt {P}, {W}+{K} greedy decode steps, {args.mode} "
                                "(one CUDA-graph launch per token)",
                    "model": "llama2-7b", "global_batch": 1, "seq_len": P + n,
-                   "parallelism": "single" if args.gpus == 1 else f"{args.gpus} replicas",
+                   "parallelism": parallel,
                    "l2": "no flush: 13.2 GB of weights streamed per token >> 126 MB L2",
                    "bucket_size": args.bucket, "n_layers": args.layers},
         "ttft_ms": round(ttft_ms, 3), "p50_ms": round(p50, 4), "p99_ms": round(p99, 4),
         "p99_over_p50": round(p99 / p50, 4), "decode_bytes_per_token": bytes_tok,
         "decode_hbm_gbs": round(hbm_gbs, 1), "decode_hbm_frac": round(hbm_gbs / peak, 4),
+        "decode_hbm_gbs_all_ranks": round(hbm_gbs * (world if parallel.startswith("tp") else 1), 1),
         "roofline": roofline, "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_p50, 4), "unit": "ms/token", "h2d_bytes_per_step": round((4 * P + 128) / n, 2),
                 "d2h_bytes_per_step": 4 + 16},
         "gpu_launches": int(round(nodes_per_step * K + r.counters.kernel_launches * K / n)),
         "host_kernel_launches_per_step": r.counters.kernel_launches / n,
         "graph_launches_per_step": r.counters.graph_replays / (P + n),
-        "clocks": clk.summary(), "kernels": kernels, "init_s": round(init_s, 1), "run_wall_s": round(wall, 3),
+        "clocks": clk.summary(), "kernels": kernels, "tp_error": tp_error, "init_s": round(init_s, 1), "run_wall_s": round(wall, 3),
     }
     if args.sweep and rank == 0:
         sw = {}

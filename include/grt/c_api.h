@@ -260,6 +260,34 @@ grt_status grt_tp_emu_reset(grt_tp_emu* e);
 grt_status grt_tp_emu_step(grt_tp_emu* e, int32_t token);
 grt_status grt_tp_emu_logits(grt_tp_emu* e, float* out, int32_t n);
 
+/* ---- two-process split (the paper's IPC, PAPER.md "two processes") ------------
+ * Process B (graph generator) owns the model and replays the static pass;
+ * process A (context generator) runs the NVRTC dynamic ops -- sampler and
+ * preprocess -- directly on B's device memory, opened through
+ * cudaIpcOpenMemHandle.  Steps are ordered by two interprocess CUDA events; a
+ * host doorbell in POSIX shared memory only sequences the event record/wait
+ * calls (no data crosses the host).  Replaces the in-process Channel
+ * (pipeline.cpp:56-78). */
+typedef struct grt_ipc_desc {
+  uint8_t arena[64];      /* cudaIpcMemHandle_t of B's arena */
+  uint8_t ev_ctx[64];     /* cudaIpcEventHandle_t: A records after its dynamic ops */
+  uint8_t ev_static[64];  /* cudaIpcEventHandle_t: B records after the static pass */
+  uint64_t off_ctrl, off_tokens, off_uniforms, off_scratch, off_emb, off_pos, off_x, off_logits;
+  int32_t d_model, vocab, max_seq, weight_bf16, arch_ref, device, bucket_size, max_gen;
+} grt_ipc_desc;
+typedef struct grt_ipc_server grt_ipc_server;
+typedef struct grt_ipc_client grt_ipc_client;
+grt_status grt_ipc_server_create(grt_session* s, const char* shm_name, grt_ipc_desc* desc, grt_ipc_server** out);
+/* Serves n_passes static passes (prompt + generated tokens), blocking. */
+grt_status grt_ipc_server_serve(grt_ipc_server* sv, int32_t n_passes);
+grt_status grt_ipc_server_destroy(grt_ipc_server* sv);
+grt_status grt_ipc_client_create(const grt_ipc_desc* desc, const char* shm_name, grt_ipc_client** out);
+/* Runs prompt_len + gen_len passes against a serving process B; tokens[gen_len],
+ * per_token_us[gen_len] (device %globaltimer gaps, may be NULL). */
+grt_status grt_ipc_client_generate(grt_ipc_client* c, const int32_t* prompt, int32_t prompt_len, int32_t gen_len,
+                                   const grt_sample_params* sampling, int32_t* tokens, double* per_token_us);
+grt_status grt_ipc_client_destroy(grt_ipc_client* c);
+
 /* ---- op-level API on device pointers (kernel parity tests) ----------------- */
 /* out[n] = W[n,k] . x[k] with W in the device ([n,k], row-major) layout. */
 grt_status grt_op_gemv(const void* w, int32_t w_dtype, const float* x, float* out, int32_t n, int32_t k,

@@ -154,6 +154,35 @@ grt_status grt_tp_emu_logits(grt_tp_emu* e, float* out, int32_t n) {
   return guard([&] { e->e->logits(out, n); });
 }
 
+grt_status grt_ipc_server_create(grt_session* s, const char* shm_name, grt_ipc_desc* desc, grt_ipc_server** out) {
+  return guard([&] {
+    if (!s || !shm_name || !desc || !out) grt::raise(GRT_InvalidConfig, "null argument");
+    *out = grt::ipc_server_create(*s->s, *s->owner->m, shm_name, desc);
+  });
+}
+grt_status grt_ipc_server_serve(grt_ipc_server* sv, int32_t n_passes) {
+  return guard([&] { grt::ipc_server_serve(sv, n_passes); });
+}
+grt_status grt_ipc_server_destroy(grt_ipc_server* sv) {
+  return guard([&] { grt_ipc_server_free(sv); });
+}
+grt_status grt_ipc_client_create(const grt_ipc_desc* desc, const char* shm_name, grt_ipc_client** out) {
+  return guard([&] {
+    if (!desc || !shm_name || !out) grt::raise(GRT_InvalidConfig, "null argument");
+    *out = grt::ipc_client_create(desc, shm_name);
+  });
+}
+grt_status grt_ipc_client_generate(grt_ipc_client* c, const int32_t* prompt, int32_t prompt_len, int32_t gen_len,
+                                   const grt_sample_params* sampling, int32_t* tokens, double* per_token_us) {
+  return guard([&] {
+    if (!c || !prompt || !sampling || !tokens) grt::raise(GRT_InvalidConfig, "null argument");
+    grt::ipc_client_generate(c, prompt, prompt_len, gen_len, *sampling, tokens, per_token_us);
+  });
+}
+grt_status grt_ipc_client_destroy(grt_ipc_client* c) {
+  return guard([&] { grt_ipc_client_free(c); });
+}
+
 grt_status grt_model_destroy(grt_model* m) {
   return guard([&] { delete m; });
 }

@@ -357,6 +357,14 @@ StepResponse Session::serve(const StepRequest& req, bool allow_cache, const Mode
   return {req.step_index, StepPath::EagerFallback};
 }
 
+ExecGraphPtr Session::static_graph(int key) {
+  const int ck = cache_key(key, false);
+  if (auto hit = cache_->lookup(ck)) return *hit;
+  ExecGraphPtr g = capture_now(key, false, dev_->capture_stream());
+  cache_->insert(ck, g);
+  return g;
+}
+
 void Session::validate(const GenerationRequest& req) const {
   // Session::validate (pipeline.cpp:172-181)
   if (req.prompt.empty()) raise(GRT_EmptyPrompt, "run: prompt is empty");

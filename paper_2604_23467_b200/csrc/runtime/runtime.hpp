@@ -97,6 +97,7 @@ class Arena {
   size_t used() const { return used_; }
   size_t capacity() const { return cap_; }
   size_t allocations() const { return count_; }
+  char* base() const { return base_; }
 
  private:
   char* base_ = nullptr;
@@ -243,6 +244,8 @@ class Model {
   void attach_comm(TpComm* c) { comm_ = c; }
   TpComm* comm() const { return comm_; }
   float* logits_local_dev() const { return logits_local_; }
+  const void* emb_dev() const { return emb_; }
+  const void* pos_dev() const { return pos_ ? pos_ : emb_; }
   void reset_pass_sync() {
     cudaMemset(pass_sync_, 0, static_cast<size_t>(sync_ints()) * 4);
     cudaMemset(&ctrl_->err, 0, sizeof(int));
@@ -516,6 +519,11 @@ class Session {
     n_sampled_ = 0;
   }
 
+  // The static pass alone (no fused dynamic ops) for `key`, from the cache or
+  // captured now; used by the two-process split, where the dynamic ops run in
+  // the other process.
+  ExecGraphPtr static_graph(int key);
+
   GraphCache& cache() { return *cache_; }
   CudaDevice& device() { return *dev_; }
   const CacheConfig& cache_config() const { return cc_; }
@@ -583,4 +591,15 @@ class TpEmu {
   GrtCtrl* h_ctrl_ = nullptr;
 };
 
+// ---------------------------------------------------------------------------
+// two-process split (ipc.cpp)
+grt_ipc_server* ipc_server_create(Session& s, Model& m, const char* shm_name, grt_ipc_desc* d);
+void ipc_server_serve(grt_ipc_server* sv, int n_passes);
+grt_ipc_client* ipc_client_create(const grt_ipc_desc* d, const char* shm_name);
+void ipc_client_generate(grt_ipc_client* c, const int* prompt, int p, int n, const grt_sample_params& sp, int* tokens,
+                         double* per_token_us);
+
 }  // namespace grt
+
+void grt_ipc_server_free(grt_ipc_server* sv);
+void grt_ipc_client_free(grt_ipc_client* c);

@@ -161,6 +161,8 @@ EXPORTS = [
     "grt_graph_cache_query", "grt_profile_plan", "grt_trace_pass",
     "grt_tp_unique_id", "grt_model_attach_nccl", "grt_tp_emu_create", "grt_tp_emu_destroy", "grt_tp_emu_reset",
     "grt_tp_emu_step", "grt_tp_emu_logits",
+    "grt_ipc_server_create", "grt_ipc_server_serve", "grt_ipc_server_destroy", "grt_ipc_client_create",
+    "grt_ipc_client_generate", "grt_ipc_client_destroy",
 ]
 
 _lib = None
@@ -193,6 +195,14 @@ def lib():
         L.grt_model_decode_bytes.argtypes = [vp, C.c_int32, C.POINTER(C.c_uint64)]
         L.grt_session_create.argtypes = [vp, C.POINTER(_CacheConfig), C.POINTER(vp)]
         L.grt_tp_unique_id.argtypes = [C.c_char_p, C.c_int32]
+        L.grt_ipc_server_create.argtypes = [vp, C.c_char_p, C.c_char_p, C.POINTER(vp)]
+        L.grt_ipc_server_serve.argtypes = [vp, C.c_int32]
+        L.grt_ipc_server_destroy.argtypes = [vp]
+        L.grt_ipc_client_create.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(vp)]
+        L.grt_ipc_client_generate.argtypes = [vp, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
+                                              C.POINTER(_SampleParams), C.POINTER(C.c_int32),
+                                              C.POINTER(C.c_double)]
+        L.grt_ipc_client_destroy.argtypes = [vp]
         L.grt_model_attach_nccl.argtypes = [vp, C.c_char_p, C.c_int32]
         L.grt_tp_emu_create.argtypes = [C.POINTER(_ModelConfig), C.POINTER(vp)]
         L.grt_tp_emu_destroy.argtypes = [vp]
@@ -432,6 +442,56 @@ class Model:
         v = C.c_uint64()
         _check(lib().grt_model_decode_bytes(self._h, length, C.byref(v)))
         return v.value
+
+
+IPC_DESC_BYTES = 3 * 64 + 8 * 8 + 8 * 4  # sizeof(grt_ipc_desc)
+
+
+class IpcServer:
+    """Process B of the two-process split: serves static passes of `session`."""
+
+    def __init__(self, session: "Session", shm_name: str):
+        self.desc = C.create_string_buffer(IPC_DESC_BYTES)
+        h = C.c_void_p()
+        _check(lib().grt_ipc_server_create(session._h, shm_name.encode(), self.desc, C.byref(h)))
+        self._h = h
+        self.session = session
+
+    def descriptor(self) -> bytes:
+        return self.desc.raw
+
+    def serve(self, n_passes: int):
+        _check(lib().grt_ipc_server_serve(self._h, int(n_passes)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().grt_ipc_server_destroy(self._h)
+            self._h = None
+
+
+class IpcClient:
+    """Process A of the two-process split: NVRTC dynamic ops on B's memory."""
+
+    def __init__(self, descriptor: bytes, shm_name: str):
+        h = C.c_void_p()
+        self._desc = C.create_string_buffer(bytes(descriptor), IPC_DESC_BYTES)
+        _check(lib().grt_ipc_client_create(self._desc, shm_name.encode(), C.byref(h)))
+        self._h = h
+
+    def generate(self, prompt, gen_len: int, strategy: "SampleStrategy" = None, seed: int = 7):
+        import numpy as np
+        strategy = strategy or SampleStrategy.greedy()
+        pr = (C.c_int32 * len(prompt))(*prompt)
+        toks = (C.c_int32 * gen_len)()
+        us = (C.c_double * gen_len)()
+        sp = strategy._c(seed)
+        _check(lib().grt_ipc_client_generate(self._h, pr, len(prompt), gen_len, C.byref(sp), toks, us))
+        return list(toks), np.ctypeslib.as_array(us).copy()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().grt_ipc_client_destroy(self._h)
+            self._h = None
 
 
 def tp_unique_id() -> bytes:

@@ -6,6 +6,8 @@ reference's golden fixtures.  Tolerances (stated per test):
     wherever the oracle's top-2 margin exceeds 2e-2;
   * samplers: bit-exact token ids given identical logits.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -417,3 +419,50 @@ def test_tp_sharded_decode_matches_single_gpu(tp, kw, tol):
         emu.step(t)
         worst = max(worst, float(np.abs(ref.logits() - emu.logits()).max()))
     assert worst <= tol, worst
+
+
+# ------------------------------------------------------------ two-process split
+
+def _ipc_server_proc(q_desc, q_done, shm, cfg_kw, n_passes):
+    from paper_2604_23467_b200 import graphrt as gg
+    s = gg.Session(gg.ModelConfig(**cfg_kw), gg.CacheConfig(bucket_size=16, warmup_hi=0))
+    sv = gg.IpcServer(s, shm)
+    q_desc.put(sv.descriptor())
+    sv.serve(n_passes)
+    q_done.get(timeout=120)
+    sv.close()
+
+
+def _ipc_client_proc(q_desc, q_out, shm, prompt, n, kind):
+    from paper_2604_23467_b200 import graphrt as gg
+    c = gg.IpcClient(q_desc.get(timeout=120), shm)
+    strat = gg.SampleStrategy.greedy() if kind == "greedy" else gg.SampleStrategy.with_temperature(0.8)
+    toks, us = c.generate(prompt, n, strat, seed=7)
+    c.close()
+    q_out.put(toks)
+
+
+@pytest.mark.parametrize("kind,fixture", [("greedy", "tiny_ref_greedy.json"), ("temp", "tiny_ref_temp08.json")])
+def test_two_process_ipc_split_reproduces_reference(golden, kind, fixture):
+    """Context generator (NVRTC sampler + preprocess) and graph generator (bucket
+    graph replay) in two OS processes on one GPU, sharing the arena through
+    cudaIpcOpenMemHandle and ordered by interprocess events: the tokens are the
+    reference binary's, as in single-process hybrid mode."""
+    import multiprocessing as mp
+    gold = golden(fixture)
+    prompt, want = gold["prompt"], gold["tokens"]
+    n = len(want)
+    ctx = mp.get_context("spawn")
+    q_desc, q_done, q_out = ctx.Queue(), ctx.Queue(), ctx.Queue()
+    shm = f"/grt_ipc_test_{os.getpid()}_{kind}"
+    sv = ctx.Process(target=_ipc_server_proc, args=(q_desc, q_done, shm, {}, len(prompt) + n))
+    cl = ctx.Process(target=_ipc_client_proc, args=(q_desc, q_out, shm, prompt, n, kind))
+    sv.start()
+    cl.start()
+    try:
+        toks = q_out.get(timeout=180)
+    finally:
+        q_done.put(1)
+        cl.join(60)
+        sv.join(60)
+    assert toks == want
