@@ -43,10 +43,8 @@ __device__ __forceinline__ float grt_bf16_to_f32(unsigned short h) { return __ui
 // The zero rows the reference appends are overwritten by the static pass before
 // they are read (build_plan writes row length-1 before attention), so the
 // append reduces to the length bump.
-extern "C" __global__ void grt_preprocess(GrtCtrl* ctrl, const void* emb, const void* pos_table, float* x) {
+__device__ __forceinline__ void preprocess_impl(GrtCtrl* ctrl, const void* emb, const void* pos_table, float* x) {
   __shared__ int s_pos, s_tok, s_ok;
-  grt_launch_dependents();
-  grt_griddep_wait();
   if (threadIdx.x == 0) {
     const int pos = ctrl->seq_len;
     int ok = 1;
@@ -89,6 +87,12 @@ extern "C" __global__ void grt_preprocess(GrtCtrl* ctrl, const void* emb, const 
   }
   __syncthreads();
   if (threadIdx.x == 0) ctrl->seq_len = s_pos + 1;
+}
+
+extern "C" __global__ void grt_preprocess(GrtCtrl* ctrl, const void* emb, const void* pos_table, float* x) {
+  grt_launch_dependents();
+  grt_griddep_wait();
+  preprocess_impl(ctrl, emb, pos_table, x);
 }
 
 // ---------------------------------------------------------------------------
@@ -184,14 +188,12 @@ __device__ void radix_pick(u64* hist, int shift, u64& prefix, u64& mask, u64& ne
   __syncthreads();
 }
 
-extern "C" __global__ void __launch_bounds__(GRT_SAMPLE_THREADS) grt_sample(GrtCtrl* ctrl, const float* logits) {
+__device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) {
   __shared__ float redf[32];
   __shared__ u64 redu[32];
   __shared__ u64 hist[256];
   __shared__ int s_tok;
   __shared__ u64 s_t0;
-  grt_launch_dependents();
-  grt_griddep_wait();
   const int pos = ctrl->seq_len;
   if (pos < ctrl->prompt_len) return;  // prefill pass: the token is given
   const int step = pos - ctrl->prompt_len;
@@ -392,4 +394,22 @@ extern "C" __global__ void __launch_bounds__(GRT_SAMPLE_THREADS) grt_sample(GrtC
     }
     __threadfence_system();
   }
+}
+
+extern "C" __global__ void __launch_bounds__(GRT_SAMPLE_THREADS) grt_sample(GrtCtrl* ctrl, const float* logits) {
+  grt_launch_dependents();
+  grt_griddep_wait();
+  sample_impl(ctrl, logits);
+}
+
+// The fused dynamic block of one step (pipeline.cpp:87-93, submit_fused_block):
+// sample_token from the previous pass's logits, then extend_position + slot
+// append for the token just produced -- one launch instead of two.
+extern "C" __global__ void __launch_bounds__(GRT_SAMPLE_THREADS)
+    grt_sample_preprocess(GrtCtrl* ctrl, const float* logits, const void* emb, const void* pos_table, float* x) {
+  grt_launch_dependents();
+  grt_griddep_wait();
+  sample_impl(ctrl, logits);
+  __syncthreads();  // the sampled token (tokens[seq_len], written by thread 0) is visible block-wide
+  preprocess_impl(ctrl, emb, pos_table, x);
 }

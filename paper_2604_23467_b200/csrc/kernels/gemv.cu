@@ -90,6 +90,33 @@ __device__ __forceinline__ void load_x_pre(const float* x, const float4* gv, con
   consumer_sync();
 }
 
+// RMSNorm with the scale deferred: xs = x * gamma right away (the dots start
+// after ONE barrier), the per-thread sum of squares is reduced after the
+// streaming loop and 1/rms is applied to the finished dot products in the
+// epilogue: out = inv * sum_k W_k (x_k g_k) == sum_k W_k (x_k inv g_k).
+template <typename WT>
+__device__ __forceinline__ float load_x_rms_deferred(const float* x, const float4* gv, int k, float* xs) {
+  const int n4 = k >> 2;
+  float4 v[LOADX_MAXV];
+#pragma unroll
+  for (int i = 0; i < LOADX_MAXV; ++i) {
+    const int j4 = threadIdx.x + i * CONSUMER_THREADS;
+    v[i] = j4 < n4 ? *reinterpret_cast<const float4*>(x + 4 * j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float ss = 0.0f;
+#pragma unroll
+  for (int i = 0; i < LOADX_MAXV; ++i) {
+    const int j4 = threadIdx.x + i * CONSUMER_THREADS;
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    if (j4 < n4) {
+      const float4 g = gv[i];
+      xs_store4<WT>(xs, j4, k, make_float4(v[i].x * g.x, v[i].y * g.y, v[i].z * g.z, v[i].w * g.w));
+    }
+  }
+  consumer_sync();
+  return ss;
+}
+
 template <typename WT, int NORM, int EPI>
 __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -142,12 +169,8 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
   }
   __syncwarp();
   griddep_launch_dependents();
-  // Weights never depend on the previous kernel: fill the whole ring now.
-  if (lane == 0) {
-    const int pre = min(S, n_tasks);
-    for (int i = 0; i < pre; ++i) issue(i);
-  }
-  // norm weights are weights too: in registers before the dependency wait
+  // norm weights are weights too: in registers before the dependency wait, and
+  // requested BEFORE the ring fill so they do not queue behind 190 KB of weights
   constexpr bool HAS_G = NORM == NORM_RMS || NORM == NORM_LN;
   float4 gv[HAS_G ? LOADX_MAXV : 1], bv[NORM == NORM_LN ? LOADX_MAXV : 1];
   const bool pre_norm = p.k <= LOADX_MAXV * 4 * CONSUMER_THREADS;
@@ -163,10 +186,27 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
       }
     }
   }
+  // Weights never depend on the previous kernel: start filling the ring now
+  // (`pre_stages` slots; the rest right after the activation is in, so the
+  // successor's whole-grid burst does not delay its own activation load).
+  const int pre = min(min(S, p.pre_stages > 0 ? p.pre_stages : S), n_tasks);
+  if (lane == 0)
+    for (int i = 0; i < pre; ++i) issue(i);
   griddep_wait();
   op_stamp(p.trace, 1);
+  const bool defer = NORM == NORM_RMS && pre_norm && p.rms_defer;
+  float ss_part = 0.0f;
+  if (defer)
+    ss_part = load_x_rms_deferred<WT>(p.x, gv, p.k, xs);
+  else if (HAS_G && pre_norm)
+    load_x_pre<WT, (HAS_G ? NORM : NORM_RMS)>(p.x, gv, bv, p.eps, p.k, xs, red);
+  else
+    load_x<WT, NORM, false>(p.x, p.gamma, p.beta, p.eps, p.k, xs, red);
+  op_stamp(p.trace, 2);
+  if (lane == 0)
+    for (int i = pre; i < min(S, n_tasks); ++i) issue(i);
   if constexpr (EPI == EPI_QKV || EPI == EPI_QKV_ROPE) {
-    // L2 prefetch (and TLB warm-up) of this layer's K/V rows [0, seq_len-1) for
+    // (after the activation load, off its critical path) L2 prefetch (and TLB warm-up) of this layer's K/V rows [0, seq_len-1) for
     // the attention kernel: one contiguous [len, dh] run per (head, K|V).
     if (threadIdx.x == 0 && p.seq_len && static_cast<int>(blockIdx.x) < 2 * p.n_heads) {
       const int hh = blockIdx.x >> 1;
@@ -178,11 +218,6 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
         prefetch_l2_bulk(base + o, static_cast<uint32_t>(bytes - o < 65536 ? bytes - o : 65536));
     }
   }
-  if (HAS_G && pre_norm)
-    load_x_pre<WT, (HAS_G ? NORM : NORM_RMS)>(p.x, gv, bv, p.eps, p.k, xs, red);
-  else
-    load_x<WT, NORM, false>(p.x, p.gamma, p.beta, p.eps, p.k, xs, red);
-  op_stamp(p.trace, 2);
 
   EpiArgs ea;
   ea.out = p.out;
@@ -222,6 +257,8 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
   }
   if (warp == 0) op_stamp(p.trace, 5);
   consumer_sync();
+  float inv = 1.0f;
+  if (defer) inv = 1.0f / sqrtf(block_sum(ss_part, red) / static_cast<float>(p.k) + p.eps);
   // Epilogues run thread-parallel (one pair per thread): their own memory
   // round trips (residual read, RoPE table) are paid once per CTA.
   for (int pl = threadIdx.x; pl < pair_end - pair_begin; pl += CONSUMER_THREADS) {
@@ -231,7 +268,7 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
       vb += part[2 * (pl * nch + c) + 1];
     }
     const int pair = pair_begin + pl;
-    epilogue<EPI>(ea, pair, va, vb, 2 * pair + 1 < p.n_rows);
+    epilogue<EPI>(ea, pair, va * inv, vb * inv, 2 * pair + 1 < p.n_rows);
   }
   if (p.trace) {
     consumer_sync();
@@ -284,6 +321,20 @@ int gemv_max_stages() {
     return std::max(1, std::min(GEMV_MAX_STAGES, s));
   }();
   return v;
+}
+
+// ring slots filled before griddepcontrol.wait (env GRT_GEMV_PRE / GRT_GEMV_PRE_NORM
+// for the normed GEMVs; 0 = all)
+static int gemv_pre_stages(int norm) {
+  static const int v_none = [] {
+    const char* e = getenv("GRT_GEMV_PRE");
+    return e ? atoi(e) : 0;
+  }();
+  static const int v_norm = [] {
+    const char* e = getenv("GRT_GEMV_PRE_NORM");
+    return e ? atoi(e) : 0;
+  }();
+  return norm == NORM_NONE ? v_none : v_norm;
 }
 
 static int stages_for(int device, int rowb, int k, int part_bytes) {
@@ -353,6 +404,33 @@ cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s,
   grid = std::max(1, std::min(grid, (n_pairs * p.nch + GEMV_WARPS - 1) / GEMV_WARPS));
   const int part_bytes = max_pairs_per_cta(n_pairs, grid) * p.nch * 2 * 4;
   p.stages = stages_for(dev, p.rowb, p.k, part_bytes);
+  p.pre_stages = gemv_pre_stages(norm);
+  static const int defer = [] {
+    const char* e = getenv("GRT_RMS_DEFER");
+    return e ? atoi(e) : 1;
+  }();
+  p.rms_defer = defer;
+  const int n_pairs = (p.n_rows + 1) / 2;
+  int grid = grid_ctas > 0 ? grid_ctas : num_sms(dev);
+  grid = std::max(1, std::min(grid, (n_pairs * p.nch + GEMV_WARPS - 1) / GEMV_WARPS));
+  const int part_bytes = max_pairs_per_cta(n_pairs, grid) * p.nch * 2 * 4;
+  p.stages = stages_for(dev, p.rowb, p.k, part_bytes);
+  p.pre_stages = gemv_pre_stages(norm);
+  static const int defer = [] {
+    const char* e = getenv("GRT_RMS_DEFER");
+    return e ? atoi(e) : 1;
+  }();
+  p.rms_defer = defer;
+  if (p.next_w) {
+    static const uint32_t pf = [] {
+      const char* e = getenv("GRT_GEMV_NEXT_PF_KB");
+      return static_cast<uint32_t>((e ? atoi(e) : 0) * 1024);
+    }();
+    p.next_pf_bytes = pf;
+    int nch_n, ch_n, rowb_n;
+    chunking(wdt, p.next_k, &ch_n, &nch_n, &rowb_n);
+    p.next_grid = std::max(1, std::min(num_sms(dev), ((p.next_rows + 1) / 2 * nch_n + GEMV_WARPS - 1) / GEMV_WARPS));
+  }
   if (static_cast<int64_t>(GEMV_WARPS) * p.stages * 2 * p.rowb + p.k * 4 + part_bytes >
       smem_optin(dev) - kStaticSmemReserve)
     return cudaErrorInvalidValue;

@@ -432,6 +432,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   jit_ = jit_get(opts, cfg_.device);
   f_pre_ = jit_->fn("grt_preprocess");
   f_sample_ = jit_->fn("grt_sample");
+  f_sample_pre_ = jit_->fn("grt_sample_preprocess");
   cuda_check(cudaDeviceSynchronize(), "model init");
 }
 
@@ -940,6 +941,33 @@ KernelInvocation Model::make_preprocess_op() {
     float* a3 = x;
     void* args[] = {&a0, &a1, &a2, &a3};
     return launch_jit(f, dim3(1), dim3(threads), args, s, true);
+  };
+  return inv;
+}
+
+KernelInvocation Model::make_sample_preprocess_op() {
+  KernelInvocation inv;
+  inv.spec.name = "sample_token+extend_position";
+  inv.spec.op_class = OpClass::Dynamic;
+  inv.spec.flops = cfg_.vocab_size + 2LL * cfg_.d_model;
+  inv.spec.bytes = static_cast<int64_t>(cfg_.vocab_size) * 4 + static_cast<int64_t>(cfg_.d_model) * 6;
+  inv.bindings = {{ctrl_, sizeof(GrtCtrl)},
+                  {logits_, static_cast<size_t>(cfg_.vocab_size) * 4},
+                  {x_, static_cast<size_t>(cfg_.d_model) * 4}};
+  CUfunction f = f_sample_pre_;
+  GrtCtrl* ctrl = ctrl_;
+  const float* logits = logits_;
+  const void* emb = emb_;
+  const void* pos = pos_ ? pos_ : emb_;
+  float* x = x_;
+  inv.launch = [f, ctrl, logits, emb, pos, x](cudaStream_t s) {
+    GrtCtrl* a0 = ctrl;
+    const float* a1 = logits;
+    const void* a2 = emb;
+    const void* a3 = pos;
+    float* a4 = x;
+    void* args[] = {&a0, &a1, &a2, &a3, &a4};
+    return launch_jit(f, dim3(1), dim3(1024), args, s, true);
   };
   return inv;
 }

@@ -241,6 +241,7 @@ Session::Session(Model& model, const CacheConfig& cc) : model_(&model), cc_(cc) 
   cache_ = std::make_unique<GraphCache>(cc_.capacity, cc_.policy);
   pre_op_ = model.make_preprocess_op();
   sample_op_ = model.make_sample_op();
+  sample_pre_op_ = model.make_sample_preprocess_op();
   void* hc = nullptr;
   cuda_check(cudaHostAlloc(&hc, sizeof(GrtCtrl), cudaHostAllocDefault), "cudaHostAlloc ctrl");
   h_ctrl_ = static_cast<GrtCtrl*>(hc);
@@ -301,10 +302,7 @@ std::vector<const KernelInvocation*> Session::step_kernels(int key, bool fused) 
   const auto& plan = model_->plan(key, cc_.bucket_size, cc_.pass_impl);
   std::vector<const KernelInvocation*> ks;
   ks.reserve(plan.size() + 2);
-  if (fused) {
-    ks.push_back(&sample_op_);
-    ks.push_back(&pre_op_);
-  }
+  if (fused) ks.push_back(&sample_pre_op_);  // the dynamic block, one launch
   for (const auto& k : plan) ks.push_back(&k);
   return ks;
 }

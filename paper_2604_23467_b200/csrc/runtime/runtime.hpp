@@ -204,6 +204,7 @@ class Model {
   // Dynamic ops (DYNAMIC, NVRTC kernels; every runtime value read from ctrl).
   KernelInvocation make_preprocess_op();   // extend_position + slot append
   KernelInvocation make_sample_op();       // sample_token
+  KernelInvocation make_sample_preprocess_op();  // both, one launch (the fused dynamic block of a step graph)
 
   // Weight I/O in the reference layout.
   void upload(const std::string& name, const void* host, size_t bytes, int host_dtype);
@@ -300,7 +301,7 @@ class Model {
   volatile unsigned long long* h_out_stamps_ = nullptr;
   uint64_t weight_bytes_ = 0;
   std::shared_ptr<JitModule> jit_;
-  CUfunction f_pre_ = nullptr, f_sample_ = nullptr;
+  CUfunction f_pre_ = nullptr, f_sample_ = nullptr, f_sample_pre_ = nullptr;
   std::mutex plan_mu_;
   std::map<std::pair<int, int>, std::vector<KernelInvocation>> plans_;
   std::set<const void*> buffers_;
@@ -543,7 +544,7 @@ class Session {
   std::unique_ptr<CudaDevice> dev_;
   std::unique_ptr<CaptureEngine> engine_;
   std::unique_ptr<GraphCache> cache_;
-  KernelInvocation pre_op_, sample_op_;
+  KernelInvocation pre_op_, sample_op_, sample_pre_op_;
   std::mt19937_64 sampler_{7};
   int cur_len_ = 0;
   int n_sampled_ = 0;  // step-level sampler draws since sampler_reset (Philox counter / uniform index)
