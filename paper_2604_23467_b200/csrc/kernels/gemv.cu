@@ -410,27 +410,6 @@ cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s,
     return e ? atoi(e) : 1;
   }();
   p.rms_defer = defer;
-  const int n_pairs = (p.n_rows + 1) / 2;
-  int grid = grid_ctas > 0 ? grid_ctas : num_sms(dev);
-  grid = std::max(1, std::min(grid, (n_pairs * p.nch + GEMV_WARPS - 1) / GEMV_WARPS));
-  const int part_bytes = max_pairs_per_cta(n_pairs, grid) * p.nch * 2 * 4;
-  p.stages = stages_for(dev, p.rowb, p.k, part_bytes);
-  p.pre_stages = gemv_pre_stages(norm);
-  static const int defer = [] {
-    const char* e = getenv("GRT_RMS_DEFER");
-    return e ? atoi(e) : 1;
-  }();
-  p.rms_defer = defer;
-  if (p.next_w) {
-    static const uint32_t pf = [] {
-      const char* e = getenv("GRT_GEMV_NEXT_PF_KB");
-      return static_cast<uint32_t>((e ? atoi(e) : 0) * 1024);
-    }();
-    p.next_pf_bytes = pf;
-    int nch_n, ch_n, rowb_n;
-    chunking(wdt, p.next_k, &ch_n, &nch_n, &rowb_n);
-    p.next_grid = std::max(1, std::min(num_sms(dev), ((p.next_rows + 1) / 2 * nch_n + GEMV_WARPS - 1) / GEMV_WARPS));
-  }
   if (static_cast<int64_t>(GEMV_WARPS) * p.stages * 2 * p.rowb + p.k * 4 + part_bytes >
       smem_optin(dev) - kStaticSmemReserve)
     return cudaErrorInvalidValue;
