@@ -321,7 +321,8 @@ def main():
                 "d2h_bytes_per_step": 4 + 16},
         "gpu_launches": int(round(nodes_per_step * K + r.counters.kernel_launches * K / n)),
         "host_kernel_launches_per_step": r.counters.kernel_launches / n,
-        "graph_launches_per_step": r.counters.graph_replays / (P + n),
+        "graph_launches_per_step": r.counters.graph_replays / (n + (0 if args.batched_prefill else P)),
+        "prefill": "batched tcgen05 (one pass over the prompt)" if args.batched_prefill else "token-by-token graphs",
         "clocks": clk.summary(), "kernels": kernels, "tp_error": tp_error, "init_s": round(init_s, 1), "run_wall_s": round(wall, 3),
     }
     if args.sweep and rank == 0:
