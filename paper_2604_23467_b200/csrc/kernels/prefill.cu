@@ -11,6 +11,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -228,6 +229,179 @@ cudaError_t launch_prefill_rmsnorm(const float* X, int P, const float* gamma, fl
   return cudaGetLastError();
 }
 
+// ---- tensor-core flash attention (bf16 KV) ------------------------------------
+// FA2-style on mma.sync.m16n8k16 (bf16 in, fp32 accumulate): a CTA = one head x
+// 64 queries (4 warps x 16 rows); 64-key K/V tiles staged in shared memory
+// (zero rows past the causal end); S = Q K^T and O += P V from ldmatrix
+// fragments, the S accumulator re-packed in registers as the P operand; online
+// softmax per row.  Attention is ~1% of the prefill flops, so the
+// legacy tensor path is enough here; the projections are the tcgen05 GEMMs.
+constexpr int FA_WARPS = 4, FA_QB = 64, FA_KB = 64;
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+template <int DH>
+__global__ void __launch_bounds__(FA_WARPS * 32)
+    prefill_fa_kernel(const float* Q, const __nv_bfloat16* k_cache, const __nv_bfloat16* v_cache, int start, int P,
+                      int d, int max_seq, float scale, __nv_bfloat16* out) {
+  constexpr int LD = DH + 8;  // bf16 row stride: 16-byte aligned, conflict-free ldmatrix
+  constexpr int KS = DH / 16, NB = DH / 8;
+  extern __shared__ __align__(16) uint8_t fa_smem[];
+  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(fa_smem);
+  __nv_bfloat16* Ks = Qs + FA_QB * LD;
+  __nv_bfloat16* Vs = Ks + FA_KB * LD;
+  const int head = blockIdx.y, q0 = blockIdx.x * FA_QB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int nq = min(FA_QB, P - q0);
+  const __nv_bfloat16* Kh = k_cache + static_cast<int64_t>(head) * max_seq * DH;
+  const __nv_bfloat16* Vh = v_cache + static_cast<int64_t>(head) * max_seq * DH;
+
+  for (int e = threadIdx.x; e < FA_QB * DH / 2; e += FA_WARPS * 32) {
+    const int r = e / (DH / 2), c = 2 * (e - r * (DH / 2));
+    float2 v = make_float2(0.f, 0.f);
+    if (r < nq) v = *reinterpret_cast<const float2*>(Q + static_cast<int64_t>(q0 + r) * d + head * DH + c);
+    *reinterpret_cast<__nv_bfloat162*>(&Qs[r * LD + c]) = __floats2bfloat162_rn(v.x, v.y);
+  }
+  __syncthreads();
+  uint32_t qf[KS][4];
+  {
+    const int r = 16 * warp + (lane & 7) + ((lane >> 3) & 1) * 8;
+    const int c = (lane >> 4) * 8;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+      ldsm_x4(smem_u32(&Qs[r * LD + 16 * ks + c]), qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3]);
+  }
+  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+  float o[NB][4];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.0f;
+  const int qpos0 = start + q0 + 16 * warp + g;  // rows g and g+8 of this warp
+  const int last_pos = start + q0 + nq - 1;
+
+  for (int kb = 0; kb <= last_pos; kb += FA_KB) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < FA_KB * DH / 8; e += FA_WARPS * 32) {
+      const int r = e / (DH / 8), c = 8 * (e - r * (DH / 8));
+      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+      if (kb + r <= last_pos) {
+        kv = *reinterpret_cast<const uint4*>(Kh + static_cast<int64_t>(kb + r) * DH + c);
+        vv = *reinterpret_cast<const uint4*>(Vh + static_cast<int64_t>(kb + r) * DH + c);
+      }
+      *reinterpret_cast<uint4*>(&Ks[r * LD + c]) = kv;
+      *reinterpret_cast<uint4*>(&Vs[r * LD + c]) = vv;
+    }
+    __syncthreads();
+    float sacc[FA_KB / 8][4];
+#pragma unroll
+    for (int nb = 0; nb < FA_KB / 8; ++nb) sacc[nb][0] = sacc[nb][1] = sacc[nb][2] = sacc[nb][3] = 0.0f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+      for (int nb = 0; nb < FA_KB / 8; nb += 2) {
+        // matrices: (keys 8nb.., dh 16ks..), (keys 8nb.., dh 16ks+8..), then nb+1
+        const int r = 8 * nb + (lane & 7) + (lane >> 4) * 8;
+        const int c = 16 * ks + ((lane >> 3) & 1) * 8;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(smem_u32(&Ks[r * LD + c]), b0, b1, b2, b3);
+        mma_bf16(sacc[nb], qf[ks], b0, b1);
+        mma_bf16(sacc[nb + 1], qf[ks], b2, b3);
+      }
+    }
+    // scale, causal mask, online softmax over rows g (i=0) and g+8 (i=1)
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int nb = 0; nb < FA_KB / 8; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = e >> 1;
+        const int key = kb + 8 * nb + 2 * t + (e & 1);
+        const float v = key <= qpos0 + 8 * i ? sacc[nb][e] * scale : -INFINITY;
+        sacc[nb][e] = v;
+        mx[i] = fmaxf(mx[i], v);
+      }
+    float f[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], 1));
+      mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], 2));
+      const float mn = fmaxf(m[i], mx[i]);
+      f[i] = (m[i] == -INFINITY) ? 0.0f : __expf(m[i] - mn);
+      m[i] = mn;
+      l[i] *= f[i];
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      o[j][0] *= f[0];
+      o[j][1] *= f[0];
+      o[j][2] *= f[1];
+      o[j][3] *= f[1];
+    }
+#pragma unroll
+    for (int nb = 0; nb < FA_KB / 8; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = e >> 1;
+        const float pv = sacc[nb][e] == -INFINITY ? 0.0f : __expf(sacc[nb][e] - m[i]);
+        sacc[nb][e] = pv;
+        l[i] += pv;
+      }
+    // O += P V  (P re-packed from the S accumulators as m16n8k16 A fragments)
+#pragma unroll
+    for (int kk = 0; kk < FA_KB / 16; ++kk) {
+      const uint32_t a[4] = {pack_bf16(sacc[2 * kk][0], sacc[2 * kk][1]), pack_bf16(sacc[2 * kk][2], sacc[2 * kk][3]),
+                             pack_bf16(sacc[2 * kk + 1][0], sacc[2 * kk + 1][1]),
+                             pack_bf16(sacc[2 * kk + 1][2], sacc[2 * kk + 1][3])};
+#pragma unroll
+      for (int jn = 0; jn < NB; jn += 2) {
+        // transposed matrices: (keys 16kk.., dh 8jn..), (keys 16kk+8.., dh 8jn..), then dh 8jn+8
+        const int r = 16 * kk + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int c = 8 * jn + (lane >> 4) * 8;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(smem_u32(&Vs[r * LD + c]), b0, b1, b2, b3);
+        mma_bf16(o[jn], a, b0, b1);
+        mma_bf16(o[jn + 1], a, b2, b3);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    l[i] += __shfl_xor_sync(0xffffffffu, l[i], 1);
+    l[i] += __shfl_xor_sync(0xffffffffu, l[i], 2);
+  }
+  const int r0 = 16 * warp + g;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + 8 * i;
+    if (r >= nq) continue;
+    const float inv = 1.0f / l[i];
+    __nv_bfloat16* op = out + static_cast<int64_t>(q0 + r) * d + head * DH + 2 * t;
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      *reinterpret_cast<__nv_bfloat162*>(op + 8 * j) = __floats2bfloat162_rn(o[j][2 * i] * inv, o[j][2 * i + 1] * inv);
+  }
+}
+
 template <typename KT, int DH>
 static cudaError_t attn_launch(const float* Q, const void* k, const void* v, int start, int P, int d, int n_heads,
                                int max_seq, float scale, void* out, cudaStream_t s) {
@@ -257,8 +431,38 @@ static cudaError_t attn_dispatch(int dh, const float* Q, const void* k, const vo
   }
 }
 
+template <int DH>
+static cudaError_t fa_launch(const float* Q, const void* k, const void* v, int start, int P, int d, int n_heads,
+                             int max_seq, float scale, void* out, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(FA_QB + 2 * FA_KB) * (DH + 8) * 2;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_fa_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((P + FA_QB - 1) / FA_QB, n_heads);
+  prefill_fa_kernel<DH><<<grid, FA_WARPS * 32, smem, s>>>(Q, static_cast<const __nv_bfloat16*>(k),
+                                                        static_cast<const __nv_bfloat16*>(v), start, P, d, max_seq,
+                                                        scale, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError();
+}
+
+static int fa_enabled() {
+  static const int v = [] {
+    const char* e = getenv("GRT_PREFILL_FA");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, const void* v, int start, int P, int d,
                                      int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s) {
+  if (kvdt == Dt::BF16 && fa_enabled()) {  // tensor cores (mma.sync) for bf16 KV
+    if (dh == 64) return fa_launch<64>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+    if (dh == 128) return fa_launch<128>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+  }
   if (kvdt == Dt::BF16) return attn_dispatch<__nv_bfloat16>(dh, Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
   return attn_dispatch<float>(dh, Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
 }
