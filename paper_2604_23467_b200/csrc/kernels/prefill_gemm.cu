@@ -191,6 +191,10 @@ __device__ __forceinline__ void pg_epilogue16(const PrefillGemmParams& p, int m,
   }
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // mbarrier wait for threads that idle through the main loop: back off so they
 // do not steal issue slots from the TMA / MMA threads on their SM sub-partition
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
@@ -198,44 +202,55 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 }
 
 // ---- the kernel -----------------------------------------------------------------
-// grid = m_tiles x n_tiles x ksplit.  A CTA owns one 128-row weight tile, one
-// tile of `ntile` tokens and one K range; each pipeline stage carries `kbox`
-// 64-wide K boxes (kbox * 128 contiguous bytes per weight row).
+// Persistent: grid = min(work items, SMs); work item w = (m tile, n tile, k
+// split), CTA c takes items c, c + grid, ...  The TMA producer streams stages
+// across item boundaries; the accumulator is double-buffered in TMEM (2 x ntile
+// fp32 columns), so the epilogue of item i overlaps the MMAs of item i+1.
+// Each pipeline stage carries `kbox` 64-wide K boxes (kbox*128 contiguous bytes
+// per weight row).
 
 __global__ void __launch_bounds__(PG_THREADS, 1)
     prefill_gemm_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                         const PrefillGemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ uint64_t full[8], empty[8], acc_bar;
+  __shared__ uint64_t full[8], empty[8], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ int s_last;
+  __shared__ int s_last[2];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int split = blockIdx.x % p.ksplit;
-  const int mn = blockIdx.x / p.ksplit;
-  const int n_tile = mn % p.n_ntiles, m_tile = mn / p.n_ntiles;
-  const int m0 = m_tile * PG_BM, n0 = n_tile * p.ntile;
+  const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
+  const int n_items = m_tiles * p.n_ntiles * p.ksplit;
   const int kstep = PG_BK * p.kbox;
   const int nkb = p.K / kstep;
-  const int kb0 = static_cast<int>(static_cast<int64_t>(split) * nkb / p.ksplit);
-  const int kb1 = static_cast<int>(static_cast<int64_t>(split + 1) * nkb / p.ksplit);
   const int S = p.stages;
   const uint32_t a_box = PG_BM * PG_BK * 2;
   const uint32_t b_box = static_cast<uint32_t>(p.ntile) * PG_BK * 2;
   const uint32_t stage_bytes = p.kbox * (a_box + b_box);
   uint32_t cols = 32;
-  while (cols < static_cast<uint32_t>(p.ntile)) cols <<= 1;
+  while (cols < static_cast<uint32_t>(2 * p.ntile)) cols <<= 1;
+
+  auto decode = [&](int w, int& m_tile, int& n_tile, int& split, int& kb0, int& kb1) {
+    split = w % p.ksplit;
+    const int mn = w / p.ksplit;
+    n_tile = mn % p.n_ntiles;
+    m_tile = mn / p.n_ntiles;
+    kb0 = static_cast<int>(static_cast<int64_t>(split) * nkb / p.ksplit);
+    kb1 = static_cast<int>(static_cast<int64_t>(split + 1) * nkb / p.ksplit);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(&acc_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
+    }
     mbar_fence_init();
   }
-  if (warp == 1) {  // TMEM accumulator: 128 lanes (weight rows) x ntile fp32 columns (tokens)
+  if (warp == 1) {  // TMEM: 128 lanes (weight rows) x 2 buffers of ntile fp32 columns (tokens)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "r"(cols)
                  : "memory");
@@ -250,82 +265,107 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       griddep_wait();
-      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
-        const int s = i % S;
-        mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
-        uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
-        for (int j = 0; j < p.kbox; ++j) {
-          const int k0 = kb * kstep + j * PG_BK;
-          tma_load_2d(st + j * a_box, &map_w, k0, m0, &full[s]);
-          tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, k0, n0, &full[s]);
+      int i = 0;  // global stage counter across items
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+        int m_tile, n_tile, split, kb0, kb1;
+        decode(w, m_tile, n_tile, split, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+          const int s = i % S;
+          mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+          uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          for (int j = 0; j < p.kbox; ++j) {
+            const int k0 = kb * kstep + j * PG_BK;
+            tma_load_2d(st + j * a_box, &map_w, k0, m_tile * PG_BM, &full[s]);
+            tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, k0, n_tile * p.ntile, &full[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(p.ntile);
-      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
-        const int s = i % S;
-        mbar_wait(&full[s], (i / S) & 1);
+      int i = 0, it = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+        int m_tile, n_tile, split, kb0, kb1;
+        decode(w, m_tile, n_tile, split, kb0, kb1);
+        const int buf = it & 1;
+        mbar_wait(&acc_empty[buf], ((it >> 1) & 1) ^ 1);  // epilogue has drained this buffer
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
-        const uint32_t sb = sa + p.kbox * a_box;
-        for (int j = 0; j < p.kbox; ++j) {
+        const uint32_t acc = tmem + buf * p.ntile;
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+          const int s = i % S;
+          mbar_wait(&full[s], (i / S) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
+          const uint32_t sb = sa + p.kbox * a_box;
+          for (int j = 0; j < p.kbox; ++j) {
 #pragma unroll
-          for (int k = 0; k < PG_BK / PG_UK; ++k) {
-            const uint64_t ad = sw128_desc(sa + j * a_box + k * PG_UK * 2);
-            const uint64_t bd = sw128_desc(sb + j * b_box + k * PG_UK * 2);
-            tc_mma_bf16(tmem, ad, bd, idesc, (i > 0 || j > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < PG_BK / PG_UK; ++k) {
+              const uint64_t ad = sw128_desc(sa + j * a_box + k * PG_UK * 2);
+              const uint64_t bd = sw128_desc(sb + j * b_box + k * PG_UK * 2);
+              tc_mma_bf16(acc, ad, bd, idesc, (kb > kb0 || j > 0 || k > 0) ? 1u : 0u);
+            }
           }
+          tc_commit(&empty[s]);  // frees the slot once these MMAs have read it
         }
-        tc_commit(&empty[s]);  // frees the slot once these MMAs have read it
+        tc_commit(&acc_full[buf]);  // this item's accumulator is complete
       }
-      tc_commit(&acc_bar);  // accumulator complete
     }
     __syncwarp();
   } else {
     // epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31 = weight rows
     const int lane_base = 32 * (warp & 3);
-    const int m = m0 + lane_base + lane;
-    mbar_wait_sleep(&acc_bar, 0);
-    tc_fence_after();
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(lane_base) << 16);
     const bool split_k = p.ksplit > 1;
-    const int tile_id = m_tile * p.n_ntiles + n_tile;
-    float* mypart = split_k ? p.part + (static_cast<int64_t>(tile_id) * p.ksplit + split) * p.ntile * PG_BM : nullptr;
-    const int n_valid = min(p.ntile, p.P - n0);
-    for (int c0 = 0; c0 < n_valid; c0 += 16) {
-      float v[16];
-      tc_ld16(t_lane + c0, v);
-      if (split_k) {
+    int it = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      int m_tile, n_tile, split, kb0, kb1;
+      decode(w, m_tile, n_tile, split, kb0, kb1);
+      const int buf = it & 1;
+      const int m = m_tile * PG_BM + lane_base + lane;
+      const int n0 = n_tile * p.ntile;
+      const int n_valid = min(p.ntile, p.P - n0);
+      mbar_wait_sleep(&acc_full[buf], (it >> 1) & 1);
+      tc_fence_after();
+      const int tile_id = m_tile * p.n_ntiles + n_tile;
+      float* mypart = split_k ? p.part + (static_cast<int64_t>(tile_id) * p.ksplit + split) * p.ntile * PG_BM : nullptr;
+      for (int c0 = 0; c0 < n_valid; c0 += 16) {
+        float v[16];
+        tc_ld16(t_lane + buf * p.ntile + c0, v);
+        if (split_k) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) mypart[static_cast<int64_t>(c0 + j) * PG_BM + lane_base + lane] = v[j];
-      } else {
-        pg_epilogue16(p, m, n0 + c0, min(16, n_valid - c0), v);
-      }
-    }
-    if (split_k) {
-      // the last CTA of this output tile sums the partials in split order
-      __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (warp == 2 && lane == 0) s_last = atomicAdd(p.counters + tile_id, 1) == p.ksplit - 1;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (s_last) {
-        __threadfence();
-        const float* base = p.part + static_cast<int64_t>(tile_id) * p.ksplit * p.ntile * PG_BM + lane_base + lane;
-        for (int n = 0; n < n_valid; n += 16) {
-          float v[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u) v[u] = 0.0f;
-          for (int s = 0; s < p.ksplit; ++s) {
-#pragma unroll
-            for (int u = 0; u < 16; ++u)
-              if (n + u < n_valid) v[u] += __ldcg(base + (static_cast<int64_t>(s) * p.ntile + n + u) * PG_BM);
-          }
-          pg_epilogue16(p, m, n0 + n, min(16, n_valid - n), v);
+          for (int j = 0; j < 16; ++j) mypart[static_cast<int64_t>(c0 + j) * PG_BM + lane_base + lane] = v[j];
+        } else {
+          pg_epilogue16(p, m, n0 + c0, min(16, n_valid - c0), v);
         }
-        if (warp == 2 && lane == 0) p.counters[tile_id] = 0;  // self-reset
+      }
+      // accumulator drained: hand the buffer back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (split_k) {
+        // the last CTA of this output tile sums the partials in split order
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) s_last[buf] = atomicAdd(p.counters + tile_id, 1) == p.ksplit - 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_last[buf]) {
+          __threadfence();
+          const float* base = p.part + static_cast<int64_t>(tile_id) * p.ksplit * p.ntile * PG_BM + lane_base + lane;
+          for (int n = 0; n < n_valid; n += 16) {
+            float v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = 0.0f;
+            for (int sp = 0; sp < p.ksplit; ++sp) {
+#pragma unroll
+              for (int u = 0; u < 16; ++u)
+                if (n + u < n_valid) v[u] += __ldcg(base + (static_cast<int64_t>(sp) * p.ntile + n + u) * PG_BM);
+            }
+            pg_epilogue16(p, m, n0 + n, min(16, n_valid - n), v);
+          }
+          if (warp == 2 && lane == 0) p.counters[tile_id] = 0;  // self-reset
+        }
       }
     }
   }
@@ -382,7 +422,7 @@ static PgShape pg_shape(int M, int K, int P, int sms) {
   sh.kbox = 1;
   sh.ksplit = 1;
   if (P <= 64) {
-    // memory-bound: one N tile; split K so the tiles fill (but do not overflow) one wave
+    // memory-bound: one N tile; split K so the items fill (but do not overflow) one wave
     sh.ntile = (P + 15) / 16 * 16;
     sh.n_ntiles = 1;
     sh.kbox = (K % (4 * PG_BK) == 0) ? 4 : ((K % (2 * PG_BK) == 0) ? 2 : 1);
@@ -390,20 +430,13 @@ static PgShape pg_shape(int M, int K, int P, int sms) {
     sh.ksplit = std::max(1, std::min({sms / m_tiles, nkb, 8}));
     return sh;
   }
-  // compute-bound: pick the token tile (16..256) minimising waves x per-tile time
-  double best = 1e30;
-  for (int nt = 64; nt <= PG_MAX_NT; nt += 16) {
-    const int n_tiles = (P + nt - 1) / nt;
-    const int nt_used = ((P + n_tiles - 1) / n_tiles + 15) / 16 * 16;
-    const int ctas = m_tiles * n_tiles;
-    const double waves = static_cast<double>((ctas + sms - 1) / sms);
-    const double cost = waves * (nt_used + 48);  // 48 ~ fixed per-tile cost (fill, epilogue) in token units
-    if (cost < best) {
-      best = cost;
-      sh.ntile = nt_used;
-      sh.n_ntiles = n_tiles;
-    }
-  }
+  // compute-bound: the widest token tile (<= 256, TMEM holds two): operand bytes
+  // per flop fall as N grows.  Measured (P=500): narrower tiles to occupy more
+  // SMs, or split-K with a last-CTA reduction, are both slower for the small-M
+  // GEMMs (Wo, down) than 64 wide tiles.
+  sh.n_ntiles = (P + PG_MAX_NT - 1) / PG_MAX_NT;
+  sh.ntile = ((P + sh.n_ntiles - 1) / sh.n_ntiles + 15) / 16 * 16;
+  (void)m_tiles;
   return sh;
 }
 
@@ -437,6 +470,7 @@ cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams 
   if (p.ksplit > 1 && (!p.part || !p.counters)) return cudaErrorInvalidValue;
   const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
   if (p.ksplit > 1 && m_tiles * p.n_ntiles > 4096) return cudaErrorInvalidValue;
+  const int n_items = m_tiles * p.n_ntiles * p.ksplit;
   const int stage_bytes = p.kbox * (PG_BM * PG_BK * 2 + p.ntile * PG_BK * 2);
   const int budget = 220 * 1024 - 1024;
   p.stages = std::min(8, budget / stage_bytes);
@@ -445,7 +479,7 @@ cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams 
   if (!make_map(&mw, w, p.M, p.K, PG_BM)) return cudaErrorInvalidValue;
   if (!make_map(&mx, x, p.P, p.K, p.ntile)) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(m_tiles * p.n_ntiles * p.ksplit);
+  cfg.gridDim = dim3(std::min(n_items, num_sms(dev)));
   cfg.blockDim = dim3(PG_THREADS);
   cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + 1024;
   cfg.stream = s;
