@@ -136,6 +136,80 @@ def cpu_model():
     return None
 
 
+def mixed_leg(g, model, cc, n_req, dist):
+    """BASELINE configs[3]: seeded top-p (T=0.8, p=0.9) through the NVRTC sampler,
+    mixed prompt lengths in [10, 500], on a COLD graph cache (new buckets are
+    captured asynchronously while the eager path serves them): tail latency."""
+    import random
+    from dataclasses import replace
+    rng = random.Random(11)
+    s2 = g.Session(model, replace(cc, warmup_hi=0))
+    gaps, ttfts, captures = [], [], 0
+    strat = g.SampleStrategy.top_kp(0.8, 0, 0.9)
+    for _ in range(n_req):
+        p = rng.randint(10, 500)
+        prompt = [rng.randrange(32000) for _ in range(p)]
+        r = s2.run(g.GenerationRequest(prompt=prompt, gen_len=64, strategy=strat, sampler_seed=7))
+        gaps += r.per_token_us[1:]
+        ttfts.append(r.ttft_us / 1000)
+        captures += r.captures_completed
+    out = {"requests": n_req, "sampling": "top-p 0.9, T 0.8, Philox seed 7", "graph_cache": "cold",
+           "p50_ms": round(reduce_max(dist, percentile(gaps, 50) / 1000), 4),
+           "p99_ms": round(reduce_max(dist, percentile(gaps, 99) / 1000), 4),
+           "max_ms": round(reduce_max(dist, max(gaps) / 1000), 4),
+           "ttft_mean_ms": round(reduce_max(dist, sum(ttfts) / len(ttfts)), 3), "captures": captures}
+    out["p99_over_p50"] = round(out["p99_ms"] / out["p50_ms"], 4)
+    return out
+
+
+def _ipc_server(q_desc, q_done, layers, max_seq, bucket, n_passes):
+    from paper_2604_23467_b200 import graphrt as g
+    cfg = g.ModelConfig.llama2_7b(n_layers=layers, max_seq_len=max_seq)
+    s = g.Session(cfg, g.CacheConfig(bucket_size=bucket, warmup_hi=10 ** 6 // bucket, capacity=4096))
+    sv = g.IpcServer(s, f"/grt_bench_{os.getppid()}")
+    q_desc.put(sv.descriptor())
+    for n in n_passes:
+        sv.serve(n)
+    q_done.get(timeout=600)
+    sv.close()
+
+
+def _ipc_client(q_desc, q_out, prompt, gens):
+    from paper_2604_23467_b200 import graphrt as g
+    c = g.IpcClient(q_desc.get(timeout=600), f"/grt_bench_{os.getppid()}")
+    res = []
+    for n in gens:
+        toks, us = c.generate(prompt, n)
+        res.append(list(us))
+    c.close()
+    q_out.put(res)
+
+
+def ipc_leg(layers, max_seq, bucket):
+    """The paper's two-process split (context generator / graph generator) over
+    cudaIpc memory + event handles, 7B, P=10, greedy: per-token p50/p99 of the
+    second of two runs (the first warms both processes)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    prompt = [(i * 7919 + 17) % 32000 for i in range(10)]
+    gens = [32, 128]
+    qd, qdone, qo = ctx.Queue(), ctx.Queue(), ctx.Queue()
+    sv = ctx.Process(target=_ipc_server, args=(qd, qdone, layers, max_seq, bucket, [10 + n for n in gens]))
+    cl = ctx.Process(target=_ipc_client, args=(qd, qo, prompt, gens))
+    sv.start()
+    cl.start()
+    try:
+        res = qo.get(timeout=900)
+    finally:
+        qdone.put(1)
+        cl.join(120)
+        sv.join(120)
+    us = res[-1][3:]
+    return {"prompt": 10, "gen": gens[-1], "p50_ms": round(percentile(us, 50) / 1000, 4),
+            "p99_ms": round(percentile(us, 99) / 1000, 4),
+            "note": "two OS processes on one GPU (time-sliced contexts, no MPS); single-process hybrid is the fast path"}
+
+
 def dist_setup(n):
     if n <= 1 or "RANK" not in os.environ:
         return 0, 1, 0, None
@@ -192,7 +266,11 @@ def main():
     ap.add_argument("--pass-impl", type=int, default=1, help="1 per-op kernel graph (default), 0 persistent single-kernel pass")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
-    ap.add_argument("--sweep", default="", help="comma list of prompt lengths for a TTFT sweep (extra key)")
+    ap.add_argument("--sweep", default="10,50,100,200,500",
+                    help="comma list of prompt lengths for the TTFT sweep (BASELINE configs[2]; '' = off)")
+    ap.add_argument("--mixed", type=int, default=6,
+                    help="requests of the cold-cache top-p / mixed-prompt-length leg (configs[3]; 0 = off)")
+    ap.add_argument("--ipc", type=int, default=1, help="1: also time the two-process (cudaIpc) split (N=1 only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -325,15 +403,23 @@ def main():
         "prefill": "batched tcgen05 (one pass over the prompt)" if args.batched_prefill else "token-by-token graphs",
         "clocks": clk.summary(), "kernels": kernels, "tp_error": tp_error, "init_s": round(init_s, 1), "run_wall_s": round(wall, 3),
     }
-    if args.sweep and rank == 0:
+    if args.sweep:  # every rank runs it (TP collectives), rank 0 reports
         sw = {}
         for pl in [int(x) for x in args.sweep.split(",") if x]:
             pr = po.make_prompt(42, pl, 32000)
             rr = sess.run(g.GenerationRequest(mode=mode, prompt=pr, gen_len=min(128, max_seq - pl)))
             gg = rr.per_token_us[3:]
-            sw[str(pl)] = {"ttft_ms": round(rr.ttft_us / 1000, 3), "p50_ms": round(percentile(gg, 50) / 1000, 4),
-                           "p99_ms": round(percentile(gg, 99) / 1000, 4)}
+            sw[str(pl)] = {"ttft_ms": round(reduce_max(dist, rr.ttft_us / 1000), 3),
+                           "p50_ms": round(reduce_max(dist, percentile(gg, 50) / 1000), 4),
+                           "p99_ms": round(reduce_max(dist, percentile(gg, 99) / 1000), 4)}
         line["ttft_sweep"] = sw
+    if args.mixed > 0:
+        line["topp_mixed"] = mixed_leg(g, sess.model, cc, args.mixed, dist)
+    if args.ipc and world == 1 and rank == 0:
+        try:
+            line["ipc_split"] = ipc_leg(args.layers, max_seq, args.bucket)
+        except Exception as e:  # reported, never silent
+            line["ipc_split"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:
