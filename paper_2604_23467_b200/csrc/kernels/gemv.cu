@@ -30,7 +30,7 @@
 namespace grt {
 
 constexpr int GEMV_WARPS = 8;
-constexpr int GEMV_MAX_STAGES = 4;
+constexpr int GEMV_MAX_STAGES = 8;
 constexpr int GEMV_THREADS = GEMV_WARPS * 32;
 
 // Activation prologue with the norm weights already in registers (they are
@@ -305,8 +305,18 @@ static int smem_optin(int device) {
 }
 
 // chunking of a k-long row: near-equal chunks of <= CH elements, multiple of 8
-static void chunking(Dt wdt, int k, int* ch, int* nch, int* rowb) {
-  const int chmax = wdt == Dt::BF16 ? WTraits<__nv_bfloat16>::CH : WTraits<float>::CH;
+static int chmax_override() {
+  static const int v = [] {
+    const char* e = getenv("GRT_GEMV_CHMAX");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+static void chunking(Dt wdt, int k, int* ch, int* nch, int* rowb, int chmax_hint = 0) {
+  int chmax = wdt == Dt::BF16 ? WTraits<__nv_bfloat16>::CH : WTraits<float>::CH;
+  if (chmax_hint > 0 && wdt == Dt::BF16) chmax = chmax_hint;
+  if (chmax_override() > 0 && wdt == Dt::BF16) chmax = chmax_override();
   *nch = (k + chmax - 1) / chmax;
   *ch = ((k + *nch - 1) / *nch + 7) / 8 * 8;
   *rowb = ((*ch * (wdt == Dt::BF16 ? 2 : 4) + 15) / 16) * 16;
@@ -398,7 +408,7 @@ cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s,
   if (p.k % 8 != 0 || p.n_rows < 1) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);
-  chunking(wdt, p.k, &p.ch, &p.nch, &p.rowb);
+  chunking(wdt, p.k, &p.ch, &p.nch, &p.rowb, p.chmax);
   const int n_pairs = (p.n_rows + 1) / 2;
   int grid = grid_ctas > 0 ? grid_ctas : num_sms(dev);
   grid = std::max(1, std::min(grid, (n_pairs * p.nch + GEMV_WARPS - 1) / GEMV_WARPS));

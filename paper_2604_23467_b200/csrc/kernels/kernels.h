@@ -32,6 +32,7 @@ struct GemvParams {
   int k = 0;
   int rowb = 0;             // bytes of one row chunk slot in shared memory (set by the launcher)
   int ch = 0, nch = 0;      // k-chunk elements and chunks per row (set by the launcher)
+  int chmax = 0;            // max chunk elements (0 = default 2048 bf16): stage size per task
   int stages = 0;           // ring slots per warp (set by the launcher from the smem budget)
   int pre_stages = 0;       // slots filled before the dependency wait (0 = all; set by the launcher)
   int rms_defer = 1;        // RMSNorm: apply 1/rms to the dot products (epilogue) instead of to x
