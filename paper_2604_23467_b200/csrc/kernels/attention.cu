@@ -65,6 +65,10 @@ __device__ __forceinline__ uint32_t cluster_nctarank() {
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
   return r;
 }
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -180,7 +184,14 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(const AttnPar
   if (len < 1 || len > ns * span) {  // live length outside the bucket this graph was built for
     if (threadIdx.x == 0 && rank == 0 && head == 0 && p.err) atomicOr(p.err, DEVERR_WRONG_LENGTH);
   }
+  op_stamp(p.trace, 4);
+  if (ns == 1) {  // whole head in this CTA: no cluster exchange
+    for (int d = threadIdx.x; d < dh; d += ATTN_THREADS) p.out[head * dh + d] = c_o[d] / L;  // own c_o[d], own L
+    op_stamp(p.trace, 3);
+    return;
+  }
   cluster_sync_all();  // partials visible cluster-wide
+  op_stamp(p.trace, 5);
   if (rank == 0) {
     float MM = -INFINITY;
     for (int r = 0; r < ns; ++r) MM = fmaxf(MM, *dsmem_map(&c_ml[0], r));
@@ -190,26 +201,47 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(const AttnPar
       if (mr != -INFINITY) LL += *dsmem_map(&c_ml[1], r) * __expf(mr - MM);
     }
     const float inv = 1.0f / LL;
-    for (int d = threadIdx.x; d < dh; d += ATTN_THREADS) {
-      float o = 0.0f;
+    // every remote read happens before rank 0's arrive; the global store of the
+    // result comes after it, so the barrier's release never waits on it
+    float res = 0.0f;
+    const int d = threadIdx.x;
+    if (d < dh) {
       for (int r = 0; r < ns; ++r) {
         const float mr = *dsmem_map(&c_ml[0], r);
-        if (mr != -INFINITY) o += *dsmem_map(&c_o[d], r) * __expf(mr - MM);
+        if (mr != -INFINITY) res += *dsmem_map(&c_o[d], r) * __expf(mr - MM);
       }
-      p.out[head * dh + d] = o * inv;
     }
+    op_stamp(p.trace, 6);
+    cluster_arrive();  // the other CTAs may now exit (their shared memory was read)
+    if (d < dh) p.out[head * dh + d] = res * inv;
+    cluster_wait();
+  } else {
+    op_stamp(p.trace, 6);
+    cluster_sync_all();  // keep this CTA's shared memory alive until rank 0 has read it
   }
-  cluster_sync_all();  // keep every CTA's shared memory alive until rank 0 has read it
   op_stamp(p.trace, 3);
   // (trigger 2: the successor launches when this CTA exits)
 }
 
 // Cluster size and passes for a bucket of max_len positions.
+// Each CTA takes up to `per_cta` passes before the head is split over a
+// cluster: a pass costs one memory round trip, a cluster costs two cluster
+// barriers and a DSMEM merge (measured: ~1 round trip each while the next
+// kernel's CTAs are being launched).
+static int attn_rounds_per_cta() {
+  static const int v = [] {
+    const char* e = getenv("GRT_ATTN_ROUNDS");
+    return e ? std::max(1, atoi(e)) : 2;
+  }();
+  return v;
+}
+
 static void attn_shape(int max_len, int head_dim, int* ns, int* rounds) {
   const int pass = attn_pass_span(head_dim);
   const int need = std::max(1, (max_len + pass - 1) / pass);  // passes over the whole bucket
+  const int want = (need + attn_rounds_per_cta() - 1) / attn_rounds_per_cta();
   int c = 1;
-  while (c < need && c < ATTN_MAX_CLUSTER) c <<= 1;
+  while (c < want && c < ATTN_MAX_CLUSTER) c <<= 1;
   *ns = c;
   *rounds = (need + c - 1) / c;
 }

@@ -69,3 +69,15 @@ for i in i_att:
     lat.append(st[:, 2] - st[:, 1])
 lat = np.concatenate(lat) / 1e3
 print("attn ready-released per CTA us: p10 %.2f p50 %.2f p90 %.2f max %.2f" % tuple(np.percentile(lat, [10, 50, 90, 100])))
+# attention phases (median over CTAs, relative to release): scores, CTA merge done, cluster barrier, rank-0 merge, exit
+ph = {k: [] for k in ("scores", "cta_merge", "cluster1", "merged", "exit")}
+for i in i_att:
+    st = tr[i]
+    st = st[(st[:, 0] > 0) & (st[:, 3] > 0)]
+    r = st[:, 1]
+    for k, c in zip(ph, (2, 4, 5, 6, 3)):
+        v = st[:, c]
+        ok = v > 0
+        if ok.any():
+            ph[k].append(np.median(v[ok] - r[ok]))
+print("attn phases (median us after release): " + " ".join(f"{k}={np.mean(v) / 1e3:.2f}" for k, v in ph.items() if v))
