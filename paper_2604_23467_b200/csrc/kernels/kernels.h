@@ -140,6 +140,18 @@ cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s,
 size_t gemv_smem_bytes(Dt wdt, int k);
 cudaError_t gemv_prepare(int device);  // raises the dynamic smem limit once per process
 
+// Two consecutive decode GEMVs in one launch (gemv_pair.cu): a = residual GEMV
+// (NORM_NONE, EPI_RESID), b = RMS-normed GEMV on its output (EPI_SWIGLU,
+// EPI_QKV_ROPE or EPI_STORE), grid-wide barrier in between; bf16 weights.
+struct GemvPairParams {
+  GemvParams a, b;
+  int* bar = nullptr;  // [2] arrive/depart counters, zero-initialised, self-resetting
+  int* err = nullptr;
+  int stages = 0, rowb = 0, xs_floats = 0;  // set by the launcher
+};
+cudaError_t launch_gemv_pair(int epi_b, GemvPairParams p, cudaStream_t s, bool pdl);
+cudaError_t gemv_pair_prepare();
+
 // Split-K flash-decode over the KV cache for live lengths up to max_len (the
 // graph bucket's end): one thread-block cluster per head, partials merged over
 // distributed shared memory.  Writes out[h*dh].

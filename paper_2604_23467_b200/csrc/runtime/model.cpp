@@ -263,6 +263,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   cuda_check(attention_prepare(), "attention_prepare");
   cuda_check(decode_pass_prepare(cfg_.device), "decode_pass_prepare");
   cuda_check(prefill_gemm_prepare(), "prefill_gemm_prepare");
+  cuda_check(gemv_pair_prepare(), "gemv_pair_prepare");
 
   const int64_t d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
   const int64_t h = cfg_.n_heads, dh = cfg_.head_dim();
@@ -307,6 +308,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   acc(V * 4);               // sampler scratch
   acc(h * max_nsplit_ * (dh + 2) * 4);
   acc(h * 4);
+  acc(cfg_.n_layers * 4 * 4);  // fused-pair barrier counters
   acc(S * (dh / 2) * 4 * 2);
   acc(sizeof(GrtCtrl));
   acc(S * 4);
@@ -361,6 +363,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   scratch_ = static_cast<float*>(arena_buf(V * 4, "scratch"));
   attn_part_ = static_cast<float*>(arena_buf(h * max_nsplit_ * (dh + 2) * 4, "attn_part"));
   attn_counters_ = static_cast<int*>(arena_buf(h * 4, "attn_counters"));
+  pair_bar_ = static_cast<int*>(arena_buf(cfg_.n_layers * 4 * 4, "pair_barriers"));
   if (pf) {
     const int64_t C = PREFILL_CHUNK;
     pf_X_ = static_cast<float*>(arena_buf(C * d * 4, "prefill_x"));
@@ -708,6 +711,18 @@ std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* gri
   return out;
 }
 
+// 0: no fusion; 1: every (residual, normed) pair; 2 (default): only Wo +
+// gate/up -- down + QKV measured slower: the down phase's 44 KB activation row
+// leaves room for only 2 ring stages.
+static int gemv_pair_mode() {
+  static const int v = [] {
+    const char* e = getenv("GRT_GEMV_PAIR");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+static bool gemv_pair_enabled() { return gemv_pair_mode() != 0; }
+
 std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   const int d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
   const int h = cfg_.n_heads, dh = cfg_.head_dim();
@@ -751,7 +766,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   auto next_trace = [&]() -> unsigned long long* {
     return op_trace_ ? op_trace_ + plan.size() * OP_TRACE_CTAS * 8 : nullptr;
   };
-  auto gemv = [&](const char* name, int epi, int nrm, GemvParams p, size_t w_bytes) {
+  auto emit_gemv = [&](const std::string& name, int epi, int nrm, GemvParams p, size_t w_bytes) {
     p.trace = next_trace();
     KernelInvocation inv;
     inv.spec.name = name;
@@ -763,6 +778,50 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
     inv.launch = [wdt, epi, nrm, p](cudaStream_t s) { return launch_gemv(wdt, nrm, epi, p, s, true, 0); };
     plan.push_back(std::move(inv));
   };
+  // A residual GEMV (Wo, down) is held back and, when the next GEMV is the
+  // RMS-normed one that consumes its output (gate/up, next layer's QKV, LM
+  // head), both run as ONE launch with a grid barrier (gemv_pair.cu): the
+  // weight ring streams across the boundary.  Single GPU, LLaMA, bf16 only.
+  struct Pending {
+    std::string name;
+    GemvParams p;
+    size_t bytes = 0;
+    bool set = false;
+  } pending;
+  const bool fuse = cfg_.tp_size == 1 && llama && wdt == Dt::BF16 && !op_trace_ && gemv_pair_enabled();
+  int n_pairs_emitted = 0;
+  auto flush = [&]() {
+    if (pending.set) emit_gemv(pending.name, EPI_RESID, NORM_NONE, pending.p, pending.bytes);
+    pending.set = false;
+  };
+  auto gemv = [&](const char* name, int epi, int nrm, GemvParams p, size_t w_bytes) {
+    if (fuse && epi == EPI_RESID && nrm == NORM_NONE) {
+      flush();
+      pending = Pending{name, p, w_bytes, true};
+      return;
+    }
+    if (fuse && pending.set && nrm == NORM_RMS &&
+        (epi == EPI_SWIGLU || (gemv_pair_mode() == 1 && (epi == EPI_QKV_ROPE || epi == EPI_STORE)))) {
+      GemvPairParams pp;
+      pp.a = pending.p;
+      pp.b = p;
+      pp.bar = pair_bar_ + 2 * n_pairs_emitted++;
+      pp.err = err;
+      KernelInvocation inv;
+      inv.spec.name = pending.name + "+" + name;
+      inv.spec.op_class = OpClass::Static;
+      inv.spec.flops = 2LL * pending.p.n_rows * pending.p.k + 2LL * p.n_rows * p.k;
+      inv.spec.bytes = static_cast<int64_t>(pending.bytes + w_bytes);
+      inv.bindings = {{pending.p.w, pending.bytes}, {p.w, w_bytes}, {pp.bar, 8},
+                      {pending.p.x, static_cast<size_t>(pending.p.k) * 4}, {p.x, static_cast<size_t>(p.k) * 4}};
+      inv.launch = [epi, pp](cudaStream_t s) { return launch_gemv_pair(epi, pp, s, true); };
+      plan.push_back(std::move(inv));
+      pending.set = false;
+      return;
+    }
+    flush();
+    emit_gemv(name, epi, nrm, p, w_bytes);
+  };
   // Tensor parallelism: this rank's shard has hl heads (dq = hl*dh
   // attention dims), ffl d_ff columns and vl vocab rows.  Row-parallel Wo/down
   // produce partial residual updates: rank 0 adds its partial to x, the other
@@ -773,6 +832,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   const int resid_epi = (T == 1 || cfg_.tp_rank == 0) ? EPI_RESID : EPI_STORE;
   TpComm** commp = &comm_;
   auto allreduce_x = [&](const char* name) {
+    flush();
     KernelInvocation inv;
     inv.spec.name = name;
     inv.spec.op_class = OpClass::Static;
@@ -814,6 +874,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       p.err = err;
       gemv("qkv", llama ? EPI_QKV_ROPE : EPI_QKV, norm, p, 3ull * dq * d * wb);
     }
+    flush();
     {  // attention over [0, seq_len) for this rank's heads
       AttnParams a;
       a.q = q_;
@@ -886,6 +947,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
     p.out = logits_local_;
     gemv("lnf_head", EPI_STORE, norm, p, 1ull * vl * d * wb);
   }
+  flush();
   if (T > 1) {
     KernelInvocation inv;
     inv.spec.name = "allgather_logits";
