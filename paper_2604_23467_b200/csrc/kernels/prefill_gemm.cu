@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
   const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
   const int n_items = m_tiles * p.n_ntiles * p.ksplit;
   const int kstep = PG_BK * p.kbox;
-  const int nkb = p.K / kstep;
+  const int nkb = (p.K + kstep - 1) / kstep;  // a ragged last block reads zeros past K (TMA OOB fill)
   const int S = p.stages;
   const uint32_t a_box = PG_BM * PG_BK * 2;
   const uint32_t b_box = static_cast<uint32_t>(p.ntile) * PG_BK * 2;
@@ -426,7 +426,7 @@ static PgShape pg_shape(int M, int K, int P, int sms) {
     sh.ntile = (P + 15) / 16 * 16;
     sh.n_ntiles = 1;
     sh.kbox = (K % (4 * PG_BK) == 0) ? 4 : ((K % (2 * PG_BK) == 0) ? 2 : 1);
-    const int nkb = K / (PG_BK * sh.kbox);
+    const int nkb = (K + PG_BK * sh.kbox - 1) / (PG_BK * sh.kbox);
     sh.ksplit = std::max(1, std::min({sms / m_tiles, nkb, 8}));
     return sh;
   }
@@ -459,7 +459,9 @@ cudaError_t prefill_gemm_prepare() {
 }
 
 cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams p, cudaStream_t s, bool pdl) {
-  if (p.K % PG_BK != 0 || p.P < 1 || p.P > PREFILL_CHUNK || p.M < 1) return cudaErrorInvalidValue;
+  // K need not be a multiple of the 64-wide K box (e.g. d_ff / 8 = 1376 under
+  // TP=8): TMA zero-fills both operands past K; rows must stay 16-byte aligned
+  if (p.K % 8 != 0 || p.P < 1 || p.P > PREFILL_CHUNK || p.M < 1) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);
   const PgShape sh = pg_shape(p.M, p.K, p.P, num_sms(dev));

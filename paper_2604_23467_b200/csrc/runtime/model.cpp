@@ -525,7 +525,7 @@ uint64_t Model::decode_bytes(int length) const {
 
 bool Model::supports_batched_prefill() const {
   const int dh = cfg_.head_dim();
-  return cfg_.llama() && cfg_.weight_dtype == GRT_BF16 && cfg_.d_model % 64 == 0 && cfg_.d_ff() % 64 == 0 &&
+  return cfg_.llama() && cfg_.weight_dtype == GRT_BF16 && cfg_.d_model % 8 == 0 && cfg_.d_ff() % 8 == 0 &&
          (dh == 16 || dh == 32 || dh == 64 || dh == 128);
 }
 

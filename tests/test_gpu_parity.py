@@ -326,7 +326,8 @@ def test_step_api_errors():
 # ------------------------------------------------------------ batched prefill
 
 @pytest.mark.parametrize("m,k,p", [(128, 64, 16), (256, 128, 10), (12288, 4096, 10), (4096, 4096, 200),
-                                   (22016, 4096, 500), (4096, 11008, 37), (192, 64, 300), (4096, 4096, 512)])
+                                   (22016, 4096, 500), (4096, 11008, 37), (192, 64, 300), (4096, 4096, 512),
+                                   (4096, 1376, 37), (4096, 1376, 300), (2752, 4096, 64), (200, 72, 5)])
 def test_prefill_gemm_tcgen05_matches_fp64(m, k, p):
     """tcgen05/TMEM GEMM (bf16 operands, fp32 accumulate) vs an fp64 product of
     the same bf16 values; covers split-K (small m), two N tiles (p > 256),
