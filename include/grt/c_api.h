@@ -259,6 +259,10 @@ grt_status grt_tp_emu_destroy(grt_tp_emu* e);
 grt_status grt_tp_emu_reset(grt_tp_emu* e);
 grt_status grt_tp_emu_step(grt_tp_emu* e, int32_t token);
 grt_status grt_tp_emu_logits(grt_tp_emu* e, float* out, int32_t n);
+/* T ranks as T host threads with an in-process communicator: batched prefill
+ * of prompt[0, n_prompt), then single steps; rank 0's logits (vocab_size). */
+grt_status grt_tp_emu_threaded(const grt_model_config* cfg, const int32_t* prompt, int32_t n_prompt,
+                               const int32_t* steps, int32_t n_steps, float* logits);
 
 /* ---- two-process split (the paper's IPC, PAPER.md "two processes") ------------
  * Process B (graph generator) owns the model and replays the static pass;

@@ -183,6 +183,16 @@ grt_status grt_ipc_client_destroy(grt_ipc_client* c) {
   return guard([&] { grt_ipc_client_free(c); });
 }
 
+grt_status grt_tp_emu_threaded(const grt_model_config* cfg, const int32_t* prompt, int32_t n_prompt,
+                               const int32_t* steps, int32_t n_steps, float* logits) {
+  return guard([&] {
+    if (!cfg || !prompt || n_prompt < 1 || !logits || (n_steps > 0 && !steps))
+      grt::raise(GRT_InvalidConfig, "bad arguments");
+    grt::tp_emu_threaded(grt::ModelConfig::from_c(*cfg), std::vector<int>(prompt, prompt + n_prompt),
+                         std::vector<int>(steps, steps + std::max(0, n_steps)), logits);
+  });
+}
+
 grt_status grt_model_destroy(grt_model* m) {
   return guard([&] { delete m; });
 }

@@ -592,6 +592,11 @@ class TpEmu {
   int cur_len_ = 0;
   GrtCtrl* h_ctrl_ = nullptr;
 };
+// T ranks as T host threads (own Model/Session/stream each) with an in-process
+// communicator: batched prefill of `prompt` then step(t) for t in `steps`;
+// rank 0's logits out.  Validates the eager TP paths on one device.
+void tp_emu_threaded(const ModelConfig& cfg, const std::vector<int>& prompt, const std::vector<int>& steps,
+                     float* logits_out);
 
 // ---------------------------------------------------------------------------
 // two-process split (ipc.cpp)

@@ -6,7 +6,9 @@
 
 #include <climits>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <type_traits>
 
 #include "runtime.hpp"
@@ -191,6 +193,104 @@ void TpEmu::step(int token) {
 void TpEmu::logits(float* out, int n) {
   if (n != ranks_[0]->config().vocab_size) raise(GRT_ShapeMismatch, "logits buffer must hold vocab_size floats");
   cuda_check(cudaMemcpy(out, ranks_[0]->logits_dev(), n * sizeof(float), cudaMemcpyDeviceToHost), "logits");
+}
+
+// ---------------------------------------------------------------------------
+// Threaded emulation: T ranks = T host threads on one device, each with its own
+// Model, Session and stream, exchanging through EmuComm.  Exercises the EAGER
+// tensor-parallel paths end to end -- batched prefill (allreduce of the [P, d]
+// residual after Wo and down, logits allgather) and single steps -- exactly as
+// the NCCL ranks run them (graphs are not captured here: a captured host
+// rendezvous would not replay).
+
+namespace {
+struct EmuGroup {
+  int T = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  TpPtrs in{}, out{};
+  size_t n = 0;
+  std::vector<cudaEvent_t> ready;
+  cudaEvent_t done = nullptr;
+};
+
+class EmuComm : public TpComm {
+ public:
+  EmuComm(EmuGroup* g, int rank) : g_(g), rank_(rank) {}
+  cudaError_t allreduce_sum(float* buf, size_t n, cudaStream_t s) override { return run(true, buf, buf, n, s); }
+  cudaError_t allgather(const float* in, float* out, size_t n, cudaStream_t s) override {
+    return run(false, const_cast<float*>(in), out, n, s);
+  }
+
+ private:
+  cudaError_t run(bool reduce, float* in, float* out, size_t n, cudaStream_t s) {
+    cudaError_t e = cudaEventRecord(g_->ready[rank_], s);
+    if (e != cudaSuccess) return e;
+    std::unique_lock<std::mutex> lk(g_->mu);
+    g_->in.p[rank_] = in;
+    g_->out.p[rank_] = out;
+    g_->n = n;
+    const uint64_t my_gen = g_->gen;
+    if (++g_->arrived == g_->T) {  // last rank in: run the exchange on its stream
+      for (int r = 0; r < g_->T; ++r) cudaStreamWaitEvent(s, g_->ready[r], 0);
+      e = reduce ? launch_emu_allreduce(g_->in, g_->T, n, s) : launch_emu_allgather(g_->in, g_->out, g_->T, n, s);
+      if (e == cudaSuccess) e = cudaEventRecord(g_->done, s);
+      g_->arrived = 0;
+      ++g_->gen;
+      g_->cv.notify_all();
+      return e;
+    }
+    g_->cv.wait(lk, [&] { return g_->gen != my_gen; });
+    return cudaStreamWaitEvent(s, g_->done, 0);
+  }
+  EmuGroup* g_;
+  int rank_;
+};
+}  // namespace
+
+void tp_emu_threaded(const ModelConfig& cfg, const std::vector<int>& prompt, const std::vector<int>& steps,
+                     float* logits_out) {
+  const int T = cfg.tp_size;
+  if (T < 2 || T > TP_MAX) raise(GRT_InvalidConfig, "tp_size must be in [2, 8]");
+  EmuGroup grp;
+  grp.T = T;
+  grp.ready.resize(T);
+  cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
+  for (int r = 0; r < T; ++r) cuda_check(cudaEventCreateWithFlags(&grp.ready[r], cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&grp.done, cudaEventDisableTiming), "event");
+  std::vector<std::unique_ptr<Model>> models(T);
+  std::vector<std::unique_ptr<EmuComm>> comms(T);
+  for (int r = 0; r < T; ++r) {
+    ModelConfig c = cfg;
+    c.tp_rank = r;
+    models[r] = std::make_unique<Model>(c);
+    comms[r] = std::make_unique<EmuComm>(&grp, r);
+    models[r]->attach_comm(comms[r].get());
+  }
+  std::vector<std::string> errors(T);
+  std::vector<std::thread> th;
+  for (int r = 0; r < T; ++r)
+    th.emplace_back([&, r] {
+      try {
+        cudaSetDevice(cfg.device);
+        CacheConfig cc;
+        cc.warmup_hi = 0;
+        cc.batched_prefill = true;
+        Session s(*models[r], cc);
+        s.prefill(prompt);
+        for (int t : steps) s.step(t);
+        if (r == 0) s.logits(logits_out, cfg.vocab_size);
+      } catch (const std::exception& e) {
+        errors[r] = e.what();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : grp.ready) cudaEventDestroy(e);
+  cudaEventDestroy(grp.done);
+  for (int r = 0; r < T; ++r)
+    if (!errors[r].empty()) raise(GRT_CudaError, "rank " + std::to_string(r) + ": " + errors[r]);
 }
 
 }  // namespace grt

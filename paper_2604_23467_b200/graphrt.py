@@ -160,7 +160,7 @@ EXPORTS = [
     "grt_graph_cache_warmup", "grt_graph_cache_begin_session", "grt_graph_cache_release_inactive",
     "grt_graph_cache_query", "grt_profile_plan", "grt_trace_pass",
     "grt_tp_unique_id", "grt_model_attach_nccl", "grt_tp_emu_create", "grt_tp_emu_destroy", "grt_tp_emu_reset",
-    "grt_tp_emu_step", "grt_tp_emu_logits",
+    "grt_tp_emu_step", "grt_tp_emu_logits", "grt_tp_emu_threaded",
     "grt_ipc_server_create", "grt_ipc_server_serve", "grt_ipc_server_destroy", "grt_ipc_client_create",
     "grt_ipc_client_generate", "grt_ipc_client_destroy",
 ]
@@ -209,6 +209,8 @@ def lib():
         L.grt_tp_emu_reset.argtypes = [vp]
         L.grt_tp_emu_step.argtypes = [vp, C.c_int32]
         L.grt_tp_emu_logits.argtypes = [vp, C.POINTER(C.c_float), C.c_int32]
+        L.grt_tp_emu_threaded.argtypes = [C.POINTER(_ModelConfig), C.POINTER(C.c_int32), C.c_int32,
+                                          C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_float)]
         L.grt_session_destroy.argtypes = [vp]
         L.grt_generate.argtypes = [vp, C.POINTER(_Request), C.POINTER(_Result)]
         L.grt_cache_stats_get.argtypes = [vp, C.POINTER(_CacheStats), C.POINTER(C.c_uint64)]
@@ -499,6 +501,19 @@ def tp_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().grt_tp_unique_id(buf, 128))
     return buf.raw
+
+
+def tp_emu_threaded(cfg: "ModelConfig", prompt, steps=()):
+    """cfg.tp_size ranks as host threads (own model/session/stream) with an
+    in-process communicator: batched prefill + single steps; rank 0's logits."""
+    import numpy as np
+    c = cfg._c()
+    pr = (C.c_int32 * len(prompt))(*prompt)
+    st = (C.c_int32 * max(1, len(steps)))(*steps)
+    out = np.zeros(cfg.vocab_size, np.float32)
+    _check(lib().grt_tp_emu_threaded(C.byref(c), pr, len(prompt), st, len(steps),
+                                     out.ctypes.data_as(C.POINTER(C.c_float))))
+    return out
 
 
 class TPEmu:

@@ -467,3 +467,25 @@ def test_two_process_ipc_split_reproduces_reference(golden, kind, fixture):
         cl.join(60)
         sv.join(60)
     assert toks == want
+
+
+@pytest.mark.parametrize("tp,kw,plen,tol", [
+    (2, dict(n_layers=2, d_model=128, n_heads=4, vocab_size=512, max_seq_len=640, d_ff_=320, seed=5), 40, 2e-3),
+    (8, dict(n_layers=2, d_model=4096, n_heads=32, vocab_size=32000, max_seq_len=640, d_ff_=11008, seed=11), 300,
+     5e-3),
+])
+def test_tp_batched_prefill_and_steps_match_single_gpu(tp, kw, plen, tol):
+    """Eager tensor-parallel paths with ranks as host threads (own model, session
+    and stream each, in-process communicator): batched prefill (tcgen05 GEMMs on
+    the shards, allreduce of the [P, d] residual, logits allgather; d_ff/8 = 1376
+    exercises the ragged-K GEMM) then two steps, vs the tp_size=1 model."""
+    base = dict(arch=g.ARCH_LLAMA, init=g.INIT_PHILOX, weight_dtype=g.BF16, kv_dtype=g.BF16, **kw)
+    import pyoracle as po
+    prompt = po.make_prompt(42, plen, kw["vocab_size"])
+    ref = g.Session(g.ModelConfig(**base), g.CacheConfig(bucket_size=64, warmup_hi=0, batched_prefill=True))
+    ref.prefill(prompt)
+    for t in (3, 9):
+        ref.step(t)
+    got = g.tp_emu_threaded(g.ModelConfig(tp_size=tp, **base), prompt, (3, 9))
+    err = float(np.abs(ref.logits() - got).max())
+    assert err <= tol, err
