@@ -195,6 +195,66 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Epilogue of one row pair (m even, m+1) for one token: the split-K reduce path.
+__device__ __forceinline__ void pg_epilogue_pair(const PrefillGemmParams& p, int m, int n, float va, float vb) {
+  const bool has_b = m + 1 < p.M;
+  switch (p.epi) {
+    case PG_EPI_STORE:
+      p.out[static_cast<int64_t>(n) * p.M + m] = va;
+      if (has_b) p.out[static_cast<int64_t>(n) * p.M + m + 1] = vb;
+      break;
+    case PG_EPI_RESID:
+      p.out[static_cast<int64_t>(n) * p.M + m] += va;
+      if (has_b) p.out[static_cast<int64_t>(n) * p.M + m + 1] += vb;
+      break;
+    case PG_EPI_SWIGLU:
+      static_cast<__nv_bfloat16*>(p.out_bf16)[static_cast<int64_t>(n) * (p.M >> 1) + (m >> 1)] =
+          __float2bfloat16_rn(va / (1.0f + expf(-va)) * vb);
+      break;
+    default: {
+      const int d = p.d_model, dh = p.head_dim;
+      const int sec = m / d;
+      const int lp = (m >> 1) - sec * (d >> 1);
+      const int pos = p.start_pos + n;
+      float ra = va, rb = vb;
+      int e0, e1, head;
+      if (p.epi == PG_EPI_QKV_ROPE && sec < 2) {
+        const int half = dh >> 1;
+        head = lp / half;
+        const int i = lp - head * half;
+        const float c = p.rope_cos[static_cast<int64_t>(pos) * half + i];
+        const float sn = p.rope_sin[static_cast<int64_t>(pos) * half + i];
+        ra = va * c - vb * sn;
+        rb = vb * c + va * sn;
+        e0 = i;
+        e1 = i + half;
+      } else {
+        const int e = 2 * lp;
+        head = e / dh;
+        e0 = e - head * dh;
+        e1 = e0 + 1;
+      }
+      if (sec == 0) {
+        float* q = p.q_out + static_cast<int64_t>(n) * d + head * dh;
+        q[e0] = ra;
+        q[e1] = rb;
+      } else {
+        void* cache = sec == 1 ? p.k_cache : p.v_cache;
+        const int64_t base = (static_cast<int64_t>(head) * p.max_seq + pos) * dh;
+        if (p.kv_bf16) {
+          __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(cache) + base;
+          c[e0] = __float2bfloat16_rn(ra);
+          c[e1] = __float2bfloat16_rn(rb);
+        } else {
+          float* c = reinterpret_cast<float*>(cache) + base;
+          c[e0] = ra;
+          c[e1] = rb;
+        }
+      }
+    }
+  }
+}
+
 // mbarrier wait for threads that idle through the main loop: back off so they
 // do not steal issue slots from the TMA / MMA threads on their SM sub-partition
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
@@ -215,7 +275,6 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ uint64_t full[8], empty[8], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ int s_last[2];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -344,35 +403,39 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
-      if (split_k) {
-        // the last CTA of this output tile sums the partials in split order
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 && lane == 0) s_last[buf] = atomicAdd(p.counters + tile_id, 1) == p.ksplit - 1;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (s_last[buf]) {
-          __threadfence();
-          const float* base = p.part + static_cast<int64_t>(tile_id) * p.ksplit * p.ntile * PG_BM + lane_base + lane;
-          for (int n = 0; n < n_valid; n += 16) {
-            float v[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) v[u] = 0.0f;
-            for (int sp = 0; sp < p.ksplit; ++sp) {
-#pragma unroll
-              for (int u = 0; u < 16; ++u)
-                if (n + u < n_valid) v[u] += __ldcg(base + (static_cast<int64_t>(sp) * p.ntile + n + u) * PG_BM);
-            }
-            pg_epilogue16(p, m, n0 + n, min(16, n_valid - n), v);
-          }
-          if (warp == 2 && lane == 0) p.counters[tile_id] = 0;  // self-reset
-        }
-      }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols) : "memory");
+}
+
+// ---- split-K reduction + epilogue --------------------------------------------------
+// Short prompts split K over work items that only store fp32 partials
+// [tile][split][token][128 rows]; this kernel sums them in split order
+// (deterministic) and applies the epilogue, one thread per (row pair, token):
+// fully parallel, instead of one CTA per tile serialising a tail reduction.
+__global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
+  griddep_wait();  // launched with PDL behind the GEMM: partials complete
+  const int n_pairs = (p.M + 1) >> 1;
+  const int64_t total = static_cast<int64_t>(n_pairs) * p.P;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int n = static_cast<int>(e / n_pairs);
+    const int pr = static_cast<int>(e - static_cast<int64_t>(n) * n_pairs);
+    const int m = 2 * pr;
+    const int m_tile = m / PG_BM, n_tile = n / p.ntile;
+    const int r = m - m_tile * PG_BM, nn = n - n_tile * p.ntile;
+    const float* base = p.part + (static_cast<int64_t>(m_tile * p.n_ntiles + n_tile) * p.ksplit) * p.ntile * PG_BM;
+    float va = 0.0f, vb = 0.0f;
+    for (int sp = 0; sp < p.ksplit; ++sp) {
+      const float* q = base + (static_cast<int64_t>(sp) * p.ntile + nn) * PG_BM + r;
+      va += q[0];
+      vb += q[1];
+    }
+    pg_epilogue_pair(p, m, n, va, vb);
+  }
 }
 
 // ---- host side --------------------------------------------------------------------
@@ -427,7 +490,17 @@ static PgShape pg_shape(int M, int K, int P, int sms) {
     sh.n_ntiles = 1;
     sh.kbox = (K % (4 * PG_BK) == 0) ? 4 : ((K % (2 * PG_BK) == 0) ? 2 : 1);
     const int nkb = (K + PG_BK * sh.kbox - 1) / (PG_BK * sh.kbox);
-    sh.ksplit = std::max(1, std::min({sms / m_tiles, nkb, 8}));
+    // persistent CTAs: pick the split whose work items tile the SMs evenly
+    // (time ~ waves / split); partials are reduced by a separate parallel kernel
+    double best = 1e30;
+    for (int ks = 1; ks <= std::min(16, nkb); ++ks) {
+      const double waves = static_cast<double>((m_tiles * ks + sms - 1) / sms);
+      const double cost = waves / ks + 0.005 * ks;
+      if (cost < best) {
+        best = cost;
+        sh.ksplit = ks;
+      }
+    }
     return sh;
   }
   // compute-bound: the widest token tile (<= 256, TMEM holds two): operand bytes
@@ -436,7 +509,20 @@ static PgShape pg_shape(int M, int K, int P, int sms) {
   // GEMMs (Wo, down) than 64 wide tiles.
   sh.n_ntiles = (P + PG_MAX_NT - 1) / PG_MAX_NT;
   sh.ntile = ((P + sh.n_ntiles - 1) / sh.n_ntiles + 15) / 16 * 16;
-  (void)m_tiles;
+  // small-M GEMMs (Wo, down: 32 tiles) split K so the items fill the SMs;
+  // the partials go through the parallel reduce kernel
+  const int items = m_tiles * sh.n_ntiles;
+  const int nkb = (K + PG_BK - 1) / PG_BK;
+  double best = 1e30;
+  const int ks_max = sh.n_ntiles > 1 ? 1 : std::min(8, nkb);  // P > 256: measured faster unsplit
+  for (int ks = 1; ks <= ks_max; ++ks) {
+    const double waves = static_cast<double>((items * ks + sms - 1) / sms);
+    const double cost = waves / ks + 0.02 * (ks - 1);
+    if (cost < best) {
+      best = cost;
+      sh.ksplit = ks;
+    }
+  }
   return sh;
 }
 
@@ -445,7 +531,7 @@ int prefill_gemm_ksplit(int M, int K, int sms) { return pg_shape(M, K, 16, sms).
 size_t prefill_gemm_part_floats(int M, int K, int P, int sms) {
   size_t worst = 0;
   (void)P;
-  for (int q = 16; q <= 64; q += 16) {  // split-K only happens for P <= 64: size for the worst case
+  for (int q = 16; q <= PREFILL_CHUNK; q += 16) {  // size for the worst token count
     const PgShape sh = pg_shape(M, K, q, sms);
     if (sh.ksplit == 1) continue;
     const int m_tiles = (M + PG_BM - 1) / PG_BM;
@@ -490,7 +576,17 @@ cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, prefill_gemm_kernel, mw, mx, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, prefill_gemm_kernel, mw, mx, p);
+  if (e != cudaSuccess || p.ksplit == 1) return e;
+  const int64_t work = static_cast<int64_t>((p.M + 1) / 2) * p.P;
+  const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 4 * num_sms(dev)));
+  cudaLaunchConfig_t rc = {};
+  rc.gridDim = dim3(blocks);
+  rc.blockDim = dim3(256);
+  rc.stream = s;
+  rc.attrs = attr;
+  rc.numAttrs = 1;  // always PDL: the reduce's launch overlaps the GEMM's tail
+  return cudaLaunchKernelEx(&rc, prefill_splitk_reduce_kernel, p);
 }
 
 }  // namespace grt

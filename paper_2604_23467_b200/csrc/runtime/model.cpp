@@ -564,7 +564,7 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       q.kv_bf16 = kvdt == Dt::BF16;
       q.part = pf_part_;
       q.counters = pf_cnt_;
-      cuda_check(launch_prefill_gemm(L.w_qkv, pf_Xn_, q, s, false), "prefill qkv");
+      cuda_check(launch_prefill_gemm(L.w_qkv, pf_Xn_, q, s, true), "prefill qkv");
       cuda_check(launch_prefill_attention(kvdt, pf_Q_, L.k, L.v, start, P, dq, hl, dh, S, scale, pf_A_, s),
                  "prefill attention");
       PrefillGemmParams o;
@@ -575,7 +575,7 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       o.out = pf_X_;
       o.part = pf_part_;
       o.counters = pf_cnt_;
-      cuda_check(launch_prefill_gemm(L.w_o, pf_A_, o, s, false), "prefill wo");
+      cuda_check(launch_prefill_gemm(L.w_o, pf_A_, o, s, true), "prefill wo");
       if (T > 1) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce wo");
       cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln2_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm2");
       PrefillGemmParams u;
@@ -586,7 +586,7 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       u.out_bf16 = pf_act_;
       u.part = pf_part_;
       u.counters = pf_cnt_;
-      cuda_check(launch_prefill_gemm(L.w_up, pf_Xn_, u, s, false), "prefill gate_up");
+      cuda_check(launch_prefill_gemm(L.w_up, pf_Xn_, u, s, true), "prefill gate_up");
       PrefillGemmParams w2;
       w2.M = d;
       w2.K = ffl;
@@ -595,7 +595,7 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       w2.out = pf_X_;
       w2.part = pf_part_;
       w2.counters = pf_cnt_;
-      cuda_check(launch_prefill_gemm(L.w_down, pf_act_, w2, s, false), "prefill down");
+      cuda_check(launch_prefill_gemm(L.w_down, pf_act_, w2, s, true), "prefill down");
       if (T > 1) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce down");
     }
   }
