@@ -34,7 +34,8 @@ namespace grt {
 constexpr int PG_BM = 128;        // weight rows per CTA (UMMA M)
 constexpr int PG_BK = 64;         // K elements per stage (one 128-byte swizzle row)
 constexpr int PG_UK = 16;         // K per tcgen05.mma (kind::f16)
-constexpr int PG_THREADS = 192;   // 6 warps
+constexpr int PG_EPI_WARPS = 8;    // max: two warps per TMEM lane quadrant, splitting the token columns
+constexpr int PG_THREADS = (2 + PG_EPI_WARPS) * 32;  // TMA warp, MMA warp, epilogue warps (max)
 constexpr int PG_MAX_NT = 256;    // tokens per N tile (UMMA N max)
 
 // ---- tcgen05 / TMA primitives (inline PTX) --------------------------------------
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
+      mbar_init(&acc_empty[b], blockDim.x / 32 - 2);  // one arrival per epilogue warp
     }
     mbar_fence_init();
   }
@@ -373,8 +374,12 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31 = weight rows
+    // epilogue warps 2..9: TMEM lanes 32*(warp%4) .. +31 = weight rows; the two
+    // warps of a lane quadrant take alternate 16-token column groups (the
+    // epilogue's own memory round trips -- RoPE table, residual -- halve)
     const int lane_base = 32 * (warp & 3);
+    const int half = (warp - 2) >> 2;                      // column group of this warp
+    const int groups = (static_cast<int>(blockDim.x) / 32 - 2) >> 2;  // warps per lane quadrant
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(lane_base) << 16);
     const bool split_k = p.ksplit > 1;
     int it = 0;
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
       tc_fence_after();
       const int tile_id = m_tile * p.n_ntiles + n_tile;
       float* mypart = split_k ? p.part + (static_cast<int64_t>(tile_id) * p.ksplit + split) * p.ntile * PG_BM : nullptr;
-      for (int c0 = 0; c0 < n_valid; c0 += 16) {
+      for (int c0 = 16 * half; c0 < n_valid; c0 += 16 * groups) {
         float v[16];
         tc_ld16(t_lane + buf * p.ntile + c0, v);
         if (split_k) {
@@ -568,7 +573,9 @@ cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams 
   if (!make_map(&mx, x, p.P, p.K, p.ntile)) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(std::min(n_items, num_sms(dev)));
-  cfg.blockDim = dim3(PG_THREADS);
+  // two token tiles (P > 256): 8 epilogue warps (the epilogue's memory round
+  // trips dominate a one-item CTA); otherwise 4 (measured faster)
+  cfg.blockDim = dim3(p.n_ntiles > 1 ? PG_THREADS : 6 * 32);
   cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + 1024;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
