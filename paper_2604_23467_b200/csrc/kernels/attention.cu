@@ -17,7 +17,7 @@
 
 namespace grt {
 
-constexpr int ATTN_THREADS = 256;
+constexpr int ATTN_THREADS = 512;
 
 template <typename KT>
 __device__ __forceinline__ float4 load4(const KT* p);
@@ -81,7 +81,7 @@ __device__ __forceinline__ const T* dsmem_map(const T* p, uint32_t rank) {
 }
 
 template <typename KT>
-__global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const AttnParams p) {
   __shared__ float s_m[ATTN_WARPS], s_l[ATTN_WARPS];
   __shared__ __align__(16) float s_o[ATTN_WARPS][256];
   __shared__ __align__(16) float c_o[256];  // this CTA's partial, read by rank 0 over DSMEM
