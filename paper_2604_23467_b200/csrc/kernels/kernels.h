@@ -69,7 +69,7 @@ struct AttnParams {
   int* err = nullptr;
   unsigned long long* trace = nullptr;  // optional [cta][4] %globaltimer stamps (profiling)
   int rounds = 1;                // passes per CTA (set by the launcher)
-  int trigger = 1;               // when the successor may launch: 0 start, 1 after KV loads, 2 at exit
+  int trigger = 0;               // when the successor may launch: 0 start, 1 after KV loads, 2 at exit
 };
 // Per-op trace stamps (8 slots per CTA): 0 CTA start, 1 dependency released
 // (griddepcontrol.wait), 2 operands ready (activation loaded / KV rows loaded),
