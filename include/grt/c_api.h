@@ -58,7 +58,7 @@ typedef enum grt_status {
 } grt_status;
 
 typedef enum grt_arch { GRT_ARCH_REF = 0, GRT_ARCH_LLAMA = 1 } grt_arch;
-typedef enum grt_dtype { GRT_F32 = 0, GRT_BF16 = 1 } grt_dtype;
+typedef enum grt_dtype { GRT_F32 = 0, GRT_BF16 = 1, GRT_F16 = 2 /* host/checkpoint data only */ } grt_dtype;
 typedef enum grt_init { GRT_INIT_MT19937 = 0, GRT_INIT_PHILOX = 1, GRT_INIT_NONE = 2 } grt_init;
 
 /* Replaces graphrt::RunMode (pipeline.hpp:18-24) -- same order. */
@@ -194,6 +194,21 @@ grt_status grt_model_upload(grt_model* m, const char* tensor, const void* host, 
                             int32_t host_dtype);
 /* Copies one weight tensor back in the reference layout as fp32. */
 grt_status grt_model_download(grt_model* m, const char* tensor, float* host, size_t numel);
+/* Loads weights from a safetensors checkpoint: one file, or a directory whose
+ * *.safetensors shards are read in name order.  Tensor names are graphrt's own
+ * (reference [k,n] layout, as grt_model_upload) or HuggingFace LLaMA names
+ * (model.layers.N.self_attn.q_proj.weight, ... [out,in] layout); dtypes BF16, F16,
+ * F32.  strict != 0: every model tensor must be present and no tensor unknown.
+ * No reference counterpart: the reference only draws seeded weights
+ * (init_model, model.cpp:30-76); SURVEY §8f rank 2. */
+grt_status grt_model_load_safetensors(grt_model* m, const char* path, int32_t strict, int32_t* n_loaded);
+/* Header-only inspection (no GPU): NUL-separated names into `names`, dtype
+ * (grt_dtype or -1), rank and up to 2 dims per tensor; *n = tensor count. */
+grt_status grt_safetensors_list(const char* path, char* names, int32_t names_len, int32_t* dtypes, int64_t* shapes,
+                                int32_t cap, int32_t* n);
+/* HuggingFace LLaMA tensor name -> graphrt name ("" if not a model weight);
+ * *out_in = 1 when the checkpoint stores it [out,in]. */
+grt_status grt_hf_tensor_name(const char* hf_name, char* out, int32_t out_len, int32_t* out_in);
 grt_status grt_model_weight_bytes(grt_model* m, uint64_t* bytes);            /* HBM bytes of weights */
 grt_status grt_model_decode_bytes(grt_model* m, int32_t length, uint64_t* bytes); /* algorithmic bytes/pass */
 

@@ -10,6 +10,7 @@
 // Either way the logical [k,n] reference tensor is scattered into the device
 // layout ([n,k] rows, RoPE pair permutation, gate/up interleave) by MapDesc.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -68,6 +69,7 @@ __device__ __forceinline__ void store_dt(void* dst, int64_t i, float v, int dt) 
 
 __device__ __forceinline__ float load_dt(const void* src, int64_t i, int dt) {
   if (dt == static_cast<int>(Dt::BF16)) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[i]);
+  if (dt == 2) return __half2float(reinterpret_cast<const __half*>(src)[i]);  // f16 (checkpoints only)
   return reinterpret_cast<const float*>(src)[i];
 }
 
@@ -96,13 +98,14 @@ __global__ void map_init_kernel(MapDesc d, void* dst, uint64_t seed, uint32_t ti
   }
 }
 
-__global__ void map_copy_kernel(MapDesc d, void* dst, const void* src, int src_dt) {
+__global__ void map_copy_kernel(MapDesc d, void* dst, const void* src, int src_dt, int src_out_in) {
   const int64_t n = (win_p1(d) - d.p0) * (win_j1(d) - d.j0);
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int64_t p, j;
     window_coords(d, t, p, j);
-    store_dt(dst, phys_index(d, p, j), load_dt(src, p * d.cols + j, src_dt), d.dst_dtype);
+    const int64_t si = src_out_in ? j * d.rows + p : p * d.cols + j;
+    store_dt(dst, phys_index(d, p, j), load_dt(src, si, src_dt), d.dst_dtype);
   }
 }
 
@@ -129,8 +132,9 @@ cudaError_t launch_map_init(const MapDesc& d, void* dst, uint64_t seed, uint32_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_map_copy(const MapDesc& d, void* dst, const void* src, int src_dtype, cudaStream_t s) {
-  map_copy_kernel<<<grid_for(d.rows * d.cols), 256, 0, s>>>(d, dst, src, src_dtype);
+cudaError_t launch_map_copy(const MapDesc& d, void* dst, const void* src, int src_dtype, bool src_out_in,
+                            cudaStream_t s) {
+  map_copy_kernel<<<grid_for(d.rows * d.cols), 256, 0, s>>>(d, dst, src, src_dtype, src_out_in ? 1 : 0);
   return cudaGetLastError();
 }
 

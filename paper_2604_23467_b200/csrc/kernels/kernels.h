@@ -226,7 +226,10 @@ struct MapDesc {
   int64_t p0 = 0, p1 = 0, j0 = 0, j1 = 0;
 };
 cudaError_t launch_map_init(const MapDesc& d, void* dst, uint64_t seed, uint32_t tensor_id, cudaStream_t s);
-cudaError_t launch_map_copy(const MapDesc& d, void* dst, const void* src, int src_dtype, cudaStream_t s);
+// src holds the logical tensor [rows, cols] row-major, or [cols, rows] when src_out_in
+// (src_dtype: 0 f32, 1 bf16, 2 f16)
+cudaError_t launch_map_copy(const MapDesc& d, void* dst, const void* src, int src_dtype, bool src_out_in,
+                            cudaStream_t s);
 cudaError_t launch_map_read(const MapDesc& d, const void* dst, float* out_ref_layout, cudaStream_t s);
 
 }  // namespace grt

@@ -205,6 +205,45 @@ grt_status grt_model_download(grt_model* m, const char* tensor, float* host, siz
   return guard([&] { m->m->download(tensor, host, numel); });
 }
 
+grt_status grt_model_load_safetensors(grt_model* m, const char* path, int32_t strict, int32_t* n_loaded) {
+  return guard([&] {
+    const int n = grt::load_safetensors(*m->m, path, strict != 0);
+    if (n_loaded) *n_loaded = n;
+  });
+}
+
+grt_status grt_safetensors_list(const char* path, char* names, int32_t names_len, int32_t* dtypes, int64_t* shapes,
+                                int32_t cap, int32_t* n) {
+  return guard([&] {
+    grt::SafetensorsFile f(path);
+    const auto& ts = f.tensors();
+    *n = static_cast<int32_t>(ts.size());
+    size_t off = 0;
+    for (size_t i = 0; i < ts.size() && static_cast<int32_t>(i) < cap; ++i) {
+      if (dtypes) dtypes[i] = ts[i].dtype;
+      if (shapes) {
+        shapes[3 * i] = static_cast<int64_t>(ts[i].shape.size());
+        shapes[3 * i + 1] = ts[i].shape.size() > 0 ? ts[i].shape[0] : 0;
+        shapes[3 * i + 2] = ts[i].shape.size() > 1 ? ts[i].shape[1] : 0;
+      }
+      if (names && off + ts[i].name.size() + 1 <= static_cast<size_t>(names_len)) {
+        memcpy(names + off, ts[i].name.c_str(), ts[i].name.size() + 1);
+        off += ts[i].name.size() + 1;
+      }
+    }
+  });
+}
+
+grt_status grt_hf_tensor_name(const char* hf_name, char* out, int32_t out_len, int32_t* out_in) {
+  return guard([&] {
+    bool oi = false;
+    const std::string s = grt::hf_to_grt_name(hf_name, &oi);
+    if (static_cast<int32_t>(s.size()) + 1 > out_len) grt::raise(GRT_InvalidConfig, "output buffer too small");
+    memcpy(out, s.c_str(), s.size() + 1);
+    if (out_in) *out_in = oi ? 1 : 0;
+  });
+}
+
 grt_status grt_model_weight_bytes(grt_model* m, uint64_t* bytes) {
   return guard([&] { *bytes = m->m->weight_bytes(); });
 }

@@ -467,7 +467,7 @@ void Model::init_weights() {
     buf.resize(n);
     for (size_t i = 0; i < n; ++i) buf[i] = uniform_symmetric(eng, 0.1f);
     cuda_check(cudaMemcpy(staging, buf.data(), n * 4, cudaMemcpyHostToDevice), "upload");
-    cuda_check(launch_map_copy(t.map, t.dev, staging, static_cast<int>(Dt::F32), nullptr), "map copy");
+    cuda_check(launch_map_copy(t.map, t.dev, staging, static_cast<int>(Dt::F32), false, nullptr), "map copy");
   }
   cuda_check(cudaDeviceSynchronize(), "mt19937 init");
   cudaFree(staging);
@@ -479,16 +479,24 @@ const LogicalTensor& Model::tensor(const std::string& name) const {
   raise(GRT_ShapeMismatch, "unknown tensor '" + name + "'");
 }
 
-void Model::upload(const std::string& name, const void* host, size_t bytes, int host_dtype) {
+bool Model::has_tensor(const std::string& name) const {
+  for (const LogicalTensor& t : tensors_)
+    if (t.name == name) return true;
+  return false;
+}
+
+void Model::upload(const std::string& name, const void* host, size_t bytes, int host_dtype, bool out_in) {
   const LogicalTensor& t = tensor(name);
   const size_t n = t.rows * t.cols;
-  const size_t eb = host_dtype == GRT_BF16 ? 2 : 4;
+  if (host_dtype != GRT_F32 && host_dtype != GRT_BF16 && host_dtype != GRT_F16)
+    raise(GRT_InvalidConfig, "upload '" + name + "': unknown host dtype");
+  const size_t eb = host_dtype == GRT_F32 ? 4 : 2;
   if (bytes != n * eb) raise(GRT_ShapeMismatch, "upload '" + name + "': byte count mismatch");
   cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
   void* staging = nullptr;
   cuda_check(cudaMalloc(&staging, bytes), "cudaMalloc staging");
   cuda_check(cudaMemcpy(staging, host, bytes, cudaMemcpyHostToDevice), "upload");
-  cuda_check(launch_map_copy(t.map, t.dev, staging, host_dtype, nullptr), "map copy");
+  cuda_check(launch_map_copy(t.map, t.dev, staging, host_dtype, out_in && t.rows > 1, nullptr), "map copy");
   cuda_check(cudaDeviceSynchronize(), "upload");
   cudaFree(staging);
 }
@@ -722,6 +730,10 @@ static int gemv_pair_mode() {
   return v;
 }
 static bool gemv_pair_enabled() { return gemv_pair_mode() != 0; }
+static int pair_chmax(const char* var, int dflt) {
+  const char* e = getenv(var);
+  return e ? atoi(e) : dflt;
+}
 
 std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   const int d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
@@ -805,6 +817,10 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       GemvPairParams pp;
       pp.a = pending.p;
       pp.b = p;
+      if (epi != EPI_SWIGLU) {  // down + (QKV | head): the 44 KB activation row leaves less room for the ring
+        pp.a.chmax = pair_chmax("GRT_PAIR_CHMAX_A", pp.a.chmax);
+        pp.b.chmax = pair_chmax("GRT_PAIR_CHMAX_B", pp.b.chmax);
+      }
       pp.bar = pair_bar_ + 2 * n_pairs_emitted++;
       pp.err = err;
       KernelInvocation inv;

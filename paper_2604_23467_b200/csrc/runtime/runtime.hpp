@@ -207,9 +207,13 @@ class Model {
   KernelInvocation make_sample_preprocess_op();  // both, one launch (the fused dynamic block of a step graph)
 
   // Weight I/O in the reference layout.
-  void upload(const std::string& name, const void* host, size_t bytes, int host_dtype);
+  // out_in: `host` holds a matrix as [n, k] (nn.Linear / checkpoint layout)
+  // instead of the reference's [k, n]
+  void upload(const std::string& name, const void* host, size_t bytes, int host_dtype, bool out_in = false);
   void download(const std::string& name, float* host, size_t numel);
   const LogicalTensor& tensor(const std::string& name) const;
+  bool has_tensor(const std::string& name) const;
+  const std::vector<LogicalTensor>& tensors() const { return tensors_; }
   uint64_t weight_bytes() const { return weight_bytes_; }
   uint64_t decode_bytes(int length) const;  // algorithmic bytes of one pass at `length`
 
@@ -310,6 +314,34 @@ class Model {
 
 // ---------------------------------------------------------------------------
 // capture / replay (exec_graph.hpp:45-141)
+// ---------------------------------------------------------------------------
+// checkpoints (checkpoint.cpp)
+struct StTensor {
+  std::string name, dtype_name;
+  int dtype = -1;  // grt_dtype, -1 = unsupported
+  std::vector<int64_t> shape;
+  uint64_t begin = 0, end = 0;  // offsets into the data block
+};
+class SafetensorsFile {
+ public:
+  explicit SafetensorsFile(const std::string& path);  // raises IoError
+  ~SafetensorsFile();
+  SafetensorsFile(const SafetensorsFile&) = delete;
+  SafetensorsFile& operator=(const SafetensorsFile&) = delete;
+  const std::vector<StTensor>& tensors() const { return tensors_; }
+  const void* data(const StTensor& t) const;
+
+ private:
+  std::string path_;
+  int fd_ = -1;
+  void* map_ = nullptr;
+  size_t size_ = 0;
+  uint64_t data_off_ = 0;
+  std::vector<StTensor> tensors_;
+};
+std::string hf_to_grt_name(const std::string& hf, bool* out_in);
+int load_safetensors(Model& m, const std::string& path, bool strict);
+
 class ExecGraph {
  public:
   ExecGraph(int key, cudaGraphExec_t exec, size_t kernels, int64_t flops, uint64_t epoch, int device);

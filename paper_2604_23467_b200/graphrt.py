@@ -99,7 +99,7 @@ class EvictionPolicy(enum.IntEnum):
 
 
 ARCH_REF, ARCH_LLAMA = 0, 1
-F32, BF16 = 0, 1
+F32, BF16, F16 = 0, 1, 2
 INIT_MT19937, INIT_PHILOX, INIT_NONE = 0, 1, 2
 
 
@@ -153,6 +153,7 @@ EXPORTS = [
     "grt_status_name", "grt_last_error", "grt_abi_version", "grt_device_count", "grt_jit_compile_check",
     "grt_model_config_default", "grt_cache_config_default", "grt_model_create", "grt_model_destroy",
     "grt_model_upload", "grt_model_download", "grt_model_weight_bytes", "grt_model_decode_bytes",
+    "grt_model_load_safetensors", "grt_safetensors_list", "grt_hf_tensor_name",
     "grt_session_create", "grt_session_destroy", "grt_generate", "grt_cache_stats_get", "grt_session_counters",
     "grt_reset", "grt_step", "grt_prefill", "grt_cur_len", "grt_get_logits", "grt_get_kv_row", "grt_sample",
     "grt_sampler_reset", "grt_op_gemv", "grt_op_attention", "grt_op_sample", "grt_op_prefill_gemm",
@@ -192,6 +193,10 @@ def lib():
         L.grt_model_upload.argtypes = [vp, C.c_char_p, vp, C.c_size_t, C.c_int32]
         L.grt_model_download.argtypes = [vp, C.c_char_p, C.POINTER(C.c_float), C.c_size_t]
         L.grt_model_weight_bytes.argtypes = [vp, C.POINTER(C.c_uint64)]
+        L.grt_model_load_safetensors.argtypes = [vp, C.c_char_p, C.c_int32, C.POINTER(C.c_int32)]
+        L.grt_safetensors_list.argtypes = [C.c_char_p, C.c_char_p, C.c_int32, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int32)]
+        L.grt_hf_tensor_name.argtypes = [C.c_char_p, C.c_char_p, C.c_int32, C.POINTER(C.c_int32)]
         L.grt_model_decode_bytes.argtypes = [vp, C.c_int32, C.POINTER(C.c_uint64)]
         L.grt_session_create.argtypes = [vp, C.POINTER(_CacheConfig), C.POINTER(vp)]
         L.grt_tp_unique_id.argtypes = [C.c_char_p, C.c_int32]
@@ -430,6 +435,13 @@ class Model:
         out = np.zeros(numel, np.float32)
         _check(lib().grt_model_download(self._h, name.encode(), out.ctypes.data_as(C.POINTER(C.c_float)), numel))
         return out
+
+    def load_safetensors(self, path: str, strict: bool = True) -> int:
+        """Loads a safetensors checkpoint (file or directory of shards); graphrt or
+        HuggingFace LLaMA tensor names.  Returns the number of tensors loaded."""
+        n = C.c_int32()
+        _check(lib().grt_model_load_safetensors(self._h, str(path).encode(), 1 if strict else 0, C.byref(n)))
+        return n.value
 
     def attach_nccl(self, unique_id: bytes) -> None:
         """Joins this rank's model to the NCCL tensor-parallel group (all ranks call it)."""
@@ -769,3 +781,55 @@ def device_count() -> int:
     n = C.c_int32()
     _check(lib().grt_device_count(C.byref(n)))
     return n.value
+
+
+# ---------------------------------------------------------------------------
+# checkpoints
+
+def safetensors_list(path: str):
+    """[(name, grt dtype or -1, shape tuple)] from a safetensors header (no GPU)."""
+    n = C.c_int32()
+    _check(lib().grt_safetensors_list(str(path).encode(), None, 0, None, None, 0, C.byref(n)))
+    cap = n.value
+    names = C.create_string_buffer(max(1, 512 * cap))
+    dts = (C.c_int32 * max(1, cap))()
+    shp = (C.c_int64 * max(1, 3 * cap))()
+    _check(lib().grt_safetensors_list(str(path).encode(), names, len(names), dts, shp, cap, C.byref(n)))
+    out, raw = [], names.raw.split(b"\0")
+    for i in range(cap):
+        rank = shp[3 * i]
+        out.append((raw[i].decode(), dts[i], tuple(shp[3 * i + 1: 3 * i + 1 + rank])))
+    return out
+
+
+def hf_tensor_name(hf_name: str):
+    """HuggingFace LLaMA name -> (graphrt name or "", stored [out,in])."""
+    buf = C.create_string_buffer(256)
+    oi = C.c_int32()
+    _check(lib().grt_hf_tensor_name(hf_name.encode(), buf, len(buf), C.byref(oi)))
+    return buf.value.decode(), bool(oi.value)
+
+
+def write_safetensors(path: str, tensors, metadata=None) -> None:
+    """Minimal safetensors writer (numpy): {name: array}; uint16 arrays are raw
+    bf16 bits, float16/float32 as themselves.  Test and tooling helper."""
+    import numpy as np
+    hdr, blobs, off = {}, [], 0
+    for name, a in tensors.items():
+        a = np.ascontiguousarray(a)
+        dt = {np.dtype(np.uint16): "BF16", np.dtype(np.float16): "F16", np.dtype(np.float32): "F32"}[a.dtype]
+        b = a.tobytes()
+        hdr[name] = {"dtype": dt, "shape": list(a.shape), "data_offsets": [off, off + len(b)]}
+        blobs.append(b)
+        off += len(b)
+    if metadata:
+        hdr["__metadata__"] = metadata
+    import json as _json
+    h = _json.dumps(hdr).encode()
+    h += b" " * ((8 - len(h) % 8) % 8)
+    with open(path, "wb") as f:
+        f.write(len(h).to_bytes(8, "little"))
+        f.write(h)
+        for b in blobs:
+            f.write(b)
+
