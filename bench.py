@@ -198,12 +198,25 @@ def ipc_leg(layers, max_seq, bucket):
     cl = ctx.Process(target=_ipc_client, args=(qd, qo, prompt, gens))
     sv.start()
     cl.start()
+    import queue
+    t_end = time.time() + 600
     try:
-        res = qo.get(timeout=900)
+        while True:  # fail fast if either process dies (never wait out the whole budget)
+            try:
+                res = qo.get(timeout=2)
+                break
+            except queue.Empty:
+                for pr, nm in ((cl, "context generator"), (sv, "graph generator")):
+                    if pr.exitcode not in (None, 0):
+                        raise RuntimeError(f"{nm} process exited with {pr.exitcode}")
+                if time.time() > t_end:
+                    raise RuntimeError("two-process split timed out")
     finally:
         qdone.put(1)
-        cl.join(120)
-        sv.join(120)
+        for pr in (cl, sv):
+            pr.join(30)
+            if pr.is_alive():
+                pr.kill()
     us = res[-1][3:]
     return {"prompt": 10, "gen": gens[-1], "p50_ms": round(percentile(us, 50) / 1000, 4),
             "p99_ms": round(percentile(us, 99) / 1000, 4),

@@ -68,7 +68,10 @@ typedef enum grt_run_mode {
   GRT_MODE_GRAPH_ONLY = 2,
   GRT_MODE_ABLATE_ASYNC = 3,
   GRT_MODE_ABLATE_FUSED = 4,
-  GRT_MODE_ABLATE_BOTH = 5
+  GRT_MODE_ABLATE_BOTH = 5,
+  /* extension: the whole decode is ONE graph launch -- a
+   * conditional WHILE node over [dynamic block, bucket SWITCH of static passes] */
+  GRT_MODE_DEVICE_LOOP = 6
 } grt_run_mode;
 
 /* Replaces graphrt::EvictionPolicy (graph_cache.hpp:13). */
@@ -135,6 +138,7 @@ typedef struct grt_generation_request {
   int32_t prompt_len;
   int32_t gen_len;
   grt_sample_params sampling;
+  int32_t eos_token;   /* GRT_MODE_DEVICE_LOOP: stop after sampling this id (-1 = never) */
 } grt_generation_request;
 
 /* Replaces graphrt::Counters (virtual_device.hpp:41-49) with real counts. */

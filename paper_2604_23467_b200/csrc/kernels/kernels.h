@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "../jit/ctrl.h"
+
 namespace grt {
 
 enum class Dt : int { F32 = 0, BF16 = 1 };
@@ -231,5 +233,20 @@ cudaError_t launch_map_init(const MapDesc& d, void* dst, uint64_t seed, uint32_t
 cudaError_t launch_map_copy(const MapDesc& d, void* dst, const void* src, int src_dtype, bool src_out_in,
                             cudaStream_t s);
 cudaError_t launch_map_read(const MapDesc& d, const void* dst, float* out_ref_layout, cudaStream_t s);
+
+// ---- device-resident decode loop (loop.cu) ----
+enum LoopStatus : int { LOOP_EOS = 1, LOOP_NO_BUCKET = 2 };
+struct LoopCtl {
+  int remaining;  // decode steps still to run
+  int bucket;     // KV positions per graph key
+  int key_lo;     // bucket key of switch body 0
+  int n_keys;     // switch bodies
+  int eos;        // stop token (-1 = none)
+  int iters;      // steps executed (device count)
+  int status;     // LoopStatus bits
+  int pad;
+};
+cudaError_t launch_loop_ctl(const GrtCtrl* ctrl, LoopCtl* lc, cudaGraphConditionalHandle h_while,
+                            cudaGraphConditionalHandle h_switch, cudaStream_t s);
 
 }  // namespace grt

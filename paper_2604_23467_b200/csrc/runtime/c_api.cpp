@@ -39,7 +39,7 @@ grt_status guard(F&& f) {
 }
 
 grt::RunMode to_mode(int32_t m) {
-  if (m < 0 || m > 5) grt::raise(GRT_InvalidConfig, "unknown mode " + std::to_string(m));
+  if (m < 0 || m > 6) grt::raise(GRT_InvalidConfig, "unknown mode " + std::to_string(m));
   return static_cast<grt::RunMode>(m);
 }
 }  // namespace
@@ -277,6 +277,7 @@ grt_status grt_generate(grt_session* s, const grt_generation_request* req, grt_g
     r.prompt.assign(req->prompt, req->prompt + std::max(0, req->prompt_len));
     r.gen_len = req->gen_len;
     r.sampling = req->sampling;
+    r.eos_token = req->eos_token;
     grt::GenerationResult out = s->s->run(r);
     if (res->tokens) std::memcpy(res->tokens, out.tokens.data(), out.tokens.size() * sizeof(int32_t));
     if (res->per_token_us) std::memcpy(res->per_token_us, out.per_token_us.data(), out.per_token_us.size() * sizeof(double));

@@ -52,15 +52,9 @@ ExecGraphPtr CaptureEngine::capture(int key, const std::vector<const KernelInvoc
     }
   } close{this, key};
 
-  if (kernels.empty()) raise(GRT_EmptyCapture, "capture recorded zero kernels");
+  validate(kernels);
   int64_t flops = 0;
-  for (const KernelInvocation* k : kernels) {
-    if (!k->launch) raise(GRT_CaptureViolation, "kernel '" + k->spec.name + "' has no device launch");
-    for (const DevRange& r : k->bindings)
-      if (!binding_allowed(r))
-        raise(GRT_ForeignBuffer, "kernel '" + k->spec.name + "' binds a buffer outside the model arena");
-    flops += k->spec.flops;
-  }
+  for (const KernelInvocation* k : kernels) flops += k->spec.flops;
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   cuda_check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
   cudaError_t launch_err = cudaSuccess;
@@ -90,6 +84,40 @@ ExecGraphPtr CaptureEngine::capture(int key, const std::vector<const KernelInvoc
     epoch = ++epoch_;
   }
   return std::make_shared<ExecGraph>(key, exec, kernels.size(), flops, epoch, device_);
+}
+
+void CaptureEngine::validate(const std::vector<const KernelInvocation*>& kernels) const {
+  if (kernels.empty()) raise(GRT_EmptyCapture, "capture recorded zero kernels");
+  for (const KernelInvocation* k : kernels) {
+    if (!k->launch) raise(GRT_CaptureViolation, "kernel '" + k->spec.name + "' has no device launch");
+    for (const DevRange& r : k->bindings)
+      if (!binding_allowed(r))
+        raise(GRT_ForeignBuffer, "kernel '" + k->spec.name + "' binds a buffer outside the model arena");
+  }
+}
+
+void CaptureEngine::record_into(cudaGraph_t body, const std::vector<const KernelInvocation*>& kernels,
+                                cudaStream_t stream) {
+  validate(kernels);
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cuda_check(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+             "cudaStreamBeginCaptureToGraph");
+  cudaError_t launch_err = cudaSuccess;
+  std::string failed;
+  for (const KernelInvocation* k : kernels) {
+    launch_err = k->launch(stream);
+    if (launch_err != cudaSuccess) {
+      failed = k->spec.name;
+      break;
+    }
+  }
+  cudaGraph_t g = nullptr;
+  const cudaError_t end_err = cudaStreamEndCapture(stream, &g);
+  if (launch_err != cudaSuccess || end_err != cudaSuccess) {
+    cudaGetLastError();
+    raise(GRT_CudaError, "capture into a conditional body failed at '" + failed +
+                             "': " + cudaGetErrorString(launch_err != cudaSuccess ? launch_err : end_err));
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -73,6 +73,7 @@ struct grt_ipc_server {
   std::string shm;
   cudaEvent_t ev_ctx = nullptr, ev_static = nullptr;
   cudaStream_t stream = nullptr;
+  int64_t passes = 0;  // passes served so far (doorbell counters are monotonic across runs)
 };
 
 struct grt_ipc_client {
@@ -86,6 +87,7 @@ struct grt_ipc_client {
   GrtCtrl* h_ctrl = nullptr;
   volatile int* h_tokens = nullptr;
   volatile unsigned long long* h_stamps = nullptr;
+  int64_t passes = 0;  // passes driven so far (matches the server's count)
 };
 
 namespace grt {
@@ -140,15 +142,18 @@ void ipc_server_serve(grt_ipc_server* sv, int n) {
   std::vector<ExecGraphPtr> graphs;
   for (int key = 1; key <= Model::key_of(n, B); ++key) graphs.push_back(sv->s->static_graph(key));
   cuda_check(cudaStreamSynchronize(sv->s->device().capture_stream()), "captures");
-  b.stat.store(0, std::memory_order_release);
+  // The counters never reset: a run's pass i is number base+i+1 on both sides,
+  // so a run can never consume the previous run's doorbell or events.
+  const int64_t base = sv->passes;
   try {
     for (int i = 0; i < n; ++i) {
-      wait_at_least(b.ctx, i + 1, b.abort_);
+      wait_at_least(b.ctx, base + i + 1, b.abort_);
       cuda_check(cudaStreamWaitEvent(sv->stream, sv->ev_ctx, 0), "wait ev_ctx");
       graphs[Model::key_of(i + 1, B) - 1]->launch(sv->stream);
       cuda_check(cudaEventRecord(sv->ev_static, sv->stream), "record ev_static");
-      b.stat.store(i + 1, std::memory_order_release);
+      b.stat.store(base + i + 1, std::memory_order_release);
     }
+    sv->passes = base + n;
     cuda_check(cudaStreamSynchronize(sv->stream), "serve");
   } catch (...) {
     b.abort_.store(1);
@@ -235,10 +240,11 @@ void ipc_client_generate(grt_ipc_client* c, const int* prompt, int p, int n, con
   float* x = reinterpret_cast<float*>(A + d.off_x);
   const float* logits = reinterpret_cast<const float*>(A + d.off_logits);
   const int pre_threads = std::min(1024, (d.d_model + 31) / 32 * 32);
+  const int64_t base = c->passes;
   try {
     for (int i = 0; i < p + n; ++i) {
       if (i > 0) {
-        wait_at_least(b.stat, i, b.abort_);
+        wait_at_least(b.stat, base + i, b.abort_);
         cuda_check(cudaStreamWaitEvent(c->stream, c->ev_static, 0), "wait ev_static");
       }
       {  // sample_token (no-op during the prompt), then extend_position + slot append
@@ -256,9 +262,13 @@ void ipc_client_generate(grt_ipc_client* c, const int* prompt, int p, int n, con
         cuda_check(launch_jit(c->f_pre, dim3(1), dim3(pre_threads), args, c->stream, false), "ipc preprocess");
       }
       cuda_check(cudaEventRecord(c->ev_ctx, c->stream), "record ev_ctx");
-      b.ctx.store(i + 1, std::memory_order_release);
+      b.ctx.store(base + i + 1, std::memory_order_release);
     }
-    wait_at_least(b.stat, p + n, b.abort_);
+    wait_at_least(b.stat, base + p + n, b.abort_);
+    // the last pass must retire before this call returns: the next run rewrites
+    // the control block the pass reads
+    cuda_check(cudaStreamWaitEvent(c->stream, c->ev_static, 0), "wait ev_static");
+    c->passes = base + p + n;
     cuda_check(cudaStreamSynchronize(c->stream), "ipc generate");
   } catch (...) {
     b.abort_.store(1);

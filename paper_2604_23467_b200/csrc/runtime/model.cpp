@@ -311,6 +311,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   acc(cfg_.n_layers * 4 * 4);  // fused-pair barrier counters
   acc(S * (dh / 2) * 4 * 2);
   acc(sizeof(GrtCtrl));
+  acc(sizeof(LoopCtl));
   acc(S * 4);
   acc(max_gen_ * 8);
   const bool pf = supports_batched_prefill();
@@ -378,6 +379,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   rope_cos_ = static_cast<float*>(arena_buf(S * (dh / 2) * 4, "rope_cos"));
   rope_sin_ = static_cast<float*>(arena_buf(S * (dh / 2) * 4, "rope_sin"));
   ctrl_ = static_cast<GrtCtrl*>(arena_buf(sizeof(GrtCtrl), "ctrl"));
+  loop_ctl_ = static_cast<LoopCtl*>(arena_buf(sizeof(LoopCtl), "loop_ctl"));
   tokens_ = static_cast<int*>(arena_buf(S * 4, "tokens"));
   uniforms_ = static_cast<double*>(arena_buf(max_gen_ * 8, "uniforms"));
   pass_layers_ = static_cast<PassLayer*>(arena_buf(cfg_.n_layers * sizeof(PassLayer), "pass_layers"));

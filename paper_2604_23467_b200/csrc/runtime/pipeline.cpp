@@ -41,6 +41,7 @@ const char* mode_name(RunMode m) noexcept {
     case RunMode::AblateAsync: return "ablate_async";
     case RunMode::AblateFused: return "ablate_fused";
     case RunMode::AblateBoth: return "ablate_both";
+    case RunMode::DeviceLoop: return "device_loop";
   }
   return "?";
 }
@@ -53,6 +54,7 @@ ModePolicy policy_for(RunMode m) noexcept {
     case RunMode::AblateAsync: return {true, true, false, true};
     case RunMode::AblateFused: return {true, true, true, false};
     case RunMode::AblateBoth: return {true, true, false, false};
+    case RunMode::DeviceLoop: return {true, false, true, true};
   }
   return {};
 }
@@ -265,9 +267,96 @@ Session::~Session() {
     }
     cudaStreamSynchronize(dev_->replay());
   }
+  if (loop_.exec) cudaGraphExecDestroy(loop_.exec);
   cache_.reset();
   dev_.reset();
   if (h_ctrl_) cudaFreeHost(h_ctrl_);
+  if (h_loop_) cudaFreeHost(h_loop_);
+}
+
+// The device-resident decode loop (loop.cu): one graph
+//   WHILE(h_while) { sample+preprocess -> loop_ctl -> SWITCH(h_switch) { pass(key_lo) .. pass(key_hi) } }
+// built once per session over every bucket key of the model.  The static
+// passes are the same plans the bucket graphs replay (same kernels, PDL
+// edges), recorded into the switch bodies with cudaStreamBeginCaptureToGraph.
+void Session::build_device_loop() {
+  if (loop_.exec) return;
+  if (model_->tp_size() > 1) raise(GRT_Unsupported, "device loop: single GPU only (NCCL nodes in conditional bodies)");
+  const double t0 = now_us();
+  const int B = cc_.bucket_size;
+  loop_.key_lo = 1;
+  loop_.n_keys = model_->max_key(B);
+  cudaStream_t s = dev_->capture_stream();
+  cuda_check(cudaSetDevice(model_->device()), "cudaSetDevice");
+  cudaGraph_t g = nullptr;
+  cuda_check(cudaGraphCreate(&g, 0), "cudaGraphCreate");
+  struct Guard {
+    cudaGraph_t g;
+    ~Guard() { cudaGraphDestroy(g); }
+  } guard{g};
+  cudaGraphConditionalHandle h_while;
+  cuda_check(cudaGraphConditionalHandleCreate(&h_while, g, 1, cudaGraphCondAssignDefault), "while handle");
+  cudaGraphNodeParams wp = {};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = h_while;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  cuda_check(cudaGraphAddNode(&wn, g, nullptr, 0, &wp), "while node");
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  cudaGraphConditionalHandle h_switch;
+  cuda_check(cudaGraphConditionalHandleCreate(&h_switch, body, 0, cudaGraphCondAssignDefault), "switch handle");
+
+  // [dynamic block, loop_ctl]
+  KernelInvocation ctl;
+  ctl.spec.name = "loop_ctl";
+  ctl.spec.op_class = OpClass::Dynamic;
+  ctl.bindings = {{model_->ctrl_dev(), sizeof(GrtCtrl)}, {model_->loop_ctl_dev(), sizeof(LoopCtl)}};
+  {
+    const GrtCtrl* c = model_->ctrl_dev();
+    LoopCtl* lc = model_->loop_ctl_dev();
+    ctl.launch = [c, lc, h_while, h_switch](cudaStream_t st) { return launch_loop_ctl(c, lc, h_while, h_switch, st); };
+  }
+  engine_->record_into(body, {&sample_pre_op_, &ctl}, s);
+  size_t nn = 0;
+  cuda_check(cudaGraphGetNodes(body, nullptr, &nn), "body nodes");
+  std::vector<cudaGraphNode_t> nodes(nn);
+  cuda_check(cudaGraphGetNodes(body, nodes.data(), &nn), "body nodes");
+  cudaGraphNode_t sink = nullptr;
+  for (cudaGraphNode_t n : nodes) {
+    size_t nd = 0;
+    cuda_check(cudaGraphNodeGetDependentNodes(n, nullptr, &nd), "dependents");
+    if (nd == 0) sink = n;
+  }
+  if (!sink) raise(GRT_CudaError, "device loop: no sink node in the loop body");
+
+  cudaGraphNodeParams sp = {};
+  sp.type = cudaGraphNodeTypeConditional;
+  sp.conditional.handle = h_switch;
+  sp.conditional.type = cudaGraphCondTypeSwitch;
+  sp.conditional.size = static_cast<unsigned>(loop_.n_keys);
+  cudaGraphNode_t sn;
+  cuda_check(cudaGraphAddNode(&sn, body, &sink, 1, &sp), "switch node");
+  size_t kernels = 2;
+  for (int i = 0; i < loop_.n_keys; ++i) {
+    const auto& plan = model_->plan(loop_.key_lo + i, B, cc_.pass_impl);
+    std::vector<const KernelInvocation*> ks;
+    for (const auto& k : plan) ks.push_back(&k);
+    engine_->record_into(sp.conditional.phGraph_out[i], ks, s);
+    kernels += ks.size();
+    if (i == 0) loop_.kernels_per_step = 2 + ks.size();
+  }
+  cuda_check(cudaGraphInstantiateWithFlags(&loop_.exec, g, 0), "device loop instantiate");
+  cuda_check(cudaGraphUpload(loop_.exec, s), "device loop upload");
+  cuda_check(cudaStreamSynchronize(s), "device loop upload");
+  loop_.kernels = kernels;
+  ++dev_->counters().captures;
+  if (!h_loop_) {
+    void* hl = nullptr;
+    cuda_check(cudaHostAlloc(&hl, sizeof(LoopCtl), cudaHostAllocDefault), "cudaHostAlloc loop");
+    h_loop_ = static_cast<LoopCtl*>(hl);
+  }
+  loop_.build_ms = (now_us() - t0) / 1000.0;
 }
 
 void Session::write_ctrl(int seq_len, int prompt_len, const grt_sample_params& sp, int max_gen) {
@@ -393,6 +482,7 @@ void Session::check_device_errors() {
 
 GenerationResult Session::run(const GenerationRequest& req) {
   validate(req);
+  if (req.mode == RunMode::DeviceLoop) build_device_loop();  // once per session, before the clock starts
   const ModePolicy pol = policy_for(req.mode);
   const int p = static_cast<int>(req.prompt.size());
   const int n = req.gen_len;
@@ -467,11 +557,29 @@ GenerationResult Session::run(const GenerationRequest& req) {
       if (now_us() > deadline) raise(GRT_CudaError, "timed out waiting for sampled tokens");
     }
   };
-  for (int i = 1; i <= n; ++i) {
-    channel.send_request({i, Model::key_of(p + i, B), pol.fuse_dynamic});
-    channel.send_response(serve(channel.take_request(), true, pol));
-    res.decode_paths.push_back(channel.take_response().path);
-    poll(i >= 2 ? 1 : 0);  // once step 2 is queued, wait for the first token (TTFT)
+  if (req.mode == RunMode::DeviceLoop) {
+    // every decode step in ONE graph launch; bucket choice and stop on the device
+    LoopCtl& lc = *h_loop_;
+    lc = LoopCtl{};
+    lc.remaining = n;
+    lc.bucket = B;
+    lc.key_lo = loop_.key_lo;
+    lc.n_keys = loop_.n_keys;
+    lc.eos = req.eos_token;
+    cuda_check(cudaMemcpyAsync(model_->loop_ctl_dev(), h_loop_, sizeof(LoopCtl), cudaMemcpyHostToDevice, s),
+               "loop ctl");
+    cuda_check(cudaGraphLaunch(loop_.exec, s), "device loop launch");
+    ++dev_->counters().dispatches;
+    ++dev_->counters().graph_replays;
+    res.decode_paths.assign(n, StepPath::Replayed);
+    poll(1);
+  } else {
+    for (int i = 1; i <= n; ++i) {
+      channel.send_request({i, Model::key_of(p + i, B), pol.fuse_dynamic});
+      channel.send_response(serve(channel.take_request(), true, pol));
+      res.decode_paths.push_back(channel.take_response().path);
+      poll(i >= 2 ? 1 : 0);  // once step 2 is queued, wait for the first token (TTFT)
+    }
   }
   poll(n);
   res.ttft_us = n > 0 ? res.host_token_us[0] : 0.0;
@@ -496,6 +604,10 @@ GenerationResult Session::run(const GenerationRequest& req) {
   res.per_token_us.resize(n);
   for (int i = 0; i < n; ++i) {
     res.tokens[i] = ht[i];
+    if (ht[i] < 0) {  // never produced (device loop stopped at the end-of-sequence token)
+      res.per_token_us[i] = 0.0;
+      continue;
+    }
     const double end_i = static_cast<double>(st[2 * i + 1]);
     const double prev = i == 0 ? static_cast<double>(st[0]) : static_cast<double>(st[2 * i - 1]);
     res.per_token_us[i] = (end_i - prev) / 1000.0;
@@ -508,6 +620,13 @@ GenerationResult Session::run(const GenerationRequest& req) {
   res.cache_delta.evictions = after.evictions - before.evictions;
   res.cache_delta.releases = after.releases - before.releases;
   cur_len_ = p + n;
+  if (req.mode == RunMode::DeviceLoop) {
+    LoopCtl lc;
+    cuda_check(cudaMemcpy(&lc, model_->loop_ctl_dev(), sizeof(LoopCtl), cudaMemcpyDeviceToHost), "loop ctl");
+    if (lc.status & LOOP_NO_BUCKET) raise(GRT_WrongLength, "device loop: live length outside every bucket");
+    cuda_check(cudaMemcpy(&cur_len_, &model_->ctrl_dev()->seq_len, sizeof(int), cudaMemcpyDeviceToHost), "seq_len");
+    res.counters.graph_kernel_nodes = static_cast<uint64_t>(lc.iters) * loop_.kernels_per_step;
+  }
   return res;
 }
 

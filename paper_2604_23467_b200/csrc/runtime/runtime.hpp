@@ -219,6 +219,7 @@ class Model {
 
   // device state
   GrtCtrl* ctrl_dev() const { return ctrl_; }
+  LoopCtl* loop_ctl_dev() const { return loop_ctl_; }
   int* tokens_dev() const { return tokens_; }
   double* uniforms_dev() const { return uniforms_; }
   float* logits_dev() const { return logits_; }
@@ -295,6 +296,7 @@ class Model {
   float* logits_local_ = nullptr;  // [vl_] before the allgather (== logits_ when tp_size == 1)
   TpComm* comm_ = nullptr;
   GrtCtrl* ctrl_ = nullptr;
+  LoopCtl* loop_ctl_ = nullptr;
   int* tokens_ = nullptr;
   double* uniforms_ = nullptr;
   int max_gen_ = 0;
@@ -374,6 +376,9 @@ class CaptureEngine {
   // instantiates them.  Raises CaptureViolation / ForeignBuffer / EmptyCapture /
   // CaptureInProgress like CaptureSession::record / end_capture.
   ExecGraphPtr capture(int key, const std::vector<const KernelInvocation*>& kernels, cudaStream_t stream);
+  // same checks, recorded into an existing (conditional body) graph
+  void record_into(cudaGraph_t body, const std::vector<const KernelInvocation*>& kernels, cudaStream_t stream);
+  void validate(const std::vector<const KernelInvocation*>& kernels) const;
   bool binding_allowed(const DevRange& r) const { return arena_->contains(r.ptr, r.bytes); }
 
  private:
@@ -421,7 +426,7 @@ class GraphCache {
 
 // ---------------------------------------------------------------------------
 // pipeline (pipeline.hpp)
-enum class RunMode { Eager = 0, Hybrid = 1, GraphOnly = 2, AblateAsync = 3, AblateFused = 4, AblateBoth = 5 };
+enum class RunMode { Eager = 0, Hybrid = 1, GraphOnly = 2, AblateAsync = 3, AblateFused = 4, AblateBoth = 5, DeviceLoop = 6 };
 const char* mode_name(RunMode m) noexcept;
 
 struct ModePolicy {
@@ -513,6 +518,7 @@ struct GenerationRequest {
   std::vector<int> prompt;
   int gen_len = 1;
   grt_sample_params sampling{GRT_SAMPLE_GREEDY, 1.0f, 0, 1.0f, 7};
+  int eos_token = -1;  // DeviceLoop only
 };
 
 struct GenerationResult {
@@ -583,6 +589,19 @@ class Session {
   int n_sampled_ = 0;  // step-level sampler draws since sampler_reset (Philox counter / uniform index)
   int captures_completed_ = 0;
   GrtCtrl* h_ctrl_ = nullptr;  // pinned staging for ctrl writes
+  // device-resident decode loop (loop.cu): one WHILE-node graph over every bucket
+  struct DeviceLoop {
+    cudaGraphExec_t exec = nullptr;
+    int key_lo = 0, n_keys = 0;
+    size_t kernels = 0, kernels_per_step = 0;
+    double build_ms = 0;
+  } loop_;
+  LoopCtl* h_loop_ = nullptr;  // pinned staging
+  void build_device_loop();
+
+ public:
+  int device_loop_keys() const { return loop_.n_keys; }
+  double device_loop_build_ms() const { return loop_.build_ms; }
 };
 
 // ---------------------------------------------------------------------------

@@ -68,11 +68,12 @@ class RunMode(enum.IntEnum):
     AblateAsync = 3
     AblateFused = 4
     AblateBoth = 5
+    DeviceLoop = 6  # extension: the whole decode as one graph launch (WHILE + SWITCH nodes)
 
 
 _MODE_NAMES = {RunMode.Eager: "eager", RunMode.Hybrid: "hybrid", RunMode.GraphOnly: "graph_only",
                RunMode.AblateAsync: "ablate_async", RunMode.AblateFused: "ablate_fused",
-               RunMode.AblateBoth: "ablate_both"}
+               RunMode.AblateBoth: "ablate_both", RunMode.DeviceLoop: "device_loop"}
 ALL_MODES = list(RunMode)
 
 
@@ -127,7 +128,7 @@ class _SampleParams(C.Structure):
 
 class _Request(C.Structure):
     _fields_ = [("mode", C.c_int32), ("prompt", C.POINTER(C.c_int32)), ("prompt_len", C.c_int32),
-                ("gen_len", C.c_int32), ("sampling", _SampleParams)]
+                ("gen_len", C.c_int32), ("sampling", _SampleParams), ("eos_token", C.c_int32)]
 
 
 class _Counters(C.Structure):
@@ -355,6 +356,7 @@ class GenerationRequest:
     gen_len: int = 1
     strategy: SampleStrategy = field(default_factory=SampleStrategy.greedy)
     sampler_seed: int = 7
+    eos_token: int = -1  # RunMode.DeviceLoop: stop after sampling this id
 
 
 @dataclass
@@ -595,7 +597,7 @@ class Session:
         n = max(req.gen_len, 0)
         prompt = (C.c_int32 * max(p, 1))(*req.prompt) if p else (C.c_int32 * 1)()
         r = _Request(int(req.mode), C.cast(prompt, C.POINTER(C.c_int32)), p, req.gen_len,
-                     req.strategy._c(req.sampler_seed))
+                     req.strategy._c(req.sampler_seed), int(req.eos_token))
         toks = (C.c_int32 * max(n, 1))()
         gaps = (C.c_double * max(n, 1))()
         pp = (C.c_int32 * max(p, 1))()

@@ -264,6 +264,58 @@ def test_hybrid_replays_warm_keys_and_captures_the_rest():
     assert r1.tokens == r2.tokens
 
 
+# ------------------------------------------------- device-resident decode loop
+
+@pytest.mark.parametrize("bucket,impl", [(4, 1), (64, 1), (8, 0)])
+def test_device_loop_is_one_launch_and_reproduces_reference(golden, bucket, impl):
+    """RunMode.DeviceLoop: the whole decode is ONE graph
+    launch (WHILE node, bucket SWITCH on the device) and yields the reference
+    binary's tokens; small buckets make the loop cross many switch bodies."""
+    gd = golden("tiny_ref_greedy.json")
+    s = g.Session(g.ModelConfig(), cache(bucket=bucket, hi=2, pass_impl=impl))
+    for _ in range(2):  # second run reuses the instantiated loop graph
+        r = s.run(g.GenerationRequest(mode=g.RunMode.DeviceLoop, prompt=gd["prompt"], gen_len=32))
+        assert r.tokens == gd["tokens"]
+        assert r.counters.kernel_launches == 0
+        assert r.decode_paths == [g.StepPath.Replayed] * 32
+    h = s.run(g.GenerationRequest(mode=g.RunMode.Hybrid, prompt=gd["prompt"], gen_len=32))
+    assert h.tokens == r.tokens
+    assert r.counters.graph_replays == h.counters.graph_replays - 32 + 1
+    assert all(t > 0 for t in r.per_token_us)
+
+
+def test_device_loop_temperature_and_eos(golden):
+    gd = golden("tiny_ref_temp08.json")
+    s = g.Session(g.ModelConfig(), cache(bucket=16))
+    strat = g.SampleStrategy.with_temperature(0.8)
+    r = s.run(g.GenerationRequest(mode=g.RunMode.DeviceLoop, prompt=gd["prompt"], gen_len=32, strategy=strat,
+                                  sampler_seed=7))
+    assert r.tokens == gd["tokens"]
+    want = gd["tokens"]
+    stop = next(i for i in range(3, 32) if want[i] not in want[:i])  # first fresh id from step 3 on
+    r = s.run(g.GenerationRequest(mode=g.RunMode.DeviceLoop, prompt=gd["prompt"], gen_len=32, strategy=strat,
+                                  sampler_seed=7, eos_token=want[stop]))
+    assert r.tokens[:stop + 1] == want[:stop + 1]
+    assert r.tokens[stop + 1:] == [-1] * (31 - stop)
+    # the session stays usable after an early stop
+    r = s.run(g.GenerationRequest(mode=g.RunMode.Hybrid, prompt=gd["prompt"], gen_len=32, strategy=strat,
+                                  sampler_seed=7))
+    assert r.tokens == want
+
+
+def test_device_loop_llama_7b_dims_matches_hybrid():
+    """2-layer LLaMA at 7B dims (bf16, fused GEMV pairs, cluster attention): the
+    device loop crosses three 16-position buckets and matches hybrid replay."""
+    kw = dict(arch=g.ARCH_LLAMA, n_layers=2, d_model=4096, n_heads=32, vocab_size=32000, max_seq_len=128,
+              d_ff_=11008, weight_dtype=g.BF16, kv_dtype=g.BF16, init=g.INIT_PHILOX, seed=3)
+    s = g.Session(g.ModelConfig(**kw), cache(bucket=16, hi=0, batched_prefill=True))
+    prompt = po.make_prompt(42, 10, 32000)
+    a = s.run(g.GenerationRequest(mode=g.RunMode.Hybrid, prompt=prompt, gen_len=40))
+    b = s.run(g.GenerationRequest(mode=g.RunMode.DeviceLoop, prompt=prompt, gen_len=40))
+    assert a.tokens == b.tokens
+    assert b.counters.graph_replays == 1 and b.counters.kernel_launches == 0
+
+
 def test_persistent_pass_matches_per_op_kernels():
     """The single-kernel pass and the per-op plan compute the same pass (chunk
     sizes differ, so fp32 summation order differs): logits agree to 1e-4."""
@@ -429,7 +481,8 @@ def _ipc_server_proc(q_desc, q_done, shm, cfg_kw, n_passes):
     s = gg.Session(gg.ModelConfig(**cfg_kw), gg.CacheConfig(bucket_size=16, warmup_hi=0))
     sv = gg.IpcServer(s, shm)
     q_desc.put(sv.descriptor())
-    sv.serve(n_passes)
+    for n in n_passes:
+        sv.serve(n)
     q_done.get(timeout=120)
     sv.close()
 
@@ -438,9 +491,12 @@ def _ipc_client_proc(q_desc, q_out, shm, prompt, n, kind):
     from paper_2604_23467_b200 import graphrt as gg
     c = gg.IpcClient(q_desc.get(timeout=120), shm)
     strat = gg.SampleStrategy.greedy() if kind == "greedy" else gg.SampleStrategy.with_temperature(0.8)
-    toks, us = c.generate(prompt, n, strat, seed=7)
+    runs = []
+    for nn in n:  # back-to-back runs: each must start from a clean doorbell/event state
+        toks, us = c.generate(prompt, nn, strat, seed=7)
+        runs.append(list(toks))
     c.close()
-    q_out.put(toks)
+    q_out.put(runs)
 
 
 @pytest.mark.parametrize("kind,fixture", [("greedy", "tiny_ref_greedy.json"), ("temp", "tiny_ref_temp08.json")])
@@ -456,17 +512,18 @@ def test_two_process_ipc_split_reproduces_reference(golden, kind, fixture):
     ctx = mp.get_context("spawn")
     q_desc, q_done, q_out = ctx.Queue(), ctx.Queue(), ctx.Queue()
     shm = f"/grt_ipc_test_{os.getpid()}_{kind}"
-    sv = ctx.Process(target=_ipc_server_proc, args=(q_desc, q_done, shm, {}, len(prompt) + n))
-    cl = ctx.Process(target=_ipc_client_proc, args=(q_desc, q_out, shm, prompt, n, kind))
+    gens = [n, 5, n]
+    sv = ctx.Process(target=_ipc_server_proc, args=(q_desc, q_done, shm, {}, [len(prompt) + k for k in gens]))
+    cl = ctx.Process(target=_ipc_client_proc, args=(q_desc, q_out, shm, prompt, gens, kind))
     sv.start()
     cl.start()
     try:
-        toks = q_out.get(timeout=180)
+        runs = q_out.get(timeout=180)
     finally:
         q_done.put(1)
         cl.join(60)
         sv.join(60)
-    assert toks == want
+    assert runs == [want, want[:5], want]
 
 
 @pytest.mark.parametrize("tp,kw,plen,tol", [
