@@ -51,53 +51,79 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML every
+    5 ms on a thread (the timed region is ~0.3 s, too short for nvidia-smi's
+    start-up); nvidia-smi -lms 100 only if NVML is unavailable."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, gpu: int):
-        self.gpu = gpu
-        self.rows = []
-        self.proc = None
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        try:
+            self.gpu = int(vis.split(",")[gpu]) if vis else gpu
+        except Exception:
+            self.gpu = gpu
+        self.rows = []  # (sm_mhz, max_mhz, reason bits)
+        self.stop = threading.Event()
+        self.thread = None
+        self.source = None
+
+    def _nvml_loop(self, nv, h):
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), int(rs)))
+            except Exception:
+                pass
+            self.stop.wait(0.005)
+
+    def _smi_loop(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
+        proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + fields,
+                                 "--format=csv,noheader,nounits", "-lms", "100"],
+                                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        bits = [0x8, 0x20, 0x40, 0x4]
+        for line in proc.stdout:
+            if self.stop.is_set():
+                break
+            r = [x.strip() for x in line.split(",")]
+            try:
+                rb = sum(b for b, v in zip(bits, r[2:6]) if v.lower() == "active")
+                self.rows.append((float(r[0]), float(r[1]), rb))
+            except Exception:
+                pass
+        proc.terminate()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.source = "nvml"
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
         except Exception:
-            self.proc = None
+            self.source = "nvidia-smi"
+            self.thread = threading.Thread(target=self._smi_loop, daemon=True)
+        self.thread.start()
+        time.sleep(0.02)  # first samples land before the timed region starts
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.thread:
+            self.thread.join(timeout=5)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            for i, n in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        reasons = sorted(n for n, b in self.REASONS.items() if any(r[2] & b for r in self.rows))
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
 def cpu_reference_sample(timeout=600):
@@ -390,7 +416,6 @@ def main():
             cpu = {"value": None, "unit": "ms/token", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
     steps_total = n
-    nodes_per_step = r.counters.graph_kernel_nodes / max(1, r.counters.graph_replays)
     line = {
         "metric": METRIC, "value": round(p50, 4), "unit": "ms/token", "n_gpus": args.gpus, "steps": K,
         "warmup": W, "ms_per_step": round(mean, 4), "higher_is_better": False,
@@ -410,7 +435,7 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_p50, 4), "unit": "ms/token", "h2d_bytes_per_step": round((4 * P + 128) / n, 2),
                 "d2h_bytes_per_step": 4 + 16},
-        "gpu_launches": int(round(nodes_per_step * K + r.counters.kernel_launches * K / n)),
+        "gpu_launches": int(round((r.counters.graph_kernel_nodes + r.counters.kernel_launches) * K / n)),
         "host_kernel_launches_per_step": r.counters.kernel_launches / n,
         "graph_launches_per_step": r.counters.graph_replays / (n + (0 if args.batched_prefill else P)),
         "prefill": "batched tcgen05 (one pass over the prompt)" if args.batched_prefill else "token-by-token graphs",

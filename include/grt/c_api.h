@@ -138,7 +138,8 @@ typedef struct grt_generation_request {
   int32_t prompt_len;
   int32_t gen_len;
   grt_sample_params sampling;
-  int32_t eos_token;   /* GRT_MODE_DEVICE_LOOP: stop after sampling this id (-1 = never) */
+  int32_t stop_on_eos; /* GRT_MODE_DEVICE_LOOP: nonzero = stop after sampling eos_token (zero-init: off) */
+  int32_t eos_token;
 } grt_generation_request;
 
 /* Replaces graphrt::Counters (virtual_device.hpp:41-49) with real counts. */

@@ -277,7 +277,7 @@ grt_status grt_generate(grt_session* s, const grt_generation_request* req, grt_g
     r.prompt.assign(req->prompt, req->prompt + std::max(0, req->prompt_len));
     r.gen_len = req->gen_len;
     r.sampling = req->sampling;
-    r.eos_token = req->eos_token;
+    r.eos_token = req->stop_on_eos ? req->eos_token : -1;
     grt::GenerationResult out = s->s->run(r);
     if (res->tokens) std::memcpy(res->tokens, out.tokens.data(), out.tokens.size() * sizeof(int32_t));
     if (res->per_token_us) std::memcpy(res->per_token_us, out.per_token_us.data(), out.per_token_us.size() * sizeof(double));

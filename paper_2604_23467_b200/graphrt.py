@@ -128,7 +128,8 @@ class _SampleParams(C.Structure):
 
 class _Request(C.Structure):
     _fields_ = [("mode", C.c_int32), ("prompt", C.POINTER(C.c_int32)), ("prompt_len", C.c_int32),
-                ("gen_len", C.c_int32), ("sampling", _SampleParams), ("eos_token", C.c_int32)]
+                ("gen_len", C.c_int32), ("sampling", _SampleParams), ("stop_on_eos", C.c_int32),
+                ("eos_token", C.c_int32)]
 
 
 class _Counters(C.Structure):
@@ -597,7 +598,8 @@ class Session:
         n = max(req.gen_len, 0)
         prompt = (C.c_int32 * max(p, 1))(*req.prompt) if p else (C.c_int32 * 1)()
         r = _Request(int(req.mode), C.cast(prompt, C.POINTER(C.c_int32)), p, req.gen_len,
-                     req.strategy._c(req.sampler_seed), int(req.eos_token))
+                     req.strategy._c(req.sampler_seed), 1 if req.eos_token >= 0 else 0,
+                     max(int(req.eos_token), 0))
         toks = (C.c_int32 * max(n, 1))()
         gaps = (C.c_double * max(n, 1))()
         pp = (C.c_int32 * max(p, 1))()

@@ -165,10 +165,13 @@ def test_graphrt_named_dump_round_trips(tmp_path):
     names = ["embedding", "lnf_gamma", "head"] + [f"layers.{l}.{n}" for l in range(LLAMA_KW["n_layers"])
                                                    for n in ("wq", "wk", "wv", "wo", "w_gate", "w_up", "w_down",
                                                              "ln1_gamma", "ln2_gamma")]
+    d, V, ff = LLAMA_KW["d_model"], LLAMA_KW["vocab_size"], D_FF
+    shape = {"embedding": (V, d), "head": (d, V), "wq": (d, d), "wk": (d, d), "wv": (d, d), "wo": (d, d),
+             "w_gate": (d, ff), "w_up": (d, ff), "w_down": (ff, d)}
     t = {}
     for n in names:
         a = src.download(n, o.weight(n).size)
-        t[n] = a if "gamma" in n else bf16_bits(a)
+        t[n] = a if "gamma" in n else bf16_bits(a).reshape(shape[n.split(".")[-1]])  # reference [k,n] layout
     path = str(tmp_path / "dump.safetensors")
     g.write_safetensors(path, t)
     m = _empty_model()
