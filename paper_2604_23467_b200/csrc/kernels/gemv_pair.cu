@@ -58,7 +58,147 @@ __device__ __forceinline__ unsigned long long gp_timer() {
   return t;
 }
 
-template <int EB>
+// ---- phase 0: decode attention (make_attention, kernels.cpp:87-137) ---------
+// Partial of head b/ns over positions [s*span, min(len, (s+1)*span)), s = b%ns:
+// every K and V row of a 64-position step is requested at once (G = dh/4 lanes
+// per row, 4 elements each), scores masked by the live length, online
+// max-subtracted softmax per warp, warps merged in warp order.  Writes
+// {o[dh], m, l} (o unnormalised) to part[(head*ns + s) * (dh+4)].
+constexpr int GP_ATT_UNROLL = 8;
+
+__device__ __forceinline__ float4 ld_bf16x4(const __nv_bfloat16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  return make_float4(bf16lo(u.x), bf16hi(u.x), bf16lo(u.y), bf16hi(u.y));
+}
+
+__device__ __forceinline__ void pair_attn_partial(const PairAttn& A, float* scratch, int* err) {
+  const int dh = A.head_dim, G = dh >> 2, RPW = 32 / G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / G, c = lane - g * G;
+  const int head = blockIdx.x / A.ns, split = blockIdx.x - head * A.ns;
+  const int len = __ldcg(A.seq_len);
+  if ((len < 1 || len > A.ns * A.span) && blockIdx.x == 0 && threadIdx.x == 0 && err)
+    atomicOr(err, DEVERR_WRONG_LENGTH);  // live length outside the bucket this graph was built for
+  const int j0 = split * A.span, j1 = min(len, j0 + A.span);
+  const __nv_bfloat16* K = static_cast<const __nv_bfloat16*>(A.k_cache) + static_cast<int64_t>(head) * A.max_seq * dh + 4 * c;
+  const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(A.v_cache) + static_cast<int64_t>(head) * A.max_seq * dh + 4 * c;
+  const float4 q4 = __ldcg(reinterpret_cast<const float4*>(A.q + head * dh) + c);
+  float m = -INFINITY, l = 0.0f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int step = GP_WARPS * GP_ATT_UNROLL * RPW;
+  for (int base = j0; base < j1; base += step) {
+    const int jw = base + warp * GP_ATT_UNROLL * RPW;
+    float4 kv[GP_ATT_UNROLL], vv[GP_ATT_UNROLL];
+#pragma unroll
+    for (int u = 0; u < GP_ATT_UNROLL; ++u) {
+      const int j = min(jw + u * RPW + g, A.max_seq - 1);  // masked below
+      kv[u] = ld_bf16x4(K + static_cast<int64_t>(j) * dh);
+      vv[u] = ld_bf16x4(V + static_cast<int64_t>(j) * dh);
+    }
+    float sc[GP_ATT_UNROLL];
+    float mr = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < GP_ATT_UNROLL; ++u) {
+      float sv = q4.x * kv[u].x + q4.y * kv[u].y + q4.z * kv[u].z + q4.w * kv[u].w;
+      for (int o = G >> 1; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+      sc[u] = jw + u * RPW + g < j1 ? sv * A.scale : -INFINITY;
+      mr = fmaxf(mr, sc[u]);
+    }
+    for (int o = G; o < 32; o <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    if (mr != -INFINITY) {
+      const float mn = fmaxf(m, mr);
+      const float f = m == -INFINITY ? 0.0f : __expf(m - mn);
+      l *= f;
+      acc = make_float4(acc.x * f, acc.y * f, acc.z * f, acc.w * f);
+      m = mn;
+#pragma unroll
+      for (int u = 0; u < GP_ATT_UNROLL; ++u) {
+        if (sc[u] == -INFINITY) continue;
+        const float e = __expf(sc[u] - m);
+        l += e;
+        acc.x = fmaf(e, vv[u].x, acc.x);
+        acc.y = fmaf(e, vv[u].y, acc.y);
+        acc.z = fmaf(e, vv[u].z, acc.z);
+        acc.w = fmaf(e, vv[u].w, acc.w);
+      }
+    }
+  }
+  for (int o = G; o < 32; o <<= 1) {
+    l += __shfl_xor_sync(0xffffffffu, l, o);
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+  }
+  const int ld = dh + 4;
+  if (lane < G) reinterpret_cast<float4*>(scratch + warp * ld)[c] = acc;
+  if (lane == 0) {
+    scratch[warp * ld + dh] = m;
+    scratch[warp * ld + dh + 1] = l;
+  }
+  consumer_sync();
+  float M = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < GP_WARPS; ++w) M = fmaxf(M, scratch[w * ld + dh]);
+  float* out = A.part + static_cast<int64_t>(head * A.ns + split) * ld;
+  for (int d = threadIdx.x; d < dh; d += CONSUMER_THREADS) {
+    float o = 0.0f;
+#pragma unroll
+    for (int w = 0; w < GP_WARPS; ++w) {
+      const float mw = scratch[w * ld + dh];
+      if (mw != -INFINITY) o += scratch[w * ld + d] * __expf(mw - M);
+    }
+    out[d] = o;
+  }
+  if (threadIdx.x == 0) {
+    float L = 0.0f;
+#pragma unroll
+    for (int w = 0; w < GP_WARPS; ++w) {
+      const float mw = scratch[w * ld + dh];
+      if (mw != -INFINITY) L += scratch[w * ld + dh + 1] * __expf(mw - M);
+    }
+    out[dh] = M;
+    out[dh + 1] = L;
+  }
+}
+
+// Merge of every head's split partials into the Wo activation row (k = h*dh),
+// in the xs layout; split order is fixed, so the result is deterministic.
+__device__ __forceinline__ void pair_attn_merge(const PairAttn& A, int k, float* xs, float* tbl) {
+  const int dh = A.head_dim, ns = A.ns, ld = dh + 4;
+  for (int hh = threadIdx.x; hh < A.n_heads; hh += CONSUMER_THREADS) {
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < ns; ++s2) M = fmaxf(M, __ldcg(A.part + static_cast<int64_t>(hh * ns + s2) * ld + dh));
+    float L = 0.0f;
+    for (int s2 = 0; s2 < ns; ++s2) {
+      const float* pp = A.part + static_cast<int64_t>(hh * ns + s2) * ld;
+      const float ms = __ldcg(pp + dh);
+      const float f = ms == -INFINITY ? 0.0f : __expf(ms - M);
+      tbl[hh * ns + s2] = f;
+      L += __ldcg(pp + dh + 1) * f;
+    }
+    const float inv = 1.0f / L;
+    for (int s2 = 0; s2 < ns; ++s2) tbl[hh * ns + s2] *= inv;
+  }
+  consumer_sync();
+  for (int j4 = threadIdx.x; j4 < (k >> 2); j4 += CONSUMER_THREADS) {
+    const int idx = 4 * j4, hh = idx / dh, d = idx - hh * dh;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s2 = 0; s2 < ns; ++s2) {
+      const float w = tbl[hh * ns + s2];
+      if (w == 0.0f) continue;
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(A.part + static_cast<int64_t>(hh * ns + s2) * ld + d));
+      o.x = fmaf(w, v.x, o.x);
+      o.y = fmaf(w, v.y, o.y);
+      o.z = fmaf(w, v.z, o.z);
+      o.w = fmaf(w, v.w, o.w);
+    }
+    xs_store4<__nv_bfloat16>(xs, j4, k, o);
+  }
+  consumer_sync();
+}
+
+template <int EB, bool ATT>
 __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvPairParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[GP_WARPS][GP_MAX_STAGES];
@@ -155,8 +295,34 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
     for (int i = 0; i < min(S, n_all); ++i) issue(i);
   griddep_wait();
 
-  // ---- phase A: residual GEMV (x_a produced by the previous kernel) ----
-  load_x<__nv_bfloat16, NORM_NONE, false>(pa.x, nullptr, nullptr, 0.0f, pa.k, xs, red);
+  // grid-wide barrier number `nb` (co-resident grid, see the header comment)
+  auto grid_barrier = [&](int nb) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(P.bar, 1);
+      const unsigned long long t0 = gp_timer();
+      int seen;
+      do {
+        asm volatile("ld.acquire.gpu.b32 %0, [%1];" : "=r"(seen) : "l"(P.bar) : "memory");
+        if (gp_timer() - t0 > GP_WATCHDOG_NS) {
+          if (P.err) atomicOr(P.err, DEVERR_TIMEOUT);
+          break;
+        }
+      } while (seen < nb * static_cast<int>(gridDim.x));
+    }
+    __syncthreads();
+  };
+
+  // ---- phase 0 (optional): attention partials, then merged into phase A's row ----
+  if constexpr (ATT) {
+    if (static_cast<int>(blockIdx.x) < P.att.n_heads * P.att.ns) pair_attn_partial(P.att, xs, P.err);
+    grid_barrier(1);
+    pair_attn_merge(P.att, pa.k, xs, part);
+  } else {
+    // ---- phase A: residual GEMV (x_a produced by the previous kernel) ----
+    load_x<__nv_bfloat16, NORM_NONE, false>(pa.x, nullptr, nullptr, 0.0f, pa.k, xs, red);
+  }
   run_phase(ga, 0, na);
   {
     const EpiArgs ea = epi_args(pa);
@@ -172,21 +338,7 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
   }
 
   // ---- grid barrier: phase B reads the residual rows every CTA just wrote ----
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(P.bar, 1);
-    const unsigned long long t0 = gp_timer();
-    int seen;
-    do {
-      asm volatile("ld.acquire.gpu.b32 %0, [%1];" : "=r"(seen) : "l"(P.bar) : "memory");
-      if (gp_timer() - t0 > GP_WATCHDOG_NS) {
-        if (P.err) atomicOr(P.err, DEVERR_TIMEOUT);
-        break;
-      }
-    } while (seen < static_cast<int>(gridDim.x));
-  }
-  __syncthreads();
+  grid_barrier(ATT ? 2 : 1);
   griddep_launch_dependents();  // only now: every CTA of this grid is resident
 
   // ---- phase B: normed GEMV on the fresh residual (L2, bypass L1) ----
@@ -258,9 +410,10 @@ static void pair_chunking(int k, int chmax, int* ch, int* nch, int* rowb) {
 }
 
 cudaError_t gemv_pair_prepare() {
-  for (const void* f : {reinterpret_cast<const void*>(gemv_pair_kernel<EPI_SWIGLU>),
-                        reinterpret_cast<const void*>(gemv_pair_kernel<EPI_QKV_ROPE>),
-                        reinterpret_cast<const void*>(gemv_pair_kernel<EPI_STORE>)}) {
+  for (const void* f : {reinterpret_cast<const void*>(gemv_pair_kernel<EPI_SWIGLU, false>),
+                        reinterpret_cast<const void*>(gemv_pair_kernel<EPI_SWIGLU, true>),
+                        reinterpret_cast<const void*>(gemv_pair_kernel<EPI_QKV_ROPE, false>),
+                        reinterpret_cast<const void*>(gemv_pair_kernel<EPI_STORE, false>)}) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaFuncAttributes fa;
@@ -283,7 +436,15 @@ cudaError_t launch_gemv_pair(int epi_b, GemvPairParams P, cudaStream_t s, bool p
   P.rowb = std::max(P.a.rowb, P.b.rowb);
   P.xs_floats = std::max(P.a.k, P.b.k);
   auto part_floats = [&](const GemvParams& p) { return ((p.n_rows + 1) / 2 + G - 1) / G * p.nch * 2; };
-  const int part = std::max(part_floats(P.a), part_floats(P.b));
+  int part = std::max(part_floats(P.a), part_floats(P.b));
+  if (P.att.enabled) {
+    const PairAttn& A = P.att;
+    if (epi_b != EPI_SWIGLU || A.head_dim % 4 || A.head_dim > 128 || (32 % (A.head_dim / 4)) ||
+        A.n_heads * A.ns > G || A.n_heads * A.head_dim != P.a.k || !A.part || !A.seq_len)
+      return cudaErrorInvalidValue;
+    part = std::max(part, A.n_heads * A.ns);                           // merge weights table
+    P.xs_floats = std::max(P.xs_floats, GP_WARPS * (A.head_dim + 4));  // per-warp partials
+  }
   const int budget = optin_smem(dev) - 1024 - (P.xs_floats + part) * 4;
   P.stages = std::max(1, std::min(GP_MAX_STAGES, budget / (GP_WARPS * 2 * P.rowb)));
   if (P.stages < 2) return cudaErrorInvalidValue;
@@ -298,11 +459,19 @@ cudaError_t launch_gemv_pair(int epi_b, GemvPairParams P, cudaStream_t s, bool p
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   switch (epi_b) {
-    case EPI_SWIGLU: return cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_SWIGLU>, P);
-    case EPI_QKV_ROPE: return cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_QKV_ROPE>, P);
-    case EPI_STORE: return cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_STORE>, P);
+    case EPI_SWIGLU:
+      return P.att.enabled ? cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_SWIGLU, true>, P)
+                           : cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_SWIGLU, false>, P);
+    case EPI_QKV_ROPE: return cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_QKV_ROPE, false>, P);
+    case EPI_STORE: return cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_STORE, false>, P);
     default: return cudaErrorInvalidValue;
   }
+}
+
+void pair_attn_shape(int max_len, int n_heads, int head_dim, int sms, int* ns, int* span) {
+  int n = std::max(1, std::min({4, sms / std::max(1, n_heads), (max_len + 31) / 32}));
+  *ns = n;
+  *span = (max_len + n - 1) / n;
 }
 
 }  // namespace grt

@@ -145,13 +145,31 @@ cudaError_t gemv_prepare(int device);  // raises the dynamic smem limit once per
 // Two consecutive decode GEMVs in one launch (gemv_pair.cu): a = residual GEMV
 // (NORM_NONE, EPI_RESID), b = RMS-normed GEMV on its output (EPI_SWIGLU,
 // EPI_QKV_ROPE or EPI_STORE), grid-wide barrier in between; bf16 weights.
+// Optional phase 0 of a pair launch: decode attention (bf16 KV) for the Wo
+// GEMV's input.  CTA b < n_heads*ns computes the softmax partial (o, m, l) of
+// head b/ns over positions [s*span, (s+1)*span) (s = b%ns) into part; after a
+// grid barrier every CTA merges the partials of all heads into its activation
+// row (replaces the separate attention launch and its kernel boundary).
+struct PairAttn {
+  int enabled = 0;
+  const float* q = nullptr;          // [h*dh] post-RoPE
+  const void* k_cache = nullptr;     // bf16 [h][max_seq][dh]
+  const void* v_cache = nullptr;
+  const int* seq_len = nullptr;
+  float* part = nullptr;             // [h][ns][dh+2]
+  int n_heads = 0, head_dim = 0, max_seq = 0, ns = 1, span = 0;
+  float scale = 1.0f;
+};
 struct GemvPairParams {
   GemvParams a, b;
+  PairAttn att;
   int* bar = nullptr;  // [2] arrive/depart counters, zero-initialised, self-resetting
   int* err = nullptr;
   int stages = 0, rowb = 0, xs_floats = 0;  // set by the launcher
 };
 cudaError_t launch_gemv_pair(int epi_b, GemvPairParams p, cudaStream_t s, bool pdl);
+// split count / span of the fused attention phase for a bucket of max_len positions
+void pair_attn_shape(int max_len, int n_heads, int head_dim, int sms, int* ns, int* span);
 cudaError_t gemv_pair_prepare();
 
 // Split-K flash-decode over the KV cache for live lengths up to max_len (the

@@ -309,6 +309,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   acc(h * max_nsplit_ * (dh + 2) * 4);
   acc(h * 4);
   acc(cfg_.n_layers * 4 * 4);  // fused-pair barrier counters
+  acc(static_cast<size_t>(h) * 4 * (dh + 4) * 4);  // fused attention partials
   acc(S * (dh / 2) * 4 * 2);
   acc(sizeof(GrtCtrl));
   acc(sizeof(LoopCtl));
@@ -365,6 +366,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   attn_part_ = static_cast<float*>(arena_buf(h * max_nsplit_ * (dh + 2) * 4, "attn_part"));
   attn_counters_ = static_cast<int*>(arena_buf(h * 4, "attn_counters"));
   pair_bar_ = static_cast<int*>(arena_buf(cfg_.n_layers * 4 * 4, "pair_barriers"));
+  pair_attn_part_ = static_cast<float*>(arena_buf(static_cast<size_t>(h) * 4 * (dh + 4) * 4, "pair_attn_part"));
   if (pf) {
     const int64_t C = PREFILL_CHUNK;
     pf_X_ = static_cast<float*>(arena_buf(C * d * 4, "prefill_x"));
@@ -732,6 +734,14 @@ static int gemv_pair_mode() {
   return v;
 }
 static bool gemv_pair_enabled() { return gemv_pair_mode() != 0; }
+// 1 (default): decode attention runs as phase 0 of the Wo + gate/up pair launch
+static bool pair_attn_enabled() {
+  static const int v = [] {
+    const char* e = getenv("GRT_PAIR_ATTN");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
 static int pair_chmax(const char* var, int dflt) {
   const char* e = getenv(var);
   return e ? atoi(e) : dflt;
@@ -804,6 +814,11 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   } pending;
   const bool fuse = cfg_.tp_size == 1 && llama && wdt == Dt::BF16 && !op_trace_ && gemv_pair_enabled();
   int n_pairs_emitted = 0;
+  PairAttn pending_att;  // attention folded into the next Wo + gate/up launch
+  int att_ns = 1, att_span = 0;
+  pair_attn_shape(max_len, h, dh, num_sms(cfg_.device), &att_ns, &att_span);
+  const bool fuse_attn = fuse && pair_attn_enabled() && kvdt == Dt::BF16 && dh % 4 == 0 && dh <= 128 &&
+                         32 % (dh / 4) == 0 && gemv_pair_mode() == 2 && h * att_ns <= num_sms(cfg_.device);
   auto flush = [&]() {
     if (pending.set) emit_gemv(pending.name, EPI_RESID, NORM_NONE, pending.p, pending.bytes);
     pending.set = false;
@@ -825,6 +840,10 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       }
       pp.bar = pair_bar_ + 2 * n_pairs_emitted++;
       pp.err = err;
+      if (epi == EPI_SWIGLU && pending_att.enabled) {
+        pp.att = pending_att;
+        pending_att.enabled = 0;
+      }
       KernelInvocation inv;
       inv.spec.name = pending.name + "+" + name;
       inv.spec.op_class = OpClass::Static;
@@ -832,6 +851,17 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       inv.spec.bytes = static_cast<int64_t>(pending.bytes + w_bytes);
       inv.bindings = {{pending.p.w, pending.bytes}, {p.w, w_bytes}, {pp.bar, 8},
                       {pending.p.x, static_cast<size_t>(pending.p.k) * 4}, {p.x, static_cast<size_t>(p.k) * 4}};
+      if (pp.att.enabled) {
+        const PairAttn& A = pp.att;
+        const size_t cache = static_cast<size_t>(A.n_heads) * A.max_seq * A.head_dim * 2;
+        inv.spec.name = "attention+" + inv.spec.name;
+        inv.spec.flops += static_cast<int64_t>(A.n_heads) * max_len * (4 * A.head_dim + 5);  // kernels.hpp:51
+        inv.spec.bytes += 2LL * max_len * A.n_heads * A.head_dim * 2;
+        inv.bindings.push_back({A.k_cache, cache});
+        inv.bindings.push_back({A.v_cache, cache});
+        inv.bindings.push_back({A.q, static_cast<size_t>(A.n_heads) * A.head_dim * 4});
+        inv.bindings.push_back({A.part, static_cast<size_t>(A.n_heads) * A.ns * (A.head_dim + 4) * 4});
+      }
       inv.launch = [epi, pp](cudaStream_t s) { return launch_gemv_pair(epi, pp, s, true); };
       plan.push_back(std::move(inv));
       pending.set = false;
@@ -893,7 +923,20 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       gemv("qkv", llama ? EPI_QKV_ROPE : EPI_QKV, norm, p, 3ull * dq * d * wb);
     }
     flush();
-    {  // attention over [0, seq_len) for this rank's heads
+    if (fuse_attn) {  // attention = phase 0 of the Wo + gate/up launch (gemv_pair.cu)
+      pending_att.enabled = 1;
+      pending_att.q = q_;
+      pending_att.k_cache = L.k;
+      pending_att.v_cache = L.v;
+      pending_att.seq_len = seq_len;
+      pending_att.part = pair_attn_part_;
+      pending_att.n_heads = hl;
+      pending_att.head_dim = dh;
+      pending_att.max_seq = S;
+      pending_att.ns = att_ns;
+      pending_att.span = att_span;
+      pending_att.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
+    } else {  // attention over [0, seq_len) for this rank's heads
       AttnParams a;
       a.q = q_;
       a.k_cache = L.k;

@@ -290,7 +290,8 @@ class Model {
   float *pf_X_ = nullptr, *pf_Q_ = nullptr, *pf_part_ = nullptr;
   void *pf_Xn_ = nullptr, *pf_A_ = nullptr, *pf_act_ = nullptr;
   int* pf_cnt_ = nullptr;
-  int* pair_bar_ = nullptr;  // [2 * n_layers][2] barrier counters of the fused GEMV pairs
+  int* pair_bar_ = nullptr;
+  float* pair_attn_part_ = nullptr;  // [h][<=4][dh+4] partials of the fused attention phase  // [2 * n_layers][2] barrier counters of the fused GEMV pairs
   // tensor-parallel shard dims: heads, attention width, d_ff, vocab per rank
   int hl_ = 0, dq_ = 0, ffl_ = 0, vl_ = 0;
   float* logits_local_ = nullptr;  // [vl_] before the allgather (== logits_ when tp_size == 1)
