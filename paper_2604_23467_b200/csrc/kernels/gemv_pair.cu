@@ -21,6 +21,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemv_core.cuh"
@@ -163,35 +164,61 @@ __device__ __forceinline__ void pair_attn_partial(const PairAttn& A, float* scra
 }
 
 // Merge of every head's split partials into the Wo activation row (k = h*dh),
-// in the xs layout; split order is fixed, so the result is deterministic.
+// in the xs layout; split order is fixed, so the result is deterministic.  All
+// partial loads of a thread are issued before any is used (one L2 round trip).
+constexpr int GP_ATT_MAX_NS = 4;
+constexpr int GP_MERGE_V = 4;  // float4 outputs per thread: k <= 4096
+
 __device__ __forceinline__ void pair_attn_merge(const PairAttn& A, int k, float* xs, float* tbl) {
   const int dh = A.head_dim, ns = A.ns, ld = dh + 4;
   for (int hh = threadIdx.x; hh < A.n_heads; hh += CONSUMER_THREADS) {
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < ns; ++s2) M = fmaxf(M, __ldcg(A.part + static_cast<int64_t>(hh * ns + s2) * ld + dh));
-    float L = 0.0f;
-    for (int s2 = 0; s2 < ns; ++s2) {
+    float ms[GP_ATT_MAX_NS], ls[GP_ATT_MAX_NS];
+#pragma unroll
+    for (int s2 = 0; s2 < GP_ATT_MAX_NS; ++s2) {
       const float* pp = A.part + static_cast<int64_t>(hh * ns + s2) * ld;
-      const float ms = __ldcg(pp + dh);
-      const float f = ms == -INFINITY ? 0.0f : __expf(ms - M);
-      tbl[hh * ns + s2] = f;
-      L += __ldcg(pp + dh + 1) * f;
+      ms[s2] = s2 < ns ? __ldcg(pp + dh) : -INFINITY;
+      ls[s2] = s2 < ns ? __ldcg(pp + dh + 1) : 0.0f;
+    }
+    float M = -INFINITY;
+#pragma unroll
+    for (int s2 = 0; s2 < GP_ATT_MAX_NS; ++s2) M = fmaxf(M, ms[s2]);
+    float L = 0.0f, f[GP_ATT_MAX_NS];
+#pragma unroll
+    for (int s2 = 0; s2 < GP_ATT_MAX_NS; ++s2) {
+      f[s2] = ms[s2] == -INFINITY ? 0.0f : __expf(ms[s2] - M);
+      L += ls[s2] * f[s2];
     }
     const float inv = 1.0f / L;
-    for (int s2 = 0; s2 < ns; ++s2) tbl[hh * ns + s2] *= inv;
+#pragma unroll
+    for (int s2 = 0; s2 < GP_ATT_MAX_NS; ++s2)
+      if (s2 < ns) tbl[hh * ns + s2] = f[s2] * inv;
   }
-  consumer_sync();
-  for (int j4 = threadIdx.x; j4 < (k >> 2); j4 += CONSUMER_THREADS) {
+  float4 v[GP_MERGE_V][GP_ATT_MAX_NS];
+#pragma unroll
+  for (int i = 0; i < GP_MERGE_V; ++i) {
+    const int j4 = threadIdx.x + i * CONSUMER_THREADS;
     const int idx = 4 * j4, hh = idx / dh, d = idx - hh * dh;
+#pragma unroll
+    for (int s2 = 0; s2 < GP_ATT_MAX_NS; ++s2)
+      v[i][s2] = (j4 < (k >> 2) && s2 < ns)
+                     ? __ldcg(reinterpret_cast<const float4*>(A.part + static_cast<int64_t>(hh * ns + s2) * ld + d))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  consumer_sync();  // tbl complete
+#pragma unroll
+  for (int i = 0; i < GP_MERGE_V; ++i) {
+    const int j4 = threadIdx.x + i * CONSUMER_THREADS;
+    if (j4 >= (k >> 2)) continue;
+    const int hh = (4 * j4) / dh;
     float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s2 = 0; s2 < ns; ++s2) {
+#pragma unroll
+    for (int s2 = 0; s2 < GP_ATT_MAX_NS; ++s2) {
+      if (s2 >= ns) break;
       const float w = tbl[hh * ns + s2];
-      if (w == 0.0f) continue;
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(A.part + static_cast<int64_t>(hh * ns + s2) * ld + d));
-      o.x = fmaf(w, v.x, o.x);
-      o.y = fmaf(w, v.y, o.y);
-      o.z = fmaf(w, v.z, o.z);
-      o.w = fmaf(w, v.w, o.w);
+      o.x = fmaf(w, v[i][s2].x, o.x);
+      o.y = fmaf(w, v[i][s2].y, o.y);
+      o.z = fmaf(w, v[i][s2].z, o.z);
+      o.w = fmaf(w, v[i][s2].w, o.w);
     }
     xs_store4<__nv_bfloat16>(xs, j4, k, o);
   }
@@ -440,7 +467,8 @@ cudaError_t launch_gemv_pair(int epi_b, GemvPairParams P, cudaStream_t s, bool p
   if (P.att.enabled) {
     const PairAttn& A = P.att;
     if (epi_b != EPI_SWIGLU || A.head_dim % 4 || A.head_dim > 128 || (32 % (A.head_dim / 4)) ||
-        A.n_heads * A.ns > G || A.n_heads * A.head_dim != P.a.k || !A.part || !A.seq_len)
+        A.n_heads * A.ns > G || A.n_heads * A.head_dim != P.a.k || !A.part || !A.seq_len || A.ns > GP_ATT_MAX_NS ||
+        P.a.k > GP_MERGE_V * 4 * CONSUMER_THREADS)
       return cudaErrorInvalidValue;
     part = std::max(part, A.n_heads * A.ns);                           // merge weights table
     P.xs_floats = std::max(P.xs_floats, GP_WARPS * (A.head_dim + 4));  // per-warp partials
@@ -469,7 +497,11 @@ cudaError_t launch_gemv_pair(int epi_b, GemvPairParams P, cudaStream_t s, bool p
 }
 
 void pair_attn_shape(int max_len, int n_heads, int head_dim, int sms, int* ns, int* span) {
-  int n = std::max(1, std::min({4, sms / std::max(1, n_heads), (max_len + 31) / 32}));
+  static const int cap = [] {
+    const char* e = getenv("GRT_PAIR_ATTN_NS");
+    return e ? std::max(1, std::min(GP_ATT_MAX_NS, atoi(e))) : GP_ATT_MAX_NS;
+  }();
+  int n = std::max(1, std::min({cap, sms / std::max(1, n_heads), (max_len + 31) / 32}));
   *ns = n;
   *span = (max_len + n - 1) / n;
 }
