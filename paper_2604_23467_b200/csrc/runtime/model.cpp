@@ -734,11 +734,15 @@ static int gemv_pair_mode() {
   return v;
 }
 static bool gemv_pair_enabled() { return gemv_pair_mode() != 0; }
-// 1 (default): decode attention runs as phase 0 of the Wo + gate/up pair launch
+// 1: decode attention runs as phase 0 of the Wo + gate/up pair launch.  Off by
+// default: measured 2.54-2.56 ms/token vs 2.48 with the separate attention
+// kernel (7B, P=10; the extra grid barrier and the partial merge cost more than
+// the kernel boundary they remove -- the separate kernel's latency is already
+// covered by the pair kernel's ring fill, which starts at attention's launch).
 static bool pair_attn_enabled() {
   static const int v = [] {
     const char* e = getenv("GRT_PAIR_ATTN");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
   return v != 0;
 }
