@@ -109,6 +109,8 @@ typedef struct grt_model_config {
   int32_t device;      /* CUDA ordinal */
   int32_t tp_size;     /* 1 = single GPU */
   int32_t tp_rank;
+  int32_t kv_page_size; /* 0 = contiguous KV [h][max_seq][dh] per layer (kv_cache.hpp:15-43);
+                           > 0 = paged pool [n_pages][h][page][dh] addressed through a block table */
 } grt_model_config;
 
 /* Replaces graphrt::CacheConfig (pipeline.hpp:122-128), plus the bucket width. */
@@ -214,6 +216,13 @@ grt_status grt_safetensors_list(const char* path, char* names, int32_t names_len
 /* HuggingFace LLaMA tensor name -> graphrt name ("" if not a model weight);
  * *out_in = 1 when the checkpoint stores it [out,in]. */
 grt_status grt_hf_tensor_name(const char* hf_name, char* out, int32_t out_len, int32_t* out_in);
+/* Paged KV cache (kv_page_size > 0): the block table maps
+ * logical page i (positions [i*page, (i+1)*page)) to a physical page of every
+ * layer's pool.  `table` must hold n_pages distinct ids in [0, n_pages); the
+ * default is the identity.  Takes effect for the next pass (the table lives in
+ * device memory and every KV read/write goes through it). */
+grt_status grt_model_kv_pages(grt_model* m, int32_t* page_size, int32_t* n_pages);
+grt_status grt_model_set_kv_block_table(grt_model* m, const int32_t* table, int32_t n);
 grt_status grt_model_weight_bytes(grt_model* m, uint64_t* bytes);            /* HBM bytes of weights */
 grt_status grt_model_decode_bytes(grt_model* m, int32_t length, uint64_t* bytes); /* algorithmic bytes/pass */
 

@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
   const int span = pass * rounds;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane / G, c = lane - g * G;
-  const KT* K = reinterpret_cast<const KT*>(p.k_cache) + static_cast<int64_t>(head) * p.max_seq * dh + 4 * c;
-  const KT* V = reinterpret_cast<const KT*>(p.v_cache) + static_cast<int64_t>(head) * p.max_seq * dh + 4 * c;
+  const KT* K = reinterpret_cast<const KT*>(p.k_cache) + 4 * c;
+  const KT* V = reinterpret_cast<const KT*>(p.v_cache) + 4 * c;
   griddep_wait();
   op_stamp(p.trace, 1);
   if (p.trigger == 0) griddep_launch_dependents();
@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
 #pragma unroll
     for (int u = 0; u < ATTN_UNROLL; ++u) {
       const int j = min(jw + u * RPW + g, p.max_seq - 1);  // bucket position (masked below)
-      kv[u] = load4<KT>(K + static_cast<int64_t>(j) * dh);
-      vv[u] = load4<KT>(V + static_cast<int64_t>(j) * dh);
+      const int64_t row = kv_row(p.kvp, head, p.max_seq, j) * dh;
+      kv[u] = load4<KT>(K + row);
+      vv[u] = load4<KT>(V + row);
     }
     float sc[ATTN_UNROLL];
     float mr = -INFINITY;

@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#include "kernels.h"
+
 namespace grt {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -95,6 +97,27 @@ __device__ __forceinline__ void op_stamp(unsigned long long* tr, int i) {
 }
 
 // ---- numerics -----------------------------------------------------------------
+// Row of position j of `head` in a layer's K or V cache (KvPaging, kernels.h).
+__device__ __forceinline__ int64_t kv_row(const KvPaging& g, int head, int max_seq, int j) {
+  if (g.page == 0) return static_cast<int64_t>(head) * max_seq + j;
+  const int pi = j / g.page;
+  return (static_cast<int64_t>(__ldg(g.table + pi)) * g.n_heads + head) * g.page + (j - pi * g.page);
+}
+
+// L2 prefetch of rows [0, n) of one head's K or V cache: one bulk request per
+// contiguous run of <= 64 KB (a page, or the whole head when contiguous).
+__device__ __forceinline__ void kv_prefetch_l2(const void* cache, const KvPaging& g, int head, int max_seq, int dh,
+                                               int eb, int n) {
+  const uint8_t* b = static_cast<const uint8_t*>(cache);
+  const int run = g.page == 0 ? n : g.page;
+  for (int j = 0; j < n; j += run) {
+    const uint8_t* base = b + kv_row(g, head, max_seq, j) * dh * eb;
+    const uint64_t bytes = static_cast<uint64_t>(min(run, n - j)) * dh * eb;
+    for (uint64_t o = 0; o < bytes; o += 65536)
+      prefetch_l2_bulk(base + o, static_cast<uint32_t>(bytes - o < 65536 ? bytes - o : 65536));
+  }
+}
+
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 

@@ -209,13 +209,8 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
     // (after the activation load, off its critical path) L2 prefetch (and TLB warm-up) of this layer's K/V rows [0, seq_len-1) for
     // the attention kernel: one contiguous [len, dh] run per (head, K|V).
     if (threadIdx.x == 0 && p.seq_len && static_cast<int>(blockIdx.x) < 2 * p.n_heads) {
-      const int hh = blockIdx.x >> 1;
-      const size_t eb = p.kv_bf16 ? 2 : 4;
-      const uint8_t* base = static_cast<const uint8_t*>((blockIdx.x & 1) ? p.v_cache : p.k_cache) +
-                            static_cast<size_t>(hh) * p.max_seq * p.head_dim * eb;
-      const uint64_t bytes = static_cast<uint64_t>(max(0, *p.seq_len - 1)) * p.head_dim * eb;
-      for (uint64_t o = 0; o < bytes; o += 65536)
-        prefetch_l2_bulk(base + o, static_cast<uint32_t>(bytes - o < 65536 ? bytes - o : 65536));
+      kv_prefetch_l2((blockIdx.x & 1) ? p.v_cache : p.k_cache, p.kvp, blockIdx.x >> 1, p.max_seq, p.head_dim,
+                     p.kv_bf16 ? 2 : 4, max(0, *p.seq_len - 1));
     }
   }
 
@@ -231,6 +226,7 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
   ea.max_seq = p.max_seq;
   ea.d_model = p.d_model;
   ea.kv_bf16 = p.kv_bf16;
+  ea.kvp = p.kvp;
 
   for (int i = 0; i < n_tasks; ++i) {
     const int slot = i % S;

@@ -276,6 +276,7 @@ struct EpiArgs {
   const float* rope_sin = nullptr;
   int head_dim = 0, max_seq = 0, d_model = 0;
   int kv_bf16 = 0;
+  KvPaging kvp;
 };
 
 template <int EPI>
@@ -322,7 +323,7 @@ __device__ __forceinline__ void epilogue(const EpiArgs& p, int pair, float va, f
       p.q_out[head * dh + e1] = rb;
     } else {
       void* cache = sec == 1 ? p.k_cache : p.v_cache;
-      const int64_t base = (static_cast<int64_t>(head) * p.max_seq + pos) * dh;
+      const int64_t base = kv_row(p.kvp, head, p.max_seq, pos) * dh;
       if (p.kv_bf16) {
         store_cast(reinterpret_cast<__nv_bfloat16*>(cache) + base + e0, ra);
         store_cast(reinterpret_cast<__nv_bfloat16*>(cache) + base + e1, rb);

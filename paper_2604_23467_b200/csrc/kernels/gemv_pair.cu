@@ -81,8 +81,8 @@ __device__ __forceinline__ void pair_attn_partial(const PairAttn& A, float* scra
   if ((len < 1 || len > A.ns * A.span) && blockIdx.x == 0 && threadIdx.x == 0 && err)
     atomicOr(err, DEVERR_WRONG_LENGTH);  // live length outside the bucket this graph was built for
   const int j0 = split * A.span, j1 = min(len, j0 + A.span);
-  const __nv_bfloat16* K = static_cast<const __nv_bfloat16*>(A.k_cache) + static_cast<int64_t>(head) * A.max_seq * dh + 4 * c;
-  const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(A.v_cache) + static_cast<int64_t>(head) * A.max_seq * dh + 4 * c;
+  const __nv_bfloat16* K = static_cast<const __nv_bfloat16*>(A.k_cache) + 4 * c;
+  const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(A.v_cache) + 4 * c;
   const float4 q4 = __ldcg(reinterpret_cast<const float4*>(A.q + head * dh) + c);
   float m = -INFINITY, l = 0.0f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -93,8 +93,9 @@ __device__ __forceinline__ void pair_attn_partial(const PairAttn& A, float* scra
 #pragma unroll
     for (int u = 0; u < GP_ATT_UNROLL; ++u) {
       const int j = min(jw + u * RPW + g, A.max_seq - 1);  // masked below
-      kv[u] = ld_bf16x4(K + static_cast<int64_t>(j) * dh);
-      vv[u] = ld_bf16x4(V + static_cast<int64_t>(j) * dh);
+      const int64_t r = kv_row(A.kvp, head, A.max_seq, j) * dh;
+      kv[u] = ld_bf16x4(K + r);
+      vv[u] = ld_bf16x4(V + r);
     }
     float sc[GP_ATT_UNROLL];
     float mr = -INFINITY;
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
     ea.max_seq = p.max_seq;
     ea.d_model = p.d_model;
     ea.kv_bf16 = p.kv_bf16;
+    ea.kvp = p.kvp;
     return ea;
   };
 
@@ -391,12 +393,8 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
   }
   if constexpr (EB == EPI_QKV_ROPE) {  // K/V rows of this layer into L2 for the attention kernel
     if (threadIdx.x == 0 && pb.seq_len && static_cast<int>(blockIdx.x) < 2 * pb.n_heads) {
-      const int hh = blockIdx.x >> 1;
-      const uint8_t* base = static_cast<const uint8_t*>((blockIdx.x & 1) ? pb.v_cache : pb.k_cache) +
-                            static_cast<size_t>(hh) * pb.max_seq * pb.head_dim * 2;
-      const uint64_t bytes = static_cast<uint64_t>(max(0, *pb.seq_len - 1)) * pb.head_dim * 2;
-      for (uint64_t o = 0; o < bytes; o += 65536)
-        prefetch_l2_bulk(base + o, static_cast<uint32_t>(bytes - o < 65536 ? bytes - o : 65536));
+      kv_prefetch_l2((blockIdx.x & 1) ? pb.v_cache : pb.k_cache, pb.kvp, blockIdx.x >> 1, pb.max_seq, pb.head_dim,
+                     pb.kv_bf16 ? 2 : 4, max(0, *pb.seq_len - 1));
     }
   }
   run_phase(gb, na, n_all);

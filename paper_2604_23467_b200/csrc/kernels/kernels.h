@@ -14,6 +14,16 @@ namespace grt {
 
 enum class Dt : int { F32 = 0, BF16 = 1 };
 
+// KV cache addressing.  page == 0: contiguous rows per head, row(head, j) =
+// head*max_seq + j (the reference KvCache layout, kv_cache.hpp:15-43).
+// page > 0: paged pool [n_pages][n_heads][page][dh] (vLLM-style); position j
+// lives in page table[j / page] at offset j % page.  Row r starts at r*dh.
+struct KvPaging {
+  int page = 0;
+  int n_heads = 0;
+  const int* table = nullptr;
+};
+
 enum NormKind : int { NORM_NONE = 0, NORM_LN = 1, NORM_RMS = 2 };
 
 // Epilogues of the fused GEMV.  Rows are processed in adjacent PAIRS (2p, 2p+1)
@@ -52,6 +62,7 @@ struct GemvParams {
   const float* rope_sin = nullptr;
   int n_heads = 0, head_dim = 0, max_seq = 0, d_model = 0;
   int kv_bf16 = 0;
+  KvPaging kvp;
   int* err = nullptr;       // device error word (WrongLength / CacheFull flags)
   unsigned long long* trace = nullptr;  // optional [cta][4] %globaltimer stamps (profiling)
 };
@@ -71,6 +82,7 @@ struct AttnParams {
   int* err = nullptr;
   unsigned long long* trace = nullptr;  // optional [cta][4] %globaltimer stamps (profiling)
   int rounds = 1;                // passes per CTA (set by the launcher)
+  KvPaging kvp;
   int trigger = 0;               // when the successor may launch: 0 start, 1 after KV loads, 2 at exit
 };
 // Per-op trace stamps (8 slots per CTA): 0 CTA start, 1 dependency released
@@ -159,6 +171,7 @@ struct PairAttn {
   float* part = nullptr;             // [h][ns][dh+2]
   int n_heads = 0, head_dim = 0, max_seq = 0, ns = 1, span = 0;
   float scale = 1.0f;
+  KvPaging kvp;
 };
 struct GemvPairParams {
   GemvParams a, b;
@@ -200,6 +213,7 @@ struct PrefillGemmParams {
   const float* rope_cos = nullptr;
   const float* rope_sin = nullptr;
   int head_dim = 0, max_seq = 0, d_model = 0, start_pos = 0, kv_bf16 = 0;
+  KvPaging kvp;
   float* part = nullptr;   // split-K scratch, prefill_gemm_part_floats()
   int* counters = nullptr; // [m_tiles], zero-initialised, self-resetting
 };
@@ -215,7 +229,8 @@ cudaError_t launch_prefill_embed(Dt wdt, const int* tokens, int start, int P, co
 cudaError_t launch_prefill_rmsnorm(const float* X, int P, const float* gamma, float eps, int d, void* Xn,
                                    cudaStream_t s);
 cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, const void* v, int start, int P, int d,
-                                     int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s);
+                                     int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s,
+                                     KvPaging kvp = KvPaging{});
 cudaError_t launch_prefill_handoff(const float* X_last, int d, float* x, int* seq_len, int len, cudaStream_t s);
 
 // ---- tensor-parallel exchange, in-process emulation (tp_emu.cu) ----------------

@@ -95,7 +95,7 @@ constexpr int PA_QB = 64, PA_KB = 64, PA_THREADS = 256;
 template <typename KT, int DH>
 __global__ void __launch_bounds__(PA_THREADS)
     prefill_attn_kernel(const float* Q, const void* k_cache, const void* v_cache, int start, int P, int d,
-                        int max_seq, float scale, __nv_bfloat16* out) {
+                        int max_seq, float scale, __nv_bfloat16* out, KvPaging kvp) {
   extern __shared__ __align__(16) float sm[];
   constexpr int KS = DH + 1;   // odd row stride: conflict-free column reads of K
   constexpr int DPT = DH / 16; // output dims per thread
@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(PA_THREADS)
   const int head = blockIdx.y, q0 = blockIdx.x * PA_QB;
   const int t = threadIdx.x, tq = t >> 4, tk = t & 15;
   const int nq = min(PA_QB, P - q0);
-  const KT* Kh = reinterpret_cast<const KT*>(k_cache) + static_cast<int64_t>(head) * max_seq * DH;
-  const KT* Vh = reinterpret_cast<const KT*>(v_cache) + static_cast<int64_t>(head) * max_seq * DH;
+  const KT* Kb = reinterpret_cast<const KT*>(k_cache);
+  const KT* Vb = reinterpret_cast<const KT*>(v_cache);
 
   for (int e = t; e < PA_QB * DH; e += PA_THREADS) {
     const int qi = e / DH, dd = e - qi * DH;
@@ -127,8 +127,9 @@ __global__ void __launch_bounds__(PA_THREADS)
     for (int e = t; e < PA_KB * DH; e += PA_THREADS) {
       const int kk = e / DH, dd = e - kk * DH;
       const int pos = min(kb + kk, last_pos);
-      Ks[kk * KS + dd] = to_f32(Kh[static_cast<int64_t>(pos) * DH + dd]);
-      Vs[kk * DH + dd] = to_f32(Vh[static_cast<int64_t>(pos) * DH + dd]);
+      const int64_t row = kv_row(kvp, head, max_seq, pos) * DH;
+      Ks[kk * KS + dd] = to_f32(Kb[row + dd]);
+      Vs[kk * DH + dd] = to_f32(Vb[row + dd]);
     }
     __syncthreads();
     // scores S[4 queries][4 keys]
@@ -263,7 +264,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 template <int DH>
 __global__ void __launch_bounds__(FA_WARPS * 32)
     prefill_fa_kernel(const float* Q, const __nv_bfloat16* k_cache, const __nv_bfloat16* v_cache, int start, int P,
-                      int d, int max_seq, float scale, __nv_bfloat16* out) {
+                      int d, int max_seq, float scale, __nv_bfloat16* out, KvPaging kvp) {
   constexpr int LD = DH + 8;  // bf16 row stride: 16-byte aligned, conflict-free ldmatrix
   constexpr int KS = DH / 16, NB = DH / 8;
   extern __shared__ __align__(16) uint8_t fa_smem[];
@@ -274,8 +275,6 @@ __global__ void __launch_bounds__(FA_WARPS * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int nq = min(FA_QB, P - q0);
-  const __nv_bfloat16* Kh = k_cache + static_cast<int64_t>(head) * max_seq * DH;
-  const __nv_bfloat16* Vh = v_cache + static_cast<int64_t>(head) * max_seq * DH;
 
   for (int e = threadIdx.x; e < FA_QB * DH / 2; e += FA_WARPS * 32) {
     const int r = e / (DH / 2), c = 2 * (e - r * (DH / 2));
@@ -305,8 +304,9 @@ __global__ void __launch_bounds__(FA_WARPS * 32)
       const int r = e / (DH / 8), c = 8 * (e - r * (DH / 8));
       uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
       if (kb + r <= last_pos) {
-        kv = *reinterpret_cast<const uint4*>(Kh + static_cast<int64_t>(kb + r) * DH + c);
-        vv = *reinterpret_cast<const uint4*>(Vh + static_cast<int64_t>(kb + r) * DH + c);
+        const int64_t row = kv_row(kvp, head, max_seq, kb + r) * DH;
+        kv = *reinterpret_cast<const uint4*>(k_cache + row + c);
+        vv = *reinterpret_cast<const uint4*>(v_cache + row + c);
       }
       *reinterpret_cast<uint4*>(&Ks[r * LD + c]) = kv;
       *reinterpret_cast<uint4*>(&Vs[r * LD + c]) = vv;
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(FA_WARPS * 32)
 
 template <typename KT, int DH>
 static cudaError_t attn_launch(const float* Q, const void* k, const void* v, int start, int P, int d, int n_heads,
-                               int max_seq, float scale, void* out, cudaStream_t s) {
+                               int max_seq, float scale, void* out, cudaStream_t s, KvPaging kvp) {
   const size_t smem = (static_cast<size_t>(PA_QB) * DH + PA_KB * (DH + 1) + PA_KB * DH + PA_QB * (PA_KB + 1)) * 4;
   static bool attr_set = false;  // idempotent
   if (!attr_set) {
@@ -415,25 +415,25 @@ static cudaError_t attn_launch(const float* Q, const void* k, const void* v, int
   }
   dim3 grid((P + PA_QB - 1) / PA_QB, n_heads);
   prefill_attn_kernel<KT, DH><<<grid, PA_THREADS, smem, s>>>(Q, k, v, start, P, d, max_seq, scale,
-                                                               static_cast<__nv_bfloat16*>(out));
+                                                               static_cast<__nv_bfloat16*>(out), kvp);
   return cudaGetLastError();
 }
 
 template <typename KT>
 static cudaError_t attn_dispatch(int dh, const float* Q, const void* k, const void* v, int start, int P, int d,
-                                 int n_heads, int max_seq, float scale, void* out, cudaStream_t s) {
+                                 int n_heads, int max_seq, float scale, void* out, cudaStream_t s, KvPaging kvp) {
   switch (dh) {
-    case 16: return attn_launch<KT, 16>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
-    case 32: return attn_launch<KT, 32>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
-    case 64: return attn_launch<KT, 64>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
-    case 128: return attn_launch<KT, 128>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+    case 16: return attn_launch<KT, 16>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
+    case 32: return attn_launch<KT, 32>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
+    case 64: return attn_launch<KT, 64>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
+    case 128: return attn_launch<KT, 128>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int DH>
 static cudaError_t fa_launch(const float* Q, const void* k, const void* v, int start, int P, int d, int n_heads,
-                             int max_seq, float scale, void* out, cudaStream_t s) {
+                             int max_seq, float scale, void* out, cudaStream_t s, KvPaging kvp) {
   const size_t smem = static_cast<size_t>(FA_QB + 2 * FA_KB) * (DH + 8) * 2;
   static bool attr_set = false;
   if (!attr_set) {
@@ -445,7 +445,7 @@ static cudaError_t fa_launch(const float* Q, const void* k, const void* v, int s
   dim3 grid((P + FA_QB - 1) / FA_QB, n_heads);
   prefill_fa_kernel<DH><<<grid, FA_WARPS * 32, smem, s>>>(Q, static_cast<const __nv_bfloat16*>(k),
                                                         static_cast<const __nv_bfloat16*>(v), start, P, d, max_seq,
-                                                        scale, static_cast<__nv_bfloat16*>(out));
+                                                        scale, static_cast<__nv_bfloat16*>(out), kvp);
   return cudaGetLastError();
 }
 
@@ -458,13 +458,14 @@ static int fa_enabled() {
 }
 
 cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, const void* v, int start, int P, int d,
-                                     int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s) {
+                                     int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s,
+                                     KvPaging kvp) {
   if (kvdt == Dt::BF16 && fa_enabled()) {  // tensor cores (mma.sync) for bf16 KV
-    if (dh == 64) return fa_launch<64>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
-    if (dh == 128) return fa_launch<128>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+    if (dh == 64) return fa_launch<64>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
+    if (dh == 128) return fa_launch<128>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
   }
-  if (kvdt == Dt::BF16) return attn_dispatch<__nv_bfloat16>(dh, Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
-  return attn_dispatch<float>(dh, Q, k, v, start, P, d, n_heads, max_seq, scale, out, s);
+  if (kvdt == Dt::BF16) return attn_dispatch<__nv_bfloat16>(dh, Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
+  return attn_dispatch<float>(dh, Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
 }
 
 cudaError_t launch_prefill_handoff(const float* X_last, int d, float* x, int* seq_len, int len, cudaStream_t s) {

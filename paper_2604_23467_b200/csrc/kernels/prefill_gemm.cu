@@ -176,7 +176,7 @@ __device__ __forceinline__ void pg_epilogue16(const PrefillGemmParams& p, int m,
           q[e1] = rb;
         } else {
           void* cache = sec == 1 ? p.k_cache : p.v_cache;
-          const int64_t base = (static_cast<int64_t>(head) * p.max_seq + p.start_pos + n) * dh;
+          const int64_t base = kv_row(p.kvp, head, p.max_seq, p.start_pos + n) * dh;
           if (p.kv_bf16) {
             __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(cache) + base;
             c[e0] = __float2bfloat16_rn(ra);
@@ -241,7 +241,7 @@ __device__ __forceinline__ void pg_epilogue_pair(const PrefillGemmParams& p, int
         q[e1] = rb;
       } else {
         void* cache = sec == 1 ? p.k_cache : p.v_cache;
-        const int64_t base = (static_cast<int64_t>(head) * p.max_seq + pos) * dh;
+        const int64_t base = kv_row(p.kvp, head, p.max_seq, pos) * dh;
         if (p.kv_bf16) {
           __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(cache) + base;
           c[e0] = __float2bfloat16_rn(ra);

@@ -91,6 +91,7 @@ void grt_model_config_default(grt_model_config* c) {
   c->device = 0;
   c->tp_size = 1;
   c->tp_rank = 0;
+  c->kv_page_size = 0;
 }
 
 void grt_cache_config_default(grt_cache_config* c) {
@@ -242,6 +243,17 @@ grt_status grt_hf_tensor_name(const char* hf_name, char* out, int32_t out_len, i
     memcpy(out, s.c_str(), s.size() + 1);
     if (out_in) *out_in = oi ? 1 : 0;
   });
+}
+
+grt_status grt_model_kv_pages(grt_model* m, int32_t* page_size, int32_t* n_pages) {
+  return guard([&] {
+    if (page_size) *page_size = m->m->kv_paging().page;
+    if (n_pages) *n_pages = m->m->kv_pages();
+  });
+}
+
+grt_status grt_model_set_kv_block_table(grt_model* m, const int32_t* table, int32_t n) {
+  return guard([&] { m->m->set_kv_block_table(table, n); });
 }
 
 grt_status grt_model_weight_bytes(grt_model* m, uint64_t* bytes) {

@@ -94,6 +94,7 @@ void ModelConfig::validate() const {
   if (kv_dtype != GRT_F32 && kv_dtype != GRT_BF16) raise(GRT_InvalidConfig, "kv_dtype");
   if (init != GRT_INIT_MT19937 && init != GRT_INIT_PHILOX && init != GRT_INIT_NONE) raise(GRT_InvalidConfig, "init");
   if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size) raise(GRT_InvalidConfig, "tp_rank must be in [0, tp_size)");
+  if (kv_page_size < 0 || kv_page_size > max_seq_len) raise(GRT_InvalidConfig, "kv_page_size must be in [0, max_seq_len]");
   if (tp_size > 1) {
     if (arch != GRT_ARCH_LLAMA) raise(GRT_Unsupported, "tensor parallelism is implemented for the LLaMA arch");
     if (n_heads % tp_size != 0) raise(GRT_InvalidConfig, "n_heads must be divisible by tp_size");
@@ -122,6 +123,7 @@ ModelConfig ModelConfig::from_c(const grt_model_config& c) {
   m.device = c.device;
   m.tp_size = c.tp_size < 1 ? 1 : c.tp_size;
   m.tp_rank = c.tp_rank;
+  m.kv_page_size = c.kv_page_size;
   return m;
 }
 
@@ -281,6 +283,10 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   vl_ = static_cast<int>(V / T);
   const int64_t dq = dq_, ffl = ffl_, Vl = vl_, hl = hl_;
   const int64_t upl = cfg_.llama() ? 2 * ffl : ffl;
+  // KV cache per layer: contiguous [hl][S][dh], or a pool of ceil(S/page) pages [hl][page][dh]
+  const int PS = cfg_.kv_page_size;
+  kv_pages_ = PS > 0 ? (S + PS - 1) / PS : 0;
+  kv_layer_elems_ = PS > 0 ? static_cast<size_t>(kv_pages_) * hl * PS * dh : static_cast<size_t>(hl) * S * dh;
 
   // size the arena: weights, KV, workspace, control
   size_t need = 0;
@@ -293,9 +299,10 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
     acc(upl * d * wb);
     acc(d * ffl * wb);
     for (int i = 0; i < 4; ++i) acc(d * 4);
-    acc(hl * S * dh * kvb);
-    acc(hl * S * dh * kvb);
+    acc(kv_layer_elems_ * kvb);
+    acc(kv_layer_elems_ * kvb);
   }
+  acc(static_cast<size_t>(std::max(kv_pages_, 1)) * 4);  // KV block table
   acc(d * 4);
   acc(d * 4);
   acc(Vl * d * wb);
@@ -350,8 +357,8 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
     L.ln1_b = static_cast<float*>(arena_buf(d * 4, "ln1_b"));
     L.ln2_g = static_cast<float*>(arena_buf(d * 4, "ln2_g"));
     L.ln2_b = static_cast<float*>(arena_buf(d * 4, "ln2_b"));
-    L.k = arena_buf(hl * S * dh * kvb, "k");
-    L.v = arena_buf(hl * S * dh * kvb, "v");
+    L.k = arena_buf(kv_layer_elems_ * kvb, "k");
+    L.v = arena_buf(kv_layer_elems_ * kvb, "v");
   }
   lnf_g_ = static_cast<float*>(arena_buf(d * 4, "lnf_g"));
   lnf_b_ = static_cast<float*>(arena_buf(d * 4, "lnf_b"));
@@ -367,6 +374,14 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   attn_counters_ = static_cast<int*>(arena_buf(h * 4, "attn_counters"));
   pair_bar_ = static_cast<int*>(arena_buf(cfg_.n_layers * 4 * 4, "pair_barriers"));
   pair_attn_part_ = static_cast<float*>(arena_buf(static_cast<size_t>(h) * 4 * (dh + 4) * 4, "pair_attn_part"));
+  kv_table_ = static_cast<int*>(arena_buf(static_cast<size_t>(std::max(kv_pages_, 1)) * 4, "kv_block_table"));
+  kvp_.page = PS;
+  kvp_.n_heads = static_cast<int>(hl);
+  kvp_.table = kv_table_;
+  kv_table_host_.resize(std::max(kv_pages_, 1));
+  for (int i = 0; i < static_cast<int>(kv_table_host_.size()); ++i) kv_table_host_[i] = PS > 0 ? i : 0;
+  cuda_check(cudaMemcpy(kv_table_, kv_table_host_.data(), kv_table_host_.size() * 4, cudaMemcpyHostToDevice),
+             "kv block table");
   if (pf) {
     const int64_t C = PREFILL_CHUNK;
     pf_X_ = static_cast<float*>(arena_buf(C * d * 4, "prefill_x"));
@@ -483,6 +498,27 @@ const LogicalTensor& Model::tensor(const std::string& name) const {
   raise(GRT_ShapeMismatch, "unknown tensor '" + name + "'");
 }
 
+void Model::set_kv_block_table(const int* table, int n) {
+  if (kvp_.page == 0) raise(GRT_InvalidConfig, "set_kv_block_table: the KV cache is contiguous (kv_page_size 0)");
+  if (n != kv_pages_) raise(GRT_ShapeMismatch, "set_kv_block_table: expected " + std::to_string(kv_pages_) + " entries");
+  std::vector<char> seen(kv_pages_, 0);
+  for (int i = 0; i < n; ++i) {
+    if (table[i] < 0 || table[i] >= kv_pages_ || seen[table[i]])
+      raise(GRT_InvalidConfig, "set_kv_block_table: entries must be distinct page ids in [0, n_pages)");
+    seen[table[i]] = 1;
+  }
+  kv_table_host_.assign(table, table + n);
+  cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
+  cuda_check(cudaDeviceSynchronize(), "kv block table");  // no pass in flight reads the old table
+  cuda_check(cudaMemcpy(kv_table_, table, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice), "kv block table");
+}
+
+int64_t Model::kv_row_host(int head, int pos) const {
+  if (kvp_.page == 0) return static_cast<int64_t>(head) * cfg_.max_seq_len + pos;
+  const int pi = pos / kvp_.page;
+  return (static_cast<int64_t>(kv_table_host_[pi]) * kvp_.n_heads + head) * kvp_.page + (pos - pi * kvp_.page);
+}
+
 bool Model::has_tensor(const std::string& name) const {
   for (const LogicalTensor& t : tensors_)
     if (t.name == name) return true;
@@ -566,6 +602,7 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       q.epi = PG_EPI_QKV_ROPE;
       q.q_out = pf_Q_;
       q.k_cache = L.k;
+      q.kvp = kvp_;
       q.v_cache = L.v;
       q.rope_cos = rope_cos_;
       q.rope_sin = rope_sin_;
@@ -577,7 +614,7 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       q.part = pf_part_;
       q.counters = pf_cnt_;
       cuda_check(launch_prefill_gemm(L.w_qkv, pf_Xn_, q, s, true), "prefill qkv");
-      cuda_check(launch_prefill_attention(kvdt, pf_Q_, L.k, L.v, start, P, dq, hl, dh, S, scale, pf_A_, s),
+      cuda_check(launch_prefill_attention(kvdt, pf_Q_, L.k, L.v, start, P, dq, hl, dh, S, scale, pf_A_, s, kvp_),
                  "prefill attention");
       PrefillGemmParams o;
       o.M = d;
@@ -767,6 +804,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   int* err = &ctrl_->err;
 
   std::vector<KernelInvocation> plan;
+  if (impl == 0 && kvp_.page > 0) raise(GRT_Unsupported, "paged KV cache: the persistent pass (pass_impl 0) is contiguous-only");
   if (impl == 0) {
     // the whole static pass (model.cpp:118-143) as one persistent kernel
     const PassParams pp = pass_params(key, B);
@@ -784,8 +822,8 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
                     {logits_, static_cast<size_t>(V) * 4}};
     for (int l = 0; l < cfg_.n_layers; ++l) {
       inv.bindings.push_back({layers_[l].w_qkv, 3ull * d * d * wb});
-      inv.bindings.push_back({layers_[l].k, static_cast<size_t>(h) * S * dh * kvb});
-      inv.bindings.push_back({layers_[l].v, static_cast<size_t>(h) * S * dh * kvb});
+      inv.bindings.push_back({layers_[l].k, kv_layer_elems_ * kvb});
+      inv.bindings.push_back({layers_[l].v, kv_layer_elems_ * kvb});
     }
     inv.launch = [wdt, kvdt, llama, pp](cudaStream_t s) { return launch_decode_pass(wdt, kvdt, llama, pp, s, true); };
     plan.push_back(std::move(inv));
@@ -857,7 +895,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
                       {pending.p.x, static_cast<size_t>(pending.p.k) * 4}, {p.x, static_cast<size_t>(p.k) * 4}};
       if (pp.att.enabled) {
         const PairAttn& A = pp.att;
-        const size_t cache = static_cast<size_t>(A.n_heads) * A.max_seq * A.head_dim * 2;
+        const size_t cache = kv_layer_elems_ * 2;
         inv.spec.name = "attention+" + inv.spec.name;
         inv.spec.flops += static_cast<int64_t>(A.n_heads) * max_len * (4 * A.head_dim + 5);  // kernels.hpp:51
         inv.spec.bytes += 2LL * max_len * A.n_heads * A.head_dim * 2;
@@ -923,6 +961,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       p.max_seq = S;
       p.d_model = dq;  // q | k | v sections of the shard are dq rows each
       p.kv_bf16 = kvdt == Dt::BF16;
+      p.kvp = kvp_;
       p.err = err;
       gemv("qkv", llama ? EPI_QKV_ROPE : EPI_QKV, norm, p, 3ull * dq * d * wb);
     }
@@ -940,6 +979,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       pending_att.ns = att_ns;
       pending_att.span = att_span;
       pending_att.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
+      pending_att.kvp = kvp_;
     } else {  // attention over [0, seq_len) for this rank's heads
       AttnParams a;
       a.q = q_;
@@ -955,12 +995,13 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       a.span_cap = span_cap;
       a.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
       a.err = err;
+      a.kvp = kvp_;
       a.trace = next_trace();
       KernelInvocation inv;
       inv.spec.name = "attention";
       inv.spec.flops = static_cast<int64_t>(hl) * max_len * (4 * dh + 5);  // kernels.hpp:51
       inv.spec.bytes = 2LL * max_len * dq * kvb;
-      inv.bindings = {{L.k, static_cast<size_t>(hl) * S * dh * kvb}, {L.v, static_cast<size_t>(hl) * S * dh * kvb},
+      inv.bindings = {{L.k, kv_layer_elems_ * kvb}, {L.v, kv_layer_elems_ * kvb},
                       {q_, static_cast<size_t>(dq) * 4}, {attn_, static_cast<size_t>(dq) * 4}};
       inv.launch = [kvdt, a, max_len](cudaStream_t s) { return launch_attention(kvdt, a, max_len, s, true); };
       plan.push_back(std::move(inv));

@@ -693,7 +693,7 @@ void Session::kv_row(int layer, int slot, int row, float* out) {
   const size_t eb = model_->kv_elem_bytes();
   std::vector<char> buf(static_cast<size_t>(dh) * eb);
   for (int hh = 0; hh < h; ++hh) {
-    cuda_check(cudaMemcpy(buf.data(), base + ((static_cast<size_t>(hh) * c.max_seq_len + row) * dh) * eb, dh * eb,
+    cuda_check(cudaMemcpy(buf.data(), base + static_cast<size_t>(model_->kv_row_host(hh, row)) * dh * eb, dh * eb,
                           cudaMemcpyDeviceToHost),
                "kv row");
     for (int e = 0; e < dh; ++e) {

@@ -74,6 +74,7 @@ struct ModelConfig {
   int device = 0;
   int tp_size = 1;
   int tp_rank = 0;
+  int kv_page_size = 0;  // 0 = contiguous KV
 
   int d_ff() const noexcept { return d_ff_ > 0 ? d_ff_ : 4 * d_model; }
   int head_dim() const noexcept { return d_model / n_heads; }
@@ -230,6 +231,11 @@ class Model {
   volatile unsigned long long* host_stamps() const { return h_out_stamps_; }
   int max_gen() const { return max_gen_; }
   int kv_elem_bytes() const { return cfg_.kv_dtype == GRT_BF16 ? 2 : 4; }
+  const KvPaging& kv_paging() const { return kvp_; }
+  int kv_pages() const { return kv_pages_; }
+  size_t kv_layer_elems() const { return kv_layer_elems_; }  // elements of one layer's K (or V) cache
+  void set_kv_block_table(const int* table, int n);
+  int64_t kv_row_host(int head, int pos) const;  // host view of kv_row (common.cuh)
   const std::set<const void*>& buffer_set() const { return buffers_; }
   int sync_ints() const { return decode_pass_sync_ints(cfg_.n_layers, cfg_.n_heads); }
 
@@ -291,7 +297,12 @@ class Model {
   void *pf_Xn_ = nullptr, *pf_A_ = nullptr, *pf_act_ = nullptr;
   int* pf_cnt_ = nullptr;
   int* pair_bar_ = nullptr;
-  float* pair_attn_part_ = nullptr;  // [h][<=4][dh+4] partials of the fused attention phase  // [2 * n_layers][2] barrier counters of the fused GEMV pairs
+  float* pair_attn_part_ = nullptr;
+  KvPaging kvp_;
+  int kv_pages_ = 0;
+  size_t kv_layer_elems_ = 0;
+  int* kv_table_ = nullptr;          // device [kv_pages_] block table
+  std::vector<int> kv_table_host_;  // [h][<=4][dh+4] partials of the fused attention phase  // [2 * n_layers][2] barrier counters of the fused GEMV pairs
   // tensor-parallel shard dims: heads, attention width, d_ff, vocab per rank
   int hl_ = 0, dq_ = 0, ffl_ = 0, vl_ = 0;
   float* logits_local_ = nullptr;  // [vl_] before the allgather (== logits_ when tp_size == 1)

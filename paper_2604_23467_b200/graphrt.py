@@ -112,7 +112,8 @@ class _ModelConfig(C.Structure):
                 ("vocab_size", C.c_int32), ("max_seq_len", C.c_int32), ("d_ff", C.c_int32),
                 ("norm_eps", C.c_float), ("seed", C.c_uint64), ("init", C.c_int32),
                 ("weight_dtype", C.c_int32), ("kv_dtype", C.c_int32), ("rope_theta", C.c_float),
-                ("device", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32)]
+                ("device", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32),
+                ("kv_page_size", C.c_int32)]
 
 
 class _CacheConfig(C.Structure):
@@ -156,6 +157,7 @@ EXPORTS = [
     "grt_model_config_default", "grt_cache_config_default", "grt_model_create", "grt_model_destroy",
     "grt_model_upload", "grt_model_download", "grt_model_weight_bytes", "grt_model_decode_bytes",
     "grt_model_load_safetensors", "grt_safetensors_list", "grt_hf_tensor_name",
+    "grt_model_kv_pages", "grt_model_set_kv_block_table",
     "grt_session_create", "grt_session_destroy", "grt_generate", "grt_cache_stats_get", "grt_session_counters",
     "grt_reset", "grt_step", "grt_prefill", "grt_cur_len", "grt_get_logits", "grt_get_kv_row", "grt_sample",
     "grt_sampler_reset", "grt_op_gemv", "grt_op_attention", "grt_op_sample", "grt_op_prefill_gemm",
@@ -195,6 +197,8 @@ def lib():
         L.grt_model_upload.argtypes = [vp, C.c_char_p, vp, C.c_size_t, C.c_int32]
         L.grt_model_download.argtypes = [vp, C.c_char_p, C.POINTER(C.c_float), C.c_size_t]
         L.grt_model_weight_bytes.argtypes = [vp, C.POINTER(C.c_uint64)]
+        L.grt_model_kv_pages.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.grt_model_set_kv_block_table.argtypes = [vp, C.POINTER(C.c_int32), C.c_int32]
         L.grt_model_load_safetensors.argtypes = [vp, C.c_char_p, C.c_int32, C.POINTER(C.c_int32)]
         L.grt_safetensors_list.argtypes = [C.c_char_p, C.c_char_p, C.c_int32, C.POINTER(C.c_int32),
                                            C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int32)]
@@ -280,6 +284,7 @@ class ModelConfig:
     device: int = 0
     tp_size: int = 1   # tensor parallel ranks; this model holds rank tp_rank's shard
     tp_rank: int = 0
+    kv_page_size: int = 0  # 0 = contiguous KV; > 0 = paged pool + block table
 
     def d_ff(self) -> int:
         return self.d_ff_ if self.d_ff_ > 0 else 4 * self.d_model
@@ -294,6 +299,7 @@ class ModelConfig:
         c.norm_eps, c.seed, c.init = self.ln_eps, self.seed, self.init
         c.weight_dtype, c.kv_dtype, c.rope_theta = self.weight_dtype, self.kv_dtype, self.rope_theta
         c.device, c.tp_size, c.tp_rank = self.device, self.tp_size, self.tp_rank
+        c.kv_page_size = self.kv_page_size
         return c
 
     @staticmethod
@@ -445,6 +451,17 @@ class Model:
         n = C.c_int32()
         _check(lib().grt_model_load_safetensors(self._h, str(path).encode(), 1 if strict else 0, C.byref(n)))
         return n.value
+
+    def kv_pages(self):
+        """(page_size, n_pages) of the paged KV pool; (0, 0) when contiguous."""
+        ps, n = C.c_int32(), C.c_int32()
+        _check(lib().grt_model_kv_pages(self._h, C.byref(ps), C.byref(n)))
+        return ps.value, n.value
+
+    def set_kv_block_table(self, table) -> None:
+        """Logical page i -> physical page table[i] (a permutation of range(n_pages))."""
+        arr = (C.c_int32 * max(1, len(table)))(*[int(t) for t in table])
+        _check(lib().grt_model_set_kv_block_table(self._h, arr, len(table)))
 
     def attach_nccl(self, unique_id: bytes) -> None:
         """Joins this rank's model to the NCCL tensor-parallel group (all ranks call it)."""
