@@ -110,12 +110,19 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
   for (int r = 0; r < rounds; ++r) {
     const int jw = rank * span + r * pass + warp * ATTN_UNROLL * RPW;  // first position of this warp
     float4 kv[ATTN_UNROLL], vv[ATTN_UNROLL];
+    int64_t row[ATTN_UNROLL];  // element offsets of this lane's rows (bucket positions, masked below)
+    if (p.kvp.page == 0) {
+#pragma unroll
+      for (int u = 0; u < ATTN_UNROLL; ++u)
+        row[u] = (static_cast<int64_t>(head) * p.max_seq + min(jw + u * RPW + g, p.max_seq - 1)) * dh;
+    } else {
+#pragma unroll
+      for (int u = 0; u < ATTN_UNROLL; ++u) row[u] = kv_row(p.kvp, head, p.max_seq, min(jw + u * RPW + g, p.max_seq - 1)) * dh;
+    }
 #pragma unroll
     for (int u = 0; u < ATTN_UNROLL; ++u) {
-      const int j = min(jw + u * RPW + g, p.max_seq - 1);  // bucket position (masked below)
-      const int64_t row = kv_row(p.kvp, head, p.max_seq, j) * dh;
-      kv[u] = load4<KT>(K + row);
-      vv[u] = load4<KT>(V + row);
+      kv[u] = load4<KT>(K + row[u]);
+      vv[u] = load4<KT>(V + row[u]);
     }
     float sc[ATTN_UNROLL];
     float mr = -INFINITY;

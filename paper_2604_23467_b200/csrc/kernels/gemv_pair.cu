@@ -90,12 +90,19 @@ __device__ __forceinline__ void pair_attn_partial(const PairAttn& A, float* scra
   for (int base = j0; base < j1; base += step) {
     const int jw = base + warp * GP_ATT_UNROLL * RPW;
     float4 kv[GP_ATT_UNROLL], vv[GP_ATT_UNROLL];
+    int64_t row[GP_ATT_UNROLL];  // masked below
+    if (A.kvp.page == 0) {
+#pragma unroll
+      for (int u = 0; u < GP_ATT_UNROLL; ++u)
+        row[u] = (static_cast<int64_t>(head) * A.max_seq + min(jw + u * RPW + g, A.max_seq - 1)) * dh;
+    } else {
+#pragma unroll
+      for (int u = 0; u < GP_ATT_UNROLL; ++u) row[u] = kv_row(A.kvp, head, A.max_seq, min(jw + u * RPW + g, A.max_seq - 1)) * dh;
+    }
 #pragma unroll
     for (int u = 0; u < GP_ATT_UNROLL; ++u) {
-      const int j = min(jw + u * RPW + g, A.max_seq - 1);  // masked below
-      const int64_t r = kv_row(A.kvp, head, A.max_seq, j) * dh;
-      kv[u] = ld_bf16x4(K + r);
-      vv[u] = ld_bf16x4(V + r);
+      kv[u] = ld_bf16x4(K + row[u]);
+      vv[u] = ld_bf16x4(V + row[u]);
     }
     float sc[GP_ATT_UNROLL];
     float mr = -INFINITY;

@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgraphrt_b200.so")
+LIB_PATH = os.environ.get("GRT_LIB_PATH") or os.path.join(_HERE, "libgraphrt_b200.so")  # override: A/B of builds
 
 
 class Errc(enum.IntEnum):
