@@ -1036,7 +1036,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       p.k = ffl;
       p.x = act_;
       p.out = x_;
-      p.chmax = 3072;  // k = 11008 in 4 chunks of 2752 (11 KB stages) measured fastest
+      p.chmax = pair_chmax("GRT_DOWN_CHMAX", 3072);  // k = 11008 in 4 chunks of 2752 (11 KB stages) measured fastest
       gemv("down_residual", resid_epi, NORM_NONE, p, 1ull * d * ffl * wb);
       if (T > 1) allreduce_x("allreduce_down");
     }
