@@ -214,12 +214,20 @@ struct PrefillGemmParams {
   const float* rope_sin = nullptr;
   int head_dim = 0, max_seq = 0, d_model = 0, start_pos = 0, kv_bf16 = 0;
   KvPaging kvp;
+  int defer_reduce = 0;    // PG_EPI_RESID + split K: leave the partials for launch_prefill_resid_norm
   float* part = nullptr;   // split-K scratch, prefill_gemm_part_floats()
   int* counters = nullptr; // [m_tiles], zero-initialised, self-resetting
 };
 // tcgen05/TMEM GEMM; w: bf16 [M, K] row-major (the device weight layout), x:
 // bf16 [P, K] row-major (P <= 512), both K % 64 == 0.
 cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams p, cudaStream_t s, bool pdl);
+// same; writes the chosen tiling (ntile, n_ntiles, ksplit) back into *p
+cudaError_t launch_prefill_gemm_ex(const void* w, const void* x, PrefillGemmParams* p, cudaStream_t s, bool pdl);
+// Deferred split-K reduce of a residual GEMM fused with the RMSNorm that reads
+// its output: X[n] += sum_s partial_s[n] (split order), Xn[n] = bf16(rmsnorm(X[n])
+// * gamma) -- one launch instead of the reduce kernel + prefill_rmsnorm.
+cudaError_t launch_prefill_resid_norm(const PrefillGemmParams& p, const float* gamma, float eps, void* Xn,
+                                      cudaStream_t s);
 cudaError_t prefill_gemm_prepare();
 int prefill_gemm_ksplit(int M, int K, int sms);
 size_t prefill_gemm_part_floats(int M, int K, int P, int sms);

@@ -443,6 +443,70 @@ __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
   }
 }
 
+// Deferred reduce of a residual GEMM (epi RESID, split K) + RMSNorm of the
+// updated rows: one CTA per token.  Per element the split partials are summed in
+// split order first and then added to X (the order prefill_splitk_reduce_kernel
+// + pg_epilogue_pair use); the norm is prefill_rmsnorm_kernel's arithmetic with
+// the same thread -> element map, so the result is bit-identical to the two
+// separate launches.
+constexpr int RN_THREADS = 256, RN_MAXV = 16;  // M = d <= 16384
+__global__ void __launch_bounds__(RN_THREADS) prefill_resid_norm_kernel(const PrefillGemmParams p, const float* gamma,
+                                                                        float eps, __nv_bfloat16* Xn) {
+  __shared__ float red[32];
+  float4 g[RN_MAXV];
+  const int d = p.M, n4 = d >> 2;
+#pragma unroll
+  for (int u = 0; u < RN_MAXV; ++u) {
+    const int j = threadIdx.x + u * RN_THREADS;
+    g[u] = j < n4 ? __ldg(reinterpret_cast<const float4*>(gamma) + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  griddep_wait();  // PDL behind the GEMM: partials complete
+  const int n = blockIdx.x;
+  const int n_tile = n / p.ntile, nn = n - n_tile * p.ntile;
+  float* X = p.out + static_cast<int64_t>(n) * d;
+  float4 v[RN_MAXV];
+#pragma unroll
+  for (int u = 0; u < RN_MAXV; ++u) {
+    const int j = threadIdx.x + u * RN_THREADS;
+    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j >= n4) continue;
+    const int m = 4 * j, m_tile = m / PG_BM, r = m - m_tile * PG_BM;
+    const float* base = p.part + (static_cast<int64_t>(m_tile * p.n_ntiles + n_tile) * p.ksplit) * p.ntile * PG_BM;
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int sp = 0; sp < p.ksplit; ++sp) {
+      const float4 q = __ldcg(reinterpret_cast<const float4*>(base + (static_cast<int64_t>(sp) * p.ntile + nn) * PG_BM + r));
+      sum.x += q.x;
+      sum.y += q.y;
+      sum.z += q.z;
+      sum.w += q.w;
+    }
+    const float4 x = __ldcg(reinterpret_cast<const float4*>(X) + j);
+    v[u] = make_float4(x.x + sum.x, x.y + sum.y, x.z + sum.z, x.w + sum.w);
+    reinterpret_cast<float4*>(X)[j] = v[u];
+  }
+  float ss = 0.0f;
+#pragma unroll
+  for (int u = 0; u < RN_MAXV; ++u) ss += v[u].x * v[u].x + v[u].y * v[u].y + v[u].z * v[u].z + v[u].w * v[u].w;
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (RN_THREADS >> 5) ? red[threadIdx.x] : 0.0f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[0] / static_cast<float>(d) + eps);
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(Xn + static_cast<int64_t>(n) * d);
+#pragma unroll
+  for (int u = 0; u < RN_MAXV; ++u) {
+    const int j = threadIdx.x + u * RN_THREADS;
+    if (j >= n4) continue;
+    o[2 * j] = __floats2bfloat162_rn(v[u].x * inv * g[u].x, v[u].y * inv * g[u].y);
+    o[2 * j + 1] = __floats2bfloat162_rn(v[u].z * inv * g[u].z, v[u].w * inv * g[u].w);
+  }
+}
+
 // ---- host side --------------------------------------------------------------------
 
 namespace {
@@ -549,7 +613,8 @@ cudaError_t prefill_gemm_prepare() {
   return cudaFuncSetAttribute(prefill_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
 }
 
-cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams p, cudaStream_t s, bool pdl) {
+static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, PrefillGemmParams p, cudaStream_t s, bool pdl,
+                                            PrefillGemmParams* out) {
   // K need not be a multiple of the 64-wide K box (e.g. d_ff / 8 = 1376 under
   // TP=8): TMA zero-fills both operands past K; rows must stay 16-byte aligned
   if (p.K % 8 != 0 || p.P < 1 || p.P > PREFILL_CHUNK || p.M < 1) return cudaErrorInvalidValue;
@@ -584,7 +649,8 @@ cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams 
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, prefill_gemm_kernel, mw, mx, p);
-  if (e != cudaSuccess || p.ksplit == 1) return e;
+  if (out) *out = p;
+  if (e != cudaSuccess || p.ksplit == 1 || (p.defer_reduce && p.epi == PG_EPI_RESID)) return e;
   const int64_t work = static_cast<int64_t>((p.M + 1) / 2) * p.P;
   const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 4 * num_sms(dev)));
   cudaLaunchConfig_t rc = {};
@@ -594,6 +660,30 @@ cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams 
   rc.attrs = attr;
   rc.numAttrs = 1;  // always PDL: the reduce's launch overlaps the GEMM's tail
   return cudaLaunchKernelEx(&rc, prefill_splitk_reduce_kernel, p);
+}
+
+cudaError_t launch_prefill_gemm(const void* w, const void* x, PrefillGemmParams p, cudaStream_t s, bool pdl) {
+  return launch_prefill_gemm_impl(w, x, p, s, pdl, nullptr);
+}
+
+cudaError_t launch_prefill_gemm_ex(const void* w, const void* x, PrefillGemmParams* p, cudaStream_t s, bool pdl) {
+  return launch_prefill_gemm_impl(w, x, *p, s, pdl, p);
+}
+
+cudaError_t launch_prefill_resid_norm(const PrefillGemmParams& p, const float* gamma, float eps, void* Xn,
+                                      cudaStream_t s) {
+  if (p.epi != PG_EPI_RESID || p.ksplit < 2 || p.M % 4 || p.M > 4 * RN_MAXV * RN_THREADS || !p.part)
+    return cudaErrorInvalidValue;
+  cudaLaunchConfig_t rc = {};
+  rc.gridDim = dim3(p.P);
+  rc.blockDim = dim3(RN_THREADS);
+  rc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  rc.attrs = attr;
+  rc.numAttrs = 1;
+  return cudaLaunchKernelEx(&rc, prefill_resid_norm_kernel, p, gamma, eps, static_cast<__nv_bfloat16*>(Xn));
 }
 
 }  // namespace grt

@@ -577,6 +577,16 @@ bool Model::supports_batched_prefill() const {
          (dh == 16 || dh == 32 || dh == 64 || dh == 128);
 }
 
+// 1 (default): a split-K residual GEMM of the batched prefill hands its partials
+// to the next RMSNorm launch (one kernel instead of reduce + norm)
+static bool fuse_resid_norm_enabled() {
+  static const int v = [] {
+    const char* e = getenv("GRT_PREFILL_FUSE_NORM");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 void Model::prefill_batched(int p, cudaStream_t s) {
   if (!supports_batched_prefill()) raise(GRT_Unsupported, "batched prefill needs the LLaMA arch with bf16 weights");
   if (p < 1 || p > cfg_.max_seq_len) raise(GRT_PromptTooLong, "batched prefill length out of range");
@@ -592,9 +602,16 @@ void Model::prefill_batched(int p, cudaStream_t s) {
     last_P = P;
     cuda_check(launch_prefill_embed(Dt::BF16, tokens_, start, P, emb_, d, pf_X_, cfg_.vocab_size, &ctrl_->err, s),
                "prefill embed");
+    // Single GPU: a residual GEMM that splits K leaves its partials to the next
+    // RMSNorm launch (reduce + residual + norm in one kernel, bit-identical).
+    const bool fuse_rn = T == 1 && fuse_resid_norm_enabled();
+    PrefillGemmParams prev_down;  // previous layer's down GEMM, if its reduce was deferred
     for (int l = 0; l < cfg_.n_layers; ++l) {
       const LayerBuffers& L = layers_[l];
-      cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln1_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm1");
+      if (prev_down.defer_reduce && prev_down.ksplit > 1)
+        cuda_check(launch_prefill_resid_norm(prev_down, L.ln1_g, cfg_.norm_eps, pf_Xn_, s), "prefill resid+rmsnorm1");
+      else
+        cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln1_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm1");
       PrefillGemmParams q;
       q.M = 3 * dq;
       q.K = d;
@@ -624,9 +641,13 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       o.out = pf_X_;
       o.part = pf_part_;
       o.counters = pf_cnt_;
-      cuda_check(launch_prefill_gemm(L.w_o, pf_A_, o, s, true), "prefill wo");
+      o.defer_reduce = fuse_rn ? 1 : 0;
+      cuda_check(launch_prefill_gemm_ex(L.w_o, pf_A_, &o, s, true), "prefill wo");
       if (T > 1) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce wo");
-      cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln2_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm2");
+      if (o.defer_reduce && o.ksplit > 1)
+        cuda_check(launch_prefill_resid_norm(o, L.ln2_g, cfg_.norm_eps, pf_Xn_, s), "prefill resid+rmsnorm2");
+      else
+        cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln2_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm2");
       PrefillGemmParams u;
       u.M = 2 * ffl;
       u.K = d;
@@ -644,7 +665,9 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       w2.out = pf_X_;
       w2.part = pf_part_;
       w2.counters = pf_cnt_;
-      cuda_check(launch_prefill_gemm(L.w_down, pf_act_, w2, s, true), "prefill down");
+      w2.defer_reduce = fuse_rn && l + 1 < cfg_.n_layers ? 1 : 0;  // the last layer's output goes to the hand-off
+      cuda_check(launch_prefill_gemm_ex(L.w_down, pf_act_, &w2, s, true), "prefill down");
+      prev_down = w2;
       if (T > 1) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce down");
     }
   }
