@@ -444,15 +444,18 @@ __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
 }
 
 // Deferred reduce of a residual GEMM (epi RESID, split K) + RMSNorm of the
-// updated rows: one CTA per token.  Per element the split partials are summed in
-// split order first and then added to X (the order prefill_splitk_reduce_kernel
-// + pg_epilogue_pair use); the norm is prefill_rmsnorm_kernel's arithmetic with
-// the same thread -> element map, so the result is bit-identical to the two
-// separate launches.
-constexpr int RN_THREADS = 256, RN_MAXV = 16;  // M = d <= 16384
+// updated rows: one 1024-thread CTA per token, groups of split partials loaded
+// together.  Per element the split partials are summed in split order first
+// and then added to X (the order prefill_splitk_reduce_kernel + pg_epilogue_pair
+// use), so the residual stream is bit-identical to the separate launches; the
+// norm's sum of squares is reduced over a different thread shape (fp32
+// reassociation only).
+constexpr int RN_THREADS = 512, RN_MAXV = 8, RN_SPLIT_GROUP = 4;  // M = d <= 16384
+constexpr int RN_NORM_THREADS = 256, RN_NORM_MAXV = 16;  // prefill_rmsnorm_kernel's thread shape
 __global__ void __launch_bounds__(RN_THREADS) prefill_resid_norm_kernel(const PrefillGemmParams p, const float* gamma,
                                                                         float eps, __nv_bfloat16* Xn) {
   __shared__ float red[32];
+  extern __shared__ float4 xrow[];  // the updated row, for the reduction below
   float4 g[RN_MAXV];
   const int d = p.M, n4 = d >> 2;
 #pragma unroll
@@ -471,27 +474,47 @@ __global__ void __launch_bounds__(RN_THREADS) prefill_resid_norm_kernel(const Pr
     v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (j >= n4) continue;
     const int m = 4 * j, m_tile = m / PG_BM, r = m - m_tile * PG_BM;
-    const float* base = p.part + (static_cast<int64_t>(m_tile * p.n_ntiles + n_tile) * p.ksplit) * p.ntile * PG_BM;
-    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int sp = 0; sp < p.ksplit; ++sp) {
-      const float4 q = __ldcg(reinterpret_cast<const float4*>(base + (static_cast<int64_t>(sp) * p.ntile + nn) * PG_BM + r));
-      sum.x += q.x;
-      sum.y += q.y;
-      sum.z += q.z;
-      sum.w += q.w;
-    }
+    const float* base = p.part + (static_cast<int64_t>(m_tile * p.n_ntiles + n_tile) * p.ksplit) * p.ntile * PG_BM +
+                        static_cast<int64_t>(nn) * PG_BM + r;
+    const int64_t sstride = static_cast<int64_t>(p.ntile) * PG_BM;
     const float4 x = __ldcg(reinterpret_cast<const float4*>(X) + j);
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < p.ksplit; s0 += RN_SPLIT_GROUP) {  // a group of split loads in flight at once
+      float4 q[RN_SPLIT_GROUP];
+#pragma unroll
+      for (int k = 0; k < RN_SPLIT_GROUP; ++k)
+        q[k] = s0 + k < p.ksplit ? __ldcg(reinterpret_cast<const float4*>(base + (s0 + k) * sstride))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < RN_SPLIT_GROUP; ++k) {
+        if (s0 + k >= p.ksplit) break;
+        sum.x += q[k].x;
+        sum.y += q[k].y;
+        sum.z += q[k].z;
+        sum.w += q[k].w;
+      }
+    }
     v[u] = make_float4(x.x + sum.x, x.y + sum.y, x.z + sum.z, x.w + sum.w);
     reinterpret_cast<float4*>(X)[j] = v[u];
+    xrow[j] = v[u];
   }
-  float ss = 0.0f;
+  __syncthreads();
+  // RMSNorm: prefill_rmsnorm_kernel's arithmetic, its sum of squares reduced
+  // over the same (256-thread) shape, so Xn is bit-identical too
+  if (threadIdx.x < RN_NORM_THREADS) {
+    float ss = 0.0f;
 #pragma unroll
-  for (int u = 0; u < RN_MAXV; ++u) ss += v[u].x * v[u].x + v[u].y * v[u].y + v[u].z * v[u].z + v[u].w * v[u].w;
-  ss = warp_sum(ss);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    for (int u = 0; u < RN_NORM_MAXV; ++u) {
+      const int j = threadIdx.x + u * RN_NORM_THREADS;
+      const float4 a = j < n4 ? xrow[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+      ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+    }
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
-    float t = threadIdx.x < (RN_THREADS >> 5) ? red[threadIdx.x] : 0.0f;
+    float t = threadIdx.x < (RN_NORM_THREADS >> 5) ? red[threadIdx.x] : 0.0f;
     t = warp_sum(t);
     if (threadIdx.x == 0) red[0] = t;
   }
@@ -672,11 +695,13 @@ cudaError_t launch_prefill_gemm_ex(const void* w, const void* x, PrefillGemmPara
 
 cudaError_t launch_prefill_resid_norm(const PrefillGemmParams& p, const float* gamma, float eps, void* Xn,
                                       cudaStream_t s) {
-  if (p.epi != PG_EPI_RESID || p.ksplit < 2 || p.M % 4 || p.M > 4 * RN_MAXV * RN_THREADS || !p.part)
+  if (p.epi != PG_EPI_RESID || p.ksplit < 2 || p.M % 4 || p.M > 4 * RN_MAXV * RN_THREADS ||
+      p.M > 4 * RN_NORM_MAXV * RN_NORM_THREADS || p.M > 48 * 1024 / 4 || !p.part)
     return cudaErrorInvalidValue;
   cudaLaunchConfig_t rc = {};
   rc.gridDim = dim3(p.P);
   rc.blockDim = dim3(RN_THREADS);
+  rc.dynamicSmemBytes = static_cast<size_t>(p.M) * 4;
   rc.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
