@@ -571,7 +571,7 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int 
 struct PgShape {
   int ntile, n_ntiles, ksplit, kbox;
 };
-static PgShape pg_shape(int M, int K, int P, int sms) {
+static PgShape pg_shape(int M, int K, int P, int sms, bool wide_split = false) {
   PgShape sh;
   const int m_tiles = (M + PG_BM - 1) / PG_BM;
   sh.kbox = 1;
@@ -606,7 +606,13 @@ static PgShape pg_shape(int M, int K, int P, int sms) {
   const int items = m_tiles * sh.n_ntiles;
   const int nkb = (K + PG_BK - 1) / PG_BK;
   double best = 1e30;
-  const int ks_max = sh.n_ntiles > 1 ? 1 : std::min(8, nkb);  // P > 256: measured faster unsplit
+  static const int wide_ks = [] {  // max split for P > 256 (env GRT_PG_WIDE_KSPLIT)
+    const char* e = getenv("GRT_PG_WIDE_KSPLIT");
+    return e ? std::max(1, atoi(e)) : 1;
+  }();
+  // P > 256: measured faster unsplit -- except (knob) a residual GEMM whose
+  // reduce is fused into the next RMSNorm launch
+  const int ks_max = sh.n_ntiles > 1 ? (wide_split ? std::min(wide_ks, nkb) : 1) : std::min(8, nkb);
   for (int ks = 1; ks <= ks_max; ++ks) {
     const double waves = static_cast<double>((items * ks + sms - 1) / sms);
     const double cost = waves / ks + 0.02 * (ks - 1);
@@ -624,10 +630,12 @@ size_t prefill_gemm_part_floats(int M, int K, int P, int sms) {
   size_t worst = 0;
   (void)P;
   for (int q = 16; q <= PREFILL_CHUNK; q += 16) {  // size for the worst token count
-    const PgShape sh = pg_shape(M, K, q, sms);
-    if (sh.ksplit == 1) continue;
-    const int m_tiles = (M + PG_BM - 1) / PG_BM;
-    worst = std::max(worst, static_cast<size_t>(m_tiles) * sh.n_ntiles * sh.ksplit * sh.ntile * PG_BM);
+    for (const bool wide : {false, true}) {
+      const PgShape sh = pg_shape(M, K, q, sms, wide);
+      if (sh.ksplit == 1) continue;
+      const int m_tiles = (M + PG_BM - 1) / PG_BM;
+      worst = std::max(worst, static_cast<size_t>(m_tiles) * sh.n_ntiles * sh.ksplit * sh.ntile * PG_BM);
+    }
   }
   return worst;
 }
@@ -643,7 +651,7 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   if (p.K % 8 != 0 || p.P < 1 || p.P > PREFILL_CHUNK || p.M < 1) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);
-  const PgShape sh = pg_shape(p.M, p.K, p.P, num_sms(dev));
+  const PgShape sh = pg_shape(p.M, p.K, p.P, num_sms(dev), p.defer_reduce && p.epi == PG_EPI_RESID);
   p.ntile = sh.ntile;
   p.n_ntiles = sh.n_ntiles;
   p.ksplit = sh.ksplit;
