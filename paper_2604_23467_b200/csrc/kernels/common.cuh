@@ -97,6 +97,12 @@ __device__ __forceinline__ void op_stamp(unsigned long long* tr, int i) {
 }
 
 // ---- numerics -----------------------------------------------------------------
+// Sum of squares of a float4 with an explicit FMA chain: one contraction
+// pattern for every kernel that must agree bit for bit (prefill RMSNorm).
+__device__ __forceinline__ float sumsq4(float4 a) {
+  return __fmaf_rn(a.w, a.w, __fmaf_rn(a.z, a.z, __fmaf_rn(a.y, a.y, __fmul_rn(a.x, a.x))));
+}
+
 // Row of position j of `head` in a layer's K or V cache (KvPaging, kernels.h).
 __device__ __forceinline__ int64_t kv_row(const KvPaging& g, int head, int max_seq, int j) {
   if (g.page == 0) return static_cast<int64_t>(head) * max_seq + j;

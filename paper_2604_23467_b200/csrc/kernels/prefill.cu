@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(PN_THREADS) prefill_rmsnorm_kernel(const float
     g[u] = j < n4 ? reinterpret_cast<const float4*>(gamma)[j] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 #pragma unroll
-  for (int u = 0; u < PN_MAXV; ++u) ss += v[u].x * v[u].x + v[u].y * v[u].y + v[u].z * v[u].z + v[u].w * v[u].w;
+  for (int u = 0; u < PN_MAXV; ++u) ss = __fadd_rn(ss, sumsq4(v[u]));
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();

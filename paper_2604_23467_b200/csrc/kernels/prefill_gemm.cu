@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(RN_THREADS) prefill_resid_norm_kernel(const Pr
     for (int u = 0; u < RN_NORM_MAXV; ++u) {
       const int j = threadIdx.x + u * RN_NORM_THREADS;
       const float4 a = j < n4 ? xrow[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-      ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+      ss = __fadd_rn(ss, sumsq4(a));
     }
     ss = warp_sum(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
