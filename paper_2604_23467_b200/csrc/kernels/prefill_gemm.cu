@@ -599,7 +599,11 @@ static PgShape pg_shape(int M, int K, int P, int sms, bool wide_split = false) {
   // per flop fall as N grows.  Measured (P=500): narrower tiles to occupy more
   // SMs, or split-K with a last-CTA reduction, are both slower for the small-M
   // GEMMs (Wo, down) than 64 wide tiles.
-  sh.n_ntiles = (P + PG_MAX_NT - 1) / PG_MAX_NT;
+  static const int nt_max = [] {  // widest token tile (env GRT_PG_NT_MAX, multiple of 16, <= 256)
+    const char* e = getenv("GRT_PG_NT_MAX");
+    return e ? std::max(16, std::min(PG_MAX_NT, atoi(e) / 16 * 16)) : PG_MAX_NT;
+  }();
+  sh.n_ntiles = (P + nt_max - 1) / nt_max;
   sh.ntile = ((P + sh.n_ntiles - 1) / sh.n_ntiles + 15) / 16 * 16;
   // small-M GEMMs (Wo, down: 32 tiles) split K so the items fill the SMs;
   // the partials go through the parallel reduce kernel
