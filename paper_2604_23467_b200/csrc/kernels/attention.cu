@@ -99,6 +99,37 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
   const int g = lane / G, c = lane - g * G;
   const KT* K = reinterpret_cast<const KT*>(p.k_cache) + 4 * c;
   const KT* V = reinterpret_cast<const KT*>(p.v_cache) + 4 * c;
+  // element offsets of this lane's rows in round r (bucket positions, masked below)
+  auto rows_of = [&](int jw, int64_t* row) {
+    if (p.kvp.page == 0) {
+#pragma unroll
+      for (int u = 0; u < ATTN_UNROLL; ++u)
+        row[u] = (static_cast<int64_t>(head) * p.max_seq + min(jw + u * RPW + g, p.max_seq - 1)) * dh;
+    } else {
+#pragma unroll
+      for (int u = 0; u < ATTN_UNROLL; ++u) row[u] = kv_row(p.kvp, head, p.max_seq, min(jw + u * RPW + g, p.max_seq - 1)) * dh;
+    }
+  };
+  // Rows [0, len_pre - 1) were written by EARLIER steps, so round 0's share of
+  // them is requested before the dependency wait (overlapping the QKV kernel's
+  // tail).  len_pre may be stale (the previous step's length) but never larger
+  // than the live length, so every prefetched row is complete; the rest of the
+  // round is loaded after the wait.
+  float4 kv[ATTN_UNROLL], vv[ATTN_UNROLL];
+  int lp = 0;
+  const int jw0 = rank * span + warp * ATTN_UNROLL * RPW;
+  if (p.prefetch && p.seq_len) {
+    lp = *reinterpret_cast<const volatile int*>(p.seq_len) - 1;
+    int64_t row[ATTN_UNROLL];
+    rows_of(jw0, row);
+#pragma unroll
+    for (int u = 0; u < ATTN_UNROLL; ++u) {
+      if (jw0 + u * RPW + g < lp) {
+        kv[u] = load4<KT>(K + row[u]);
+        vv[u] = load4<KT>(V + row[u]);
+      }
+    }
+  }
   griddep_wait();
   op_stamp(p.trace, 1);
   if (p.trigger == 0) griddep_launch_dependents();
@@ -109,18 +140,11 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int r = 0; r < rounds; ++r) {
     const int jw = rank * span + r * pass + warp * ATTN_UNROLL * RPW;  // first position of this warp
-    float4 kv[ATTN_UNROLL], vv[ATTN_UNROLL];
-    int64_t row[ATTN_UNROLL];  // element offsets of this lane's rows (bucket positions, masked below)
-    if (p.kvp.page == 0) {
-#pragma unroll
-      for (int u = 0; u < ATTN_UNROLL; ++u)
-        row[u] = (static_cast<int64_t>(head) * p.max_seq + min(jw + u * RPW + g, p.max_seq - 1)) * dh;
-    } else {
-#pragma unroll
-      for (int u = 0; u < ATTN_UNROLL; ++u) row[u] = kv_row(p.kvp, head, p.max_seq, min(jw + u * RPW + g, p.max_seq - 1)) * dh;
-    }
+    int64_t row[ATTN_UNROLL];
+    rows_of(jw, row);
 #pragma unroll
     for (int u = 0; u < ATTN_UNROLL; ++u) {
+      if (r == 0 && jw + u * RPW + g < lp) continue;  // prefetched before the wait
       kv[u] = load4<KT>(K + row[u]);
       vv[u] = load4<KT>(V + row[u]);
     }
@@ -280,6 +304,11 @@ cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s,
     return e ? atoi(e) : 0;
   }();
   p.trigger = trig;
+  static const int pref = [] {  // 1: round 0's old rows requested before the dependency wait
+    const char* e = getenv("GRT_ATTN_PREFETCH");
+    return e ? atoi(e) : 1;
+  }();
+  p.prefetch = pref;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_heads * ns);
   cfg.blockDim = dim3(ATTN_THREADS);

@@ -84,6 +84,7 @@ struct AttnParams {
   int rounds = 1;                // passes per CTA (set by the launcher)
   KvPaging kvp;
   int trigger = 0;               // when the successor may launch: 0 start, 1 after KV loads, 2 at exit
+  int prefetch = 0;              // round 0's rows of earlier steps loaded before the dependency wait
 };
 // Per-op trace stamps (8 slots per CTA): 0 CTA start, 1 dependency released
 // (griddepcontrol.wait), 2 operands ready (activation loaded / KV rows loaded),
