@@ -216,6 +216,7 @@ struct PrefillGemmParams {
   int head_dim = 0, max_seq = 0, d_model = 0, start_pos = 0, kv_bf16 = 0;
   KvPaging kvp;
   int defer_reduce = 0;    // PG_EPI_RESID + split K: leave the partials for launch_prefill_resid_norm
+  int wide_split = 0;      // allow split K for P > 256 (partials through the reduce kernel)
   float* part = nullptr;   // split-K scratch, prefill_gemm_part_floats()
   int* counters = nullptr; // [m_tiles], zero-initialised, self-resetting
 };

@@ -655,7 +655,7 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   if (p.K % 8 != 0 || p.P < 1 || p.P > PREFILL_CHUNK || p.M < 1) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);
-  const PgShape sh = pg_shape(p.M, p.K, p.P, num_sms(dev), p.defer_reduce && p.epi == PG_EPI_RESID);
+  const PgShape sh = pg_shape(p.M, p.K, p.P, num_sms(dev), p.wide_split || (p.defer_reduce && p.epi == PG_EPI_RESID));
   p.ntile = sh.ntile;
   p.n_ntiles = sh.n_ntiles;
   p.ksplit = sh.ksplit;

@@ -587,6 +587,16 @@ static bool fuse_resid_norm_enabled() {
   return v != 0;
 }
 
+// 1: the QKV GEMM of prompts > 256 tokens may split K too (partials through the
+// parallel reduce kernel, which applies RoPE / the KV write)
+static bool wide_qkv_split_enabled() {
+  static const int v = [] {
+    const char* e = getenv("GRT_PG_WIDE_QKV");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 void Model::prefill_batched(int p, cudaStream_t s) {
   if (!supports_batched_prefill()) raise(GRT_Unsupported, "batched prefill needs the LLaMA arch with bf16 weights");
   if (p < 1 || p > cfg_.max_seq_len) raise(GRT_PromptTooLong, "batched prefill length out of range");
@@ -630,6 +640,7 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       q.kv_bf16 = kvdt == Dt::BF16;
       q.part = pf_part_;
       q.counters = pf_cnt_;
+      q.wide_split = wide_qkv_split_enabled() ? 1 : 0;
       cuda_check(launch_prefill_gemm(L.w_qkv, pf_Xn_, q, s, true), "prefill qkv");
       cuda_check(launch_prefill_attention(kvdt, pf_Q_, L.k, L.v, start, P, dq, hl, dh, S, scale, pf_A_, s, kvp_),
                  "prefill attention");
