@@ -68,6 +68,7 @@ class ClockSampler:
         self.stop = threading.Event()
         self.thread = None
         self.source = None
+        self.mem = None  # [current, max] memory clock MHz (box-to-box context for HBM-bound numbers)
 
     def _nvml_loop(self, nv, h):
         mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
@@ -76,6 +77,9 @@ class ClockSampler:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.rows.append((float(sm), float(mx), int(rs)))
+                if not self.mem:
+                    self.mem = [nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM),
+                                nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_MEM)]
             except Exception:
                 pass
             self.stop.wait(0.005)
@@ -123,7 +127,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         reasons = sorted(n for n, b in self.REASONS.items() if any(r[2] & b for r in self.rows))
         return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
-                "reasons": reasons, "samples": len(self.rows), "source": self.source}
+                "reasons": reasons, "samples": len(self.rows), "source": self.source,
+                "mem_mhz": self.mem[0] if self.mem else None, "mem_max_mhz": self.mem[1] if self.mem else None}
 
 
 def cpu_reference_sample(timeout=600):
