@@ -122,3 +122,18 @@ def test_fused_pair_attention_phase_matches_oracle():
                          timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= 2e-2
+
+
+@pytest.mark.gpu
+def test_paged_tensor_parallel_shards_match_single_gpu():
+    """TP ranks (host threads, head-sharded KV pools with their own identity
+    block tables) with paging vs the contiguous tp_size=1 model."""
+    kw = dict(arch=g.ARCH_LLAMA, init=g.INIT_PHILOX, weight_dtype=g.BF16, kv_dtype=g.BF16, n_layers=2,
+              d_model=128, n_heads=4, vocab_size=512, max_seq_len=256, d_ff_=320, seed=5)
+    prompt = po.make_prompt(42, 40, 512)
+    ref = g.Session(g.ModelConfig(**kw), g.CacheConfig(bucket_size=64, warmup_hi=0, batched_prefill=True))
+    ref.prefill(prompt)
+    for t in (3, 9):
+        ref.step(t)
+    got = g.tp_emu_threaded(g.ModelConfig(tp_size=2, kv_page_size=16, **kw), prompt, (3, 9))
+    assert float(np.abs(ref.logits() - got).max()) <= 2e-3
