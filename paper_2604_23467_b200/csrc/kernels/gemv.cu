@@ -161,6 +161,16 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
     bulk_g2s(dst, src, bytes, bar, pol);
     if (has_b) bulk_g2s(dst + rowb, src + p.k, bytes, bar, pol);
   };
+  auto prefetch_l2 = [&](int i) {  // task i's rows into L2 only (keeps HBM busy while x is loaded)
+    const int t = warp + i * GEMV_WARPS;
+    const int pl = t / nch, c = t - pl * nch;
+    const int row0 = 2 * (pair_begin + pl);
+    const int c0 = c * CH;
+    const uint32_t bytes = static_cast<uint32_t>(min(CH, p.k - c0)) * sizeof(WT);
+    const WT* src = Wt + static_cast<int64_t>(row0) * p.k + c0;
+    prefetch_l2_bulk(src, bytes);
+    if (row0 + 1 < p.n_rows) prefetch_l2_bulk(src + p.k, bytes);
+  };
 
   op_stamp(p.trace, 0);
   if (lane == 0) {
@@ -190,8 +200,11 @@ __global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(const GemvParams 
   // (`pre_stages` slots; the rest right after the activation is in, so the
   // successor's whole-grid burst does not delay its own activation load).
   const int pre = min(min(S, p.pre_stages > 0 ? p.pre_stages : S), n_tasks);
-  if (lane == 0)
+  if (lane == 0) {
     for (int i = 0; i < pre; ++i) issue(i);
+    if (pre == min(S, n_tasks))
+      for (int i = pre; i < min(pre + p.l2_pre, n_tasks); ++i) prefetch_l2(i);
+  }
   griddep_wait();
   op_stamp(p.trace, 1);
   const bool defer = NORM == NORM_RMS && pre_norm && p.rms_defer;
@@ -411,6 +424,11 @@ cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s,
   const int part_bytes = max_pairs_per_cta(n_pairs, grid) * p.nch * 2 * 4;
   p.stages = stages_for(dev, p.rowb, p.k, part_bytes);
   p.pre_stages = gemv_pre_stages(norm);
+  static const int l2pre = [] {
+    const char* e = getenv("GRT_GEMV_L2PRE");
+    return e ? std::max(0, atoi(e)) : 0;
+  }();
+  p.l2_pre = l2pre;
   static const int defer = [] {
     const char* e = getenv("GRT_RMS_DEFER");
     return e ? atoi(e) : 1;

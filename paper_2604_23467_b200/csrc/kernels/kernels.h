@@ -47,6 +47,7 @@ struct GemvParams {
   int chmax = 0;            // max chunk elements (0 = default 2048 bf16): stage size per task
   int stages = 0;           // ring slots per warp (set by the launcher from the smem budget)
   int pre_stages = 0;       // slots filled before the dependency wait (0 = all; set by the launcher)
+  int l2_pre = 0;           // tasks per warp beyond the ring prefetched into L2 before the wait (launcher)
   int rms_defer = 1;        // RMSNorm: apply 1/rms to the dot products (epilogue) instead of to x
   const float* x = nullptr; // input activation [k] fp32
   const float* gamma = nullptr;
