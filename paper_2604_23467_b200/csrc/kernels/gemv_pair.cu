@@ -269,6 +269,17 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
     bulk_g2s(dst, src, bytes, bar, pol);
     if (has_b) bulk_g2s(dst + rowb, src + g.k, bytes, bar, pol);
   };
+  auto prefetch_l2 = [&](int i) {  // global task i's rows into L2 only
+    const PhaseGeom& g = i < na ? ga : gb;
+    const int t = warp + (i < na ? i : i - na) * GP_WARPS;
+    const int pl = t / g.nch, c = t - pl * g.nch;
+    const int row0 = 2 * (g.pair_begin + pl);
+    const int c0 = c * g.ch;
+    const uint32_t bytes = static_cast<uint32_t>(min(g.ch, g.k - c0)) * 2;
+    const __nv_bfloat16* src = g.w + static_cast<int64_t>(row0) * g.k + c0;
+    prefetch_l2_bulk(src, bytes);
+    if (row0 + 1 < g.n_rows) prefetch_l2_bulk(src + g.k, bytes);
+  };
   // consume tasks [i0, i1) of one phase into `part`, refilling the ring
   auto run_phase = [&](const PhaseGeom& g, int i0, int i1) {
     for (int i = i0; i < i1; ++i) {
@@ -327,8 +338,10 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
       gv[i] = j4 < n4 ? __ldg(reinterpret_cast<const float4*>(pb.gamma) + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  if (lane == 0)
+  if (lane == 0) {
     for (int i = 0; i < min(S, n_all); ++i) issue(i);
+    for (int i = S; i < min(S + P.l2_pre, n_all); ++i) prefetch_l2(i);
+  }
   griddep_wait();
 
   // grid-wide barrier number `nb` (co-resident grid, see the header comment)
@@ -480,6 +493,11 @@ cudaError_t launch_gemv_pair(int epi_b, GemvPairParams P, cudaStream_t s, bool p
   }
   const int budget = optin_smem(dev) - 1024 - (P.xs_floats + part) * 4;
   P.stages = std::max(1, std::min(GP_MAX_STAGES, budget / (GP_WARPS * 2 * P.rowb)));
+  static const int l2pre = [] {
+    const char* e = getenv("GRT_PAIR_L2PRE");
+    return e ? std::max(0, atoi(e)) : 0;
+  }();
+  P.l2_pre = l2pre;
   if (P.stages < 2) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);

@@ -181,6 +181,7 @@ struct GemvPairParams {
   int* bar = nullptr;  // [2] arrive/depart counters, zero-initialised, self-resetting
   int* err = nullptr;
   int stages = 0, rowb = 0, xs_floats = 0;  // set by the launcher
+  int l2_pre = 0;                           // tasks per warp beyond the ring L2-prefetched before the wait
 };
 cudaError_t launch_gemv_pair(int epi_b, GemvPairParams p, cudaStream_t s, bool pdl);
 // split count / span of the fused attention phase for a bucket of max_len positions
