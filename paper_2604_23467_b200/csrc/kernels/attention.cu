@@ -268,12 +268,29 @@ static int attn_rounds_per_cta() {
   return v;
 }
 
-static void attn_shape(int max_len, int head_dim, int* ns, int* rounds) {
+// cap: the largest cluster for which all n_heads clusters fit on the SMs at once
+// (one 512-thread CTA per SM): a second wave would double the latency.
+static int attn_cluster_cap(int n_heads) {
+  if (n_heads <= 0) return ATTN_MAX_CLUSTER;
+  static const int off = [] {
+    const char* e = getenv("GRT_ATTN_WAVE_CAP");
+    return e ? atoi(e) == 0 : 0;
+  }();
+  if (off) return ATTN_MAX_CLUSTER;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int c = 1;
+  while (2 * c <= ATTN_MAX_CLUSTER && 2 * c * n_heads <= num_sms(dev)) c <<= 1;
+  return c;
+}
+
+static void attn_shape(int max_len, int head_dim, int* ns, int* rounds, int n_heads = 0) {
   const int pass = attn_pass_span(head_dim);
   const int need = std::max(1, (max_len + pass - 1) / pass);  // passes over the whole bucket
   const int want = (need + attn_rounds_per_cta() - 1) / attn_rounds_per_cta();
+  const int cap = attn_cluster_cap(n_heads);
   int c = 1;
-  while (c < want && c < ATTN_MAX_CLUSTER) c <<= 1;
+  while (c < want && c < cap) c <<= 1;
   *ns = c;
   *rounds = (need + c - 1) / c;
 }
@@ -295,7 +312,7 @@ cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s,
   if (p.head_dim % 4 != 0 || gs < 1 || gs > 32 || (gs & (gs - 1)) != 0 || p.head_dim > 256)
     return cudaErrorInvalidValue;
   int ns, rounds;
-  attn_shape(max_len, p.head_dim, &ns, &rounds);
+  attn_shape(max_len, p.head_dim, &ns, &rounds, p.n_heads);
   p.rounds = rounds;
   // 0 (default): the successor (Wo + gate/up) launches at once and fills its
   // weight ring on the SMs this small grid leaves free (measured fastest)
