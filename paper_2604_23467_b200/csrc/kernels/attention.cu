@@ -110,24 +110,20 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
       for (int u = 0; u < ATTN_UNROLL; ++u) row[u] = kv_row(p.kvp, head, p.max_seq, min(jw + u * RPW + g, p.max_seq - 1)) * dh;
     }
   };
-  // Rows [0, len_pre - 1) were written by EARLIER steps, so round 0's share of
-  // them is requested before the dependency wait (overlapping the QKV kernel's
-  // tail).  len_pre may be stale (the previous step's length) but never larger
-  // than the live length, so every prefetched row is complete; the rest of the
-  // round is loaded after the wait.
+  // Every row of round 0 except the current step's (position len-1, written by
+  // the QKV kernel this kernel depends on) holds data of EARLIER steps or lies
+  // past the live length (masked, never read into the result), so the whole
+  // round is requested before the dependency wait -- overlapping the QKV
+  // kernel's tail -- and only the new row is re-read after it.
   float4 kv[ATTN_UNROLL], vv[ATTN_UNROLL];
-  int lp = 0;
-  const int jw0 = rank * span + warp * ATTN_UNROLL * RPW;
-  if (p.prefetch && p.seq_len) {
-    lp = *reinterpret_cast<const volatile int*>(p.seq_len) - 1;
+  const bool pre = p.prefetch && p.seq_len;
+  if (pre) {
     int64_t row[ATTN_UNROLL];
-    rows_of(jw0, row);
+    rows_of(rank * span + warp * ATTN_UNROLL * RPW, row);
 #pragma unroll
     for (int u = 0; u < ATTN_UNROLL; ++u) {
-      if (jw0 + u * RPW + g < lp) {
-        kv[u] = load4<KT>(K + row[u]);
-        vv[u] = load4<KT>(V + row[u]);
-      }
+      kv[u] = load4<KT>(K + row[u]);
+      vv[u] = load4<KT>(V + row[u]);
     }
   }
   griddep_wait();
@@ -144,7 +140,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
     rows_of(jw, row);
 #pragma unroll
     for (int u = 0; u < ATTN_UNROLL; ++u) {
-      if (r == 0 && jw + u * RPW + g < lp) continue;  // prefetched before the wait
+      if (r == 0 && pre && jw + u * RPW + g != len - 1) continue;  // requested before the wait
       kv[u] = load4<KT>(K + row[u]);
       vv[u] = load4<KT>(V + row[u]);
     }
