@@ -584,10 +584,14 @@ static PgShape pg_shape(int M, int K, int P, int sms, bool wide_split = false) {
     const int nkb = (K + PG_BK * sh.kbox - 1) / (PG_BK * sh.kbox);
     // persistent CTAs: pick the split whose work items tile the SMs evenly
     // (time ~ waves / split); partials are reduced by a separate parallel kernel
+    static const double per_split = [] {  // cost of one more split (env GRT_PG_KS_COST)
+      const char* e = getenv("GRT_PG_KS_COST");
+      return e ? atof(e) : 0.005;
+    }();
     double best = 1e30;
     for (int ks = 1; ks <= std::min(16, nkb); ++ks) {
       const double waves = static_cast<double>((m_tiles * ks + sms - 1) / sms);
-      const double cost = waves / ks + 0.005 * ks;
+      const double cost = waves / ks + per_split * ks;
       if (cost < best) {
         best = cost;
         sh.ksplit = ks;
