@@ -204,9 +204,32 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
 
   if (kind == 0 || !(temperature > 0.0f)) {
     // greedy: strict >, lowest index wins ties (kernels.cpp:265-270)
+    // every logit load of a thread is issued before the first compare (one
+    // memory round trip, not GRT_V / threads dependent ones)
     float bv = -INFINITY;
     int bi = 0x7fffffff;
-    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+    constexpr int NV4 = GRT_V / 4;
+    constexpr int PER = NV4 > 0 ? (NV4 + GRT_SAMPLE_THREADS - 1) / GRT_SAMPLE_THREADS : 1;
+    float4 lv[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int j4 = tid + k * GRT_SAMPLE_THREADS;
+      lv[k] = j4 < NV4 ? reinterpret_cast<const float4*>(logits)[j4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int j4 = tid + k * GRT_SAMPLE_THREADS;
+      if (j4 >= NV4) continue;
+      const float e[4] = {lv[k].x, lv[k].y, lv[k].z, lv[k].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (e[c] > bv || bi == 0x7fffffff) {
+          bv = e[c];
+          bi = 4 * j4 + c;
+        }
+      }
+    }
+    for (int i = 4 * NV4 + tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {  // V % 4 tail
       const float v = logits[i];
       if (v > bv || bi == 0x7fffffff) {
         bv = v;
