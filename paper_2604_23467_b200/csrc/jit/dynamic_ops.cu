@@ -22,6 +22,15 @@ typedef unsigned long long u64;
 typedef unsigned int u32;
 
 #define GRT_SAMPLE_THREADS 1024
+// top-k/top-p: the per-token weights are computed once into dynamic shared
+// memory (u32: w = e * 2^31 <= 2^31) when they fit; the host launches the
+// sampler kernels with GRT_V * 4 bytes of dynamic shared memory then (jit.cpp)
+#define GRT_SAMPLE_SMEM_MAX 196608
+#if GRT_V * 4 <= GRT_SAMPLE_SMEM_MAX
+#define GRT_TOPKP_SMEM 1
+#else
+#define GRT_TOPKP_SMEM 0
+#endif
 #ifndef INFINITY
 #define INFINITY __int_as_float(0x7f800000)
 #endif
@@ -168,18 +177,56 @@ __device__ u64 block_sum_u64(u64 v, u64* red) {
 }
 
 // Finds, among keys with (key & mask) == prefix and key >= floor, the digit
-// bucket where the descending cumulative (count or weight) reaches `need`.
+// bucket where the descending cumulative (count or weight) reaches `need`:
+// the highest digit dg >= 1 whose inclusive suffix sum reaches `need` (else 0),
+// and the remainder need - (sum of the buckets above dg).  Warp 0 scans the
+// 256 buckets in parallel (lane l owns buckets 8l..8l+7); integer sums, so the
+// result equals the serial top-down walk exactly.
 __device__ void radix_pick(u64* hist, int shift, u64& prefix, u64& mask, u64& need) {
   __shared__ u64 s_prefix, s_need;
-  if (threadIdx.x == 0) {
-    u64 nd = need;
-    int dg = 255;
-    for (; dg > 0; --dg) {
-      if (hist[dg] >= nd) break;
-      nd -= hist[dg];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    u64 hb[8];
+    u64 tot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      hb[k] = hist[8 * lane + k];
+      tot += hb[k];
     }
-    s_prefix = prefix | ((u64)dg << shift);
-    s_need = nd;
+    u64 suf = tot;  // inclusive suffix over lanes >= lane
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 n = __shfl_down_sync(0xffffffffu, suf, o);
+      if (lane + o < 32) suf += n;
+    }
+    u64 run = suf - tot;  // buckets above this lane's range
+    int best = -1;
+    u64 excl = 0;
+#pragma unroll
+    for (int k = 7; k >= 0; --k) {
+      const int d = 8 * lane + k;
+      if (best < 0 && d >= 1) {
+        if (run + hb[k] >= need) {
+          best = d;
+          excl = run;
+        }
+      }
+      run += hb[k];
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, best >= 1);
+    int dg;
+    u64 above;
+    if (hit) {
+      const int src = 31 - __clz(hit);
+      dg = __shfl_sync(0xffffffffu, best, src);
+      above = __shfl_sync(0xffffffffu, excl, src);
+    } else {  // fall through to digit 0: every bucket above it is consumed
+      dg = 0;
+      above = __shfl_sync(0xffffffffu, suf - hb[0], 0);
+    }
+    if (lane == 0) {
+      s_prefix = prefix | ((u64)dg << shift);
+      s_need = need - above;
+    }
   }
   __syncthreads();
   prefix = s_prefix;
@@ -318,6 +365,14 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
     float m = -INFINITY;
     for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) m = fmaxf(m, logits[i]);
     m = block_max_f(m, redf);
+#if GRT_TOPKP_SMEM
+    extern __shared__ u32 wsm[];  // [GRT_V] weights, computed once (every pass below reads them)
+    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) wsm[i] = (u32)topkp_weight(logits, i, m, temperature);
+    __syncthreads();
+#define GRT_W(i) ((u64)wsm[i])
+#else
+#define GRT_W(i) topkp_weight(logits, (i), m, temperature)
+#endif
     const int top_k = ctrl->top_k;
     const float top_p = ctrl->top_p;
     // (1) top-k threshold key
@@ -328,7 +383,7 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
         for (int b = tid; b < 256; b += GRT_SAMPLE_THREADS) hist[b] = 0;
         __syncthreads();
         for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
-          const u64 key = topkp_key(topkp_weight(logits, i, m, temperature), i);
+          const u64 key = topkp_key(GRT_W(i), i);
           if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1ull);
         }
         __syncthreads();
@@ -339,7 +394,7 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
     // (2) top-p threshold key among keys >= kth
     u64 W = 0;
     for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
-      const u64 w = topkp_weight(logits, i, m, temperature);
+      const u64 w = GRT_W(i);
       if (topkp_key(w, i) >= kth) W += w;
     }
     W = block_sum_u64(W, redu);
@@ -352,7 +407,7 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
         for (int b = tid; b < 256; b += GRT_SAMPLE_THREADS) hist[b] = 0;
         __syncthreads();
         for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
-          const u64 w = topkp_weight(logits, i, m, temperature);
+          const u64 w = GRT_W(i);
           const u64 key = topkp_key(w, i);
           if (key >= kth && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], w);
         }
@@ -366,22 +421,35 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
     const int b0 = tid * per, b1 = min(GRT_V, b0 + per);
     u64 local = 0;
     for (int i = b0; i < b1; ++i) {
-      const u64 w = topkp_weight(logits, i, m, temperature);
+      const u64 w = GRT_W(i);
       if (topkp_key(w, i) >= kappa) local += w;
     }
+    // exclusive prefix of the per-thread sums in thread order (parallel scan;
+    // integer, so identical to the serial walk)
     __shared__ u64 sc[GRT_SAMPLE_THREADS];
-    sc[tid] = local;
-    __syncthreads();
+    __shared__ u64 wsum[32];
     __shared__ u64 s_S;
-    if (tid == 0) {
-      u64 acc = 0;
-      for (int t = 0; t < GRT_SAMPLE_THREADS; ++t) {
-        const u64 v = sc[t];
-        sc[t] = acc;
-        acc += v;
+    {
+      const int lane = tid & 31, wp = tid >> 5;
+      u64 v = local;
+      for (int o = 1; o < 32; o <<= 1) {
+        const u64 n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
       }
-      s_S = acc;
-      s_tok = 0x7fffffff;
+      if (lane == 31) wsum[wp] = v;
+      __syncthreads();
+      if (wp == 0) {
+        u64 t = lane < (GRT_SAMPLE_THREADS >> 5) ? wsum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const u64 n = __shfl_up_sync(0xffffffffu, t, o);
+          if (lane >= o) t += n;
+        }
+        wsum[lane] = t;
+        if (lane == 31) s_S = t;
+      }
+      if (tid == 0) s_tok = 0x7fffffff;
+      __syncthreads();
+      sc[tid] = v - local + (wp > 0 ? wsum[wp - 1] : 0);
     }
     __syncthreads();
     const u64 S = s_S;
@@ -395,7 +463,7 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
     u64 acc = sc[tid];
     if (S > 0 && acc <= r && r < acc + local) {
       for (int i = b0; i < b1; ++i) {
-        const u64 w = topkp_weight(logits, i, m, temperature);
+        const u64 w = GRT_W(i);
         if (topkp_key(w, i) < kappa) continue;
         acc += w;
         if (acc > r) {

@@ -107,7 +107,16 @@ std::string jit_compile(const std::vector<std::string>& opts) {
   return cubin;
 }
 
+// Dynamic shared memory of the NVRTC sampler kernels (top-k/top-p weights cache,
+// dynamic_ops.cu GRT_TOPKP_SMEM): registered per CUfunction by JitModule::fn,
+// applied by launch_jit.
+static std::mutex g_dyn_mu;
+static std::map<CUfunction, unsigned> g_dyn_smem;
+constexpr int kSampleSmemMax = 196608;  // GRT_SAMPLE_SMEM_MAX in dynamic_ops.cu
+
 JitModule::JitModule(const std::string& /*key*/, const std::vector<std::string>& opts, int device) {
+  for (const auto& o : opts)
+    if (o.rfind("-DGRT_V=", 0) == 0) vocab_ = atoi(o.c_str() + 8);
   const auto t0 = std::chrono::steady_clock::now();
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cuda_check(cudaFree(nullptr), "context init");
@@ -126,6 +135,12 @@ CUfunction JitModule::fn(const char* name) const {
   // same L1/shared carveout as the GEMVs: PDL successors can co-reside without
   // an SM reconfiguration
   cu_check(drv().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100), name);
+  if (std::string(name).rfind("grt_sample", 0) == 0 && vocab_ > 0 && vocab_ * 4 <= kSampleSmemMax) {
+    const unsigned bytes = static_cast<unsigned>(vocab_) * 4;
+    cu_check(drv().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, static_cast<int>(bytes)), name);
+    std::lock_guard<std::mutex> lk(g_dyn_mu);
+    g_dyn_smem[f] = bytes;
+  }
   return f;
 }
 
@@ -150,7 +165,11 @@ cudaError_t launch_jit(CUfunction f, dim3 grid, dim3 block, void** args, cudaStr
   cfg.blockDimX = block.x;
   cfg.blockDimY = block.y;
   cfg.blockDimZ = block.z;
-  cfg.sharedMemBytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_dyn_mu);
+    auto it = g_dyn_smem.find(f);
+    cfg.sharedMemBytes = it == g_dyn_smem.end() ? 0 : it->second;
+  }
   cfg.hStream = reinterpret_cast<CUstream>(s);
   CUlaunchAttribute attr[1];
   attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;

@@ -158,6 +158,7 @@ class JitModule {
  private:
   CUmodule mod_ = nullptr;
   double compile_ms_ = 0;
+  int vocab_ = 0;  // -DGRT_V of this specialisation
 };
 std::string jit_compile(const std::vector<std::string>& opts);  // NVRTC -> sm_100a cubin (no GPU needed)
 std::shared_ptr<JitModule> jit_get(const std::vector<std::string>& opts, int device);
