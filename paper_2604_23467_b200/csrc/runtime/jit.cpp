@@ -126,6 +126,10 @@ JitModule::JitModule(const std::string& /*key*/, const std::vector<std::string>&
 }
 
 JitModule::~JitModule() {
+  {
+    std::lock_guard<std::mutex> lk(g_dyn_mu);
+    for (CUfunction f : fns_) g_dyn_smem.erase(f);
+  }
   if (mod_) drv().ModuleUnload(mod_);
 }
 
@@ -135,12 +139,15 @@ CUfunction JitModule::fn(const char* name) const {
   // same L1/shared carveout as the GEMVs: PDL successors can co-reside without
   // an SM reconfiguration
   cu_check(drv().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100), name);
+  unsigned bytes = 0;
   if (std::string(name).rfind("grt_sample", 0) == 0 && vocab_ > 0 && vocab_ * 4 <= kSampleSmemMax) {
-    const unsigned bytes = static_cast<unsigned>(vocab_) * 4;
+    bytes = static_cast<unsigned>(vocab_) * 4;
     cu_check(drv().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, static_cast<int>(bytes)), name);
-    std::lock_guard<std::mutex> lk(g_dyn_mu);
-    g_dyn_smem[f] = bytes;
   }
+  // every function is (re)registered: a handle of an unloaded module may be reused
+  std::lock_guard<std::mutex> lk(g_dyn_mu);
+  g_dyn_smem[f] = bytes;
+  fns_.push_back(f);
   return f;
 }
 
@@ -177,6 +184,7 @@ cudaError_t launch_jit(CUfunction f, dim3 grid, dim3 block, void** args, cudaStr
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   CUresult r = drv().LaunchKernelEx(&cfg, f, args, nullptr);
+  if (r == CUDA_ERROR_INVALID_VALUE) return cudaErrorInvalidValue;
   if (r != CUDA_SUCCESS) return cudaErrorLaunchFailure;
   return cudaSuccess;
 }

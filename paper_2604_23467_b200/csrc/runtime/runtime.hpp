@@ -159,6 +159,7 @@ class JitModule {
   CUmodule mod_ = nullptr;
   double compile_ms_ = 0;
   int vocab_ = 0;  // -DGRT_V of this specialisation
+  mutable std::vector<CUfunction> fns_;  // handed out by fn() (dynamic-smem registry entries)
 };
 std::string jit_compile(const std::vector<std::string>& opts);  // NVRTC -> sm_100a cubin (no GPU needed)
 std::shared_ptr<JitModule> jit_get(const std::vector<std::string>& opts, int device);
