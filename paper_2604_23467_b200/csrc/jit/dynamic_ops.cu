@@ -176,23 +176,6 @@ __device__ u64 block_sum_u64(u64 v, u64* red) {
   return red[0];
 }
 
-// Warp-aggregated shared-memory histogram add: lanes with the same bucket
-// combine their values first (integer sums), one atomic per distinct bucket.
-// Almost every weight lands in the same low bucket, so per-lane atomics would
-// serialise on one address.  Inactive lanes pass bucket -1.
-__device__ __forceinline__ void hist_add_warp(u64* hist, int bucket, u64 v) {
-  const unsigned peers = __match_any_sync(0xffffffffu, bucket);
-  const int lane = threadIdx.x & 31;
-  u64 sum = 0;
-  unsigned rest = peers;
-  while (rest) {
-    const int src = __ffs(rest) - 1;
-    sum += __shfl_sync(peers, v, src);
-    rest &= rest - 1;
-  }
-  if (bucket >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[bucket], sum);
-}
-
 // Finds, among keys with (key & mask) == prefix and key >= floor, the digit
 // bucket where the descending cumulative (count or weight) reaches `need`:
 // the highest digit dg >= 1 whose inclusive suffix sum reaches `need` (else 0),
@@ -399,14 +382,9 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
       for (int shift = 40; shift >= 0; shift -= 8) {
         for (int b = tid; b < 256; b += GRT_SAMPLE_THREADS) hist[b] = 0;
         __syncthreads();
-        for (int i0 = 0; i0 < GRT_V; i0 += GRT_SAMPLE_THREADS) {  // whole warps iterate together
-          const int i = i0 + tid;
-          int b = -1;
-          if (i < GRT_V) {
-            const u64 key = topkp_key(GRT_W(i), i);
-            if ((key & mask) == prefix) b = (int)((key >> shift) & 255);
-          }
-          hist_add_warp(hist, b, 1ull);
+        for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+          const u64 key = topkp_key(GRT_W(i), i);
+          if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1ull);
         }
         __syncthreads();
         radix_pick(hist, shift, prefix, mask, need);
@@ -428,16 +406,10 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
       for (int shift = 40; shift >= 0; shift -= 8) {
         for (int b = tid; b < 256; b += GRT_SAMPLE_THREADS) hist[b] = 0;
         __syncthreads();
-        for (int i0 = 0; i0 < GRT_V; i0 += GRT_SAMPLE_THREADS) {
-          const int i = i0 + tid;
-          int b = -1;
-          u64 w = 0;
-          if (i < GRT_V) {
-            w = GRT_W(i);
-            const u64 key = topkp_key(w, i);
-            if (key >= kth && (key & mask) == prefix) b = (int)((key >> shift) & 255);
-          }
-          hist_add_warp(hist, b, w);
+        for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+          const u64 w = GRT_W(i);
+          const u64 key = topkp_key(w, i);
+          if (key >= kth && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], w);
         }
         __syncthreads();
         radix_pick(hist, shift, prefix, mask, need);
