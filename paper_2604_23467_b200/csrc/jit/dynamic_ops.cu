@@ -382,10 +382,17 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
       for (int shift = 40; shift >= 0; shift -= 8) {
         for (int b = tid; b < 256; b += GRT_SAMPLE_THREADS) hist[b] = 0;
         __syncthreads();
+        u64 zero = 0;  // digit 0 (tiny weights: most of the vocabulary) summed locally, one atomic per warp
         for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
           const u64 key = topkp_key(GRT_W(i), i);
-          if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1ull);
+          if ((key & mask) == prefix) {
+            const int b = (int)((key >> shift) & 255);
+            if (b == 0) zero += 1ull;
+            else atomicAdd(&hist[b], 1ull);
+          }
         }
+        for (int o = 16; o > 0; o >>= 1) zero += __shfl_xor_sync(0xffffffffu, zero, o);
+        if ((tid & 31) == 0 && zero) atomicAdd(&hist[0], zero);
         __syncthreads();
         radix_pick(hist, shift, prefix, mask, need);
       }
@@ -406,11 +413,18 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
       for (int shift = 40; shift >= 0; shift -= 8) {
         for (int b = tid; b < 256; b += GRT_SAMPLE_THREADS) hist[b] = 0;
         __syncthreads();
+        u64 zero = 0;
         for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
           const u64 w = GRT_W(i);
           const u64 key = topkp_key(w, i);
-          if (key >= kth && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], w);
+          if (key >= kth && (key & mask) == prefix) {
+            const int b = (int)((key >> shift) & 255);
+            if (b == 0) zero += w;
+            else atomicAdd(&hist[b], w);
+          }
         }
+        for (int o = 16; o > 0; o >>= 1) zero += __shfl_xor_sync(0xffffffffu, zero, o);
+        if ((tid & 31) == 0 && zero) atomicAdd(&hist[0], zero);
         __syncthreads();
         radix_pick(hist, shift, prefix, mask, need);
       }
