@@ -141,6 +141,11 @@ __device__ __forceinline__ float grt_expf(float z) {
   return ldexpf(y, (int)n);
 }
 
+__device__ __forceinline__ u64 topkp_weight_v(float logit, float m, float t) {
+  const float z = (logit - m) / t;
+  const float e = grt_expf(z);
+  return (u64)(e * 2147483648.0f);
+}
 __device__ __forceinline__ u64 topkp_weight(const float* logits, int i, float m, float t) {
   const float z = (logits[i] - m) / t;
   const float e = grt_expf(z);
@@ -362,15 +367,39 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
     __syncthreads();
   } else {
     // integer-CDF top-k / top-p (oracle.c:oc_sample_topkp)
-    float m = -INFINITY;
-    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) m = fmaxf(m, logits[i]);
-    m = block_max_f(m, redf);
 #if GRT_TOPKP_SMEM
+    // the logits are read ONCE (all loads of a thread in flight together), the
+    // weights computed from registers into dynamic shared memory
+    constexpr int NV4 = GRT_V / 4;
+    constexpr int PER = NV4 > 0 ? (NV4 + GRT_SAMPLE_THREADS - 1) / GRT_SAMPLE_THREADS : 1;
+    float4 lv[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int j4 = tid + k * GRT_SAMPLE_THREADS;
+      lv[k] = j4 < NV4 ? reinterpret_cast<const float4*>(logits)[j4] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    }
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) m = fmaxf(m, fmaxf(fmaxf(lv[k].x, lv[k].y), fmaxf(lv[k].z, lv[k].w)));
+    for (int i = 4 * NV4 + tid; i < GRT_V; i += GRT_SAMPLE_THREADS) m = fmaxf(m, logits[i]);
+    m = block_max_f(m, redf);
     extern __shared__ u32 wsm[];  // [GRT_V] weights, computed once (every pass below reads them)
-    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) wsm[i] = (u32)topkp_weight(logits, i, m, temperature);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int j4 = tid + k * GRT_SAMPLE_THREADS;
+      if (j4 >= NV4) continue;
+      wsm[4 * j4] = (u32)topkp_weight_v(lv[k].x, m, temperature);
+      wsm[4 * j4 + 1] = (u32)topkp_weight_v(lv[k].y, m, temperature);
+      wsm[4 * j4 + 2] = (u32)topkp_weight_v(lv[k].z, m, temperature);
+      wsm[4 * j4 + 3] = (u32)topkp_weight_v(lv[k].w, m, temperature);
+    }
+    for (int i = 4 * NV4 + tid; i < GRT_V; i += GRT_SAMPLE_THREADS) wsm[i] = (u32)topkp_weight(logits, i, m, temperature);
     __syncthreads();
 #define GRT_W(i) ((u64)wsm[i])
 #else
+    float m = -INFINITY;
+    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) m = fmaxf(m, logits[i]);
+    m = block_max_f(m, redf);
 #define GRT_W(i) topkp_weight(logits, (i), m, temperature)
 #endif
     const int top_k = ctrl->top_k;
