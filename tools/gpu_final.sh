@@ -5,5 +5,5 @@ timeout 700 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_be
 timeout 300 python bench.py --impl reference > gpurun_out/final_bench_ref.json 2> gpurun_out/final_bench_ref.err
 NCU=/usr/local/cuda/bin/ncu
 B="python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-profile --sweep= --mixed 0 --ipc 0"
-timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01d_launches.csv $B > gpurun_out/r01d_launches.log 2>&1
-timeout 600 $NCU --set full --clock-control none --import-source on -k regex:attn_decode --launch-skip 100 -c 1 -o gpurun_out/r01d_attn -f $B > gpurun_out/r01d_attn.log 2>&1
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01e_launches.csv $B > gpurun_out/r01e_launches.log 2>&1
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:attn_decode --launch-skip 100 -c 1 -o gpurun_out/r01e_attn -f $B > gpurun_out/r01e_attn.log 2>&1
