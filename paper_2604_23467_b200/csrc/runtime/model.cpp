@@ -913,6 +913,9 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       if (epi != EPI_SWIGLU) {  // down + (QKV | head): the 44 KB activation row leaves less room for the ring
         pp.a.chmax = pair_chmax("GRT_PAIR_CHMAX_A", pp.a.chmax);
         pp.b.chmax = pair_chmax("GRT_PAIR_CHMAX_B", pp.b.chmax);
+      } else {  // Wo + gate/up (k = 4096 both): 2048-element chunks (8 KB stages) by default
+        pp.a.chmax = pair_chmax("GRT_WOUP_CHMAX", pp.a.chmax);
+        pp.b.chmax = pair_chmax("GRT_WOUP_CHMAX", pp.b.chmax);
       }
       pp.bar = pair_bar_ + 2 * n_pairs_emitted++;
       pp.err = err;
@@ -997,6 +1000,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       p.kv_bf16 = kvdt == Dt::BF16;
       p.kvp = kvp_;
       p.err = err;
+      p.chmax = pair_chmax("GRT_QKV_CHMAX", 0);  // 0: 2048-element chunks
       gemv("qkv", llama ? EPI_QKV_ROPE : EPI_QKV, norm, p, 3ull * dq * d * wb);
     }
     flush();
