@@ -71,3 +71,25 @@ def test_mode_names_round_trip():
     with pytest.raises(g.Error) as e:
         g.mode_from_name("turbo")
     assert e.value.code == g.Errc.InvalidConfig
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/grt/c_api.h is a C99 header (no C++ or torch types) and a C program
+    links against the shared library and calls the GPU-free entry points."""
+    src = tmp_path / "probe.c"
+    src.write_text(
+        '#include <stdio.h>\n#include "grt/c_api.h"\n'
+        "int main(void) {\n"
+        "  grt_model_config c; grt_cache_config cc; grt_generation_request r = {0};\n"
+        "  grt_model_config_default(&c); grt_cache_config_default(&cc); (void)r;\n"
+        "  int32_t out_in = 0; char name[64];\n"
+        '  if (grt_hf_tensor_name("lm_head.weight", name, 64, &out_in) != GRT_OK) return 2;\n'
+        '  printf("%d %s %s %d %d\\n", grt_abi_version(), grt_status_name(GRT_CacheFull), name, out_in,\n'
+        "         c.kv_page_size);\n"
+        "  return 0;\n}\n")
+    exe = tmp_path / "probe"
+    libdir = os.path.dirname(g.LIB_PATH)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                    "-L" + libdir, "-lgraphrt_b200", "-Wl,-rpath," + libdir], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    assert out == [str(g.lib().grt_abi_version()), "CacheFull", "head", "1", "0"]
