@@ -52,6 +52,48 @@ __device__ __forceinline__ float grt_bf16_to_f32(unsigned short h) { return __ui
 // The zero rows the reference appends are overwritten by the static pass before
 // they are read (build_plan writes row length-1 before attention), so the
 // append reduces to the length bump.
+// x = emb[tok] (+ pos_table[pos]); then cur_len = pos + 1.
+__device__ __forceinline__ void gather_row(GrtCtrl* ctrl, int pos, int tok, const void* emb, const void* pos_table,
+                                           float* x) {
+  const long long erow = (long long)tok * GRT_D;
+#if GRT_WBF16 && !GRT_ARCH_REF && (GRT_D % 8 == 0)
+  (void)pos_table;
+  // 16-byte loads (8 bf16) -> two float4 stores
+  for (int j8 = threadIdx.x; j8 < GRT_D / 8; j8 += blockDim.x) {
+    const uint4 u = ((const uint4*)((const unsigned short*)emb + erow))[j8];
+    float4 a, b;
+    a.x = __uint_as_float(u.x << 16); a.y = __uint_as_float(u.x & 0xFFFF0000u);
+    a.z = __uint_as_float(u.y << 16); a.w = __uint_as_float(u.y & 0xFFFF0000u);
+    b.x = __uint_as_float(u.z << 16); b.y = __uint_as_float(u.z & 0xFFFF0000u);
+    b.z = __uint_as_float(u.w << 16); b.w = __uint_as_float(u.w & 0xFFFF0000u);
+    ((float4*)x)[2 * j8] = a;
+    ((float4*)x)[2 * j8 + 1] = b;
+  }
+#else
+#if GRT_ARCH_REF
+  const long long prow = (long long)pos * GRT_D;
+#else
+  (void)pos_table;
+#endif
+  for (int j = threadIdx.x; j < GRT_D; j += blockDim.x) {
+#if GRT_WBF16
+    float e = grt_bf16_to_f32(((const unsigned short*)emb)[erow + j]);
+#if GRT_ARCH_REF
+    e = e + grt_bf16_to_f32(((const unsigned short*)pos_table)[prow + j]);
+#endif
+#else
+    float e = ((const float*)emb)[erow + j];
+#if GRT_ARCH_REF
+    e = e + ((const float*)pos_table)[prow + j];
+#endif
+#endif
+    x[j] = e;
+  }
+#endif
+  __syncthreads();
+  if (threadIdx.x == 0) ctrl->seq_len = pos + 1;
+}
+
 __device__ __forceinline__ void preprocess_impl(GrtCtrl* ctrl, const void* emb, const void* pos_table, float* x) {
   __shared__ int s_pos, s_tok, s_ok;
   if (threadIdx.x == 0) {
@@ -74,28 +116,7 @@ __device__ __forceinline__ void preprocess_impl(GrtCtrl* ctrl, const void* emb, 
   }
   __syncthreads();
   if (!s_ok) return;
-  const long long erow = (long long)s_tok * GRT_D;
-#if GRT_ARCH_REF
-  const long long prow = (long long)s_pos * GRT_D;
-#else
-  (void)pos_table;
-#endif
-  for (int j = threadIdx.x; j < GRT_D; j += blockDim.x) {
-#if GRT_WBF16
-    float e = grt_bf16_to_f32(((const unsigned short*)emb)[erow + j]);
-#if GRT_ARCH_REF
-    e = e + grt_bf16_to_f32(((const unsigned short*)pos_table)[prow + j]);
-#endif
-#else
-    float e = ((const float*)emb)[erow + j];
-#if GRT_ARCH_REF
-    e = e + ((const float*)pos_table)[prow + j];
-#endif
-#endif
-    x[j] = e;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) ctrl->seq_len = s_pos + 1;
+  gather_row(ctrl, s_pos, s_tok, emb, pos_table, x);
 }
 
 extern "C" __global__ void grt_preprocess(GrtCtrl* ctrl, const void* emb, const void* pos_table, float* x) {
@@ -240,14 +261,16 @@ __device__ void radix_pick(u64* hist, int shift, u64& prefix, u64& mask, u64& ne
   __syncthreads();
 }
 
-__device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) {
+// Returns the sampled token (block-uniform) or -1 on a prefill pass.  With
+// fence == false the caller issues the system fence for the host-mapped slots.
+__device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, bool fence = true) {
   __shared__ float redf[32];
   __shared__ u64 redu[32];
   __shared__ u64 hist[256];
   __shared__ int s_tok;
   __shared__ u64 s_t0;
   const int pos = ctrl->seq_len;
-  if (pos < ctrl->prompt_len) return;  // prefill pass: the token is given
+  if (pos < ctrl->prompt_len) return -1;  // prefill pass: the token is given
   const int step = pos - ctrl->prompt_len;
   if (threadIdx.x == 0) s_t0 = grt_globaltimer();
   const int kind = ctrl->sample_kind;
@@ -526,8 +549,9 @@ __device__ __forceinline__ void sample_impl(GrtCtrl* ctrl, const float* logits) 
       ctrl->out_stamps[2 * step] = s_t0;
       ctrl->out_stamps[2 * step + 1] = grt_globaltimer();
     }
-    __threadfence_system();
+    if (fence) __threadfence_system();
   }
+  return s_tok;
 }
 
 extern "C" __global__ void __launch_bounds__(GRT_SAMPLE_THREADS) grt_sample(GrtCtrl* ctrl, const float* logits) {
@@ -543,7 +567,14 @@ extern "C" __global__ void __launch_bounds__(GRT_SAMPLE_THREADS)
     grt_sample_preprocess(GrtCtrl* ctrl, const float* logits, const void* emb, const void* pos_table, float* x) {
   grt_launch_dependents();
   grt_griddep_wait();
-  sample_impl(ctrl, logits);
-  __syncthreads();  // the sampled token (tokens[seq_len], written by thread 0) is visible block-wide
-  preprocess_impl(ctrl, emb, pos_table, x);
+  const int pos = ctrl->seq_len;
+  const int tok = sample_impl(ctrl, logits, false);  // block-uniform
+  if (tok >= 0 && tok < GRT_V && pos < GRT_MAXSEQ) {
+    // the token is known here: no re-read of seq_len / tokens[pos]
+    gather_row(ctrl, pos, tok, emb, pos_table, x);
+  } else {
+    __syncthreads();  // tokens[seq_len] (given or sampled) visible block-wide
+    preprocess_impl(ctrl, emb, pos_table, x);
+  }
+  if (threadIdx.x == 0) __threadfence_system();  // host-mapped token + stamps
 }
