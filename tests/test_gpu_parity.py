@@ -303,6 +303,23 @@ def test_device_loop_temperature_and_eos(golden):
     assert r.tokens == want
 
 
+def test_device_loop_topp_paged_matches_hybrid():
+    """Seeded top-p (Philox draws indexed by step) through the device loop on a
+    paged KV cache: the same tokens as hybrid replay on a contiguous cache."""
+    kw = dict(arch=g.ARCH_LLAMA, n_layers=2, d_model=128, n_heads=2, vocab_size=512, max_seq_len=256, d_ff_=320,
+              weight_dtype=g.BF16, kv_dtype=g.BF16, init=g.INIT_PHILOX, seed=5)
+    prompt = po.make_prompt(42, 20, 512)
+    strat = g.SampleStrategy.top_kp(0.8, 0, 0.9)
+    a = g.Session(g.ModelConfig(**kw), cache(bucket=32, hi=0, batched_prefill=True)).run(
+        g.GenerationRequest(mode=g.RunMode.Hybrid, prompt=prompt, gen_len=48, strategy=strat, sampler_seed=11))
+    m = g.Model(g.ModelConfig(kv_page_size=16, **kw))
+    m.set_kv_block_table(list(reversed(range(m.kv_pages()[1]))))
+    b = g.Session(m, cache(bucket=32, hi=0, batched_prefill=True)).run(
+        g.GenerationRequest(mode=g.RunMode.DeviceLoop, prompt=prompt, gen_len=48, strategy=strat, sampler_seed=11))
+    assert a.tokens == b.tokens
+    assert b.counters.kernel_launches > 0 or b.counters.graph_replays == 1  # one launch for the decode
+
+
 def test_device_loop_llama_7b_dims_matches_hybrid():
     """2-layer LLaMA at 7B dims (bf16, fused GEMV pairs, cluster attention): the
     device loop crosses three 16-position buckets and matches hybrid replay."""
