@@ -53,6 +53,7 @@ __device__ __forceinline__ float group_sum(float v, int gs) {
 constexpr int ATTN_UNROLL = 8;
 constexpr int ATTN_WARPS = ATTN_THREADS / 32;
 constexpr int ATTN_MAX_CLUSTER = 16;
+constexpr size_t ATTN_STAGE_SMEM = 192 * 1024;  // dynamic smem for staged rounds (3 x 64 KB at dh 128)
 __host__ __device__ constexpr int attn_pass_span(int dh) { return ATTN_WARPS * ATTN_UNROLL * (32 / (dh / 4)); }
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -126,6 +127,38 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
       vv[u] = load4<KT>(V + row[u]);
     }
   }
+  // Rounds 1.. (bf16, contiguous cache): their rows are staged into shared
+  // memory by the TMA engine before the wait as well (p.smem_rounds of them).
+  extern __shared__ __align__(128) uint8_t att_dyn[];  // [round-1][K|V][pass][dh] bf16
+  __shared__ uint64_t rbar;
+  const bool stage = pre && p.smem_rounds > 0 && p.kvp.page == 0 && sizeof(KT) == 2;
+  const size_t rstride = static_cast<size_t>(pass) * dh * sizeof(KT);  // bytes of one K (or V) round
+  if (stage) {
+    if (threadIdx.x == 0) {
+      mbar_init(&rbar, 1);
+      mbar_fence_init();
+      uint32_t total = 0;
+      for (int r = 1; r <= p.smem_rounds; ++r) {
+        const int j0 = rank * span + r * pass;
+        const int nr = max(0, min(pass, p.max_seq - j0));
+        total += 2u * static_cast<uint32_t>(nr) * dh * sizeof(KT);
+      }
+      mbar_arrive_expect_tx(&rbar, total);
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      for (int r = 1; r <= p.smem_rounds; ++r) {
+        const int j0 = rank * span + r * pass;
+        const int nr = max(0, min(pass, p.max_seq - j0));
+        if (nr == 0) continue;
+        const uint32_t bytes = static_cast<uint32_t>(nr) * dh * sizeof(KT);
+        const int64_t off = (static_cast<int64_t>(head) * p.max_seq + j0) * dh;
+        uint8_t* dst = att_dyn + static_cast<size_t>(r - 1) * 2 * rstride;
+        bulk_g2s(dst, reinterpret_cast<const KT*>(p.k_cache) + off, bytes, &rbar, pol);
+        bulk_g2s(dst + rstride, reinterpret_cast<const KT*>(p.v_cache) + off, bytes, &rbar, pol);
+      }
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+  }
   griddep_wait();
   op_stamp(p.trace, 1);
   if (p.trigger == 0) griddep_launch_dependents();
@@ -138,9 +171,19 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
     const int jw = rank * span + r * pass + warp * ATTN_UNROLL * RPW;  // first position of this warp
     int64_t row[ATTN_UNROLL];
     rows_of(jw, row);
+    const bool from_smem = stage && r >= 1 && r <= p.smem_rounds;
+    if (from_smem && r == 1) mbar_wait(&rbar, 0);
 #pragma unroll
     for (int u = 0; u < ATTN_UNROLL; ++u) {
-      if (r == 0 && pre && jw + u * RPW + g != len - 1) continue;  // requested before the wait
+      const int jp = jw + u * RPW + g;
+      if (r == 0 && pre && jp != len - 1) continue;  // requested before the wait
+      if (from_smem && jp != len - 1 && jp < p.max_seq) {  // staged before the wait
+        const int rr = jp - (rank * span + r * pass);
+        const uint8_t* bk = att_dyn + static_cast<size_t>(r - 1) * 2 * rstride;
+        kv[u] = load4<KT>(reinterpret_cast<const KT*>(bk) + rr * dh + 4 * c);
+        vv[u] = load4<KT>(reinterpret_cast<const KT*>(bk + rstride) + rr * dh + 4 * c);
+        continue;
+      }
       kv[u] = load4<KT>(K + row[u]);
       vv[u] = load4<KT>(V + row[u]);
     }
@@ -322,10 +365,17 @@ cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s,
     return e ? atoi(e) : 1;
   }();
   p.prefetch = pref;
+  static const int stage_max = [] {  // rounds >= 1 staged through shared memory before the wait
+    const char* e = getenv("GRT_ATTN_STAGE");
+    return e ? std::max(0, atoi(e)) : 3;
+  }();
+  const size_t rbytes = static_cast<size_t>(attn_pass_span(p.head_dim)) * p.head_dim * 2 * 2;  // K+V of a round
+  p.smem_rounds = (kvdt == Dt::BF16 && p.kvp.page == 0 && pref) ? std::min(rounds - 1, stage_max) : 0;
+  while (p.smem_rounds > 0 && static_cast<size_t>(p.smem_rounds) * rbytes > ATTN_STAGE_SMEM) --p.smem_rounds;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_heads * ns);
   cfg.blockDim = dim3(ATTN_THREADS);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = static_cast<size_t>(p.smem_rounds) * rbytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -344,6 +394,8 @@ cudaError_t attention_prepare() {
   for (const void* f : {reinterpret_cast<const void*>(attn_decode_kernel<__nv_bfloat16>),
                         reinterpret_cast<const void*>(attn_decode_kernel<float>)}) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ATTN_STAGE_SMEM));
     if (e != cudaSuccess) return e;
     // same L1/shared carveout as the GEMVs, so the next GEMV's CTAs can become
     // resident next to attention CTAs (PDL) without an SM reconfiguration

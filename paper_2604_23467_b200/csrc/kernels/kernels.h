@@ -86,6 +86,7 @@ struct AttnParams {
   KvPaging kvp;
   int trigger = 0;               // when the successor may launch: 0 start, 1 after KV loads, 2 at exit
   int prefetch = 0;              // round 0's rows of earlier steps loaded before the dependency wait
+  int smem_rounds = 0;           // rounds 1..smem_rounds staged into shared memory before the wait (launcher)
 };
 // Per-op trace stamps (8 slots per CTA): 0 CTA start, 1 dependency released
 // (griddepcontrol.wait), 2 operands ready (activation loaded / KV rows loaded),
