@@ -131,30 +131,93 @@ class ClockSampler:
                 "mem_mhz": self.mem[0] if self.mem else None, "mem_max_mhz": self.mem[1] if self.mem else None}
 
 
-def cpu_reference_sample(timeout=600):
+def cpu_reference_sample(layers=(1, 2), gen=4, warmup=1, timeout=600):
     """Times the UNMODIFIED reference CPU path (oracle/_ref/refdump = graphrt core
-    built from the reference sources) at 7B dims in its own architecture
-    (GPT-style, fp32, d_ff 16384; LLaMA is not expressible there).
-    Bounded sample: 1- and 2-layer models, 3 timed decode passes each; per-token
-    time at 32 layers is extrapolated linearly (t1 + 31*(t2-t1)); matmul is
-    99.9% of the path, so the layer term is linear."""
+    built from the reference sources, its own step_math, model.cpp:168-183) at 7B
+    dims in its own architecture (GPT-style, fp32, d_ff 16384; LLaMA is not
+    expressible there).  The reference is single-threaded (1 core).
+
+    layers=(32,): the full-depth model is timed directly (init_model's serial
+    mt19937 stream takes ~80 s, then 2 prompt tokens and `gen` step_math passes;
+    the first `warmup` passes are untimed).  layers=(1, 2): a bounded ~10 s
+    sample, extrapolated linearly to 32 layers (t1 + 31*(t2-t1); matmul is 99.9%
+    of the pass, so the layer term is linear)."""
     exe = os.path.join(ROOT, "oracle", "_ref", "refdump")
     if not os.path.exists(exe):
         return None
     res = {}
-    for L in (1, 2):
+    t_wall = time.time()
+    for L in layers:
         cmd = [exe, "--layers", str(L), "--d", "4096", "--heads", "32", "--vocab", "32000", "--max-seq", "640",
-               "--prompt-len", "2", "--gen", "4", "--time", "--dump-logits", "0"]
+               "--prompt-len", "2", "--gen", str(gen), "--time", "--dump-logits", "0"]
         out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, check=True)
         d = json.loads(out.stdout)
-        res[L] = (statistics.median(d["pass_ms"]), d["prefill_ms"] / 2.0)
+        timed = d["pass_ms"][warmup:] or d["pass_ms"]
+        res[L] = (percentile(timed, 50), len(timed), d["init_ms"])
+    base = {"unit": "ms/token", "cores": 1, "kind": "reference", "cpu": cpu_model(), "nproc": os.cpu_count()}
+    if len(layers) == 1:
+        L = layers[0]
+        t, n, init_ms = res[L]
+        return dict(base, value=t, steps_timed=n,
+                    sample=f"graphrt core (reference sources, -O2, 1 thread) at 7B dims (d4096 h32 V32000 L{L}, ref "
+                           f"arch fp32), prompt 2 tokens, {warmup} untimed + {n} timed step_math passes, p50; "
+                           f"init_model {init_ms / 1000:.1f} s", wall_s=round(time.time() - t_wall, 1))
     t1, t2 = res[1][0], res[2][0]
-    per_token_ms = t1 + 31.0 * (t2 - t1)
-    return {"value": per_token_ms, "unit": "ms/token", "cores": 1, "kind": "reference",
-            "sample": "graphrt core (reference sources, -O2, 1 thread) at 7B dims (d4096 h32 V32000, ref arch "
-                      "fp32), 1- and 2-layer models x 4 timed step_math passes, extrapolated to 32 layers: "
-                      f"t1={t1:.1f} ms, t2={t2:.1f} ms",
-            "cpu": cpu_model()}
+    return dict(base, value=t1 + 31.0 * (t2 - t1), steps_timed=res[1][1],
+                sample="graphrt core (reference sources, -O2, 1 thread) at 7B dims (d4096 h32 V32000, ref arch "
+                       f"fp32), 1- and 2-layer models x {res[1][1]} timed step_math passes, extrapolated to 32 "
+                       f"layers: t1={t1:.1f} ms, t2={t2:.1f} ms", wall_s=round(time.time() - t_wall, 1))
+
+
+def parity_leg(sess, prompt, run_tokens, layers, n_steps=2, timeout=1200):
+    """Parity stamp of the benched configuration (VERDICT r01 #1c): the C oracle
+    (oracle/trajectory.py, in its OWN process so the checker is never mapped into
+    the measured one) walks the benched prompt and the timed run's first n_steps
+    greedy tokens at full depth; the GPU side is the benched session's step API
+    (batched prefill, then the same plan kernels the graphs replay).  Reports
+    max-abs over the n_steps+1 logit vectors, the timed run's token agreement
+    (margin-aware, tolerance 2e-2), and the oracle's all-core time per token --
+    the LLaMA CPU baseline on this host."""
+    import tempfile
+
+    import numpy as np
+    toks = [int(t) for t in run_tokens[:n_steps]]
+    sess.reset()
+    sess.prefill(prompt)
+    gpu = [sess.logits()]
+    for t in toks:
+        sess.step(t)
+        gpu.append(sess.logits())
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "traj.npz")
+        cmd = [sys.executable, os.path.join(ROOT, "oracle", "trajectory.py"), out, "--layers", str(layers),
+               "--max-seq", str(max(64, len(prompt) + n_steps + 1)), "--prompt", ",".join(map(str, prompt)),
+               "--tokens", ",".join(map(str, toks))]
+        t0 = time.time()
+        subprocess.run(cmd, check=True, timeout=timeout, capture_output=True, text=True)
+        wall = time.time() - t0
+        d = np.load(out)
+        ref, step_s, init_s, threads = d["logits"], d["step_s"], float(d["init_s"]), int(d["threads"])
+    tol = 2e-2
+    max_abs = max(float(np.abs(a - b).max()) for a, b in zip(gpu, ref))
+    agree, checked = 0, 0
+    for i in range(min(len(run_tokens), len(ref))):
+        want = int(np.argmax(ref[i]))
+        top2 = np.sort(ref[i].astype(np.float64))[-2:]
+        checked += 1
+        agree += int(run_tokens[i]) == want or (top2[1] - top2[0]) <= tol
+    par = {"oracle": "oracle/oracle.c (C restatement of model.cpp:168-183 step_math, LLaMA extension; bf16 "
+                     "weights + KV, fp32 activations; pinned bit-exact to the reference library)",
+           "n_layers": layers, "positions_compared": len(gpu), "max_abs_logit": float(f"{max_abs:.3e}"), "tol": tol,
+           "ok": bool(max_abs <= tol and agree == checked),
+           "timed_run_tokens_agree": f"{agree}/{checked}", "oracle_wall_s": round(wall, 1)}
+    port = {"value": round(float(np.median(step_s)) * 1000.0, 1), "unit": "ms/token", "cores": threads,
+            "kind": "port",
+            "sample": f"oracle.c LLaMA-2 7B ({layers} layers, bf16 weights, fp32 math, OpenMP over output columns) "
+                      f"on {threads} host threads: {len(step_s)} decode steps after the P={len(prompt)} prefill "
+                      f"(weights init {init_s:.1f} s untimed), median",
+            "cpu": cpu_model(), "nproc": os.cpu_count()}
+    return par, port
 
 
 def cpu_model():
@@ -165,6 +228,57 @@ def cpu_model():
     except Exception:
         pass
     return None
+
+
+def sweep_leg(model, cc, plens, modes, gen, trials, max_seq, dist):
+    """bench.cpp:51-138 through the product's restatement (bench_harness.run_bench):
+    per (mode, P) cell a fresh Session on the shared weights, 1 warm + `trials`
+    kept requests of `gen` decode steps; per-token p50/p99 pooled over the kept
+    trials (nearest rank), TTFT mean/p99 over trials."""
+    from paper_2604_23467_b200 import bench_harness as bh
+    out = {}
+    for mode in modes:
+        for pl in plens:
+            gl = min(gen, max_seq - pl)
+            cfg = bh.BenchConfig(model=model.cfg, cache=cc, modes=[mode], prompt_lens=[pl], gen_lens=[gl],
+                                 trials=trials)
+            res = bh.run_bench(cfg, model=model)
+            sm = res.summaries[0]
+            kept = [rw for rw in res.rows if rw.trial >= 0]
+            key = str(pl) if len(modes) == 1 else g_mode_name(mode)
+            out[key] = {"prompt": pl, "gen": gl, "mode": g_mode_name(mode), "kept_trials": sm.kept_trials,
+                        "ttft_mean_ms": round(reduce_max(dist, sm.ttft_mean_us / 1000), 3),
+                        "ttft_p99_ms": round(reduce_max(dist, sm.ttft_p99_us / 1000), 3),
+                        "p50_ms": round(reduce_max(dist, sm.tok_p50_us / 1000), 4),
+                        "p99_ms": round(reduce_max(dist, sm.tok_p99_us / 1000), 4),
+                        "mean_ms": round(reduce_max(dist, sm.tok_mean_us / 1000), 4),
+                        "graph_replays_per_request": sm.replays_mean,
+                        "dispatches_per_request": sum(rw.dispatches for rw in kept) / len(kept)}
+    return out
+
+
+def g_mode_name(m):
+    from paper_2604_23467_b200 import graphrt as g
+    return g.mode_name(m)
+
+
+def cold_leg(model, cc, prompt, dist, gen=64):
+    """Cold graph cache (no warm-up): hybrid captures new buckets asynchronously on
+    the side stream while the eager path serves; ablate_async captures inline on
+    the submitting thread; eager never captures (PAPER.md:522-528 ablations)."""
+    from dataclasses import replace
+
+    from paper_2604_23467_b200 import graphrt as g
+    out = {}
+    for m in (g.RunMode.Hybrid, g.RunMode.AblateAsync, g.RunMode.Eager):
+        s2 = g.Session(model, replace(cc, warmup_hi=0))
+        r = s2.run(g.GenerationRequest(mode=m, prompt=prompt, gen_len=gen))
+        out[g.mode_name(m)] = {"ttft_ms": round(reduce_max(dist, r.ttft_us / 1000), 3),
+                               "total_ms": round(reduce_max(dist, r.total_us / 1000), 3),
+                               "mean_ms": round(reduce_max(dist, sum(r.per_token_us) / len(r.per_token_us) / 1000), 4),
+                               "captures": r.captures_completed}
+        s2.close()
+    return out
 
 
 def mixed_leg(g, model, cc, n_req, dist):
@@ -273,21 +387,30 @@ def reduce_max(dist, v):
 
 
 def run_reference(args):
+    """The reference arm: the unmodified reference CPU path timed on this host,
+    full depth (32 layers at 7B dims, its own architecture) -- W untimed + K
+    timed step_math passes, as the contract's steps/warmup say; rank 0 only."""
     rank, world, local, dist = dist_setup(args.gpus)
     if rank != 0:
         return 0
     t0 = time.time()
-    cb = cpu_reference_sample()
+    L = args.ref_layers
+    try:
+        cb = cpu_reference_sample(layers=(L,), gen=args.warmup + args.steps, warmup=args.warmup, timeout=3600)
+    except Exception as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference run failed: {type(e).__name__}: {e}"[:300]}))
+        return 0
     if cb is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/refdump not built (needs /root/reference at build time)"}))
         return 0
-    line = {"metric": METRIC, "value": cb["value"], "unit": "ms/token", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": cb["value"], "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference init_model U[-0.1,0.1])",
+    line = {"metric": METRIC, "value": cb["value"], "unit": "ms/token", "n_gpus": args.gpus,
+            "steps": cb["steps_timed"], "warmup": args.warmup, "ms_per_step": cb["value"], "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference init_model U[-0.1,0.1])",
             "impl": "reference",
-            "config": {"workload": "reference graphrt CPU decode at LLaMA-2-7B dims (ref arch: LN, learned pos, "
-                                   "ReLU, d_ff 16384), bs1", "global_batch": 1, "parallelism": "1 CPU thread"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": {"workload": f"reference graphrt CPU decode at LLaMA-2-7B dims ({L} layers; ref arch: LN, learned "
+                                   "pos, ReLU, d_ff 16384), bs1, p50 ms/token", "global_batch": 1,
+                       "parallelism": "1 CPU thread (the reference is single-threaded)", "n_layers": L},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu", "nproc")},
             "e2e": {"value": cb["value"], "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": round(time.time() - t0, 1)}
     print(json.dumps(line))
@@ -308,10 +431,17 @@ def main():
                     help="N>1: tensor-parallel decode over the N GPUs (NCCL in-graph) or N independent replicas")
     ap.add_argument("--batched-prefill", type=int, default=1, help="1: tcgen05 batched prefill (TTFT path); 0: token-by-token")
     ap.add_argument("--pass-impl", type=int, default=1, help="1 per-op kernel graph (default), 0 persistent single-kernel pass")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true",
+                    help="skip the CPU legs (LLaMA port + parity stamp, reference sample)")
+    ap.add_argument("--ref-layers", type=int, default=32, help="--impl reference: layers of the timed reference model")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--sweep", default="10,50,100,200,500",
                     help="comma list of prompt lengths for the TTFT sweep (BASELINE configs[2]; '' = off)")
+    ap.add_argument("--trials", type=int, default=10,
+                    help="kept trials per sweep cell (bench.cpp default 100; 1 warm trial runs first)")
+    ap.add_argument("--modes", default="hybrid,eager,ablate_fused,device_loop",
+                    help="configs[1] leg: run modes compared at the bench prompt ('' = off)")
+    ap.add_argument("--mode-trials", type=int, default=3)
     ap.add_argument("--mixed", type=int, default=6,
                     help="requests of the cold-cache top-p / mixed-prompt-length leg (configs[3]; 0 = off)")
     ap.add_argument("--ipc", type=int, default=1, help="1: also time the two-process (cudaIpc) split (N=1 only)")
@@ -324,7 +454,7 @@ def main():
     rank, world, local, dist = dist_setup(args.gpus)
     import torch  # noqa: F401  (device plumbing / distributed only)
     from paper_2604_23467_b200 import graphrt as g
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from paper_2604_23467_b200.bench_harness import make_prompt
 
     W, K, P = args.warmup, args.steps, args.prompt_len
     n = W + K
@@ -354,12 +484,7 @@ def main():
         parallel = "single" if world == 1 else f"{world} replicas"
     init_s = time.time() - t_init
     model = sess.model
-    prompt = [(i * 7919 + 17) % 32000 for i in range(P)]
-    try:
-        import pyoracle as po
-        prompt = po.make_prompt(42, P, 32000)  # bench.cpp:34-39 (checker lib, not on the measured path)
-    except Exception:
-        pass
+    prompt = make_prompt(42, P, 32000)  # bench.cpp:34-39 (product restatement, bench_harness)
     mode = g.mode_from_name(args.mode)
     req = g.GenerationRequest(mode=mode, prompt=prompt, gen_len=n)
     sess.run(req)  # warm the whole path once (graphs already pre-captured)
@@ -411,14 +536,22 @@ def main():
         kernels = {k: {"launches_per_step": v[2], "ms_per_step_isolated": round(v[0], 4),
                        "gbs": round(v[1] / (v[0] * 1e-3) / 1e9, 1) if v[0] > 0 else None} for k, v in agg.items()}
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # parity stamp + the LLaMA port on all host cores (same model, same prompt)
         try:
-            cb = cpu_reference_sample()
-            if cb:
-                cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            parity, cpu = parity_leg(sess, prompt, r.tokens, args.layers)
+        except Exception as e:  # reported, never silent
+            parity = {"error": f"{type(e).__name__}: {e}"[:400]}
+        try:  # the reference library itself (1 thread, its own architecture): bounded ~10 s sample
+            ref = cpu_reference_sample()
+            if ref and cpu is not None:
+                cpu["reference_1thread"] = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            elif ref:
+                cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu", "nproc")}
         except Exception as e:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": "ms/token", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+            if cpu is None:
+                cpu = {"value": None, "unit": "ms/token", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
     steps_total = n
     line = {
@@ -437,7 +570,7 @@ def main():
         "p99_over_p50": round(p99 / p50, 4), "decode_bytes_per_token": bytes_tok,
         "decode_hbm_gbs": round(hbm_gbs, 1), "decode_hbm_frac": round(hbm_gbs / peak, 4),
         "decode_hbm_gbs_all_ranks": round(hbm_gbs * (world if parallel.startswith("tp") else 1), 1),
-        "roofline": roofline, "cpu_baseline": cpu,
+        "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
         "e2e": {"value": round(e2e_p50, 4), "unit": "ms/token", "h2d_bytes_per_step": round((4 * P + 128) / n, 2),
                 "d2h_bytes_per_step": 4 + 16},
         "gpu_launches": int(round((r.counters.graph_kernel_nodes + r.counters.kernel_launches) * K / n)),
@@ -446,16 +579,13 @@ def main():
         "prefill": "batched tcgen05 (one pass over the prompt)" if args.batched_prefill else "token-by-token graphs",
         "clocks": clk.summary(), "kernels": kernels, "tp_error": tp_error, "init_s": round(init_s, 1), "run_wall_s": round(wall, 3),
     }
-    if args.sweep:  # every rank runs it (TP collectives), rank 0 reports
-        sw = {}
-        for pl in [int(x) for x in args.sweep.split(",") if x]:
-            pr = po.make_prompt(42, pl, 32000)
-            rr = sess.run(g.GenerationRequest(mode=mode, prompt=pr, gen_len=min(128, max_seq - pl)))
-            gg = rr.per_token_us[3:]
-            sw[str(pl)] = {"ttft_ms": round(reduce_max(dist, rr.ttft_us / 1000), 3),
-                           "p50_ms": round(reduce_max(dist, percentile(gg, 50) / 1000), 4),
-                           "p99_ms": round(reduce_max(dist, percentile(gg, 99) / 1000), 4)}
-        line["ttft_sweep"] = sw
+    if args.sweep:  # configs[2]; every rank runs it (TP collectives), rank 0 reports
+        line["ttft_sweep"] = sweep_leg(sess.model, cc, [int(x) for x in args.sweep.split(",") if x],
+                                       [g.RunMode.Hybrid], 128, args.trials, max_seq, dist)
+    if args.modes:  # configs[1]: graph replay vs eager launch, and the paper's ablations
+        line["modes"] = sweep_leg(sess.model, cc, [P], [g.mode_from_name(m) for m in args.modes.split(",") if m],
+                                  128, args.mode_trials, max_seq, dist)
+        line["cold_cache"] = cold_leg(sess.model, cc, prompt, dist)
     if args.mixed > 0:
         line["topp_mixed"] = mixed_leg(g, sess.model, cc, args.mixed, dist)
     if args.ipc and world == 1 and rank == 0:

@@ -254,6 +254,40 @@ grt_status grt_get_kv_row(grt_session* s, int32_t layer, int32_t slot, int32_t r
 grt_status grt_sample(grt_session* s, const grt_sample_params* p, int32_t* token); /* make_sample_op */
 grt_status grt_sampler_reset(grt_session* s, uint64_t seed);        /* SamplerRng::reset */
 
+/* ---- explicit capture (replaces graphrt::CaptureEngine::begin_capture /
+ * CaptureSession::record / end_capture and validate_replay,
+ * exec_graph.hpp:73-141, exec_graph.cpp:49-103).  A capture is Open until
+ * end_capture (Closed) or the first violation (Aborted: nothing kept, the key
+ * released).  Errors: CaptureInProgress (key already open), CaptureViolation
+ * (a host-valued op, or a dynamic op into a static-only graph), ForeignBuffer
+ * (a binding outside the model arena), EmptyCapture, SessionClosed (use after
+ * close/abort).  The graph lands in the session's cache under the step key. */
+typedef struct grt_capture grt_capture;
+typedef enum grt_capture_state { GRT_CAPTURE_OPEN = 0, GRT_CAPTURE_CLOSED = 1, GRT_CAPTURE_ABORTED = 2 } grt_capture_state;
+typedef enum grt_capture_op {
+  GRT_OP_PLAN = 0,              /* plan(plan_key)[index]: a static kernel */
+  GRT_OP_SAMPLE_PREPROCESS = 1, /* the fused dynamic block (NVRTC sampler + extend_position + slot append) */
+  GRT_OP_PREPROCESS = 2,        /* extend_position + slot append alone (NVRTC) */
+  GRT_OP_HOST_TOKEN = 3         /* the step API's host->device token upload (needs a host value) */
+} grt_capture_op;
+/* fused != 0: a hybrid step graph (dynamic device ops allowed); 0: static-only */
+grt_status grt_capture_begin(grt_session* s, int32_t key, int32_t fused, grt_capture** out);
+grt_status grt_capture_record(grt_capture* c, int32_t op, int32_t plan_key, int32_t index);
+/* records an op that binds caller memory [ptr, ptr+bytes) (a device memset) */
+grt_status grt_capture_record_external(grt_capture* c, void* ptr, uint64_t bytes);
+grt_status grt_capture_end(grt_capture* c, int32_t* kernel_count, uint64_t* epoch);
+grt_status grt_capture_state_get(grt_capture* c, int32_t* state, int32_t* recorded);
+void grt_capture_destroy(grt_capture* c);
+/* number of static kernels in plan(key) (Model::plan, model.cpp:118-154) */
+grt_status grt_plan_size(grt_session* s, int32_t key, int32_t* n);
+/* One step through the cached graph of `key` with `token` at position cur_len.
+ * validate != 0: validate_replay first (host WrongLength unless key_of(cur_len+1)
+ * == key); validate == 0: launch anyway -- a live length beyond the bucket trips
+ * the device-side check (WrongLength). */
+grt_status grt_session_replay(grt_session* s, int32_t key, int32_t fused, int32_t token, int32_t validate);
+/* arena of the model: bytes reserved, bytes used, sub-allocations (never grows per capture) */
+grt_status grt_model_arena_info(grt_model* m, uint64_t* capacity, uint64_t* used, uint64_t* allocations);
+
 /* ---- graph cache policy (replaces graphrt::GraphCache, graph_cache.hpp:29-81) ---
  * The session owns its own cache of cudaGraphExec_t; this standalone handle runs
  * the identical policy code on placeholder graphs (no GPU), for policy tests. */
@@ -325,7 +359,8 @@ grt_status grt_ipc_client_destroy(grt_ipc_client* c);
 /* out[n] = W[n,k] . x[k] with W in the device ([n,k], row-major) layout. */
 grt_status grt_op_gemv(const void* w, int32_t w_dtype, const float* x, float* out, int32_t n, int32_t k,
                        void* stream);
-/* Single-query attention over positions [0,len) of K/V laid out [h, max_seq, dh]. */
+/* Single-query attention over positions [0,len) of K/V laid out [h, max_seq, dh].
+ * q, k, v and out must be 16-byte aligned (vector loads; else GRT_InvalidConfig). */
 grt_status grt_op_attention(const float* q, const void* k, const void* v, int32_t kv_dtype, float* out,
                             int32_t n_heads, int32_t head_dim, int32_t max_seq, int32_t len, float scale,
                             void* stream);
@@ -334,7 +369,8 @@ grt_status grt_op_attention(const float* q, const void* k, const void* v, int32_
  * k % 64 == 0, n_tok <= 512); out fp32 [n_tok, m_rows]. */
 grt_status grt_op_prefill_gemm(const void* w, const void* x, float* out, int32_t m_rows, int32_t k, int32_t n_tok,
                                void* stream);
-/* Samples from device logits; writes the token to *token_dev (device int32). */
+/* Samples from device logits (16-byte aligned, else GRT_InvalidConfig); writes
+ * the token to *token_dev (device int32). */
 grt_status grt_op_sample(const float* logits, int32_t vocab, const grt_sample_params* p, uint64_t step,
                          double uniform, int32_t* token_dev, void* stream);
 

@@ -147,13 +147,13 @@ def mode_name(m: g.RunMode) -> str:
     return g.mode_name(m)
 
 
-def run_bench(cfg: BenchConfig, progress: Optional[TextIO] = None) -> BenchResult:
-    """bench.cpp:51-138.  The weights are built once; every cell gets a fresh
-    Session (its own graph cache), as the reference builds a Session per cell."""
+def run_bench(cfg: BenchConfig, progress: Optional[TextIO] = None, model: Optional[g.Model] = None) -> BenchResult:
+    """bench.cpp:51-138.  The weights are built once (or `model` is reused, its
+    config must be cfg.model's); every cell gets a fresh Session (its own graph
+    cache), as the reference builds a Session per cell."""
     if cfg.trials < 1:
         raise g.Error(g.Errc.InvalidConfig, "bench trials must be >= 1")
     out = BenchResult()
-    model = None
     for mode in cfg.modes:
         for p in cfg.prompt_lens:
             for gl in cfg.gen_lens:

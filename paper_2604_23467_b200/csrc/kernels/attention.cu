@@ -370,7 +370,9 @@ cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s,
     return e ? std::max(0, atoi(e)) : 3;
   }();
   const size_t rbytes = static_cast<size_t>(attn_pass_span(p.head_dim)) * p.head_dim * 2 * 2;  // K+V of a round
-  p.smem_rounds = (kvdt == Dt::BF16 && p.kvp.page == 0 && pref) ? std::min(rounds - 1, stage_max) : 0;
+  // bulk copies need 16-byte aligned sources and sizes: rows of dh bf16 with dh % 8 == 0
+  p.smem_rounds = (kvdt == Dt::BF16 && p.kvp.page == 0 && pref && p.head_dim % 8 == 0)
+                      ? std::min(rounds - 1, stage_max) : 0;
   while (p.smem_rounds > 0 && static_cast<size_t>(p.smem_rounds) * rbytes > ATTN_STAGE_SMEM) --p.smem_rounds;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_heads * ns);

@@ -16,6 +16,12 @@ struct grt_session {
   grt_model* owner;
   std::unique_ptr<grt::Session> s;
 };
+struct grt_capture {
+  grt_session* owner;
+  bool fused;
+  std::unique_ptr<grt::CaptureSession> cs;
+  std::vector<std::unique_ptr<grt::KernelInvocation>> external;  // caller-bound ops (kept alive)
+};
 
 namespace {
 thread_local std::string g_last_error;
@@ -345,6 +351,71 @@ grt_status grt_cache_stats_get(grt_session* s, grt_cache_stats* st, uint64_t* si
   });
 }
 
+grt_status grt_capture_begin(grt_session* s, int32_t key, int32_t fused, grt_capture** out) {
+  return guard([&] {
+    auto c = std::make_unique<grt_capture>();
+    c->owner = s;
+    c->fused = fused != 0;
+    c->cs = s->s->begin_capture(key, c->fused);
+    *out = c.release();
+  });
+}
+
+grt_status grt_capture_record(grt_capture* c, int32_t op, int32_t plan_key, int32_t index) {
+  return guard([&] {
+    const grt::KernelInvocation* k = c->owner->s->capture_op(op, plan_key, index);
+    c->cs->record(k);
+  });
+}
+
+grt_status grt_capture_record_external(grt_capture* c, void* ptr, uint64_t bytes) {
+  return guard([&] {
+    auto k = std::make_unique<grt::KernelInvocation>();
+    k->spec.name = "external_memset";
+    k->bindings = {{ptr, static_cast<size_t>(bytes)}};
+    k->launch = [ptr, bytes](cudaStream_t st) { return cudaMemsetAsync(ptr, 0, bytes, st); };
+    c->cs->record(k.get());
+    c->external.push_back(std::move(k));
+  });
+}
+
+grt_status grt_capture_end(grt_capture* c, int32_t* kernel_count, uint64_t* epoch) {
+  return guard([&] {
+    grt::ExecGraphPtr g = c->owner->s->end_capture(*c->cs, c->fused);
+    if (kernel_count) *kernel_count = static_cast<int32_t>(g->kernel_count());
+    if (epoch) *epoch = g->capture_epoch();
+  });
+}
+
+grt_status grt_capture_state_get(grt_capture* c, int32_t* state, int32_t* recorded) {
+  return guard([&] {
+    if (state) *state = static_cast<int32_t>(c->cs->state());
+    if (recorded) *recorded = static_cast<int32_t>(c->cs->recorded());
+  });
+}
+
+void grt_capture_destroy(grt_capture* c) { delete c; }
+
+grt_status grt_plan_size(grt_session* s, int32_t key, int32_t* n) {
+  return guard([&] {
+    const grt::CacheConfig& cc = s->s->cache_config();
+    *n = static_cast<int32_t>(s->owner->m->plan(key, cc.bucket_size, cc.pass_impl).size());
+  });
+}
+
+grt_status grt_session_replay(grt_session* s, int32_t key, int32_t fused, int32_t token, int32_t validate) {
+  return guard([&] { s->s->replay(key, fused != 0, token, validate != 0); });
+}
+
+grt_status grt_model_arena_info(grt_model* m, uint64_t* capacity, uint64_t* used, uint64_t* allocations) {
+  return guard([&] {
+    const grt::Arena& a = m->m->arena();
+    if (capacity) *capacity = a.capacity();
+    if (used) *used = a.used();
+    if (allocations) *allocations = a.allocations();
+  });
+}
+
 grt_status grt_session_counters(grt_session* s, grt_counters* c) {
   return guard([&] { *c = s->s->device().counters(); });
 }
@@ -495,6 +566,10 @@ grt_status grt_op_prefill_gemm(const void* w, const void* x, float* out, int32_t
 grt_status grt_op_attention(const float* q, const void* k, const void* v, int32_t kv_dtype, float* out, int32_t n_heads,
                             int32_t head_dim, int32_t max_seq, int32_t len, float scale, void* stream) {
   return guard([&] {
+    // the kernel loads q and the K/V rows with 16-byte vector loads
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+         reinterpret_cast<uintptr_t>(out)) & 15)
+      grt::raise(GRT_InvalidConfig, "op_attention: q, k, v and out must be 16-byte aligned");
     int dev = 0;
     grt::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     grt::cuda_check(grt::attention_prepare(), "attention_prepare");
@@ -519,6 +594,8 @@ grt_status grt_op_sample(const float* logits, int32_t vocab, const grt_sample_pa
                          int32_t* token_dev, void* stream) {
   return guard([&] {
     if (!p || vocab < 1 || step > (1u << 20)) grt::raise(GRT_InvalidConfig, "grt_op_sample: bad arguments");
+    if (reinterpret_cast<uintptr_t>(logits) & 15)  // float4 loads of the logits
+      grt::raise(GRT_InvalidConfig, "grt_op_sample: logits must be 16-byte aligned");
     int dev = 0;
     grt::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     auto jit = grt::jit_get({"-DGRT_D=8", "-DGRT_V=" + std::to_string(vocab), "-DGRT_MAXSEQ=1", "-DGRT_WBF16=0",

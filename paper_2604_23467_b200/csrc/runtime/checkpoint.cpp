@@ -17,6 +17,7 @@
 // layouts are rotate-half (HF's convention, the one the oracle and the
 // kernels use), so q_proj/k_proj need no permutation beyond the arena's own
 // RoPE pair interleave (MapDesc.rope_pair).
+#include <cstdint>
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -79,9 +80,14 @@ struct JsonCursor {
       ++p;
     }
     if (p >= e || *p < '0' || *p > '9') fail("expected an integer");
+    if (neg) fail("negative integer");  // offsets and dims are never negative
     int64_t v = 0;
-    while (p < e && *p >= '0' && *p <= '9') v = v * 10 + (*p++ - '0');
-    return neg ? -v : v;
+    while (p < e && *p >= '0' && *p <= '9') {
+      const int dgt = *p++ - '0';
+      if (v > (INT64_MAX - dgt) / 10) fail("integer overflow");
+      v = v * 10 + dgt;
+    }
+    return v;
   }
   void skip_value() {
     ws();
@@ -189,8 +195,18 @@ SafetensorsFile::SafetensorsFile(const std::string& path) : path_(path) {
         c.expect('}');
         break;
       }
-      if (!have_off || t.end < t.begin || data_off_ + t.end > size_)
+      if (!have_off || t.end < t.begin || t.end > size_ - data_off_)  // data_off_ <= size_ (checked above)
         raise(GRT_IoError, "'" + path + "': bad data_offsets for '" + key + "'");
+      {  // the payload must be exactly numel x element size
+        const int64_t es = t.dtype == GRT_F32 ? 4 : 2;
+        int64_t numel = 1;
+        for (int64_t dim : t.shape) {
+          if (dim != 0 && numel > INT64_MAX / dim) raise(GRT_IoError, "'" + path + "': shape overflow for '" + key + "'");
+          numel *= dim;
+        }
+        if (t.dtype >= 0 && (numel > INT64_MAX / es || t.end - t.begin != numel * es))
+          raise(GRT_IoError, "'" + path + "': data_offsets of '" + key + "' do not match its shape and dtype");
+      }
       tensors_.push_back(std::move(t));
     }
     if (c.peek(',')) {

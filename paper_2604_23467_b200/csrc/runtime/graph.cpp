@@ -37,22 +37,30 @@ void ExecGraph::mark_launched(cudaStream_t s) {
 // ---------------------------------------------------------------------------
 // CaptureEngine
 
+void CaptureEngine::open_key(int key) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (open_keys_.count(key)) raise(GRT_CaptureInProgress, "capture already open for key " + std::to_string(key));
+  open_keys_.insert(key);
+}
+
+void CaptureEngine::close_key(int key) {
+  std::lock_guard<std::mutex> lk(mu_);
+  open_keys_.erase(key);
+}
+
 ExecGraphPtr CaptureEngine::capture(int key, const std::vector<const KernelInvocation*>& kernels, cudaStream_t stream) {
-  {
-    std::lock_guard<std::mutex> lk(mu_);
-    if (open_keys_.count(key)) raise(GRT_CaptureInProgress, "capture already open for key " + std::to_string(key));
-    open_keys_.insert(key);
-  }
+  open_key(key);
   struct Close {
     CaptureEngine* e;
     int key;
-    ~Close() {
-      std::lock_guard<std::mutex> lk(e->mu_);
-      e->open_keys_.erase(key);
-    }
+    ~Close() { e->close_key(key); }
   } close{this, key};
-
   validate(kernels);
+  return instantiate(key, kernels, stream);
+}
+
+ExecGraphPtr CaptureEngine::instantiate(int key, const std::vector<const KernelInvocation*>& kernels,
+                                        cudaStream_t stream) {
   int64_t flops = 0;
   for (const KernelInvocation* k : kernels) flops += k->spec.flops;
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
@@ -86,14 +94,66 @@ ExecGraphPtr CaptureEngine::capture(int key, const std::vector<const KernelInvoc
   return std::make_shared<ExecGraph>(key, exec, kernels.size(), flops, epoch, device_);
 }
 
+void CaptureEngine::check(const KernelInvocation& k, bool allow_dynamic) const {
+  if (!k.launch || k.spec.op_class == OpClass::Host)
+    raise(GRT_CaptureViolation, "kernel '" + k.spec.name + "' needs host values at launch (not capturable)");
+  if (k.spec.op_class == OpClass::Dynamic && !allow_dynamic)
+    raise(GRT_CaptureViolation, "dynamic kernel '" + k.spec.name + "' recorded into a static-only graph");
+  for (const DevRange& r : k.bindings)
+    if (!binding_allowed(r))
+      raise(GRT_ForeignBuffer, "kernel '" + k.spec.name + "' binds a buffer outside the model arena");
+}
+
 void CaptureEngine::validate(const std::vector<const KernelInvocation*>& kernels) const {
   if (kernels.empty()) raise(GRT_EmptyCapture, "capture recorded zero kernels");
-  for (const KernelInvocation* k : kernels) {
-    if (!k->launch) raise(GRT_CaptureViolation, "kernel '" + k->spec.name + "' has no device launch");
-    for (const DevRange& r : k->bindings)
-      if (!binding_allowed(r))
-        raise(GRT_ForeignBuffer, "kernel '" + k->spec.name + "' binds a buffer outside the model arena");
+  for (const KernelInvocation* k : kernels) check(*k, true);
+}
+
+// ---------------------------------------------------------------------------
+// CaptureSession (exec_graph.cpp:49-103)
+
+CaptureSession::CaptureSession(CaptureEngine& engine, int key, bool allow_dynamic)
+    : engine_(&engine), key_(key), allow_dynamic_(allow_dynamic) {
+  engine_->open_key(key);  // CaptureInProgress when the key is already open
+}
+
+CaptureSession::~CaptureSession() {
+  if (state_ == Open) engine_->close_key(key_);
+}
+
+void CaptureSession::abort() {
+  kernels_.clear();  // no partial graphs
+  if (state_ == Open) engine_->close_key(key_);
+  state_ = Aborted;
+}
+
+void CaptureSession::record(const KernelInvocation* k) {
+  if (state_ != Open) raise(GRT_SessionClosed, "capture session is not open");
+  try {
+    engine_->check(*k, allow_dynamic_);
+  } catch (...) {
+    abort();
+    throw;
   }
+  kernels_.push_back(k);
+}
+
+ExecGraphPtr CaptureSession::end_capture(cudaStream_t stream) {
+  if (state_ != Open) raise(GRT_SessionClosed, "capture session is not open");
+  if (kernels_.empty()) {
+    abort();
+    raise(GRT_EmptyCapture, "capture recorded zero kernels");
+  }
+  ExecGraphPtr g;
+  try {
+    g = engine_->instantiate(key_, kernels_, stream);
+  } catch (...) {
+    abort();
+    throw;
+  }
+  engine_->close_key(key_);
+  state_ = Closed;
+  return g;
 }
 
 void CaptureEngine::record_into(cudaGraph_t body, const std::vector<const KernelInvocation*>& kernels,

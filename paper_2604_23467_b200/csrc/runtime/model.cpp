@@ -397,7 +397,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   rope_sin_ = static_cast<float*>(arena_buf(S * (dh / 2) * 4, "rope_sin"));
   ctrl_ = static_cast<GrtCtrl*>(arena_buf(sizeof(GrtCtrl), "ctrl"));
   loop_ctl_ = static_cast<LoopCtl*>(arena_buf(sizeof(LoopCtl), "loop_ctl"));
-  tokens_ = static_cast<int*>(arena_buf(S * 4, "tokens"));
+  tokens_ = static_cast<int*>(arena_buf((S + 1) * 4, "tokens"));  // +1: a token sampled at a full cache (pos == S)
   uniforms_ = static_cast<double*>(arena_buf(max_gen_ * 8, "uniforms"));
   pass_layers_ = static_cast<PassLayer*>(arena_buf(cfg_.n_layers * sizeof(PassLayer), "pass_layers"));
   pass_sync_ = static_cast<int*>(arena_buf(static_cast<size_t>(sync_ints()) * 4, "pass_sync"));

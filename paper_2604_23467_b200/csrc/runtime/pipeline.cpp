@@ -244,6 +244,12 @@ Session::Session(Model& model, const CacheConfig& cc) : model_(&model), cc_(cc) 
   pre_op_ = model.make_preprocess_op();
   sample_op_ = model.make_sample_op();
   sample_pre_op_ = model.make_sample_preprocess_op();
+  host_token_op_.spec.name = "host_token_upload";
+  host_token_op_.spec.op_class = OpClass::Host;
+  host_token_op_.bindings = {{model.tokens_dev(), static_cast<size_t>(model.config().max_seq_len) * sizeof(int)}};
+  host_token_op_.launch = [this](cudaStream_t s) {
+    return cudaMemcpyAsync(model_->tokens_dev() + cur_len_, &step_token_, sizeof(int), cudaMemcpyHostToDevice, s);
+  };
   void* hc = nullptr;
   cuda_check(cudaHostAlloc(&hc, sizeof(GrtCtrl), cudaHostAllocDefault), "cudaHostAlloc ctrl");
   h_ctrl_ = static_cast<GrtCtrl*>(hc);
@@ -647,13 +653,61 @@ void Session::step(int token) {
     raise(GRT_CacheFull, "kv cache at max_seq");
   }
   cudaStream_t s = dev_->replay();
-  cuda_check(cudaMemcpyAsync(model_->tokens_dev() + cur_len_, &token, sizeof(int), cudaMemcpyHostToDevice, s),
-             "token");
+  step_token_ = token;
+  cuda_check(host_token_op_.launch(s), "token");
   dev_->submit_kernel(pre_op_);
   for (const KernelInvocation& inv :
        model_->plan(Model::key_of(cur_len_ + 1, cc_.bucket_size), cc_.bucket_size, cc_.pass_impl))
     dev_->submit_kernel(inv);
   cuda_check(cudaStreamSynchronize(s), "step");
+  ++cur_len_;
+  check_device_errors();
+}
+
+std::unique_ptr<CaptureSession> Session::begin_capture(int key, bool fused) {
+  if (key < 1 || key > model_->max_key(cc_.bucket_size))
+    raise(GRT_LengthOutOfRange, "capture key " + std::to_string(key) + " outside [1, max key]");
+  return std::make_unique<CaptureSession>(*engine_, cache_key(key, fused), fused);
+}
+
+const KernelInvocation* Session::capture_op(int kind, int plan_key, int index) {
+  switch (kind) {
+    case OP_PLAN: {
+      const auto& plan = model_->plan(plan_key, cc_.bucket_size, cc_.pass_impl);  // LengthOutOfRange
+      if (index < 0 || index >= static_cast<int>(plan.size()))
+        raise(GRT_InvalidConfig, "plan op index " + std::to_string(index) + " outside the plan");
+      return &plan[index];
+    }
+    case OP_SAMPLE_PREPROCESS: return &sample_pre_op_;
+    case OP_PREPROCESS: return &pre_op_;
+    case OP_HOST_TOKEN: return &host_token_op_;
+  }
+  raise(GRT_InvalidConfig, "unknown capture op kind " + std::to_string(kind));
+}
+
+ExecGraphPtr Session::end_capture(CaptureSession& cs, bool fused) {
+  ExecGraphPtr g = cs.end_capture(dev_->capture_stream());
+  cuda_check(cudaStreamSynchronize(dev_->capture_stream()), "capture");
+  cache_->insert(cs.key(), g);
+  ++dev_->counters().captures;
+  return g;
+}
+
+void Session::replay(int key, bool fused, int token, bool validate) {
+  const ModelConfig& c = model_->config();
+  if (token < 0 || token >= c.vocab_size) raise(GRT_TokenOutOfRange, "token id " + std::to_string(token));
+  if (cur_len_ >= c.max_seq_len) raise(GRT_CacheFull, "kv cache at max_seq");
+  auto hit = cache_->lookup(cache_key(key, fused));
+  if (!hit) raise(GRT_InvalidConfig, "no cached graph for key " + std::to_string(key));
+  if (validate && Model::key_of(cur_len_ + 1, cc_.bucket_size) != key)  // validate_replay: cur_len == length key
+    raise(GRT_WrongLength, "replay of key " + std::to_string(key) + " at length " + std::to_string(cur_len_ + 1));
+  cudaStream_t s = dev_->replay();
+  step_token_ = token;
+  cuda_check(host_token_op_.launch(s), "token");
+  if (!fused) dev_->submit_kernel(pre_op_);  // static-only graph: the dynamic op runs outside it
+  dev_->submit_replay(*hit);
+  (*hit)->mark_launched(s);
+  cuda_check(cudaStreamSynchronize(s), "replay");
   ++cur_len_;
   check_device_errors();
 }

@@ -107,7 +107,14 @@ class Arena {
 
 // ---------------------------------------------------------------------------
 // operator API (kernels.hpp:14-45)
-enum class OpClass { Static, Dynamic };
+// Static: a plan kernel (graph-capturable).  Dynamic: a context op (sampler,
+// preprocess) -- NVRTC code that reads token, position and RNG draw from device
+// memory, so it is capturable too, but only into a FUSED step graph (hybrid);
+// a static-only graph (graph_only / ablate_fused / the IPC split) rejects it,
+// as CaptureSession::record rejects every dynamic op (exec_graph.cpp:56-70).
+// Host: needs a host value at launch (the step API's token upload) -- never
+// capturable (CaptureViolation).
+enum class OpClass { Static, Dynamic, Host };
 
 struct DevRange {
   const void* ptr;
@@ -386,6 +393,13 @@ using ExecGraphPtr = std::shared_ptr<ExecGraph>;
 class CaptureEngine {
  public:
   CaptureEngine(const Arena& arena, int device) : arena_(&arena), device_(device) {}
+  // exec_graph.cpp:49-55 begin_capture: one open capture per key
+  void open_key(int key);
+  void close_key(int key);
+  // capture + instantiate a validated list under an already-open key
+  ExecGraphPtr instantiate(int key, const std::vector<const KernelInvocation*>& kernels, cudaStream_t stream);
+  // the per-kernel checks of CaptureSession::record (exec_graph.cpp:56-77)
+  void check(const KernelInvocation& k, bool allow_dynamic) const;
   // Captures `kernels` on `stream` (cudaStreamCaptureModeThreadLocal) and
   // instantiates them.  Raises CaptureViolation / ForeignBuffer / EmptyCapture /
   // CaptureInProgress like CaptureSession::record / end_capture.
@@ -401,6 +415,31 @@ class CaptureEngine {
   std::mutex mu_;
   std::set<int> open_keys_;
   uint64_t epoch_ = 0;
+};
+
+// CaptureSession (exec_graph.hpp:73-103): Open -> record()* -> end_capture()
+// -> Closed; any violation aborts it (Aborted, nothing recorded kept) and
+// releases the key.  A closed or aborted session raises SessionClosed.
+class CaptureSession {
+ public:
+  enum State { Open = 0, Closed = 1, Aborted = 2 };
+  CaptureSession(CaptureEngine& engine, int key, bool allow_dynamic);
+  ~CaptureSession();
+  CaptureSession(const CaptureSession&) = delete;
+  CaptureSession& operator=(const CaptureSession&) = delete;
+  void record(const KernelInvocation* k);
+  ExecGraphPtr end_capture(cudaStream_t stream);
+  State state() const { return state_; }
+  size_t recorded() const { return kernels_.size(); }
+  int key() const { return key_; }
+
+ private:
+  void abort();
+  CaptureEngine* engine_;
+  int key_;
+  bool allow_dynamic_;
+  State state_ = Open;
+  std::vector<const KernelInvocation*> kernels_;
 };
 
 // graph_cache.hpp:29-81, ported with the same policy and statistics.
@@ -578,6 +617,17 @@ class Session {
   // the other process.
   ExecGraphPtr static_graph(int key);
 
+  // Explicit capture (exec_graph.hpp:73-103 CaptureSession over this session's
+  // engine): the graph lands in the session's cache under the step key.
+  enum CaptureOp { OP_PLAN = 0, OP_SAMPLE_PREPROCESS = 1, OP_PREPROCESS = 2, OP_HOST_TOKEN = 3 };
+  std::unique_ptr<CaptureSession> begin_capture(int key, bool fused);
+  const KernelInvocation* capture_op(int kind, int plan_key, int index);
+  ExecGraphPtr end_capture(CaptureSession& cs, bool fused);
+  // validate_replay (exec_graph.cpp:91-103) + one replay of the cached graph for
+  // `key` as step cur_len+1 with `token`; validate=false skips the host check so
+  // the device-side length check is what trips
+  void replay(int key, bool fused, int token, bool validate);
+
   GraphCache& cache() { return *cache_; }
   CudaDevice& device() { return *dev_; }
   const CacheConfig& cache_config() const { return cc_; }
@@ -598,6 +648,8 @@ class Session {
   std::unique_ptr<CaptureEngine> engine_;
   std::unique_ptr<GraphCache> cache_;
   KernelInvocation pre_op_, sample_op_, sample_pre_op_;
+  KernelInvocation host_token_op_;  // step API: tokens[cur_len] = step_token_ (OpClass::Host)
+  int step_token_ = 0;
   std::mt19937_64 sampler_{7};
   int cur_len_ = 0;
   int n_sampled_ = 0;  // step-level sampler draws since sampler_reset (Philox counter / uniform index)

@@ -168,6 +168,8 @@ EXPORTS = [
     "grt_tp_emu_step", "grt_tp_emu_logits", "grt_tp_emu_threaded",
     "grt_ipc_server_create", "grt_ipc_server_serve", "grt_ipc_server_destroy", "grt_ipc_client_create",
     "grt_ipc_client_generate", "grt_ipc_client_destroy",
+    "grt_capture_begin", "grt_capture_record", "grt_capture_record_external", "grt_capture_end",
+    "grt_capture_state_get", "grt_capture_destroy", "grt_plan_size", "grt_session_replay", "grt_model_arena_info",
 ]
 
 _lib = None
@@ -243,6 +245,16 @@ def lib():
                                        C.c_char_p, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]
         L.grt_trace_pass.argtypes = [vp, C.c_int32, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int32),
                                      C.POINTER(C.c_int32)]
+        L.grt_capture_begin.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(vp)]
+        L.grt_capture_record.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32]
+        L.grt_capture_record_external.argtypes = [vp, vp, C.c_uint64]
+        L.grt_capture_end.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_uint64)]
+        L.grt_capture_state_get.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.grt_capture_destroy.argtypes = [vp]
+        L.grt_capture_destroy.restype = None
+        L.grt_plan_size.argtypes = [vp, C.c_int32, C.POINTER(C.c_int32)]
+        L.grt_session_replay.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32]
+        L.grt_model_arena_info.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.grt_graph_cache_create.argtypes = [C.c_uint64, C.c_int32, C.POINTER(vp)]
         L.grt_graph_cache_destroy.argtypes = [vp]
         L.grt_graph_cache_lookup.argtypes = [vp, C.c_int32, C.POINTER(C.c_int32)]
@@ -425,6 +437,12 @@ class Model:
             self.close()
         except Exception:
             pass
+
+    def arena_info(self):
+        """-> (capacity, used, allocations) of the model's single device arena."""
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().grt_model_arena_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
 
     def upload(self, name: str, array) -> None:
         """Overwrites a weight from a host array in the REFERENCE layout ([k,n])."""
@@ -701,6 +719,78 @@ class Session:
 
     def sampler_reset(self, seed: int):
         _check(lib().grt_sampler_reset(self._h, seed))
+
+    # explicit capture / replay (exec_graph.hpp:73-141)
+    def plan_size(self, key: int) -> int:
+        n = C.c_int32()
+        _check(lib().grt_plan_size(self._h, int(key), C.byref(n)))
+        return n.value
+
+    def begin_capture(self, key: int, fused: bool = False) -> "CaptureSession":
+        h = C.c_void_p()
+        _check(lib().grt_capture_begin(self._h, int(key), 1 if fused else 0, C.byref(h)))
+        return CaptureSession(self, h)
+
+    def replay(self, key: int, token: int, fused: bool = True, validate: bool = True):
+        _check(lib().grt_session_replay(self._h, int(key), 1 if fused else 0, int(token), 1 if validate else 0))
+
+
+class CaptureState(enum.IntEnum):
+    Open = 0
+    Closed = 1
+    Aborted = 2
+
+
+class CaptureOp(enum.IntEnum):
+    Plan = 0
+    SamplePreprocess = 1
+    Preprocess = 2
+    HostToken = 3
+
+
+class CaptureSession:
+    """graphrt::CaptureSession (exec_graph.hpp:73-103) over a Session's engine."""
+
+    def __init__(self, sess: "Session", h):
+        self.sess, self._h = sess, h
+
+    def record(self, op: CaptureOp, plan_key: int = 0, index: int = 0):
+        _check(lib().grt_capture_record(self._h, int(op), int(plan_key), int(index)))
+
+    def record_plan(self, plan_key: int, index: int):
+        self.record(CaptureOp.Plan, plan_key, index)
+
+    def record_external(self, ptr: int, nbytes: int):
+        _check(lib().grt_capture_record_external(self._h, C.c_void_p(ptr), nbytes))
+
+    def end_capture(self):
+        """-> (kernel_count, capture_epoch)"""
+        n, ep = C.c_int32(), C.c_uint64()
+        _check(lib().grt_capture_end(self._h, C.byref(n), C.byref(ep)))
+        return n.value, ep.value
+
+    @property
+    def state(self) -> CaptureState:
+        st, rec = C.c_int32(), C.c_int32()
+        _check(lib().grt_capture_state_get(self._h, C.byref(st), C.byref(rec)))
+        return CaptureState(st.value)
+
+    @property
+    def recorded(self) -> int:
+        st, rec = C.c_int32(), C.c_int32()
+        _check(lib().grt_capture_state_get(self._h, C.byref(st), C.byref(rec)))
+        return rec.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().grt_capture_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class GraphCache:

@@ -65,7 +65,10 @@ def test_gemv_matches_fp64(dtype, n, k):
 
 @pytest.mark.parametrize("kvdt", [g.F32, g.BF16])
 @pytest.mark.parametrize("h,dh,length", [(2, 8, 1), (4, 16, 5), (4, 16, 42), (32, 128, 1), (32, 128, 10),
-                                         (32, 128, 138), (32, 128, 628), (8, 64, 300)])
+                                         (32, 128, 138), (32, 128, 628), (8, 64, 300),
+                                         # 4-CTA clusters x 3 and 4 passes: the later passes staged in
+                                         # shared memory by the TMA engine
+                                         (32, 128, 1500), (32, 128, 2000), (2, 4, 301)])
 def test_attention_matches_fp64(kvdt, h, dh, length):
     rs = np.random.RandomState(h * dh + length)
     S = max(length, 8) + 3
