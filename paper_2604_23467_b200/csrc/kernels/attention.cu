@@ -252,7 +252,9 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
     c_ml[0] = M;
     c_ml[1] = L;
   }
-  if (len < 1 || len > ns * span) {  // live length outside the bucket this graph was built for
+  // live length outside the bucket this graph was built for (lengths below the
+  // bucket are served correctly -- masked -- so only the upper end is unsafe)
+  if (len < 1 || len > ns * span || (p.max_len > 0 && len > p.max_len)) {
     if (threadIdx.x == 0 && rank == 0 && head == 0 && p.err) atomicOr(p.err, DEVERR_WRONG_LENGTH);
   }
   op_stamp(p.trace, 4);
@@ -353,6 +355,7 @@ cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s,
   int ns, rounds;
   attn_shape(max_len, p.head_dim, &ns, &rounds, p.n_heads);
   p.rounds = rounds;
+  p.max_len = max_len;
   // 0 (default): the successor (Wo + gate/up) launches at once and fills its
   // weight ring on the SMs this small grid leaves free (measured fastest)
   static const int trig = [] {

@@ -87,6 +87,7 @@ struct AttnParams {
   int trigger = 0;               // when the successor may launch: 0 start, 1 after KV loads, 2 at exit
   int prefetch = 0;              // round 0's rows of earlier steps loaded before the dependency wait
   int smem_rounds = 0;           // rounds 1..smem_rounds staged into shared memory before the wait (launcher)
+  int max_len = 0;               // the bucket's last length: longer live lengths flag DEVERR_WRONG_LENGTH (launcher)
 };
 // Per-op trace stamps (8 slots per CTA): 0 CTA start, 1 dependency released
 // (griddepcontrol.wait), 2 operands ready (activation loaded / KV rows loaded),
@@ -185,6 +186,29 @@ struct GemvPairParams {
   int l2_pre = 0;                           // tasks per warp beyond the ring L2-prefetched before the wait
 };
 cudaError_t launch_gemv_pair(int epi_b, GemvPairParams p, cudaStream_t s, bool pdl);
+
+// ---- streaming pass (stream_pass.cu, pass_impl 2): the whole static pass as
+// one persistent launch whose per-warp weight rings stream across every phase
+// and layer boundary (LLaMA arch, bf16 weights + KV).
+struct StreamPassParams {
+  PassParams p;        // dims, per-layer weights, activations, seq_len / err
+  PairAttn att;        // attention phase: part [h][ns][dh+4], ns / span, scale, paging (k/v set per layer)
+  int* bar = nullptr;  // [2] arrive / depart counters, zero-initialised, self-resetting
+  unsigned long long* trace = nullptr;  // optional [grid][trace_stride] %globaltimer phase stamps
+  int trace_stride = 0;
+  // set by stream_pass_configure
+  int ch_d = 0, nch_d = 0, ch_f = 0, nch_fa = 0, nch_fb = 0, k_split = 0, rowb = 0, stages = 0, xs_floats = 0;
+  int part_floats = 0, part_a_floats = 0, grid = 0;
+  int max_stages = 0;          // ring slots per warp cap (0 = as many as fit)
+  int pf_att = 0, pf_bar = 0;  // tasks per warp requested into L2 beyond the ring before the attention / other waits
+  size_t smem_bytes = 0;
+};
+// chunking (elements per k chunk <= chmax), ring depth, smem, grid; fails when
+// one CTA per SM cannot be resident (the grid barrier needs the whole grid)
+cudaError_t stream_pass_configure(StreamPassParams* p, int chmax);
+cudaError_t launch_stream_pass(const StreamPassParams& p, cudaStream_t s, bool pdl);
+cudaError_t stream_pass_prepare();
+constexpr int STREAM_TRACE_PER_LAYER = 8;  // stamps: qkv, attn partial, merge, wo, up, down (+ start, wait)
 // split count / span of the fused attention phase for a bucket of max_len positions
 void pair_attn_shape(int max_len, int n_heads, int head_dim, int sms, int* ns, int* span);
 cudaError_t gemv_pair_prepare();

@@ -316,6 +316,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   acc(h * max_nsplit_ * (dh + 2) * 4);
   acc(h * 4);
   acc(cfg_.n_layers * 4 * 4);  // fused-pair barrier counters
+  acc(64);                     // streaming-pass barrier counters
   acc(static_cast<size_t>(h) * 4 * (dh + 4) * 4);  // fused attention partials
   acc(S * (dh / 2) * 4 * 2);
   acc(sizeof(GrtCtrl));
@@ -373,6 +374,8 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   attn_part_ = static_cast<float*>(arena_buf(h * max_nsplit_ * (dh + 2) * 4, "attn_part"));
   attn_counters_ = static_cast<int*>(arena_buf(h * 4, "attn_counters"));
   pair_bar_ = static_cast<int*>(arena_buf(cfg_.n_layers * 4 * 4, "pair_barriers"));
+  stream_bar_ = static_cast<int*>(arena_buf(64, "stream_barrier"));
+  if (const char* e = getenv("GRT_STREAM_CHMAX")) stream_chmax_ = std::max(64, atoi(e));  // tuning only
   pair_attn_part_ = static_cast<float*>(arena_buf(static_cast<size_t>(h) * 4 * (dh + 4) * 4, "pair_attn_part"));
   kv_table_ = static_cast<int*>(arena_buf(static_cast<size_t>(std::max(kv_pages_, 1)) * 4, "kv_block_table"));
   kvp_.page = PS;
@@ -740,6 +743,31 @@ PassParams Model::pass_params(int key, int B) const {
   return pp;
 }
 
+StreamPassParams Model::stream_params(int key, int B) {
+  const int h = cfg_.n_heads, dh = cfg_.head_dim();
+  const int max_len = std::min(key * B, cfg_.max_seq_len);
+  StreamPassParams sp;
+  sp.p = pass_params(key, B);
+  PairAttn& A = sp.att;
+  A.enabled = 1;
+  A.q = q_;
+  A.seq_len = &ctrl_->seq_len;
+  A.part = pair_attn_part_;
+  A.n_heads = h;
+  A.head_dim = dh;
+  A.max_seq = cfg_.max_seq_len;
+  pair_attn_shape(max_len, h, dh, num_sms(cfg_.device), &A.ns, &A.span);
+  A.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
+  A.kvp = kvp_;
+  sp.bar = stream_bar_;
+  if (const char* e = getenv("GRT_STREAM_PF_ATT")) sp.pf_att = atoi(e);  // tuning only
+  if (const char* e = getenv("GRT_STREAM_PF_BAR")) sp.pf_bar = atoi(e);
+  if (const char* e = getenv("GRT_STREAM_STAGES")) sp.max_stages = atoi(e);
+  cuda_check(stream_pass_prepare(), "stream_pass_prepare");
+  cuda_check(stream_pass_configure(&sp, stream_chmax_), "stream_pass_configure");
+  return sp;
+}
+
 std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* grid, int* stride, int impl) {
   if (impl == 1) {
     const int n_k = 5 * cfg_.n_layers + 1;
@@ -773,6 +801,23 @@ std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* gri
     cudaFree(buf);
     *grid = n_k;
     *stride = OP_TRACE_CTAS * 8;
+    return out;
+  }
+  if (impl == 2) {
+    StreamPassParams sp = stream_params(key, B);
+    *grid = sp.grid;
+    *stride = cfg_.n_layers * STREAM_TRACE_PER_LAYER + 8;
+    sp.trace_stride = *stride;
+    const size_t n = static_cast<size_t>(*grid) * *stride;
+    unsigned long long* buf = nullptr;
+    cuda_check(cudaMalloc(&buf, n * 8), "cudaMalloc trace");
+    cuda_check(cudaMemsetAsync(buf, 0, n * 8, s), "memset trace");
+    sp.trace = buf;
+    cuda_check(launch_stream_pass(sp, s, false), "trace pass");
+    cuda_check(cudaStreamSynchronize(s), "trace pass");
+    std::vector<uint64_t> out(n);
+    cuda_check(cudaMemcpy(out.data(), buf, n * 8, cudaMemcpyDeviceToHost), "trace copy");
+    cudaFree(buf);
     return out;
   }
   PassParams pp = pass_params(key, B);
@@ -860,6 +905,30 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       inv.bindings.push_back({layers_[l].v, kv_layer_elems_ * kvb});
     }
     inv.launch = [wdt, kvdt, llama, pp](cudaStream_t s) { return launch_decode_pass(wdt, kvdt, llama, pp, s, true); };
+    plan.push_back(std::move(inv));
+    return plan;
+  }
+  if (impl == 2) {
+    // the whole static pass as one persistent launch streaming across phases (stream_pass.cu)
+    const StreamPassParams sp = stream_params(key, B);
+    KernelInvocation inv;
+    inv.spec.name = "stream_pass";
+    inv.spec.op_class = OpClass::Static;
+    inv.spec.flops = 2LL * cfg_.n_layers * (3LL * d * d + 1LL * d * d + 2LL * ff * d + 1LL * d * ff) + 2LL * V * d +
+                     static_cast<int64_t>(cfg_.n_layers) * h * max_len * (4 * dh + 5);
+    inv.spec.bytes = static_cast<int64_t>(decode_bytes(max_len));
+    inv.bindings = {{pass_layers_, cfg_.n_layers * sizeof(PassLayer)},
+                    {stream_bar_, 64},
+                    {pair_attn_part_, static_cast<size_t>(h) * 4 * (dh + 4) * 4},
+                    {head_, static_cast<size_t>(V) * d * wb},
+                    {x_, static_cast<size_t>(d) * 4},
+                    {logits_, static_cast<size_t>(V) * 4}};
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+      inv.bindings.push_back({layers_[l].w_qkv, 3ull * d * d * wb});
+      inv.bindings.push_back({layers_[l].k, kv_layer_elems_ * kvb});
+      inv.bindings.push_back({layers_[l].v, kv_layer_elems_ * kvb});
+    }
+    inv.launch = [sp](cudaStream_t s) { return launch_stream_pass(sp, s, true); };
     plan.push_back(std::move(inv));
     return plan;
   }
@@ -1116,12 +1185,14 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
 
 const std::vector<KernelInvocation>& Model::plan(int key, int B, int impl) {
   if (B < 1) raise(GRT_InvalidConfig, "bucket_size must be >= 1");
-  if (impl != 0 && impl != 1) raise(GRT_InvalidConfig, "pass_impl must be 0 or 1");
+  if (impl < 0 || impl > 2) raise(GRT_InvalidConfig, "pass_impl must be 0, 1 or 2");
+  if (impl == 2 && (cfg_.tp_size > 1 || !cfg_.llama() || cfg_.weight_dtype != GRT_BF16 || cfg_.kv_dtype != GRT_BF16))
+    raise(GRT_Unsupported, "the streaming pass (pass_impl 2) is single-GPU, LLaMA arch, bf16 weights and KV");
   if (impl == 0 && cfg_.tp_size > 1) raise(GRT_Unsupported, "the persistent pass (pass_impl 0) is single-GPU only");
   if (key < 1 || key > max_key(B))
     raise(GRT_LengthOutOfRange, "plan key " + std::to_string(key) + " outside [1, " + std::to_string(max_key(B)) + "]");
   std::lock_guard<std::mutex> lk(plan_mu_);
-  const auto mk = std::make_pair(key, B * 2 + impl);
+  const auto mk = std::make_pair(key, B * 4 + impl);
   auto it = plans_.find(mk);
   if (it == plans_.end()) it = plans_.emplace(mk, build_plan(key, B, impl)).first;
   return it->second;

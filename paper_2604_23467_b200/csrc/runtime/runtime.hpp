@@ -269,6 +269,8 @@ class Model {
   const void* pos_dev() const { return pos_ ? pos_ : emb_; }
   void reset_pass_sync() {
     cudaMemset(pass_sync_, 0, static_cast<size_t>(sync_ints()) * 4);
+    cudaMemset(pair_bar_, 0, static_cast<size_t>(cfg_.n_layers) * 4 * 4);
+    cudaMemset(stream_bar_, 0, 64);
     cudaMemset(&ctrl_->err, 0, sizeof(int));
     cudaDeviceSynchronize();
   }
@@ -283,6 +285,7 @@ class Model {
 
  public:
   PassParams pass_params(int key, int bucket_size) const;
+  StreamPassParams stream_params(int key, int bucket_size);  // pass_impl 2 (configured for this device)
   // Runs one persistent pass with per-CTA %globaltimer phase stamps (profiling).
   // impl 0: per-CTA phase stamps of the persistent pass ([grid][stride]);
   // impl 1: the per-op plan captured as a graph, [n_kernels][OP_TRACE_CTAS*4]
@@ -306,6 +309,8 @@ class Model {
   void *pf_Xn_ = nullptr, *pf_A_ = nullptr, *pf_act_ = nullptr;
   int* pf_cnt_ = nullptr;
   int* pair_bar_ = nullptr;
+  int* stream_bar_ = nullptr;  // [2] streaming-pass barrier (self-resetting)
+  int stream_chmax_ = 2048;    // streaming pass: k-chunk elements per ring stage
   float* pair_attn_part_ = nullptr;
   KvPaging kvp_;
   int kv_pages_ = 0;

@@ -182,9 +182,10 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     return bytes * 5 / (ms * 1e-3) / 1e9;
   };
-  const int cfgs[][3] = {{2048, 5, 8},  {4096, 5, 8},  {8192, 2, 8},  {8192, 3, 8},  {4096, 8, 8},
-                         {16384, 2, 8}, {8192, 6, 4},  {4096, 12, 4}, {2048, 10, 16}, {4096, 6, 16},
-                         {16384, 3, 4}, {32768, 3, 2}, {8192, 3, 16}, {4096, 3, 16}};
+  const int cfgs[][3] = {{8192, 1, 8},  {8192, 2, 8},  {8192, 3, 8},  {4096, 2, 8},  {4096, 4, 8},
+                         {4096, 6, 8},  {2048, 4, 8},  {2048, 8, 8},  {16384, 1, 8}, {16384, 2, 8},
+                         {8192, 1, 16}, {8192, 2, 16}, {4096, 2, 16}, {4096, 3, 16}, {2048, 6, 16},
+                         {32768, 3, 2}, {16384, 3, 4}, {8192, 6, 4},  {8192, 4, 4},  {8192, 2, 4}};
   for (int compute = 0; compute < 2; ++compute)
     for (auto& c : cfgs) {
       const int sb = c[0], depth = c[1], nw = c[2];
