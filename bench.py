@@ -430,7 +430,6 @@ def main():
     ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
                     help="N>1: tensor-parallel decode over the N GPUs (NCCL in-graph) or N independent replicas")
     ap.add_argument("--batched-prefill", type=int, default=1, help="1: tcgen05 batched prefill (TTFT path); 0: token-by-token")
-    ap.add_argument("--pass-impl", type=int, default=1, help="1 per-op kernel graph (default), 0 persistent single-kernel pass")
     ap.add_argument("--no-cpu-baseline", action="store_true",
                     help="skip the CPU legs (LLaMA port + parity stamp, reference sample)")
     ap.add_argument("--ref-layers", type=int, default=32, help="--impl reference: layers of the timed reference model")
@@ -460,7 +459,7 @@ def main():
     n = W + K
     max_seq = max(640, ((P + n + 63) // 64) * 64)
     cc = g.CacheConfig(bucket_size=args.bucket, warmup_lo=1, warmup_hi=10 ** 6 // args.bucket, capacity=4096,
-                       pass_impl=args.pass_impl, batched_prefill=bool(args.batched_prefill))
+                       batched_prefill=bool(args.batched_prefill))
     t_init = time.time()
     parallel = "single"
     tp_error = None

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define GRT_ABI_VERSION 1
+#define GRT_ABI_VERSION 2
 
 /* Replaces graphrt::Errc (error.hpp:10-39) + Error exceptions. */
 typedef enum grt_status {
@@ -81,7 +81,8 @@ typedef enum grt_eviction { GRT_EVICT_LEAST_USED = 0, GRT_EVICT_LRU = 1 } grt_ev
 typedef enum grt_step_path {
   GRT_PATH_REPLAYED = 0,
   GRT_PATH_EAGER_FALLBACK = 1,
-  GRT_PATH_BATCHED = 2 /* extension: prompt token served by the batched (tcgen05) prefill */
+  GRT_PATH_BATCHED = 2,        /* extension: prompt served by the batched (tcgen05) prefill, launched eagerly */
+  GRT_PATH_BATCHED_REPLAYED = 3 /* extension: the batched prefill replayed as one graph (per prompt length) */
 } grt_step_path;
 
 /* Replaces graphrt::SampleStrategy (kernels.hpp:105-115), extended with top-k/top-p. */
@@ -122,7 +123,9 @@ typedef struct grt_cache_config {
   int32_t policy;      /* grt_eviction */
   int32_t bucket_size; /* KV positions per graph key; 1 = the reference's exact-length keys */
   int32_t batched_prefill; /* 1 = one batched prefill pass (TTFT path); 0 = token-by-token like the reference */
-  int32_t pass_impl;   /* 1 = per-op kernels, 5 per layer (default); 0 = persistent single-kernel static pass */
+  int32_t pass_impl;   /* 1 = the per-op kernel graph, 4 kernels per layer (the only supported value) */
+  int32_t prefill_fuse_norm; /* 1 (default): a split-K residual GEMM of the batched prefill hands its partials
+                                to the next RMSNorm launch (bit-identical to 0: separate reduce + norm) */
 } grt_cache_config;
 
 typedef struct grt_sample_params {
@@ -238,9 +241,9 @@ grt_status grt_cache_stats_get(grt_session* s, grt_cache_stats* st, uint64_t* si
  * and names (NUL-separated into `names`, `names_len` bytes); *n = plan size. */
 grt_status grt_profile_plan(grt_session* s, int32_t key, int32_t iters, double* avg_ms, int64_t* bytes,
                             char* names, int32_t names_len, int32_t cap, int32_t* n);
-/* Runs one persistent static pass for bucket `key` with per-CTA %globaltimer
- * stamps at every phase boundary: out[cta * stride + layer * 10 + e] (ns),
- * e = qkv start/end, attention start/end, wo, up, down start/end. */
+/* Profiling: replays bucket `key`'s static plan once as a graph with per-CTA
+ * %globaltimer stamps: out[kernel * stride + cta * 8 + e] (ns), e = start,
+ * dependency released, operands ready, done, first weight stage, loop done. */
 grt_status grt_trace_pass(grt_session* s, int32_t key, uint64_t* out, int64_t cap, int32_t* grid, int32_t* stride);
 grt_status grt_session_counters(grt_session* s, grt_counters* c);
 

@@ -389,7 +389,7 @@ def apply_config(cfg: BenchConfig, kv: Dict[str, str]) -> List[str]:
             cfg.model.init = inits[value]
         elif sec == "cache" and name in _CACHE_INT:
             setattr(cfg.cache, name, _num(value, key, int))
-        elif key in ("cache.prefill_uses_graphs", "cache.batched_prefill"):
+        elif key in ("cache.prefill_uses_graphs", "cache.batched_prefill", "cache.prefill_fuse_norm"):
             setattr(cfg.cache, name, _bool(value, key))
         elif key == "cache.policy":
             if value == "least_used":

@@ -302,22 +302,13 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_decode_kernel(const Attn
 // barriers and a DSMEM merge (measured: ~1 round trip each while the next
 // kernel's CTAs are being launched).
 static int attn_rounds_per_cta() {
-  static const int v = [] {
-    const char* e = getenv("GRT_ATTN_ROUNDS");
-    return e ? std::max(1, atoi(e)) : 1;  // measured: 2-CTA clusters beat 2 rounds in one CTA (p99 2.56 vs 2.58 ms)
-  }();
-  return v;
+  return 1;  // measured: 2-CTA clusters beat 2 rounds in one CTA (p99 2.56 vs 2.58 ms)
 }
 
 // cap: the largest cluster for which all n_heads clusters fit on the SMs at once
 // (one 512-thread CTA per SM): a second wave would double the latency.
 static int attn_cluster_cap(int n_heads) {
   if (n_heads <= 0) return ATTN_MAX_CLUSTER;
-  static const int off = [] {
-    const char* e = getenv("GRT_ATTN_WAVE_CAP");
-    return e ? atoi(e) == 0 : 0;
-  }();
-  if (off) return ATTN_MAX_CLUSTER;
   int dev = 0;
   cudaGetDevice(&dev);
   int c = 1;
@@ -358,20 +349,10 @@ cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s,
   p.max_len = max_len;
   // 0 (default): the successor (Wo + gate/up) launches at once and fills its
   // weight ring on the SMs this small grid leaves free (measured fastest)
-  static const int trig = [] {
-    const char* e = getenv("GRT_ATTN_TRIGGER");
-    return e ? atoi(e) : 0;
-  }();
-  p.trigger = trig;
-  static const int pref = [] {  // 1: round 0's old rows requested before the dependency wait
-    const char* e = getenv("GRT_ATTN_PREFETCH");
-    return e ? atoi(e) : 1;
-  }();
-  p.prefetch = pref;
-  static const int stage_max = [] {  // rounds >= 1 staged through shared memory before the wait
-    const char* e = getenv("GRT_ATTN_STAGE");
-    return e ? std::max(0, atoi(e)) : 3;
-  }();
+  p.trigger = 0;
+  p.prefetch = 1;  // round 0's old rows requested before the dependency wait (2.588 -> 2.442 ms/token)
+  const int stage_max = 3;  // rounds >= 1 staged through shared memory before the wait (P=500: 2.745 -> 2.681 ms)
+  const int pref = p.prefetch;
   const size_t rbytes = static_cast<size_t>(attn_pass_span(p.head_dim)) * p.head_dim * 2 * 2;  // K+V of a round
   // bulk copies need 16-byte aligned sources and sizes: rows of dh bf16 with dh % 8 == 0
   p.smem_rounds = (kvdt == Dt::BF16 && p.kvp.page == 0 && pref && p.head_dim % 8 == 0)

@@ -1,5 +1,5 @@
 // gemv.cu -- per-op fused GEMV kernels (K1 QKV, K4 Wo, K5 gate/up, K6 down,
-// K7 LM head) for sm_100a: the default static decode pass (pass_impl 1) is a
+// K7 LM head) for sm_100a: the static decode pass is a
 // graph of these plus the split-K attention kernel.
 //
 // Memory-bound design (decode is ~1 flop/byte; tensor cores stay idle):
@@ -314,18 +314,10 @@ static int smem_optin(int device) {
 }
 
 // chunking of a k-long row: near-equal chunks of <= CH elements, multiple of 8
-static int chmax_override() {
-  static const int v = [] {
-    const char* e = getenv("GRT_GEMV_CHMAX");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
 
 static void chunking(Dt wdt, int k, int* ch, int* nch, int* rowb, int chmax_hint = 0) {
   int chmax = wdt == Dt::BF16 ? WTraits<__nv_bfloat16>::CH : WTraits<float>::CH;
   if (chmax_hint > 0 && wdt == Dt::BF16) chmax = chmax_hint;
-  if (chmax_override() > 0 && wdt == Dt::BF16) chmax = chmax_override();
   *nch = (k + chmax - 1) / chmax;
   *ch = ((k + *nch - 1) / *nch + 7) / 8 * 8;
   *rowb = ((*ch * (wdt == Dt::BF16 ? 2 : 4) + 15) / 16) * 16;
@@ -333,28 +325,7 @@ static void chunking(Dt wdt, int k, int* ch, int* nch, int* rowb, int chmax_hint
 
 static constexpr int kStaticSmemReserve = 1024;  // bars + red + alignment
 
-int gemv_max_stages() {
-  static const int v = [] {
-    const char* e = getenv("GRT_GEMV_STAGES");
-    const int s = e ? atoi(e) : GEMV_MAX_STAGES;
-    return std::max(1, std::min(GEMV_MAX_STAGES, s));
-  }();
-  return v;
-}
-
-// ring slots filled before griddepcontrol.wait (env GRT_GEMV_PRE / GRT_GEMV_PRE_NORM
-// for the normed GEMVs; 0 = all)
-static int gemv_pre_stages(int norm) {
-  static const int v_none = [] {
-    const char* e = getenv("GRT_GEMV_PRE");
-    return e ? atoi(e) : 0;
-  }();
-  static const int v_norm = [] {
-    const char* e = getenv("GRT_GEMV_PRE_NORM");
-    return e ? atoi(e) : 0;
-  }();
-  return norm == NORM_NONE ? v_none : v_norm;
-}
+int gemv_max_stages() { return GEMV_MAX_STAGES; }
 
 static int stages_for(int device, int rowb, int k, int part_bytes) {
   const int budget = smem_optin(device) - kStaticSmemReserve - k * 4 - part_bytes;
@@ -423,17 +394,12 @@ cudaError_t launch_gemv(Dt wdt, int norm, int epi, GemvParams p, cudaStream_t s,
   grid = std::max(1, std::min(grid, (n_pairs * p.nch + GEMV_WARPS - 1) / GEMV_WARPS));
   const int part_bytes = max_pairs_per_cta(n_pairs, grid) * p.nch * 2 * 4;
   p.stages = stages_for(dev, p.rowb, p.k, part_bytes);
-  p.pre_stages = gemv_pre_stages(norm);
-  static const int l2pre = [] {
-    const char* e = getenv("GRT_GEMV_L2PRE");
-    return e ? std::max(0, atoi(e)) : 0;
-  }();
-  p.l2_pre = l2pre;
-  static const int defer = [] {
-    const char* e = getenv("GRT_RMS_DEFER");
-    return e ? atoi(e) : 1;
-  }();
-  p.rms_defer = defer;
+  // the whole first ring fill goes out before the dependency wait; no L2
+  // prefetch beyond the ring (measured slower: 2.63-2.73 vs 2.58 ms/token);
+  // RMSNorm's 1/rms applied to the finished dot products
+  p.pre_stages = 0;
+  p.l2_pre = 0;
+  p.rms_defer = 1;
   if (static_cast<int64_t>(GEMV_WARPS) * p.stages * 2 * p.rowb + p.k * 4 + part_bytes >
       smem_optin(dev) - kStaticSmemReserve)
     return cudaErrorInvalidValue;

@@ -1,5 +1,5 @@
 // gemv_core.cuh -- device building blocks of the batch-1 GEMV family, shared by
-// the per-op kernels (gemv.cu) and the persistent decode pass (decode_pass.cu).
+// the per-op kernels (gemv.cu) and the fused pair kernel (gemv_pair.cu).
 //
 // Reference ops: make_layernorm (kernels.cpp:52-85) + make_matmul
 // (kernels.cpp:23-50) + make_kv_write (kernels.cpp:188-203) + make_residual_add /
@@ -45,7 +45,7 @@ __device__ __forceinline__ int xs_index(int j, int k) {
 }
 
 // The compute ("consumer") warps of a CTA: 8 warps.  They synchronise on named
-// barrier 1 so a dedicated producer warp (decode_pass.cu) never has to join.
+// barrier 1, so the block-wide syncs never involve a non-consumer warp.
 #ifndef GRT_CONSUMER_THREADS
 #define GRT_CONSUMER_THREADS 256
 #endif

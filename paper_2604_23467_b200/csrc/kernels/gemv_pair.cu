@@ -1,7 +1,6 @@
-// gemv_pair.cu -- two consecutive decode GEMVs in ONE launch: a residual GEMV
-// (Wo or down, phase A) and the normed GEMV that consumes its output (gate/up,
-// or the next layer's QKV, or the LM head; phase B), separated by a grid-wide
-// barrier.
+// gemv_pair.cu -- two consecutive decode GEMVs in ONE launch: the residual Wo
+// GEMV (phase A) and the normed gate/up GEMV that consumes its output (phase
+// B), separated by a grid-wide barrier.
 //
 // Why: between two per-op kernels the successor's CTAs only become resident
 // when the predecessor's exit, and then pay the dependency release, the
@@ -14,10 +13,11 @@
 // round-robin (pair, chunk) tasks, per-task partials summed in chunk order,
 // deferred RMSNorm scale) -- results are identical to the two per-op kernels.
 //
-// Co-residency: grid = one CTA per SM with the SM's whole shared memory, and
-// the kernel triggers its dependents only after the barrier, so every CTA of
-// the grid is resident before any successor can take an SM; a watchdog turns a
-// barrier that never completes into DEVERR_TIMEOUT instead of a hang.
+// Co-residency: grid = one CTA per SM, launched COOPERATIVELY (the driver
+// guarantees every CTA is resident at once or refuses the launch -- e.g. under
+// MPS or next to a kernel holding SMs), and the kernel triggers its dependents
+// only after the barrier; a watchdog still turns a barrier that never completes
+// into DEVERR_TIMEOUT instead of a hang.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -26,10 +26,10 @@
 #include "common.cuh"
 #include "gemv_core.cuh"
 #include "kernels.h"
-#include "pair_attn.cuh"
 
 namespace grt {
 
+constexpr int GP_WARPS = 8;
 constexpr int GP_MAX_STAGES = 8;
 constexpr unsigned long long GP_WATCHDOG_NS = 1000000000ull;  // 1 s
 
@@ -59,7 +59,7 @@ __device__ __forceinline__ unsigned long long gp_timer() {
   return t;
 }
 
-template <int EB, bool ATT>
+template <int EB>
 __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvPairParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bars[GP_WARPS][GP_MAX_STAGES];
@@ -94,17 +94,6 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
     const __nv_bfloat16* src = g.w + static_cast<int64_t>(row0) * g.k + c0;
     bulk_g2s(dst, src, bytes, bar, pol);
     if (has_b) bulk_g2s(dst + rowb, src + g.k, bytes, bar, pol);
-  };
-  auto prefetch_l2 = [&](int i) {  // global task i's rows into L2 only
-    const PhaseGeom& g = i < na ? ga : gb;
-    const int t = warp + (i < na ? i : i - na) * GP_WARPS;
-    const int pl = t / g.nch, c = t - pl * g.nch;
-    const int row0 = 2 * (g.pair_begin + pl);
-    const int c0 = c * g.ch;
-    const uint32_t bytes = static_cast<uint32_t>(min(g.ch, g.k - c0)) * 2;
-    const __nv_bfloat16* src = g.w + static_cast<int64_t>(row0) * g.k + c0;
-    prefetch_l2_bulk(src, bytes);
-    if (row0 + 1 < g.n_rows) prefetch_l2_bulk(src + g.k, bytes);
   };
   // consume tasks [i0, i1) of one phase into `part`, refilling the ring
   auto run_phase = [&](const PhaseGeom& g, int i0, int i1) {
@@ -166,7 +155,6 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
   }
   if (lane == 0) {
     for (int i = 0; i < min(S, n_all); ++i) issue(i);
-    for (int i = S; i < min(S + P.l2_pre, n_all); ++i) prefetch_l2(i);
   }
   griddep_wait();
 
@@ -189,15 +177,8 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
     __syncthreads();
   };
 
-  // ---- phase 0 (optional): attention partials, then merged into phase A's row ----
-  if constexpr (ATT) {
-    if (static_cast<int>(blockIdx.x) < P.att.n_heads * P.att.ns) pair_attn_partial<false>(P.att, xs, P.err);
-    grid_barrier(1);
-    pair_attn_merge(P.att, pa.k, xs, part);
-  } else {
-    // ---- phase A: residual GEMV (x_a produced by the previous kernel) ----
-    load_x<__nv_bfloat16, NORM_NONE, false>(pa.x, nullptr, nullptr, 0.0f, pa.k, xs, red);
-  }
+  // ---- phase A: residual GEMV (x_a produced by the previous kernel) ----
+  load_x<__nv_bfloat16, NORM_NONE, false>(pa.x, nullptr, nullptr, 0.0f, pa.k, xs, red);
   run_phase(ga, 0, na);
   {
     const EpiArgs ea = epi_args(pa);
@@ -213,7 +194,7 @@ __global__ void __launch_bounds__(GP_WARPS * 32, 1) gemv_pair_kernel(const GemvP
   }
 
   // ---- grid barrier: phase B reads the residual rows every CTA just wrote ----
-  grid_barrier(ATT ? 2 : 1);
+  grid_barrier(1);
   griddep_launch_dependents();  // only now: every CTA of this grid is resident
 
   // ---- phase B: normed GEMV on the fresh residual (L2, bypass L1) ----
@@ -281,82 +262,52 @@ static void pair_chunking(int k, int chmax, int* ch, int* nch, int* rowb) {
 }
 
 cudaError_t gemv_pair_prepare() {
-  for (const void* f : {reinterpret_cast<const void*>(gemv_pair_kernel<EPI_SWIGLU, false>),
-                        reinterpret_cast<const void*>(gemv_pair_kernel<EPI_SWIGLU, true>),
-                        reinterpret_cast<const void*>(gemv_pair_kernel<EPI_QKV_ROPE, false>),
-                        reinterpret_cast<const void*>(gemv_pair_kernel<EPI_STORE, false>)}) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, f);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             optin_smem(dev) - static_cast<int>(fa.sharedSizeBytes));
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void* f = reinterpret_cast<const void*>(gemv_pair_kernel<EPI_SWIGLU>);
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, f);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin_smem(dev) - static_cast<int>(fa.sharedSizeBytes));
 }
 
+// Wo + gate/up (epi_b = EPI_SWIGLU) -- the only pairing the plan uses.
 cudaError_t launch_gemv_pair(int epi_b, GemvPairParams P, cudaStream_t s, bool pdl) {
   int dev = 0;
   cudaGetDevice(&dev);
   const int G = num_sms(dev);
-  if (P.a.k % 8 || P.b.k % 8 || !P.bar) return cudaErrorInvalidValue;
+  if (epi_b != EPI_SWIGLU || P.a.k % 8 || P.b.k % 8 || !P.bar) return cudaErrorInvalidValue;
   pair_chunking(P.a.k, P.a.chmax > 0 ? P.a.chmax : 2048, &P.a.ch, &P.a.nch, &P.a.rowb);
   pair_chunking(P.b.k, P.b.chmax > 0 ? P.b.chmax : 2048, &P.b.ch, &P.b.nch, &P.b.rowb);
   P.rowb = std::max(P.a.rowb, P.b.rowb);
   P.xs_floats = std::max(P.a.k, P.b.k);
   auto part_floats = [&](const GemvParams& p) { return ((p.n_rows + 1) / 2 + G - 1) / G * p.nch * 2; };
-  int part = std::max(part_floats(P.a), part_floats(P.b));
-  if (P.att.enabled) {
-    const PairAttn& A = P.att;
-    if (epi_b != EPI_SWIGLU || A.head_dim % 4 || A.head_dim > 128 || (32 % (A.head_dim / 4)) ||
-        A.n_heads * A.ns > G || A.n_heads * A.head_dim != P.a.k || !A.part || !A.seq_len || A.ns > GP_ATT_MAX_NS ||
-        P.a.k > GP_MERGE_V * 4 * CONSUMER_THREADS)
-      return cudaErrorInvalidValue;
-    part = std::max(part, A.n_heads * A.ns);                           // merge weights table
-    P.xs_floats = std::max(P.xs_floats, GP_WARPS * (A.head_dim + 4));  // per-warp partials
-  }
+  const int part = std::max(part_floats(P.a), part_floats(P.b));
   const int budget = optin_smem(dev) - 1024 - (P.xs_floats + part) * 4;
-  static const int smax = [] {  // tuning only
-    const char* e = getenv("GRT_PAIR_STAGES");
-    return e ? std::max(2, atoi(e)) : GP_MAX_STAGES;
-  }();
-  P.stages = std::max(1, std::min({GP_MAX_STAGES, smax, budget / (GP_WARPS * 2 * P.rowb)}));
-  static const int l2pre = [] {
-    const char* e = getenv("GRT_PAIR_L2PRE");
-    return e ? std::max(0, atoi(e)) : 0;
-  }();
-  P.l2_pre = l2pre;
+  P.stages = std::max(1, std::min(GP_MAX_STAGES, budget / (GP_WARPS * 2 * P.rowb)));
   if (P.stages < 2) return cudaErrorInvalidValue;
+  const size_t smem = static_cast<size_t>(GP_WARPS) * P.stages * 2 * P.rowb + (P.xs_floats + part) * 4;
+  // The grid barrier needs all G CTAs resident at once.  The launch is
+  // cooperative (the driver refuses it rather than let a CTA wait for an SM
+  // another CTA holds), and one CTA per SM must fit this configuration.
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemv_pair_kernel<EPI_SWIGLU>, GP_WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(GP_WARPS * 32);
-  cfg.dynamicSmemBytes = static_cast<size_t>(GP_WARPS) * P.stages * 2 * P.rowb + (P.xs_floats + part) * 4;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  switch (epi_b) {
-    case EPI_SWIGLU:
-      return P.att.enabled ? cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_SWIGLU, true>, P)
-                           : cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_SWIGLU, false>, P);
-    case EPI_QKV_ROPE: return cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_QKV_ROPE, false>, P);
-    case EPI_STORE: return cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_STORE, false>, P);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-void pair_attn_shape(int max_len, int n_heads, int head_dim, int sms, int* ns, int* span) {
-  static const int cap = [] {
-    const char* e = getenv("GRT_PAIR_ATTN_NS");
-    return e ? std::max(1, std::min(GP_ATT_MAX_NS, atoi(e))) : GP_ATT_MAX_NS;
-  }();
-  int n = std::max(1, std::min({cap, sms / std::max(1, n_heads), (max_len + 31) / 32}));
-  *ns = n;
-  *span = (max_len + n - 1) / n;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, gemv_pair_kernel<EPI_SWIGLU>, P);
 }
 
 }  // namespace grt

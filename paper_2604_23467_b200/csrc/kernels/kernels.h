@@ -102,55 +102,6 @@ enum DevErr : int {
   DEVERR_TIMEOUT = 8,       // persistent pass watchdog (a CTA never arrived)
 };
 
-// ---- persistent decode pass (decode_pass.cu) --------------------------------
-struct PassLayer {
-  const void* w_qkv;
-  const void* w_o;
-  const void* w_up;
-  const void* w_down;
-  const float* ln1_g;
-  const float* ln1_b;
-  const float* ln2_g;
-  const float* ln2_b;
-  void* k;
-  void* v;
-};
-
-struct PassParams {
-  int n_layers = 0, d = 0, ff = 0, V = 0, h = 0, dh = 0, max_seq = 0;
-  float eps = 1e-5f;
-  const PassLayer* layers = nullptr;  // device array [n_layers]
-  const void* head = nullptr;
-  const float* lnf_g = nullptr;
-  const float* lnf_b = nullptr;
-  float* x = nullptr;      // residual stream [d]
-  float* q = nullptr;      // [d]
-  float* attn = nullptr;   // [d]
-  float* act = nullptr;    // [ff]
-  float* logits = nullptr; // [V]
-  float* part = nullptr;   // [h][nsplit][dh+2]
-  const float* rope_cos = nullptr;
-  const float* rope_sin = nullptr;
-  int* sync = nullptr;     // [n_layers][sync_stride] counters, zeroed by grt_preprocess each pass
-  int sync_stride = 0;
-  const int* seq_len = nullptr;
-  int* err = nullptr;
-  int nsplit = 1, span_cap = 0;
-  float scale = 1.0f;
-  unsigned long long* trace = nullptr;  // optional [grid][trace_stride] %globaltimer phase stamps
-  int trace_stride = 0;
-};
-constexpr int PASS_TRACE_PER_LAYER = 10;  // qkv start/end, attn, wo, up, down (start/end each)
-
-// Static pass of one decode step as ONE persistent kernel (one CTA per SM):
-// every layer's QKV | attention | Wo | gate-up | down phases separated by
-// device-side dependency counters, with each warp's weight ring streaming
-// across phase boundaries.  arch_llama selects RMSNorm/RoPE/SwiGLU.
-cudaError_t launch_decode_pass(Dt wdt, Dt kvdt, bool arch_llama, const PassParams& p, cudaStream_t s, bool pdl);
-cudaError_t decode_pass_prepare(int device);
-int decode_pass_sync_stride(int n_heads);
-int decode_pass_sync_ints(int n_layers, int n_heads);  // size of PassParams::sync
-
 int num_sms(int device);
 
 // Fused (norm) + GEMV + epilogue.  grid_ctas <= 0 picks one CTA per SM.
@@ -159,65 +110,23 @@ size_t gemv_smem_bytes(Dt wdt, int k);
 cudaError_t gemv_prepare(int device);  // raises the dynamic smem limit once per process
 
 // Two consecutive decode GEMVs in one launch (gemv_pair.cu): a = residual GEMV
-// (NORM_NONE, EPI_RESID), b = RMS-normed GEMV on its output (EPI_SWIGLU,
-// EPI_QKV_ROPE or EPI_STORE), grid-wide barrier in between; bf16 weights.
-// Optional phase 0 of a pair launch: decode attention (bf16 KV) for the Wo
-// GEMV's input.  CTA b < n_heads*ns computes the softmax partial (o, m, l) of
-// head b/ns over positions [s*span, (s+1)*span) (s = b%ns) into part; after a
-// grid barrier every CTA merges the partials of all heads into its activation
-// row (replaces the separate attention launch and its kernel boundary).
-struct PairAttn {
-  int enabled = 0;
-  const float* q = nullptr;          // [h*dh] post-RoPE
-  const void* k_cache = nullptr;     // bf16 [h][max_seq][dh]
-  const void* v_cache = nullptr;
-  const int* seq_len = nullptr;
-  float* part = nullptr;             // [h][ns][dh+2]
-  int n_heads = 0, head_dim = 0, max_seq = 0, ns = 1, span = 0;
-  float scale = 1.0f;
-  KvPaging kvp;
-};
+// (Wo: NORM_NONE, EPI_RESID), b = the RMS-normed gate/up GEMV on its output
+// (EPI_SWIGLU), grid-wide barrier in between (cooperative launch); bf16 weights.
 struct GemvPairParams {
   GemvParams a, b;
-  PairAttn att;
   int* bar = nullptr;  // [2] arrive/depart counters, zero-initialised, self-resetting
   int* err = nullptr;
   int stages = 0, rowb = 0, xs_floats = 0;  // set by the launcher
-  int l2_pre = 0;                           // tasks per warp beyond the ring L2-prefetched before the wait
 };
 cudaError_t launch_gemv_pair(int epi_b, GemvPairParams p, cudaStream_t s, bool pdl);
 
-// ---- streaming pass (stream_pass.cu, pass_impl 2): the whole static pass as
-// one persistent launch whose per-warp weight rings stream across every phase
-// and layer boundary (LLaMA arch, bf16 weights + KV).
-struct StreamPassParams {
-  PassParams p;        // dims, per-layer weights, activations, seq_len / err
-  PairAttn att;        // attention phase: part [h][ns][dh+4], ns / span, scale, paging (k/v set per layer)
-  int* bar = nullptr;  // [2] arrive / depart counters, zero-initialised, self-resetting
-  unsigned long long* trace = nullptr;  // optional [grid][trace_stride] %globaltimer phase stamps
-  int trace_stride = 0;
-  // set by stream_pass_configure
-  int ch_d = 0, nch_d = 0, ch_f = 0, nch_fa = 0, nch_fb = 0, k_split = 0, rowb = 0, stages = 0, xs_floats = 0;
-  int part_floats = 0, part_a_floats = 0, grid = 0;
-  int max_stages = 0;          // ring slots per warp cap (0 = as many as fit)
-  int pf_att = 0, pf_bar = 0;  // tasks per warp requested into L2 beyond the ring before the attention / other waits
-  size_t smem_bytes = 0;
-};
-// chunking (elements per k chunk <= chmax), ring depth, smem, grid; fails when
-// one CTA per SM cannot be resident (the grid barrier needs the whole grid)
-cudaError_t stream_pass_configure(StreamPassParams* p, int chmax);
-cudaError_t launch_stream_pass(const StreamPassParams& p, cudaStream_t s, bool pdl);
-cudaError_t stream_pass_prepare();
-constexpr int STREAM_TRACE_PER_LAYER = 8;  // stamps: qkv, attn partial, merge, wo, up, down (+ start, wait)
-// split count / span of the fused attention phase for a bucket of max_len positions
-void pair_attn_shape(int max_len, int n_heads, int head_dim, int sms, int* ns, int* span);
 cudaError_t gemv_pair_prepare();
 
 // Split-K flash-decode over the KV cache for live lengths up to max_len (the
 // graph bucket's end): one thread-block cluster per head, partials merged over
 // distributed shared memory.  Writes out[h*dh].
 cudaError_t launch_attention(Dt kvdt, AttnParams p, int max_len, cudaStream_t s, bool pdl);
-int attention_nsplit(int max_len, int n_heads, int sms);  // persistent pass split count
+int attention_nsplit(int max_len, int n_heads, int sms);  // split partial buffer sizing (AttnParams::part)
 int attention_splits(int max_len, int head_dim);         // cluster size of attn_decode_kernel for a bucket
 cudaError_t attention_prepare();
 

@@ -449,18 +449,10 @@ static cudaError_t fa_launch(const float* Q, const void* k, const void* v, int s
   return cudaGetLastError();
 }
 
-static int fa_enabled() {
-  static const int v = [] {
-    const char* e = getenv("GRT_PREFILL_FA");
-    return e ? atoi(e) : 1;
-  }();
-  return v;
-}
-
 cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, const void* v, int start, int P, int d,
                                      int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s,
                                      KvPaging kvp) {
-  if (kvdt == Dt::BF16 && fa_enabled()) {  // tensor cores (mma.sync) for bf16 KV
+  if (kvdt == Dt::BF16) {  // tensor cores for bf16 KV
     if (dh == 64) return fa_launch<64>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
     if (dh == 128) return fa_launch<128>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
   }

@@ -584,10 +584,7 @@ static PgShape pg_shape(int M, int K, int P, int sms, bool wide_split = false) {
     const int nkb = (K + PG_BK * sh.kbox - 1) / (PG_BK * sh.kbox);
     // persistent CTAs: pick the split whose work items tile the SMs evenly
     // (time ~ waves / split); partials are reduced by a separate parallel kernel
-    static const double per_split = [] {  // cost of one more split (env GRT_PG_KS_COST)
-      const char* e = getenv("GRT_PG_KS_COST");
-      return e ? atof(e) : 0.05;  // measured: TTFT P=10 3.66 -> 3.49 ms (vs 0.005)
-    }();
+    const double per_split = 0.05;  // cost of one more split; measured: TTFT P=10 3.66 -> 3.49 ms (vs 0.005)
     double best = 1e30;
     for (int ks = 1; ks <= std::min(16, nkb); ++ks) {
       const double waves = static_cast<double>((m_tiles * ks + sms - 1) / sms);
@@ -603,10 +600,7 @@ static PgShape pg_shape(int M, int K, int P, int sms, bool wide_split = false) {
   // per flop fall as N grows.  Measured (P=500): narrower tiles to occupy more
   // SMs, or split-K with a last-CTA reduction, are both slower for the small-M
   // GEMMs (Wo, down) than 64 wide tiles.
-  static const int nt_max = [] {  // widest token tile (env GRT_PG_NT_MAX, multiple of 16, <= 256)
-    const char* e = getenv("GRT_PG_NT_MAX");
-    return e ? std::max(16, std::min(PG_MAX_NT, atoi(e) / 16 * 16)) : PG_MAX_NT;
-  }();
+  const int nt_max = PG_MAX_NT;  // 192 / 176 / 128 measured slower at P=500
   sh.n_ntiles = (P + nt_max - 1) / nt_max;
   sh.ntile = ((P + sh.n_ntiles - 1) / sh.n_ntiles + 15) / 16 * 16;
   // small-M GEMMs (Wo, down: 32 tiles) split K so the items fill the SMs;
@@ -614,10 +608,7 @@ static PgShape pg_shape(int M, int K, int P, int sms, bool wide_split = false) {
   const int items = m_tiles * sh.n_ntiles;
   const int nkb = (K + PG_BK - 1) / PG_BK;
   double best = 1e30;
-  static const int wide_ks = [] {  // max split for P > 256 (env GRT_PG_WIDE_KSPLIT)
-    const char* e = getenv("GRT_PG_WIDE_KSPLIT");
-    return e ? std::max(1, atoi(e)) : 2;  // measured: TTFT P=500 12.3 -> 10.9 ms (32 -> 128 CTAs busy)
-  }();
+  const int wide_ks = 2;  // max split for P > 256; measured: TTFT P=500 12.3 -> 10.9 ms (32 -> 128 CTAs busy)
   // P > 256: measured faster unsplit -- except (knob) a residual GEMM whose
   // reduce is fused into the next RMSNorm launch
   const int ks_max = sh.n_ntiles > 1 ? (wide_split ? std::min(wide_ks, nkb) : 1) : std::min(8, nkb);

@@ -111,6 +111,7 @@ void grt_cache_config_default(grt_cache_config* c) {
   c->bucket_size = d.bucket_size;
   c->batched_prefill = d.batched_prefill ? 1 : 0;
   c->pass_impl = d.pass_impl;
+  c->prefill_fuse_norm = d.prefill_fuse_norm ? 1 : 0;
 }
 
 grt_status grt_model_create(const grt_model_config* cfg, grt_model** out) {

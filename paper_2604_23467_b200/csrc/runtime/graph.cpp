@@ -94,6 +94,47 @@ ExecGraphPtr CaptureEngine::instantiate(int key, const std::vector<const KernelI
   return std::make_shared<ExecGraph>(key, exec, kernels.size(), flops, epoch, device_);
 }
 
+ExecGraphPtr CaptureEngine::capture_fn(int key, const std::function<void(cudaStream_t)>& fn, cudaStream_t stream) {
+  open_key(key);
+  struct Close {
+    CaptureEngine* e;
+    int key;
+    ~Close() { e->close_key(key); }
+  } close{this, key};
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cuda_check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+  std::string what;
+  try {
+    fn(stream);
+  } catch (const std::exception& e) {
+    what = e.what();
+  }
+  cudaGraph_t graph = nullptr;
+  const cudaError_t end_err = cudaStreamEndCapture(stream, &graph);
+  if (!what.empty() || end_err != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    raise(GRT_CudaError, "capture of key " + std::to_string(key) + " failed: " +
+                             (what.empty() ? std::string(cudaGetErrorString(end_err)) : what));
+  }
+  size_t n_nodes = 0;
+  cudaGraphGetNodes(graph, nullptr, &n_nodes);
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiateWithFlags(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  cuda_check(ie, "cudaGraphInstantiate");
+  if (n_nodes == 0) {
+    cudaGraphExecDestroy(exec);
+    raise(GRT_EmptyCapture, "capture recorded zero kernels");
+  }
+  uint64_t epoch;
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    epoch = ++epoch_;
+  }
+  return std::make_shared<ExecGraph>(key, exec, n_nodes, 0, epoch, device_);
+}
+
 void CaptureEngine::check(const KernelInvocation& k, bool allow_dynamic) const {
   if (!k.launch || k.spec.op_class == OpClass::Host)
     raise(GRT_CaptureViolation, "kernel '" + k.spec.name + "' needs host values at launch (not capturable)");

@@ -263,7 +263,6 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   cuda_check(cudaSetDevice(cfg_.device), "cudaSetDevice");
   cuda_check(gemv_prepare(cfg_.device), "gemv_prepare");
   cuda_check(attention_prepare(), "attention_prepare");
-  cuda_check(decode_pass_prepare(cfg_.device), "decode_pass_prepare");
   cuda_check(prefill_gemm_prepare(), "prefill_gemm_prepare");
   cuda_check(gemv_pair_prepare(), "gemv_pair_prepare");
 
@@ -316,8 +315,6 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   acc(h * max_nsplit_ * (dh + 2) * 4);
   acc(h * 4);
   acc(cfg_.n_layers * 4 * 4);  // fused-pair barrier counters
-  acc(64);                     // streaming-pass barrier counters
-  acc(static_cast<size_t>(h) * 4 * (dh + 4) * 4);  // fused attention partials
   acc(S * (dh / 2) * 4 * 2);
   acc(sizeof(GrtCtrl));
   acc(sizeof(LoopCtl));
@@ -340,9 +337,6 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
     acc(std::max<size_t>(pf_part, 1) * 4);
     acc(4096 * 4);           // split-K tile counters
   }
-  sync_stride_ = decode_pass_sync_stride(static_cast<int>(h));
-  acc(cfg_.n_layers * sizeof(PassLayer));
-  acc(static_cast<size_t>(sync_ints()) * 4);
   arena_.reserve(need);
 
   layers_.resize(cfg_.n_layers);
@@ -374,9 +368,6 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   attn_part_ = static_cast<float*>(arena_buf(h * max_nsplit_ * (dh + 2) * 4, "attn_part"));
   attn_counters_ = static_cast<int*>(arena_buf(h * 4, "attn_counters"));
   pair_bar_ = static_cast<int*>(arena_buf(cfg_.n_layers * 4 * 4, "pair_barriers"));
-  stream_bar_ = static_cast<int*>(arena_buf(64, "stream_barrier"));
-  if (const char* e = getenv("GRT_STREAM_CHMAX")) stream_chmax_ = std::max(64, atoi(e));  // tuning only
-  pair_attn_part_ = static_cast<float*>(arena_buf(static_cast<size_t>(h) * 4 * (dh + 4) * 4, "pair_attn_part"));
   kv_table_ = static_cast<int*>(arena_buf(static_cast<size_t>(std::max(kv_pages_, 1)) * 4, "kv_block_table"));
   kvp_.page = PS;
   kvp_.n_heads = static_cast<int>(hl);
@@ -402,17 +393,6 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
   loop_ctl_ = static_cast<LoopCtl*>(arena_buf(sizeof(LoopCtl), "loop_ctl"));
   tokens_ = static_cast<int*>(arena_buf((S + 1) * 4, "tokens"));  // +1: a token sampled at a full cache (pos == S)
   uniforms_ = static_cast<double*>(arena_buf(max_gen_ * 8, "uniforms"));
-  pass_layers_ = static_cast<PassLayer*>(arena_buf(cfg_.n_layers * sizeof(PassLayer), "pass_layers"));
-  pass_sync_ = static_cast<int*>(arena_buf(static_cast<size_t>(sync_ints()) * 4, "pass_sync"));
-  {
-    std::vector<PassLayer> pl(cfg_.n_layers);
-    for (int l = 0; l < cfg_.n_layers; ++l) {
-      const LayerBuffers& L = layers_[l];
-      pl[l] = PassLayer{L.w_qkv, L.w_o, L.w_up, L.w_down, L.ln1_g, L.ln1_b, L.ln2_g, L.ln2_b, L.k, L.v};
-    }
-    cuda_check(cudaMemcpy(pass_layers_, pl.data(), pl.size() * sizeof(PassLayer), cudaMemcpyHostToDevice),
-               "pass layers");
-  }
 
   (void)up_rows;
   weight_bytes_ = (V * d + (cfg_.llama() ? 0 : S * d) + Vl * d) * wb +
@@ -580,27 +560,7 @@ bool Model::supports_batched_prefill() const {
          (dh == 16 || dh == 32 || dh == 64 || dh == 128);
 }
 
-// 1 (default): a split-K residual GEMM of the batched prefill hands its partials
-// to the next RMSNorm launch (one kernel instead of reduce + norm)
-static bool fuse_resid_norm_enabled() {
-  static const int v = [] {
-    const char* e = getenv("GRT_PREFILL_FUSE_NORM");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
-}
-
-// 1: the QKV GEMM of prompts > 256 tokens may split K too (partials through the
-// parallel reduce kernel, which applies RoPE / the KV write)
-static bool wide_qkv_split_enabled() {
-  static const int v = [] {
-    const char* e = getenv("GRT_PG_WIDE_QKV");
-    return e ? atoi(e) : 0;
-  }();
-  return v != 0;
-}
-
-void Model::prefill_batched(int p, cudaStream_t s) {
+void Model::prefill_batched(int p, cudaStream_t s, bool fuse_norm) {
   if (!supports_batched_prefill()) raise(GRT_Unsupported, "batched prefill needs the LLaMA arch with bf16 weights");
   if (p < 1 || p > cfg_.max_seq_len) raise(GRT_PromptTooLong, "batched prefill length out of range");
   const int d = cfg_.d_model, dh = cfg_.head_dim(), S = cfg_.max_seq_len;
@@ -617,7 +577,7 @@ void Model::prefill_batched(int p, cudaStream_t s) {
                "prefill embed");
     // Single GPU: a residual GEMM that splits K leaves its partials to the next
     // RMSNorm launch (reduce + residual + norm in one kernel, bit-identical).
-    const bool fuse_rn = T == 1 && fuse_resid_norm_enabled();
+    const bool fuse_rn = T == 1 && fuse_norm;
     PrefillGemmParams prev_down;  // previous layer's down GEMM, if its reduce was deferred
     for (int l = 0; l < cfg_.n_layers; ++l) {
       const LayerBuffers& L = layers_[l];
@@ -643,7 +603,6 @@ void Model::prefill_batched(int p, cudaStream_t s) {
       q.kv_bf16 = kvdt == Dt::BF16;
       q.part = pf_part_;
       q.counters = pf_cnt_;
-      q.wide_split = wide_qkv_split_enabled() ? 1 : 0;
       cuda_check(launch_prefill_gemm(L.w_qkv, pf_Xn_, q, s, true), "prefill qkv");
       cuda_check(launch_prefill_attention(kvdt, pf_Q_, L.k, L.v, start, P, dq, hl, dh, S, scale, pf_A_, s, kvp_),
                  "prefill attention");
@@ -712,62 +671,6 @@ void Model::attention_split(int key, int B, int* nsplit, int* span_cap) const {
   *span_cap = ((max_len + ns - 1) / ns + 3) / 4 * 4;
 }
 
-PassParams Model::pass_params(int key, int B) const {
-  PassParams pp;
-  pp.n_layers = cfg_.n_layers;
-  pp.d = cfg_.d_model;
-  pp.ff = cfg_.d_ff();
-  pp.V = cfg_.vocab_size;
-  pp.h = cfg_.n_heads;
-  pp.dh = cfg_.head_dim();
-  pp.max_seq = cfg_.max_seq_len;
-  pp.eps = cfg_.norm_eps;
-  pp.layers = pass_layers_;
-  pp.head = head_;
-  pp.lnf_g = lnf_g_;
-  pp.lnf_b = lnf_b_;
-  pp.x = x_;
-  pp.q = q_;
-  pp.attn = attn_;
-  pp.act = act_;
-  pp.logits = logits_;
-  pp.part = attn_part_;
-  pp.rope_cos = rope_cos_;
-  pp.rope_sin = rope_sin_;
-  pp.sync = pass_sync_;
-  pp.sync_stride = sync_stride_;
-  pp.seq_len = &ctrl_->seq_len;
-  pp.err = &ctrl_->err;
-  attention_split(key, B, &pp.nsplit, &pp.span_cap);
-  pp.scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim()));  // model.cpp:119
-  return pp;
-}
-
-StreamPassParams Model::stream_params(int key, int B) {
-  const int h = cfg_.n_heads, dh = cfg_.head_dim();
-  const int max_len = std::min(key * B, cfg_.max_seq_len);
-  StreamPassParams sp;
-  sp.p = pass_params(key, B);
-  PairAttn& A = sp.att;
-  A.enabled = 1;
-  A.q = q_;
-  A.seq_len = &ctrl_->seq_len;
-  A.part = pair_attn_part_;
-  A.n_heads = h;
-  A.head_dim = dh;
-  A.max_seq = cfg_.max_seq_len;
-  pair_attn_shape(max_len, h, dh, num_sms(cfg_.device), &A.ns, &A.span);
-  A.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
-  A.kvp = kvp_;
-  sp.bar = stream_bar_;
-  if (const char* e = getenv("GRT_STREAM_PF_ATT")) sp.pf_att = atoi(e);  // tuning only
-  if (const char* e = getenv("GRT_STREAM_PF_BAR")) sp.pf_bar = atoi(e);
-  if (const char* e = getenv("GRT_STREAM_STAGES")) sp.max_stages = atoi(e);
-  cuda_check(stream_pass_prepare(), "stream_pass_prepare");
-  cuda_check(stream_pass_configure(&sp, stream_chmax_), "stream_pass_configure");
-  return sp;
-}
-
 std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* grid, int* stride, int impl) {
   if (impl == 1) {
     const int n_k = 5 * cfg_.n_layers + 1;
@@ -803,70 +706,14 @@ std::vector<uint64_t> Model::trace_pass(int key, int B, cudaStream_t s, int* gri
     *stride = OP_TRACE_CTAS * 8;
     return out;
   }
-  if (impl == 2) {
-    StreamPassParams sp = stream_params(key, B);
-    *grid = sp.grid;
-    *stride = cfg_.n_layers * STREAM_TRACE_PER_LAYER + 8;
-    sp.trace_stride = *stride;
-    const size_t n = static_cast<size_t>(*grid) * *stride;
-    unsigned long long* buf = nullptr;
-    cuda_check(cudaMalloc(&buf, n * 8), "cudaMalloc trace");
-    cuda_check(cudaMemsetAsync(buf, 0, n * 8, s), "memset trace");
-    sp.trace = buf;
-    cuda_check(launch_stream_pass(sp, s, false), "trace pass");
-    cuda_check(cudaStreamSynchronize(s), "trace pass");
-    std::vector<uint64_t> out(n);
-    cuda_check(cudaMemcpy(out.data(), buf, n * 8, cudaMemcpyDeviceToHost), "trace copy");
-    cudaFree(buf);
-    return out;
-  }
-  PassParams pp = pass_params(key, B);
-  *grid = num_sms(cfg_.device);
-  *stride = cfg_.n_layers * PASS_TRACE_PER_LAYER + 8;  // + head start/end, kernel start, ready/waited counts
-  pp.trace_stride = *stride;
-  const size_t n = static_cast<size_t>(*grid) * *stride;
-  unsigned long long* buf = nullptr;
-  cuda_check(cudaMalloc(&buf, n * 8), "cudaMalloc trace");
-  cuda_check(cudaMemsetAsync(buf, 0, n * 8, s), "memset trace");
-  pp.trace = buf;
-  const Dt wdt = cfg_.weight_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
-  const Dt kvdt = cfg_.kv_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
-  cuda_check(launch_decode_pass(wdt, kvdt, cfg_.llama(), pp, s, false), "trace pass");
-  cuda_check(cudaStreamSynchronize(s), "trace pass");
-  std::vector<uint64_t> out(n);
-  cuda_check(cudaMemcpy(out.data(), buf, n * 8, cudaMemcpyDeviceToHost), "trace copy");
-  cudaFree(buf);
-  return out;
+  raise(GRT_InvalidConfig, "trace_pass: only the per-op plan (pass_impl 1) is traced");
 }
 
-// 0: no fusion; 1: every (residual, normed) pair; 2 (default): only Wo +
-// gate/up -- down + QKV measured slower: the down phase's 44 KB activation row
-// leaves room for only 2 ring stages.
-static int gemv_pair_mode() {
-  static const int v = [] {
-    const char* e = getenv("GRT_GEMV_PAIR");
-    return e ? atoi(e) : 2;
-  }();
-  return v;
-}
-static bool gemv_pair_enabled() { return gemv_pair_mode() != 0; }
-// 1: decode attention runs as phase 0 of the Wo + gate/up pair launch.  Off by
-// default: measured 2.54-2.56 ms/token vs 2.48 with the separate attention
-// kernel (7B, P=10; the extra grid barrier and the partial merge cost more than
-// the kernel boundary they remove -- the separate kernel's latency is already
-// covered by the pair kernel's ring fill, which starts at attention's launch).
-static bool pair_attn_enabled() {
-  static const int v = [] {
-    const char* e = getenv("GRT_PAIR_ATTN");
-    return e ? atoi(e) : 0;
-  }();
-  return v != 0;
-}
-static int pair_chmax(const char* var, int dflt) {
-  const char* e = getenv(var);
-  return e ? atoi(e) : dflt;
-}
-
+// The fused pair launch (gemv_pair.cu) covers Wo + gate/up only.  Measured and
+// rejected: down + next QKV as a pair (the down GEMV's 44 KB
+// activation row leaves two ring stages), decode attention as phase 0 of the
+// pair launch (an extra grid barrier + partial merge cost more than the kernel
+// boundary they remove), and a persistent whole-pass kernel.
 std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   const int d = cfg_.d_model, ff = cfg_.d_ff(), V = cfg_.vocab_size, S = cfg_.max_seq_len;
   const int h = cfg_.n_heads, dh = cfg_.head_dim();
@@ -883,55 +730,6 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
   int* err = &ctrl_->err;
 
   std::vector<KernelInvocation> plan;
-  if (impl == 0 && kvp_.page > 0) raise(GRT_Unsupported, "paged KV cache: the persistent pass (pass_impl 0) is contiguous-only");
-  if (impl == 0) {
-    // the whole static pass (model.cpp:118-143) as one persistent kernel
-    const PassParams pp = pass_params(key, B);
-    KernelInvocation inv;
-    inv.spec.name = "decode_pass";
-    inv.spec.op_class = OpClass::Static;
-    const int64_t up_rows = llama ? 2LL * ff : ff;
-    inv.spec.flops = 2LL * cfg_.n_layers * (3LL * d * d + 1LL * d * d + up_rows * d + 1LL * d * ff) + 2LL * V * d +
-                     static_cast<int64_t>(cfg_.n_layers) * h * max_len * (4 * dh + 5);
-    inv.spec.bytes = static_cast<int64_t>(decode_bytes(max_len));
-    inv.bindings = {{pass_layers_, cfg_.n_layers * sizeof(PassLayer)},
-                    {pass_sync_, static_cast<size_t>(sync_ints()) * 4},
-                    {head_, static_cast<size_t>(V) * d * wb},
-                    {x_, static_cast<size_t>(d) * 4},
-                    {logits_, static_cast<size_t>(V) * 4}};
-    for (int l = 0; l < cfg_.n_layers; ++l) {
-      inv.bindings.push_back({layers_[l].w_qkv, 3ull * d * d * wb});
-      inv.bindings.push_back({layers_[l].k, kv_layer_elems_ * kvb});
-      inv.bindings.push_back({layers_[l].v, kv_layer_elems_ * kvb});
-    }
-    inv.launch = [wdt, kvdt, llama, pp](cudaStream_t s) { return launch_decode_pass(wdt, kvdt, llama, pp, s, true); };
-    plan.push_back(std::move(inv));
-    return plan;
-  }
-  if (impl == 2) {
-    // the whole static pass as one persistent launch streaming across phases (stream_pass.cu)
-    const StreamPassParams sp = stream_params(key, B);
-    KernelInvocation inv;
-    inv.spec.name = "stream_pass";
-    inv.spec.op_class = OpClass::Static;
-    inv.spec.flops = 2LL * cfg_.n_layers * (3LL * d * d + 1LL * d * d + 2LL * ff * d + 1LL * d * ff) + 2LL * V * d +
-                     static_cast<int64_t>(cfg_.n_layers) * h * max_len * (4 * dh + 5);
-    inv.spec.bytes = static_cast<int64_t>(decode_bytes(max_len));
-    inv.bindings = {{pass_layers_, cfg_.n_layers * sizeof(PassLayer)},
-                    {stream_bar_, 64},
-                    {pair_attn_part_, static_cast<size_t>(h) * 4 * (dh + 4) * 4},
-                    {head_, static_cast<size_t>(V) * d * wb},
-                    {x_, static_cast<size_t>(d) * 4},
-                    {logits_, static_cast<size_t>(V) * 4}};
-    for (int l = 0; l < cfg_.n_layers; ++l) {
-      inv.bindings.push_back({layers_[l].w_qkv, 3ull * d * d * wb});
-      inv.bindings.push_back({layers_[l].k, kv_layer_elems_ * kvb});
-      inv.bindings.push_back({layers_[l].v, kv_layer_elems_ * kvb});
-    }
-    inv.launch = [sp](cudaStream_t s) { return launch_stream_pass(sp, s, true); };
-    plan.push_back(std::move(inv));
-    return plan;
-  }
   auto next_trace = [&]() -> unsigned long long* {
     return op_trace_ ? op_trace_ + plan.size() * OP_TRACE_CTAS * 8 : nullptr;
   };
@@ -957,13 +755,8 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
     size_t bytes = 0;
     bool set = false;
   } pending;
-  const bool fuse = cfg_.tp_size == 1 && llama && wdt == Dt::BF16 && !op_trace_ && gemv_pair_enabled();
+  const bool fuse = cfg_.tp_size == 1 && llama && wdt == Dt::BF16 && !op_trace_;
   int n_pairs_emitted = 0;
-  PairAttn pending_att;  // attention folded into the next Wo + gate/up launch
-  int att_ns = 1, att_span = 0;
-  pair_attn_shape(max_len, h, dh, num_sms(cfg_.device), &att_ns, &att_span);
-  const bool fuse_attn = fuse && pair_attn_enabled() && kvdt == Dt::BF16 && dh % 4 == 0 && dh <= 128 &&
-                         32 % (dh / 4) == 0 && gemv_pair_mode() == 2 && h * att_ns <= num_sms(cfg_.device);
   auto flush = [&]() {
     if (pending.set) emit_gemv(pending.name, EPI_RESID, NORM_NONE, pending.p, pending.bytes);
     pending.set = false;
@@ -974,24 +767,12 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       pending = Pending{name, p, w_bytes, true};
       return;
     }
-    if (fuse && pending.set && nrm == NORM_RMS &&
-        (epi == EPI_SWIGLU || (gemv_pair_mode() == 1 && (epi == EPI_QKV_ROPE || epi == EPI_STORE)))) {
-      GemvPairParams pp;
+    if (fuse && pending.set && nrm == NORM_RMS && epi == EPI_SWIGLU) {
+      GemvPairParams pp;  // Wo + gate/up (k = 4096 both): 2048-element chunks (8 KB stages)
       pp.a = pending.p;
       pp.b = p;
-      if (epi != EPI_SWIGLU) {  // down + (QKV | head): the 44 KB activation row leaves less room for the ring
-        pp.a.chmax = pair_chmax("GRT_PAIR_CHMAX_A", pp.a.chmax);
-        pp.b.chmax = pair_chmax("GRT_PAIR_CHMAX_B", pp.b.chmax);
-      } else {  // Wo + gate/up (k = 4096 both): 2048-element chunks (8 KB stages) by default
-        pp.a.chmax = pair_chmax("GRT_WOUP_CHMAX", pp.a.chmax);
-        pp.b.chmax = pair_chmax("GRT_WOUP_CHMAX", pp.b.chmax);
-      }
       pp.bar = pair_bar_ + 2 * n_pairs_emitted++;
       pp.err = err;
-      if (epi == EPI_SWIGLU && pending_att.enabled) {
-        pp.att = pending_att;
-        pending_att.enabled = 0;
-      }
       KernelInvocation inv;
       inv.spec.name = pending.name + "+" + name;
       inv.spec.op_class = OpClass::Static;
@@ -999,17 +780,6 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       inv.spec.bytes = static_cast<int64_t>(pending.bytes + w_bytes);
       inv.bindings = {{pending.p.w, pending.bytes}, {p.w, w_bytes}, {pp.bar, 8},
                       {pending.p.x, static_cast<size_t>(pending.p.k) * 4}, {p.x, static_cast<size_t>(p.k) * 4}};
-      if (pp.att.enabled) {
-        const PairAttn& A = pp.att;
-        const size_t cache = kv_layer_elems_ * 2;
-        inv.spec.name = "attention+" + inv.spec.name;
-        inv.spec.flops += static_cast<int64_t>(A.n_heads) * max_len * (4 * A.head_dim + 5);  // kernels.hpp:51
-        inv.spec.bytes += 2LL * max_len * A.n_heads * A.head_dim * 2;
-        inv.bindings.push_back({A.k_cache, cache});
-        inv.bindings.push_back({A.v_cache, cache});
-        inv.bindings.push_back({A.q, static_cast<size_t>(A.n_heads) * A.head_dim * 4});
-        inv.bindings.push_back({A.part, static_cast<size_t>(A.n_heads) * A.ns * (A.head_dim + 4) * 4});
-      }
       inv.launch = [epi, pp](cudaStream_t s) { return launch_gemv_pair(epi, pp, s, true); };
       plan.push_back(std::move(inv));
       pending.set = false;
@@ -1069,25 +839,10 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       p.kv_bf16 = kvdt == Dt::BF16;
       p.kvp = kvp_;
       p.err = err;
-      p.chmax = pair_chmax("GRT_QKV_CHMAX", 0);  // 0: 2048-element chunks
       gemv("qkv", llama ? EPI_QKV_ROPE : EPI_QKV, norm, p, 3ull * dq * d * wb);
     }
     flush();
-    if (fuse_attn) {  // attention = phase 0 of the Wo + gate/up launch (gemv_pair.cu)
-      pending_att.enabled = 1;
-      pending_att.q = q_;
-      pending_att.k_cache = L.k;
-      pending_att.v_cache = L.v;
-      pending_att.seq_len = seq_len;
-      pending_att.part = pair_attn_part_;
-      pending_att.n_heads = hl;
-      pending_att.head_dim = dh;
-      pending_att.max_seq = S;
-      pending_att.ns = att_ns;
-      pending_att.span = att_span;
-      pending_att.scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
-      pending_att.kvp = kvp_;
-    } else {  // attention over [0, seq_len) for this rank's heads
+    {  // attention over [0, seq_len) for this rank's heads
       AttnParams a;
       a.q = q_;
       a.k_cache = L.k;
@@ -1143,7 +898,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       p.k = ffl;
       p.x = act_;
       p.out = x_;
-      p.chmax = pair_chmax("GRT_DOWN_CHMAX", 3072);  // k = 11008 in 4 chunks of 2752 (11 KB stages) measured fastest
+      p.chmax = 3072;  // k = 11008 in 4 chunks of 2752 (11 KB stages): measured fastest
       gemv("down_residual", resid_epi, NORM_NONE, p, 1ull * d * ffl * wb);
       if (T > 1) allreduce_x("allreduce_down");
     }
@@ -1185,10 +940,9 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
 
 const std::vector<KernelInvocation>& Model::plan(int key, int B, int impl) {
   if (B < 1) raise(GRT_InvalidConfig, "bucket_size must be >= 1");
-  if (impl < 0 || impl > 2) raise(GRT_InvalidConfig, "pass_impl must be 0, 1 or 2");
-  if (impl == 2 && (cfg_.tp_size > 1 || !cfg_.llama() || cfg_.weight_dtype != GRT_BF16 || cfg_.kv_dtype != GRT_BF16))
-    raise(GRT_Unsupported, "the streaming pass (pass_impl 2) is single-GPU, LLaMA arch, bf16 weights and KV");
-  if (impl == 0 && cfg_.tp_size > 1) raise(GRT_Unsupported, "the persistent pass (pass_impl 0) is single-GPU only");
+  // pass_impl 0 (one persistent kernel for the whole pass) was measured slower
+  // than the per-op graph and removed
+  if (impl != 1) raise(GRT_Unsupported, "pass_impl must be 1 (the per-op kernel graph)");
   if (key < 1 || key > max_key(B))
     raise(GRT_LengthOutOfRange, "plan key " + std::to_string(key) + " outside [1, " + std::to_string(max_key(B)) + "]");
   std::lock_guard<std::mutex> lk(plan_mu_);

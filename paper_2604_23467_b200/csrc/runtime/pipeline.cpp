@@ -93,6 +93,7 @@ CacheConfig CacheConfig::from_c(const grt_cache_config& c) {
   cc.bucket_size = c.bucket_size;
   cc.batched_prefill = c.batched_prefill != 0;
   cc.pass_impl = c.pass_impl;
+  cc.prefill_fuse_norm = c.prefill_fuse_norm != 0;
   return cc;
 }
 
@@ -450,6 +451,41 @@ StepResponse Session::serve(const StepRequest& req, bool allow_cache, const Mode
   return {req.step_index, StepPath::EagerFallback};
 }
 
+// The batched prefill through the graph cache (the reference serves every
+// prefill pass through it, pipeline.cpp:207-214, prefill_uses_graphs): keyed
+// by the exact prompt length (the GEMM tilings, split-K choices and chunking
+// are functions of it); a miss runs the ~10 launches per layer eagerly and
+// captures the sequence (asynchronously on the capture thread in hybrid mode,
+// inline for ablate_async and under tensor parallelism), so the next prompt of
+// this length is ONE cudaGraphLaunch.
+StepPath Session::serve_prefill(int p, const ModePolicy& pol) {
+  harvest();
+  const bool use_cache = pol.use_cache && cc_.prefill_uses_graphs;
+  const int ck = kPrefillKeyBase + p;
+  if (use_cache) {
+    if (auto hit = cache_->lookup(ck)) {
+      dev_->submit_replay(*hit);
+      (*hit)->mark_launched(dev_->replay());
+      return StepPath::BatchedReplayed;
+    }
+  }
+  model_->prefill_batched(p, dev_->replay(), cc_.prefill_fuse_norm);
+  ++dev_->counters().dispatches;
+  if (use_cache && pol.capture_on_miss && !cache_->contains(ck)) {
+    auto job = [this, p, ck](cudaStream_t cs) {
+      return engine_->capture_fn(ck, [this, p](cudaStream_t st) { model_->prefill_batched(p, st, cc_.prefill_fuse_norm); }, cs);
+    };
+    if (pol.async_capture && model_->tp_size() == 1) {
+      if (!dev_->capture_pending(ck)) dev_->submit_capture(ck, job);
+    } else {
+      ++dev_->counters().captures;
+      cache_->insert(ck, job(dev_->capture_stream()));
+      ++captures_completed_;
+    }
+  }
+  return StepPath::Batched;
+}
+
 ExecGraphPtr Session::static_graph(int key) {
   const int ck = cache_key(key, false);
   if (auto hit = cache_->lookup(ck)) return *hit;
@@ -532,9 +568,9 @@ GenerationResult Session::run(const GenerationRequest& req) {
   cuda_check(cudaEventRecord(ev0, s), "event");
   if (cc_.batched_prefill && model_->supports_batched_prefill()) {
     // all p prompt tokens through each layer at once (tcgen05 GEMMs); leaves
-    // the device exactly where p single-token passes would
-    model_->prefill_batched(p, s);
-    res.prefill_paths.assign(p, StepPath::Batched);
+    // the device exactly where p single-token passes would -- one graph replay
+    // when this prompt length was captured before
+    res.prefill_paths.assign(p, serve_prefill(p, pol));
   } else {
     for (int j = 1; j <= p; ++j) {
       channel.send_request({j, Model::key_of(j, B), pol.fuse_dynamic});
@@ -722,7 +758,7 @@ void Session::prefill(const std::vector<int>& ids) {
     cudaStream_t s = dev_->replay();
     cuda_check(cudaMemcpyAsync(model_->tokens_dev(), ids.data(), ids.size() * sizeof(int), cudaMemcpyHostToDevice, s),
                "prompt");
-    model_->prefill_batched(static_cast<int>(ids.size()), s);
+    model_->prefill_batched(static_cast<int>(ids.size()), s, cc_.prefill_fuse_norm);
     cuda_check(cudaStreamSynchronize(s), "prefill");
     cur_len_ = static_cast<int>(ids.size());
     check_device_errors();

@@ -205,9 +205,9 @@ class Model {
   // Static plan for one bucket key (lengths ((key-1)*B, key*B]).  Memoized;
   // the returned reference is stable for the model's lifetime.  Raises
   // LengthOutOfRange outside [1, max_key].
-  // impl 0: the whole pass is ONE persistent kernel (decode_pass.cu);
-  // impl 1: 5 per-op kernels per layer + head (gemv.cu / attention.cu).
-  const std::vector<KernelInvocation>& plan(int key, int bucket_size, int impl = 0);
+  // impl 1 (the only one): 4 kernels per layer + LM head (gemv.cu, attention.cu,
+  // gemv_pair.cu); a persistent single-kernel pass was measured slower and removed.
+  const std::vector<KernelInvocation>& plan(int key, int bucket_size, int impl = 1);
   int max_key(int bucket_size) const { return (cfg_.max_seq_len + bucket_size - 1) / bucket_size; }
   static int key_of(int length, int bucket_size) { return (length + bucket_size - 1) / bucket_size; }
 
@@ -246,7 +246,6 @@ class Model {
   void set_kv_block_table(const int* table, int n);
   int64_t kv_row_host(int head, int pos) const;  // host view of kv_row (common.cuh)
   const std::set<const void*>& buffer_set() const { return buffers_; }
-  int sync_ints() const { return decode_pass_sync_ints(cfg_.n_layers, cfg_.n_heads); }
 
   // Batched prefill (LLaMA arch, bf16 weights): tokens_dev()[0, p) pass through
   // each layer together -- tcgen05 GEMMs for the projections, one causal
@@ -254,7 +253,7 @@ class Model {
   // the state p token-by-token passes would (KV rows [0, p), seq_len = p,
   // residual/logits of the last token).  Enqueued on `s`, no host sync.
   bool supports_batched_prefill() const;
-  void prefill_batched(int p, cudaStream_t s);
+  void prefill_batched(int p, cudaStream_t s, bool fuse_norm = true);
 
   // Tensor parallelism (tp_size > 1): this model holds rank tp_rank's shard --
   // QKV/gate/up/head column-parallel (heads, d_ff and vocab split), Wo/down
@@ -267,10 +266,8 @@ class Model {
   float* logits_local_dev() const { return logits_local_; }
   const void* emb_dev() const { return emb_; }
   const void* pos_dev() const { return pos_ ? pos_ : emb_; }
-  void reset_pass_sync() {
-    cudaMemset(pass_sync_, 0, static_cast<size_t>(sync_ints()) * 4);
+  void reset_pass_sync() {  // after a grid-barrier watchdog expiry
     cudaMemset(pair_bar_, 0, static_cast<size_t>(cfg_.n_layers) * 4 * 4);
-    cudaMemset(stream_bar_, 0, 64);
     cudaMemset(&ctrl_->err, 0, sizeof(int));
     cudaDeviceSynchronize();
   }
@@ -284,13 +281,10 @@ class Model {
   void attention_split(int key, int bucket_size, int* nsplit, int* span_cap) const;
 
  public:
-  PassParams pass_params(int key, int bucket_size) const;
-  StreamPassParams stream_params(int key, int bucket_size);  // pass_impl 2 (configured for this device)
-  // Runs one persistent pass with per-CTA %globaltimer phase stamps (profiling).
-  // impl 0: per-CTA phase stamps of the persistent pass ([grid][stride]);
-  // impl 1: the per-op plan captured as a graph, [n_kernels][OP_TRACE_CTAS*4]
-  // stamps (start, released, operands ready, done) per CTA.
-  std::vector<uint64_t> trace_pass(int key, int bucket_size, cudaStream_t s, int* grid, int* stride, int impl = 0);
+  // Profiling: the per-op plan captured as a graph and replayed once with
+  // per-CTA %globaltimer stamps, [n_kernels][OP_TRACE_CTAS*8] (start,
+  // released, operands ready, done, first stage, loop done).
+  std::vector<uint64_t> trace_pass(int key, int bucket_size, cudaStream_t s, int* grid, int* stride, int impl = 1);
 
  private:
   void* arena_buf(size_t bytes, const char* what);
@@ -309,9 +303,6 @@ class Model {
   void *pf_Xn_ = nullptr, *pf_A_ = nullptr, *pf_act_ = nullptr;
   int* pf_cnt_ = nullptr;
   int* pair_bar_ = nullptr;
-  int* stream_bar_ = nullptr;  // [2] streaming-pass barrier (self-resetting)
-  int stream_chmax_ = 2048;    // streaming pass: k-chunk elements per ring stage
-  float* pair_attn_part_ = nullptr;
   KvPaging kvp_;
   int kv_pages_ = 0;
   size_t kv_layer_elems_ = 0;
@@ -327,9 +318,6 @@ class Model {
   double* uniforms_ = nullptr;
   int max_gen_ = 0;
   int max_nsplit_ = 1;
-  PassLayer* pass_layers_ = nullptr;  // device [n_layers]
-  int* pass_sync_ = nullptr;          // device [n_layers * sync_stride + 1]
-  int sync_stride_ = 0;
   volatile int* h_out_tokens_ = nullptr;
   volatile unsigned long long* h_out_stamps_ = nullptr;
   uint64_t weight_bytes_ = 0;
@@ -409,6 +397,9 @@ class CaptureEngine {
   // instantiates them.  Raises CaptureViolation / ForeignBuffer / EmptyCapture /
   // CaptureInProgress like CaptureSession::record / end_capture.
   ExecGraphPtr capture(int key, const std::vector<const KernelInvocation*>& kernels, cudaStream_t stream);
+  // captures whatever `fn` enqueues on `stream` (an internal, arena-only
+  // sequence such as the batched prefill) under `key`
+  ExecGraphPtr capture_fn(int key, const std::function<void(cudaStream_t)>& fn, cudaStream_t stream);
   // same checks, recorded into an existing (conditional body) graph
   void record_into(cudaGraph_t body, const std::vector<const KernelInvocation*>& kernels, cudaStream_t stream);
   void validate(const std::vector<const KernelInvocation*>& kernels) const;
@@ -495,7 +486,12 @@ struct ModePolicy {
 };
 ModePolicy policy_for(RunMode m) noexcept;
 
-enum class StepPath { Replayed = GRT_PATH_REPLAYED, EagerFallback = GRT_PATH_EAGER_FALLBACK, Batched = GRT_PATH_BATCHED };
+enum class StepPath {
+  Replayed = GRT_PATH_REPLAYED,
+  EagerFallback = GRT_PATH_EAGER_FALLBACK,
+  Batched = GRT_PATH_BATCHED,
+  BatchedReplayed = GRT_PATH_BATCHED_REPLAYED
+};
 
 struct StepRequest {
   int step_index = 0;
@@ -530,7 +526,8 @@ struct CacheConfig {
   EvictionPolicy policy = EvictionPolicy::LeastUsed;
   int bucket_size = 64;
   bool batched_prefill = false;
-  int pass_impl = 1;  // 1: per-op kernel graph (default, fastest); 0: persistent single-kernel pass
+  int pass_impl = 1;  // 1: the per-op kernel graph (the only supported value)
+  bool prefill_fuse_norm = true;  // split-K residual partials reduced inside the next RMSNorm launch
   static CacheConfig from_c(const grt_cache_config& c);
 };
 
@@ -645,6 +642,9 @@ class Session {
   std::vector<const KernelInvocation*> step_kernels(int key, bool fused);
   ExecGraphPtr capture_now(int key, bool fused, cudaStream_t s);
   int cache_key(int key, bool fused) const { return fused ? key : -key; }
+  // prefill graphs live in the same cache under keys kPrefillKeyBase + prompt length
+  static constexpr int kPrefillKeyBase = 1 << 24;
+  StepPath serve_prefill(int p, const ModePolicy& pol);
   void check_device_errors();
 
   Model* model_;

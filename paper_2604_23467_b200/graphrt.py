@@ -91,7 +91,8 @@ def mode_from_name(name: str) -> RunMode:
 class StepPath(enum.IntEnum):
     Replayed = 0
     EagerFallback = 1
-    Batched = 2  # prompt token served by the batched (tcgen05) prefill
+    Batched = 2  # prompt served by the batched (tcgen05) prefill, launched eagerly
+    BatchedReplayed = 3  # the batched prefill replayed as one CUDA graph (per prompt length)
 
 
 class EvictionPolicy(enum.IntEnum):
@@ -119,7 +120,7 @@ class _ModelConfig(C.Structure):
 class _CacheConfig(C.Structure):
     _fields_ = [("capacity", C.c_uint64), ("warmup_lo", C.c_int32), ("warmup_hi", C.c_int32),
                 ("prefill_uses_graphs", C.c_int32), ("policy", C.c_int32), ("bucket_size", C.c_int32),
-                ("batched_prefill", C.c_int32), ("pass_impl", C.c_int32)]
+                ("batched_prefill", C.c_int32), ("pass_impl", C.c_int32), ("prefill_fuse_norm", C.c_int32)]
 
 
 class _SampleParams(C.Structure):
@@ -332,7 +333,8 @@ class CacheConfig:
     policy: EvictionPolicy = EvictionPolicy.LeastUsed
     bucket_size: int = 64
     batched_prefill: bool = False
-    pass_impl: int = 1  # 1 per-op kernel graph (default), 0 persistent single-kernel pass
+    pass_impl: int = 1  # 1: the per-op kernel graph (the only supported value)
+    prefill_fuse_norm: bool = True  # split-K residual partials reduced inside the next RMSNorm launch
 
     def _c(self) -> _CacheConfig:
         c = _CacheConfig()
@@ -341,6 +343,7 @@ class CacheConfig:
         c.policy, c.bucket_size = int(self.policy), self.bucket_size
         c.batched_prefill = 1 if self.batched_prefill else 0
         c.pass_impl = int(self.pass_impl)
+        c.prefill_fuse_norm = 1 if self.prefill_fuse_norm else 0
         return c
 
 
@@ -671,12 +674,10 @@ class Session:
         return [(nm[i].decode(), ms[i], by[i]) for i in range(min(n.value, cap))]
 
     def trace_pass(self, key: int):
-        """Per-CTA %globaltimer stamps of one persistent pass: array [grid, stride] (ns)."""
+        """Per-CTA %globaltimer stamps of one replay of the static plan: array
+        [kernels, OP_TRACE_CTAS * 8] (ns)."""
         import numpy as np
-        if self.cache_cfg.pass_impl == 1:
-            cap = (5 * self.model.cfg.n_layers + 1) * 8192
-        else:
-            cap = 160 * (self.model.cfg.n_layers * 10 + 8)
+        cap = (5 * self.model.cfg.n_layers + 1) * 8192
         buf = (C.c_uint64 * cap)()
         gr, st = C.c_int32(), C.c_int32()
         _check(lib().grt_trace_pass(self._h, key, buf, cap, C.byref(gr), C.byref(st)))

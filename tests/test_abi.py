@@ -46,7 +46,7 @@ def test_status_names_follow_reference_errc_order():
     for i, n in enumerate(names):
         assert L.grt_status_name(i).decode() == n
         assert g.Errc(i).name == n
-    assert L.grt_abi_version() == 1
+    assert L.grt_abi_version() == 2
 
 
 @pytest.mark.parametrize("shape", [(64, 256, 600, 0, 1), (16, 32, 24, 0, 1), (4096, 32000, 640, 1, 0),

@@ -143,22 +143,20 @@ def test_sampler_greedy_and_temperature(vocab):
 
 # --------------------------------------------------------------------- models
 
-@pytest.mark.parametrize("impl", [0, 1])
-def test_tiny_ref_fp32_matches_reference_fixture(golden, impl):
-    """Reference defaults (tiny-ref): SURVEY Appendix A tokens, logits <= 1e-4,
-    for the persistent pass (impl 0) and the per-op kernels (impl 1)."""
+def test_tiny_ref_fp32_matches_reference_fixture(golden):
+    """Reference defaults (tiny-ref): SURVEY Appendix A tokens, logits <= 1e-4."""
     gd = golden("tiny_ref_greedy.json")
-    s = g.Session(g.ModelConfig(), cache(bucket=64, pass_impl=impl))
+    s = g.Session(g.ModelConfig(), cache(bucket=64))
     toks, worst = step_parity(s, gd["prompt"], len(gd["tokens"]), gd["tokens"], gd["logits"], 1e-4)
     assert worst <= 1e-4, worst
     assert toks == gd["tokens"]
 
 
-@pytest.mark.parametrize("bucket,impl", [(1, 0), (64, 0), (64, 1)])
-def test_all_modes_reproduce_reference_tokens(golden, bucket, impl):
+@pytest.mark.parametrize("bucket", [1, 64])
+def test_all_modes_reproduce_reference_tokens(golden, bucket):
     """c1/c2 (acceptance_main.cpp:77-113): every RunMode yields the reference tokens."""
     gd = golden("tiny_ref_greedy.json")
-    s = g.Session(g.ModelConfig(), cache(bucket=bucket, hi=20, pass_impl=impl))
+    s = g.Session(g.ModelConfig(), cache(bucket=bucket, hi=20))
     for mode in g.ALL_MODES:
         r = s.run(g.GenerationRequest(mode=mode, prompt=gd["prompt"], gen_len=32))
         assert r.tokens == gd["tokens"], g.mode_name(mode)
@@ -199,22 +197,20 @@ def test_wide_temperature(golden):
     assert r.tokens == gd["tokens"]
 
 
-@pytest.mark.parametrize("impl", [0, 1])
 @pytest.mark.parametrize("name,tol", [("llama_tiny_f32", 1e-4), ("llama_tiny_bf16", 2e-2),
                                       ("llama_tiny_philox_bf16", 2e-2)])
-def test_llama_tiny_vs_oracle(golden, name, tol, impl):
+def test_llama_tiny_vs_oracle(golden, name, tol):
     gd = golden(name + ".json")
     c = gd["config"]
     mc = g.ModelConfig(arch=g.ARCH_LLAMA, d_ff_=c["d_ff"], weight_dtype=c.get("weight_dtype", 0),
                        kv_dtype=c.get("kv_dtype", 0), init=c.get("init", 0))
-    s = g.Session(mc, cache(pass_impl=impl))
+    s = g.Session(mc, cache())
     toks, worst = step_parity(s, gd["prompt"], len(gd["tokens"]), gd["tokens"], gd["logits"], tol)
     assert worst <= tol, worst
     margin_ok_tokens(toks, gd["tokens"], gd["logits"], tol)
 
 
-@pytest.mark.parametrize("impl", [0, 1])
-def test_llama_7b_dims_two_layers_vs_oracle(impl):
+def test_llama_7b_dims_two_layers_vs_oracle():
     """LLaMA-2 7B layer shapes (d 4096, ff 11008, V 32000, bf16, Philox init) on
     2 layers against the C oracle: logits max-abs <= 2e-2 after the final norm."""
     kw = dict(arch=g.ARCH_LLAMA, n_layers=2, d_model=4096, n_heads=32, vocab_size=32000, max_seq_len=64,
@@ -224,7 +220,7 @@ def test_llama_7b_dims_two_layers_vs_oracle(impl):
                        n_threads=0)
     prompt = po.make_prompt(42, 6, 32000)
     ref_toks, ref_logits = o.generate_greedy(prompt, 4)
-    s = g.Session(g.ModelConfig(**kw), cache(pass_impl=impl))
+    s = g.Session(g.ModelConfig(**kw), cache())
     toks, worst = step_parity(s, prompt, 4, ref_toks, ref_logits, 2e-2)
     assert worst <= 2e-2, worst
     margin_ok_tokens(toks, ref_toks, ref_logits, 2e-2)
@@ -269,13 +265,13 @@ def test_hybrid_replays_warm_keys_and_captures_the_rest():
 
 # ------------------------------------------------- device-resident decode loop
 
-@pytest.mark.parametrize("bucket,impl", [(4, 1), (64, 1), (8, 0)])
-def test_device_loop_is_one_launch_and_reproduces_reference(golden, bucket, impl):
+@pytest.mark.parametrize("bucket", [4, 8, 64])
+def test_device_loop_is_one_launch_and_reproduces_reference(golden, bucket):
     """RunMode.DeviceLoop: the whole decode is ONE graph
     launch (WHILE node, bucket SWITCH on the device) and yields the reference
     binary's tokens; small buckets make the loop cross many switch bodies."""
     gd = golden("tiny_ref_greedy.json")
-    s = g.Session(g.ModelConfig(), cache(bucket=bucket, hi=50, pass_impl=impl))  # prefill keys warm
+    s = g.Session(g.ModelConfig(), cache(bucket=bucket, hi=50))  # prefill keys warm
     for _ in range(2):  # second run reuses the instantiated loop graph
         r = s.run(g.GenerationRequest(mode=g.RunMode.DeviceLoop, prompt=gd["prompt"], gen_len=32))
         assert r.tokens == gd["tokens"]
@@ -334,23 +330,6 @@ def test_device_loop_llama_7b_dims_matches_hybrid():
     b = s.run(g.GenerationRequest(mode=g.RunMode.DeviceLoop, prompt=prompt, gen_len=40))
     assert a.tokens == b.tokens
     assert b.counters.graph_replays == 1 and b.counters.kernel_launches == 0
-
-
-def test_persistent_pass_matches_per_op_kernels():
-    """The single-kernel pass and the per-op plan compute the same pass (chunk
-    sizes differ, so fp32 summation order differs): logits agree to 1e-4."""
-    mc = g.ModelConfig(arch=g.ARCH_LLAMA, d_ff_=176, weight_dtype=g.BF16, kv_dtype=g.BF16, init=g.INIT_PHILOX,
-                       n_layers=3, max_seq_len=200, seed=11)
-    prompt = po.make_prompt(5, 40, 256)
-    outs = []
-    for impl in (0, 1):
-        s = g.Session(g.Model(mc), cache(bucket=32, pass_impl=impl))
-        r = s.run(g.GenerationRequest(prompt=prompt, gen_len=100))
-        assert len(r.tokens) == 100
-        s.reset()
-        s.prefill(prompt)
-        outs.append(s.logits())
-    assert np.abs(outs[0] - outs[1]).max() < 1e-4
 
 
 def test_long_context_attention_splits():
@@ -566,3 +545,33 @@ def test_tp_batched_prefill_and_steps_match_single_gpu(tp, kw, plen, tol):
     got = g.tp_emu_threaded(g.ModelConfig(tp_size=tp, **base), prompt, (3, 9))
     err = float(np.abs(ref.logits() - got).max())
     assert err <= tol, err
+
+
+@pytest.mark.parametrize("mode", [g.RunMode.Hybrid, g.RunMode.AblateAsync])
+def test_batched_prefill_is_captured_per_prompt_length(mode):
+    """The TTFT path through the graph cache (pipeline.cpp:207-214,
+    prefill_uses_graphs): the first request of a prompt length runs the batched
+    prefill eagerly and captures it (async on the capture thread in hybrid,
+    inline for ablate_async); the next request of that length replays it as ONE
+    graph launch with identical results.  Eager mode never uses graphs."""
+    kw = dict(arch=g.ARCH_LLAMA, n_layers=2, d_model=128, n_heads=2, vocab_size=512, max_seq_len=256, seed=9,
+              d_ff_=320, weight_dtype=g.BF16, kv_dtype=g.BF16, init=g.INIT_PHILOX)
+    from paper_2604_23467_b200.bench_harness import make_prompt
+    prompt = make_prompt(42, 37, 512)
+    s = g.Session(g.ModelConfig(**kw), g.CacheConfig(bucket_size=32, batched_prefill=True))
+    r1 = s.run(g.GenerationRequest(mode=mode, prompt=prompt, gen_len=8))
+    assert r1.prefill_paths == [g.StepPath.Batched] * 37
+    r2 = s.run(g.GenerationRequest(mode=mode, prompt=prompt, gen_len=8))
+    assert r2.prefill_paths == [g.StepPath.BatchedReplayed] * 37
+    assert r2.tokens == r1.tokens
+    # one graph launch for the whole prompt + one per decode step
+    assert r2.counters.graph_replays == 1 + 8
+    lg2 = s.logits()
+    # another prompt length misses, the first length still replays
+    r3 = s.run(g.GenerationRequest(mode=mode, prompt=prompt[:20], gen_len=4))
+    assert r3.prefill_paths == [g.StepPath.Batched] * 20
+    e = g.Session(s.model, g.CacheConfig(bucket_size=32, batched_prefill=True))
+    re = e.run(g.GenerationRequest(mode=g.RunMode.Eager, prompt=prompt, gen_len=8))
+    re2 = e.run(g.GenerationRequest(mode=g.RunMode.Eager, prompt=prompt, gen_len=8))
+    assert re2.prefill_paths == [g.StepPath.Batched] * 37 and re2.tokens == r1.tokens
+    assert np.array_equal(e.logits(), lg2)
