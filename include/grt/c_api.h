@@ -280,7 +280,8 @@ grt_status grt_capture_record(grt_capture* c, int32_t op, int32_t plan_key, int3
 grt_status grt_capture_record_external(grt_capture* c, void* ptr, uint64_t bytes);
 grt_status grt_capture_end(grt_capture* c, int32_t* kernel_count, uint64_t* epoch);
 grt_status grt_capture_state_get(grt_capture* c, int32_t* state, int32_t* recorded);
-void grt_capture_destroy(grt_capture* c);
+void grt_capture_destroy(grt_capture* c);  /* also after its session: destroying a session closes its
+                                             captures (calls then return SessionClosed) */
 /* number of static kernels in plan(key) (Model::plan, model.cpp:118-154) */
 grt_status grt_plan_size(grt_session* s, int32_t key, int32_t* n);
 /* One step through the cached graph of `key` with `token` at position cur_len.

@@ -316,7 +316,9 @@ int oc_create(const oc_config* cfg, oc_model** out) {
   m->d_ff = cfg->d_ff > 0 ? cfg->d_ff : 4 * cfg->d_model;
   m->head_dim = cfg->d_model / cfg->n_heads;
 #ifdef _OPENMP
-  if (cfg->n_threads > 0) omp_set_num_threads(cfg->n_threads);
+  /* the OpenMP team size is process-global: set it on every create (0 = all
+     cores), so an earlier 1-thread model does not leave later ones serial */
+  omp_set_num_threads(cfg->n_threads > 0 ? cfg->n_threads : omp_get_num_procs());
 #endif
   declare_tensors(m);
   init_weights(m);

@@ -26,7 +26,11 @@ typedef unsigned int u32;
 // memory (u32: w = e * 2^31 <= 2^31) when they fit; the host launches the
 // sampler kernels with GRT_V * 4 bytes of dynamic shared memory then (jit.cpp)
 #define GRT_SAMPLE_SMEM_MAX 196608
-#if GRT_V * 4 <= GRT_SAMPLE_SMEM_MAX
+// 2: weights + a u16 candidate list (radix select with compaction, below);
+// 1: weights only (8-bit radix passes over the whole vocabulary); 0: recomputed
+#if GRT_V * 6 <= GRT_SAMPLE_SMEM_MAX && GRT_V <= 65535
+#define GRT_TOPKP_SMEM 2
+#elif GRT_V * 4 <= GRT_SAMPLE_SMEM_MAX
 #define GRT_TOPKP_SMEM 1
 #else
 #define GRT_TOPKP_SMEM 0
@@ -261,6 +265,158 @@ __device__ void radix_pick(u64* hist, int shift, u64& prefix, u64& mask, u64& ne
   __syncthreads();
 }
 
+#if GRT_TOPKP_SMEM == 2
+// ---- radix select with candidate compaction (11-bit digits) -------------------
+// The threshold key of oc_sample_topkp (oracle.c) -- walking the rank keys in
+// descending order, the key at which the running total of `val` (1 for top-k,
+// the weight for top-p) first reaches `need` -- found digit by digit from the
+// top (bits 37-47, 26-36, 15-25, 4-14, 0-10; the last pass overlaps bits already
+// fixed, which every candidate shares).  Pass 0 scans the whole vocabulary
+// (keys >= kfloor); every pass keeps only the keys in the chosen digit bucket,
+// compacted into a u16 list in shared memory, so later passes touch a handful
+// of candidates instead of 32000 keys.  Integer sums throughout: the result is
+// the serial walk's exactly.
+#define RS_B 2048
+#define RS_PER ((GRT_V + GRT_SAMPLE_THREADS - 1) / GRT_SAMPLE_THREADS)
+
+__device__ __forceinline__ u64 rs_key(const u32* wsm, int i) { return ((u64)wsm[i] << 16) | (u64)(0xFFFF - i); }
+
+// block-wide exclusive scan of one int per thread; returns the total
+__device__ __forceinline__ int rs_scan(int v, int* excl, int* warp_tot) {
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += n;
+  }
+  if (lane == 31) warp_tot[wp] = x;
+  __syncthreads();
+  if (wp == 0) {
+    int t = lane < (GRT_SAMPLE_THREADS >> 5) ? warp_tot[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += n;
+    }
+    warp_tot[lane] = t;  // inclusive over warps
+  }
+  __syncthreads();
+  *excl = x - v + (wp > 0 ? warp_tot[wp - 1] : 0);
+  const int total = warp_tot[31];
+  __syncthreads();
+  return total;
+}
+
+// the highest digit whose inclusive descending cumulative reaches need (else 0)
+// and the cumulative above it; thread t owns buckets 2t, 2t+1
+__device__ __forceinline__ void rs_pick(const u64* hist, u64 need, int* s_dg, u64* s_above, u64* wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const u64 h0 = hist[2 * tid], h1 = hist[2 * tid + 1], sm = h0 + h1;
+  u64 v = sm;  // inclusive suffix within the warp
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 n = __shfl_down_sync(0xffffffffu, v, o);
+    if (lane + o < 32) v += n;
+  }
+  if (lane == 0) wsum[wp] = v;
+  if (tid == 0) *s_dg = 0;
+  __syncthreads();
+  if (wp == 0) {  // exclusive suffix over the warps
+    u64 t = wsum[lane];
+    u64 incl = t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 n = __shfl_down_sync(0xffffffffu, incl, o);
+      if (lane + o < 32) incl += n;
+    }
+    wsum[lane] = incl - t;
+  }
+  __syncthreads();
+  const u64 S = v + wsum[wp];  // cumulative from bucket 2*tid upward
+  const u64 E = S - sm;        // above bucket 2*tid+1
+  int b = -1;
+  if (E + h1 >= need) b = 2 * tid + 1;
+  else if (tid > 0 && S >= need) b = 2 * tid;
+  if (b >= 1) atomicMax(s_dg, b);
+  __syncthreads();
+  const int dg = *s_dg;
+  if (dg >= 1 && (dg >> 1) == tid) *s_above = (dg & 1) ? E : E + h1;
+  if (dg == 0 && tid == 0) *s_above = E + h1;  // total - hist[0]
+  __syncthreads();
+}
+
+__device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kfloor, bool by_weight, u64 need,
+                                    u64* hist) {
+  __shared__ int s_dg, s_n, warp_tot[32];
+  __shared__ u64 s_above, wsum[32];
+  const int tid = threadIdx.x;
+  int n = -1;  // -1: every index of the vocabulary with key >= kfloor
+  u64 prefix = 0;
+  const int shifts[5] = {37, 26, 15, 4, 0};
+#pragma unroll 1
+  for (int ps = 0; ps < 5; ++ps) {
+    const int sh = shifts[ps];
+    for (int b = tid; b < RS_B; b += GRT_SAMPLE_THREADS) hist[b] = 0;
+    __syncthreads();
+    if (n < 0) {
+      for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+        const u64 key = rs_key(wsm, i);
+        if (key >= kfloor) atomicAdd(&hist[(key >> sh) & (RS_B - 1)], by_weight ? (u64)wsm[i] : 1ull);
+      }
+    } else {
+      for (int j = tid; j < n; j += GRT_SAMPLE_THREADS) {
+        const int i = cand[j];
+        atomicAdd(&hist[(rs_key(wsm, i) >> sh) & (RS_B - 1)], by_weight ? (u64)wsm[i] : 1ull);
+      }
+    }
+    __syncthreads();
+    rs_pick(hist, need, &s_dg, &s_above, wsum);
+    const u64 dg = (u64)s_dg;
+    need -= s_above;
+    prefix |= dg << sh;
+    // keep the keys of bucket dg, compacted into cand (order is irrelevant: the
+    // select works on the candidate SET, so warp-aggregated slots are fine)
+    if (n < 0) {
+      if (tid == 0) s_n = 0;
+      __syncthreads();
+      const int lane = tid & 31;
+      for (int base = 0; base < GRT_V; base += GRT_SAMPLE_THREADS) {
+        const int i = base + tid;  // consecutive indices per warp: no bank conflicts
+        bool f = false;
+        if (i < GRT_V) {
+          const u64 key = rs_key(wsm, i);
+          f = key >= kfloor && ((key >> sh) & (RS_B - 1)) == dg;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        int slot = 0;
+        if (lane == 0 && bal) slot = atomicAdd(&s_n, __popc(bal));
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (f) cand[slot + __popc(bal & ((1u << lane) - 1))] = (unsigned short)i;
+      }
+      __syncthreads();
+      n = s_n;
+    } else {
+      int out = 0;
+      for (int base = 0; base < n; base += GRT_SAMPLE_THREADS) {  // tile: read all, then write
+        const int j = base + tid;
+        const int i = j < n ? cand[j] : 0;
+        const int f = j < n && ((rs_key(wsm, i) >> sh) & (RS_B - 1)) == dg;
+        int pos;
+        const int total = rs_scan(f, &pos, warp_tot);  // (its barriers order the reads before the writes)
+        if (f) cand[out + pos] = (unsigned short)i;
+        out += total;
+        __syncthreads();
+      }
+      n = out;
+    }
+    if (tid == 0) s_n = n;
+    __syncthreads();
+    n = s_n;
+    if (n <= 0) break;  // cannot happen (need <= total at every pass); the prefix stands
+  }
+  const u64 r = n == 1 ? rs_key(wsm, cand[0]) : prefix;
+  __syncthreads();
+  return r;
+}
+#endif
+
 // Returns the sampled token (block-uniform) or -1 on a prefill pass.  With
 // fence == false the caller issues the system fence for the host-mapped slots.
 __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, bool fence = true) {
@@ -427,6 +583,27 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
 #endif
     const int top_k = ctrl->top_k;
     const float top_p = ctrl->top_p;
+#if GRT_TOPKP_SMEM == 2
+    unsigned short* cand = (unsigned short*)(wsm + GRT_V);
+    __shared__ u64 rs_hist[RS_B];
+    // (1) top-k threshold key: the top_k-th largest key
+    u64 kth = 0;
+    if (top_k > 0 && top_k < GRT_V) kth = radix_select_compact(wsm, cand, 0, false, (u64)top_k, rs_hist);
+    // (2) top-p threshold key among keys >= kth
+    u64 W = 0;
+    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+      const u64 w = GRT_W(i);
+      if (topkp_key(w, i) >= kth) W += w;
+    }
+    W = block_sum_u64(W, redu);
+    u64 kappa = kth;
+    if (top_p > 0.0f && top_p < 1.0f) {
+      u64 thresh = (u64)((double)top_p * (double)W);
+      if (thresh < 1) thresh = 1;
+      const u64 kp = radix_select_compact(wsm, cand, kth, true, thresh, rs_hist);
+      kappa = kp > kth ? kp : kth;
+    }
+#else
     // (1) top-k threshold key
     u64 kth = 0;
     if (top_k > 0 && top_k < GRT_V) {
@@ -482,6 +659,73 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
       }
       kappa = prefix > kth ? prefix : kth;
     }
+#endif
+#if GRT_TOPKP_SMEM == 2
+    // (3) draw and inverse CDF in index order over the kept set: warp w owns the
+    // contiguous index block [w*VB, (w+1)*VB) and its lanes read consecutive
+    // indices (no bank conflicts); warp totals are scanned in warp order, the
+    // warp holding the draw walks its block 32 indices at a time (integer
+    // prefix sums: the serial walk's result exactly)
+    {
+      constexpr int NW = GRT_SAMPLE_THREADS / 32;
+      constexpr int VB = ((GRT_V + NW - 1) / NW + 31) / 32 * 32;
+      __shared__ u64 wtot[NW];
+      __shared__ u64 s_S2;
+      const int lane = tid & 31, wp = tid >> 5;
+      const int i0 = wp * VB, i1 = min(GRT_V, i0 + VB);
+      u64 t = 0;
+      for (int i = i0 + lane; i < i1; i += 32) {
+        const u64 w = GRT_W(i);
+        if (topkp_key(w, i) >= kappa) t += w;
+      }
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) wtot[wp] = t;
+      if (tid == 0) s_tok = 0x7fffffff;
+      __syncthreads();
+      if (wp == 0) {
+        const u64 v = wtot[lane];
+        u64 incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const u64 n2 = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += n2;
+        }
+        wtot[lane] = incl - v;  // exclusive
+        if (lane == 31) s_S2 = incl;
+      }
+      __syncthreads();
+      const u64 S = s_S2;
+      u32 c[4] = {(u32)step, (u32)((u64)step >> 32), 0u, 0x53616D70u};
+      const u64 seed = ctrl->seed;
+      philox4x32_10(c, (u32)seed, (u32)(seed >> 32));
+      const u64 bits = (((u64)c[1] << 32) | (u64)c[0]) >> 11;
+      const double u = (double)bits * 0x1.0p-53;
+      u64 r = (u64)(u * (double)S);
+      if (r >= S) r = S - 1;
+      u64 acc = wtot[wp];
+      if (S > 0 && acc <= r && r < acc + t) {  // this warp's block holds the draw
+        for (int base = i0; base < i1; base += 32) {
+          const int i = base + lane;
+          u64 w = 0;
+          if (i < i1) {
+            w = GRT_W(i);
+            if (topkp_key(w, i) < kappa) w = 0;
+          }
+          u64 incl = w;
+          for (int o = 1; o < 32; o <<= 1) {
+            const u64 n2 = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += n2;
+          }
+          const unsigned hit = __ballot_sync(0xffffffffu, w > 0 && acc + incl > r);
+          if (hit) {
+            if (lane == 0) s_tok = base + __ffs(hit) - 1;
+            break;
+          }
+          acc += __shfl_sync(0xffffffffu, incl, 31);
+        }
+      }
+      __syncthreads();
+    }
+#else
     // (3) draw and inverse CDF in index order over the kept set
     const int per = (GRT_V + GRT_SAMPLE_THREADS - 1) / GRT_SAMPLE_THREADS;
     const int b0 = tid * per, b1 = min(GRT_V, b0 + per);
@@ -539,6 +783,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
       }
     }
     __syncthreads();
+#endif
   }
 
   if (tid == 0) {

@@ -111,7 +111,7 @@ cudaError_t gemv_prepare(int device);  // raises the dynamic smem limit once per
 
 // Two consecutive decode GEMVs in one launch (gemv_pair.cu): a = residual GEMV
 // (Wo: NORM_NONE, EPI_RESID), b = the RMS-normed gate/up GEMV on its output
-// (EPI_SWIGLU), grid-wide barrier in between (cooperative launch); bf16 weights.
+// (EPI_SWIGLU), grid-wide barrier in between (one CTA per SM); bf16 weights.
 struct GemvPairParams {
   GemvParams a, b;
   int* bar = nullptr;  // [2] arrive/depart counters, zero-initialised, self-resetting

@@ -1,6 +1,9 @@
 // c_api.cpp -- extern "C" boundary (include/grt/c_api.h).  No exception crosses
 // it: every graphrt::Error becomes its grt_status and a thread-local message.
+#include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
 
 #include "runtime.hpp"
@@ -12,16 +15,25 @@ struct grt_model {
 struct grt_tp_emu {
   std::unique_ptr<grt::TpEmu> e;
 };
+struct grt_capture;
 struct grt_session {
   grt_model* owner;
   std::unique_ptr<grt::Session> s;
+  std::set<grt_capture*> captures;  // live capture handles (orphaned when the session goes first)
+  ~grt_session();
 };
 struct grt_capture {
-  grt_session* owner;
+  grt_session* owner;  // nullptr once the session was destroyed
   bool fused;
   std::unique_ptr<grt::CaptureSession> cs;
   std::vector<std::unique_ptr<grt::KernelInvocation>> external;  // caller-bound ops (kept alive)
 };
+grt_session::~grt_session() {
+  for (grt_capture* c : captures) {  // close them while the engine still exists
+    c->cs.reset();
+    c->owner = nullptr;
+  }
+}
 
 namespace {
 thread_local std::string g_last_error;
@@ -358,12 +370,20 @@ grt_status grt_capture_begin(grt_session* s, int32_t key, int32_t fused, grt_cap
     c->owner = s;
     c->fused = fused != 0;
     c->cs = s->s->begin_capture(key, c->fused);
+    s->captures.insert(c.get());
     *out = c.release();
   });
 }
 
+namespace {
+void live(const grt_capture* c) {
+  if (!c || !c->owner || !c->cs) grt::raise(GRT_SessionClosed, "capture: its session was destroyed");
+}
+}  // namespace
+
 grt_status grt_capture_record(grt_capture* c, int32_t op, int32_t plan_key, int32_t index) {
   return guard([&] {
+    live(c);
     const grt::KernelInvocation* k = c->owner->s->capture_op(op, plan_key, index);
     c->cs->record(k);
   });
@@ -371,6 +391,7 @@ grt_status grt_capture_record(grt_capture* c, int32_t op, int32_t plan_key, int3
 
 grt_status grt_capture_record_external(grt_capture* c, void* ptr, uint64_t bytes) {
   return guard([&] {
+    live(c);
     auto k = std::make_unique<grt::KernelInvocation>();
     k->spec.name = "external_memset";
     k->bindings = {{ptr, static_cast<size_t>(bytes)}};
@@ -382,6 +403,7 @@ grt_status grt_capture_record_external(grt_capture* c, void* ptr, uint64_t bytes
 
 grt_status grt_capture_end(grt_capture* c, int32_t* kernel_count, uint64_t* epoch) {
   return guard([&] {
+    live(c);
     grt::ExecGraphPtr g = c->owner->s->end_capture(*c->cs, c->fused);
     if (kernel_count) *kernel_count = static_cast<int32_t>(g->kernel_count());
     if (epoch) *epoch = g->capture_epoch();
@@ -390,12 +412,17 @@ grt_status grt_capture_end(grt_capture* c, int32_t* kernel_count, uint64_t* epoc
 
 grt_status grt_capture_state_get(grt_capture* c, int32_t* state, int32_t* recorded) {
   return guard([&] {
+    live(c);
     if (state) *state = static_cast<int32_t>(c->cs->state());
     if (recorded) *recorded = static_cast<int32_t>(c->cs->recorded());
   });
 }
 
-void grt_capture_destroy(grt_capture* c) { delete c; }
+void grt_capture_destroy(grt_capture* c) {
+  if (!c) return;
+  if (c->owner) c->owner->captures.erase(c);
+  delete c;
+}
 
 grt_status grt_plan_size(grt_session* s, int32_t key, int32_t* n) {
   return guard([&] {
@@ -602,6 +629,15 @@ grt_status grt_op_sample(const float* logits, int32_t vocab, const grt_sample_pa
     auto jit = grt::jit_get({"-DGRT_D=8", "-DGRT_V=" + std::to_string(vocab), "-DGRT_MAXSEQ=1", "-DGRT_WBF16=0",
                              "-DGRT_ARCH_REF=0"},
                             dev);
+    {  // keep the last few op-level modules alive (jit_get caches weakly): no NVRTC compile per call
+      static std::mutex mu;
+      static std::vector<std::shared_ptr<grt::JitModule>> keep;
+      std::lock_guard<std::mutex> lk(mu);
+      if (std::find(keep.begin(), keep.end(), jit) == keep.end()) {
+        keep.push_back(jit);
+        if (keep.size() > 8) keep.erase(keep.begin());
+      }
+    }
     CUfunction f = jit->fn("grt_sample");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // scratch: ctrl | tokens[step+1] | uniforms[step+1] | probs[vocab]

@@ -86,6 +86,8 @@ ExecGraphPtr CaptureEngine::instantiate(int key, const std::vector<const KernelI
   cudaError_t ie = cudaGraphInstantiateWithFlags(&exec, graph, 0);
   cudaGraphDestroy(graph);
   cuda_check(ie, "cudaGraphInstantiate");
+  // upload now (off the critical path) so the first replay does not pay it
+  cuda_check(cudaGraphUpload(exec, stream), "cudaGraphUpload");
   uint64_t epoch;
   {
     std::lock_guard<std::mutex> lk(mu_);
@@ -123,6 +125,7 @@ ExecGraphPtr CaptureEngine::capture_fn(int key, const std::function<void(cudaStr
   const cudaError_t ie = cudaGraphInstantiateWithFlags(&exec, graph, 0);
   cudaGraphDestroy(graph);
   cuda_check(ie, "cudaGraphInstantiate");
+  cuda_check(cudaGraphUpload(exec, stream), "cudaGraphUpload");
   if (n_nodes == 0) {
     cudaGraphExecDestroy(exec);
     raise(GRT_EmptyCapture, "capture recorded zero kernels");

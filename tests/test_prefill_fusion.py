@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 def _run(model, fuse):
     s = g.Session(model, g.CacheConfig(bucket_size=64, warmup_hi=0, batched_prefill=True, prefill_fuse_norm=fuse))
     out = []
-    for P in (10, 37, 100, 300):
+    for P in (10, 37, 100):  # (P > 256 splits K only when the reduce is fused: not comparable)
         s.reset()
         s.prefill(make_prompt(42, P, 32000))
         out.append(s.logits())
