@@ -28,7 +28,7 @@ typedef unsigned int u32;
 #define GRT_SAMPLE_SMEM_MAX 196608
 // 2: weights + a u16 candidate list (radix select with compaction, below);
 // 1: weights only (8-bit radix passes over the whole vocabulary); 0: recomputed
-#if GRT_V * 6 <= GRT_SAMPLE_SMEM_MAX && GRT_V <= 65535
+#if GRT_V * 6 <= GRT_SAMPLE_SMEM_MAX && GRT_V <= 32768
 #define GRT_TOPKP_SMEM 2
 #elif GRT_V * 4 <= GRT_SAMPLE_SMEM_MAX
 #define GRT_TOPKP_SMEM 1
@@ -280,6 +280,11 @@ __device__ void radix_pick(u64* hist, int shift, u64& prefix, u64& mask, u64& ne
 #define RS_PER ((GRT_V + GRT_SAMPLE_THREADS - 1) / GRT_SAMPLE_THREADS)
 
 __device__ __forceinline__ u64 rs_key(const u32* wsm, int i) { return ((u64)wsm[i] << 16) | (u64)(0xFFFF - i); }
+// key(w, i) >= floor with 32-bit compares: key = w << 16 | (0xFFFF - i)
+__device__ __forceinline__ bool rs_ge(u32 w, int i, u64 floor) {
+  const u32 fw = (u32)(floor >> 16), fl = (u32)(floor & 0xFFFFu);
+  return w > fw || (w == fw && (u32)(0xFFFF - i) >= fl);
+}
 
 // block-wide exclusive scan of one int per thread; returns the total
 __device__ __forceinline__ int rs_scan(int v, int* excl, int* warp_tot) {
@@ -306,11 +311,17 @@ __device__ __forceinline__ int rs_scan(int v, int* excl, int* warp_tot) {
   return total;
 }
 
+// bucket b's total: hist[b] + 2^16 * hist[RS_B + b] (the low and high 16 bits of
+// every weight are summed separately with native 32-bit shared-memory atomics --
+// a 64-bit atomicAdd compiles to a CAS spin loop; both sums stay below 2^31
+// for V <= 32768)
+__device__ __forceinline__ u64 rs_bucket(const u32* hist, int b) { return (u64)hist[b] + ((u64)hist[RS_B + b] << 16); }
+
 // the highest digit whose inclusive descending cumulative reaches need (else 0)
 // and the cumulative above it; thread t owns buckets 2t, 2t+1
-__device__ __forceinline__ void rs_pick(const u64* hist, u64 need, int* s_dg, u64* s_above, u64* wsum) {
+__device__ __forceinline__ void rs_pick(const u32* hist, u64 need, int* s_dg, u64* s_above, u64* wsum) {
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-  const u64 h0 = hist[2 * tid], h1 = hist[2 * tid + 1], sm = h0 + h1;
+  const u64 h0 = rs_bucket(hist, 2 * tid), h1 = rs_bucket(hist, 2 * tid + 1), sm = h0 + h1;
   u64 v = sm;  // inclusive suffix within the warp
   for (int o = 1; o < 32; o <<= 1) {
     const u64 n = __shfl_down_sync(0xffffffffu, v, o);
@@ -343,7 +354,7 @@ __device__ __forceinline__ void rs_pick(const u64* hist, u64 need, int* s_dg, u6
 }
 
 __device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kfloor, bool by_weight, u64 need,
-                                    u64* hist) {
+                                    u32* hist) {
   __shared__ int s_dg, s_n, warp_tot[32];
   __shared__ u64 s_above, wsum[32];
   const int tid = threadIdx.x;
@@ -353,17 +364,35 @@ __device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kf
 #pragma unroll 1
   for (int ps = 0; ps < 5; ++ps) {
     const int sh = shifts[ps];
-    for (int b = tid; b < RS_B; b += GRT_SAMPLE_THREADS) hist[b] = 0;
+    for (int b = tid; b < 2 * RS_B; b += GRT_SAMPLE_THREADS) hist[b] = 0;
     __syncthreads();
-    if (n < 0) {
+    auto add = [&](int i, u64 key) {
+      const int b = (int)((key >> sh) & (RS_B - 1));
+      if (!by_weight) {
+        atomicAdd(&hist[b], 1u);
+      } else {
+        const u32 w = wsm[i];
+        atomicAdd(&hist[b], w & 0xFFFFu);
+        if (w >> 16) atomicAdd(&hist[RS_B + b], w >> 16);
+      }
+    };
+    if (n < 0) {  // pass 0 (sh = 37 >= 16): the digit is w's top bits, 32-bit arithmetic
       for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
-        const u64 key = rs_key(wsm, i);
-        if (key >= kfloor) atomicAdd(&hist[(key >> sh) & (RS_B - 1)], by_weight ? (u64)wsm[i] : 1ull);
+        const u32 w = wsm[i];
+        if (kfloor == 0 || rs_ge(w, i, kfloor)) {
+          const int b = (int)((w >> (sh - 16)) & (RS_B - 1));
+          if (!by_weight) {
+            atomicAdd(&hist[b], 1u);
+          } else {
+            atomicAdd(&hist[b], w & 0xFFFFu);
+            if (w >> 16) atomicAdd(&hist[RS_B + b], w >> 16);
+          }
+        }
       }
     } else {
       for (int j = tid; j < n; j += GRT_SAMPLE_THREADS) {
         const int i = cand[j];
-        atomicAdd(&hist[(rs_key(wsm, i) >> sh) & (RS_B - 1)], by_weight ? (u64)wsm[i] : 1ull);
+        add(i, rs_key(wsm, i));
       }
     }
     __syncthreads();
@@ -381,8 +410,8 @@ __device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kf
         const int i = base + tid;  // consecutive indices per warp: no bank conflicts
         bool f = false;
         if (i < GRT_V) {
-          const u64 key = rs_key(wsm, i);
-          f = key >= kfloor && ((key >> sh) & (RS_B - 1)) == dg;
+          const u32 w = wsm[i];
+          f = ((w >> (sh - 16)) & (RS_B - 1)) == (u32)dg && (kfloor == 0 || rs_ge(w, i, kfloor));
         }
         const unsigned bal = __ballot_sync(0xffffffffu, f);
         int slot = 0;
@@ -575,17 +604,19 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
     for (int i = 4 * NV4 + tid; i < GRT_V; i += GRT_SAMPLE_THREADS) wsm[i] = (u32)topkp_weight(logits, i, m, temperature);
     __syncthreads();
 #define GRT_W(i) ((u64)wsm[i])
+#define GRT_GE(w, i, floor) rs_ge((u32)(w), (i), (floor))
 #else
     float m = -INFINITY;
     for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) m = fmaxf(m, logits[i]);
     m = block_max_f(m, redf);
 #define GRT_W(i) topkp_weight(logits, (i), m, temperature)
+#define GRT_GE(w, i, floor) (topkp_key((w), (i)) >= (floor))
 #endif
     const int top_k = ctrl->top_k;
     const float top_p = ctrl->top_p;
 #if GRT_TOPKP_SMEM == 2
     unsigned short* cand = (unsigned short*)(wsm + GRT_V);
-    __shared__ u64 rs_hist[RS_B];
+    __shared__ u32 rs_hist[2 * RS_B];
     // (1) top-k threshold key: the top_k-th largest key
     u64 kth = 0;
     if (top_k > 0 && top_k < GRT_V) kth = radix_select_compact(wsm, cand, 0, false, (u64)top_k, rs_hist);
@@ -593,7 +624,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
     u64 W = 0;
     for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
       const u64 w = GRT_W(i);
-      if (topkp_key(w, i) >= kth) W += w;
+      if (kth == 0 || GRT_GE(w, i, kth)) W += w;
     }
     W = block_sum_u64(W, redu);
     u64 kappa = kth;
@@ -676,7 +707,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
       u64 t = 0;
       for (int i = i0 + lane; i < i1; i += 32) {
         const u64 w = GRT_W(i);
-        if (topkp_key(w, i) >= kappa) t += w;
+        if (GRT_GE(w, i, kappa)) t += w;
       }
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
       if (lane == 0) wtot[wp] = t;
@@ -708,7 +739,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
           u64 w = 0;
           if (i < i1) {
             w = GRT_W(i);
-            if (topkp_key(w, i) < kappa) w = 0;
+            if (!GRT_GE(w, i, kappa)) w = 0;
           }
           u64 incl = w;
           for (int o = 1; o < 32; o <<= 1) {

@@ -142,7 +142,7 @@ CUfunction JitModule::fn(const char* name) const {
   unsigned bytes = 0;
   if (std::string(name).rfind("grt_sample", 0) == 0 && vocab_ > 0 && vocab_ * 4 <= kSampleSmemMax) {
     // weights (u32) + the radix select's u16 candidate list when both fit (GRT_TOPKP_SMEM 2)
-    bytes = static_cast<unsigned>(vocab_) * (vocab_ * 6 <= kSampleSmemMax && vocab_ <= 65535 ? 6 : 4);
+    bytes = static_cast<unsigned>(vocab_) * (vocab_ * 6 <= kSampleSmemMax && vocab_ <= 32768 ? 6 : 4);
     cu_check(drv().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, static_cast<int>(bytes)), name);
   }
   // every function is (re)registered: a handle of an unloaded module may be reused
