@@ -147,7 +147,6 @@ grt_status grt_model_attach_nccl(grt_model* m, const uint8_t* unique_id, int32_t
   return guard([&] {
     if (!m || !unique_id || len < GRT_TP_UNIQUE_ID_BYTES) grt::raise(GRT_InvalidConfig, "bad arguments");
     const grt::ModelConfig& c = m->m->config();
-    if (c.tp_size < 2) grt::raise(GRT_InvalidConfig, "model is not tensor parallel (tp_size < 2)");
     m->comm = std::make_unique<grt::NcclComm>(unique_id, c.tp_size, c.tp_rank, c.device);
     m->m->attach_comm(m->comm.get());
   });

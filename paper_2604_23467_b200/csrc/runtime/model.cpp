@@ -577,7 +577,7 @@ void Model::prefill_batched(int p, cudaStream_t s, bool fuse_norm) {
                "prefill embed");
     // Single GPU: a residual GEMM that splits K leaves its partials to the next
     // RMSNorm launch (reduce + residual + norm in one kernel, bit-identical).
-    const bool fuse_rn = T == 1 && fuse_norm;
+    const bool fuse_rn = !comm_ && fuse_norm;
     PrefillGemmParams prev_down;  // previous layer's down GEMM, if its reduce was deferred
     for (int l = 0; l < cfg_.n_layers; ++l) {
       const LayerBuffers& L = layers_[l];
@@ -616,7 +616,7 @@ void Model::prefill_batched(int p, cudaStream_t s, bool fuse_norm) {
       o.counters = pf_cnt_;
       o.defer_reduce = fuse_rn ? 1 : 0;
       cuda_check(launch_prefill_gemm_ex(L.w_o, pf_A_, &o, s, true), "prefill wo");
-      if (T > 1) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce wo");
+      if (comm_) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce wo");
       if (o.defer_reduce && o.ksplit > 1)
         cuda_check(launch_prefill_resid_norm(o, L.ln2_g, cfg_.norm_eps, pf_Xn_, s), "prefill resid+rmsnorm2");
       else
@@ -641,7 +641,7 @@ void Model::prefill_batched(int p, cudaStream_t s, bool fuse_norm) {
       w2.defer_reduce = fuse_rn && l + 1 < cfg_.n_layers ? 1 : 0;  // the last layer's output goes to the hand-off
       cuda_check(launch_prefill_gemm_ex(L.w_down, pf_act_, &w2, s, true), "prefill down");
       prev_down = w2;
-      if (T > 1) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce down");
+      if (comm_) cuda_check(comm_->allreduce_sum(pf_X_, static_cast<size_t>(P) * d, s), "prefill allreduce down");
     }
   }
   // hand off to the decode state: last token's residual row, seq_len = p; then
@@ -658,7 +658,7 @@ void Model::prefill_batched(int p, cudaStream_t s, bool fuse_norm) {
   hp.eps = cfg_.norm_eps;
   hp.out = logits_local_;
   cuda_check(launch_gemv(Dt::BF16, NORM_RMS, EPI_STORE, hp, s, false, 0), "prefill head");
-  if (T > 1) cuda_check(comm_->allgather(logits_local_, logits_, static_cast<size_t>(vl_), s), "prefill allgather");
+  if (comm_) cuda_check(comm_->allgather(logits_local_, logits_, static_cast<size_t>(vl_), s), "prefill allgather");
 }
 
 // ---------------------------------------------------------------------------
@@ -755,7 +755,9 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
     size_t bytes = 0;
     bool set = false;
   } pending;
-  const bool fuse = cfg_.tp_size == 1 && llama && wdt == Dt::BF16 && !op_trace_;
+  // collectives: every tensor-parallel plan, and a 1-rank group with a communicator
+  const bool coll = comm_ != nullptr || cfg_.tp_size > 1;
+  const bool fuse = !coll && llama && wdt == Dt::BF16 && !op_trace_;
   int n_pairs_emitted = 0;
   auto flush = [&]() {
     if (pending.set) emit_gemv(pending.name, EPI_RESID, NORM_NONE, pending.p, pending.bytes);
@@ -876,7 +878,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       p.x = attn_;
       p.out = x_;
       gemv("wo_residual", resid_epi, NORM_NONE, p, 1ull * d * dq * wb);
-      if (T > 1) allreduce_x("allreduce_wo");
+      if (coll) allreduce_x("allreduce_wo");
     }
     {  // ln2 + w1 + relu  |  rms + gate/up + SwiGLU   (column-parallel)
       GemvParams p;
@@ -900,7 +902,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
       p.out = x_;
       p.chmax = 3072;  // k = 11008 in 4 chunks of 2752 (11 KB stages): measured fastest
       gemv("down_residual", resid_epi, NORM_NONE, p, 1ull * d * ffl * wb);
-      if (T > 1) allreduce_x("allreduce_down");
+      if (coll) allreduce_x("allreduce_down");
     }
   }
   {  // ln_f + head (vocab-parallel)
@@ -916,7 +918,7 @@ std::vector<KernelInvocation> Model::build_plan(int key, int B, int impl) {
     gemv("lnf_head", EPI_STORE, norm, p, 1ull * vl * d * wb);
   }
   flush();
-  if (T > 1) {
+  if (coll) {
     KernelInvocation inv;
     inv.spec.name = "allgather_logits";
     inv.spec.op_class = OpClass::Static;

@@ -230,13 +230,11 @@ void CudaDevice::sync_all() {
 // Session
 
 Session::Session(Model& model, const CacheConfig& cc) : model_(&model), cc_(cc) {
-  if (model.tp_size() > 1) {
-    // tensor parallel: per-op plan with in-graph NCCL collectives; captures run
-    // on the submitting thread (one NCCL communicator must not be driven from
-    // two host threads), so every rank captures/launches in the same order
-    if (!model.comm()) raise(GRT_InvalidConfig, "tensor-parallel model has no communicator (grt_model_attach_nccl)");
-    cc_.pass_impl = 1;
-  }
+  if (model.tp_size() > 1 && !model.comm())
+    raise(GRT_InvalidConfig, "tensor-parallel model has no communicator (grt_model_attach_nccl)");
+  // with a communicator the plans hold in-graph NCCL collectives; captures run
+  // on the submitting thread (one NCCL communicator must not be driven from two
+  // host threads), so every rank captures and launches in the same order
   if (cc_.bucket_size < 1) raise(GRT_InvalidConfig, "bucket_size must be >= 1");
   cuda_check(cudaSetDevice(model.device()), "cudaSetDevice");
   dev_ = std::make_unique<CudaDevice>(model.device());
@@ -288,7 +286,6 @@ Session::~Session() {
 // edges), recorded into the switch bodies with cudaStreamBeginCaptureToGraph.
 void Session::build_device_loop() {
   if (loop_.exec) return;
-  if (model_->tp_size() > 1) raise(GRT_Unsupported, "device loop: single GPU only (NCCL nodes in conditional bodies)");
   const double t0 = now_us();
   const int B = cc_.bucket_size;
   loop_.key_lo = 1;
@@ -438,7 +435,7 @@ StepResponse Session::serve(const StepRequest& req, bool allow_cache, const Mode
   if (use_cache && pol.capture_on_miss && !cache_->contains(ck)) {
     ++dev_->counters().events_recorded;  // ordering point, as record_event/wait_event in the reference
     ++dev_->counters().events_waited;
-    if (pol.async_capture && model_->tp_size() == 1) {
+    if (pol.async_capture && !model_->comm()) {
       if (!dev_->capture_pending(ck))
         dev_->submit_capture(ck, [this, key, fused](cudaStream_t s) { return capture_now(key, fused, s); });
     } else {
@@ -475,7 +472,7 @@ StepPath Session::serve_prefill(int p, const ModePolicy& pol) {
     auto job = [this, p, ck](cudaStream_t cs) {
       return engine_->capture_fn(ck, [this, p](cudaStream_t st) { model_->prefill_batched(p, st, cc_.prefill_fuse_norm); }, cs);
     };
-    if (pol.async_capture && model_->tp_size() == 1) {
+    if (pol.async_capture && !model_->comm()) {
       if (!dev_->capture_pending(ck)) dev_->submit_capture(ck, job);
     } else {
       ++dev_->counters().captures;

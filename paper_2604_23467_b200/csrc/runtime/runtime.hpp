@@ -261,7 +261,13 @@ class Model {
   // caller owns and must attach before any plan is built.
   int tp_size() const { return cfg_.tp_size; }
   int tp_rank() const { return cfg_.tp_rank; }
-  void attach_comm(TpComm* c) { comm_ = c; }
+  // Collectives are planned whenever a communicator is attached -- including a
+  // 1-rank group (tp_size 1), where they are identities: the NCCL capture path
+  // exercised on one GPU.  Plans built before attaching are dropped.
+  void attach_comm(TpComm* c) {
+    comm_ = c;
+    plans_.clear();
+  }
   TpComm* comm() const { return comm_; }
   float* logits_local_dev() const { return logits_local_; }
   const void* emb_dev() const { return emb_; }
