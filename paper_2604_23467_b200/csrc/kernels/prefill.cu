@@ -256,6 +256,15 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], 
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// 16-byte global -> shared copy (LDGSTS), zero-filled when !valid
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&v);
@@ -269,9 +278,10 @@ __global__ void __launch_bounds__(FA_WARPS * 32)
   constexpr int KS = DH / 16, NB = DH / 8;
   extern __shared__ __align__(16) uint8_t fa_smem[];
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(fa_smem);
-  __nv_bfloat16* Ks = Qs + FA_QB * LD;
-  __nv_bfloat16* Vs = Ks + FA_KB * LD;
-  const int head = blockIdx.y, q0 = blockIdx.x * FA_QB;
+  __nv_bfloat16* Kb = Qs + FA_QB * LD;      // [2][FA_KB][LD] double-buffered K tiles
+  __nv_bfloat16* Vb = Kb + 2 * FA_KB * LD;  // [2][FA_KB][LD] V tiles
+  // the q tiles with the most key blocks (causal) are scheduled first
+  const int head = blockIdx.y, q0 = (gridDim.x - 1 - blockIdx.x) * FA_QB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int nq = min(FA_QB, P - q0);
@@ -298,20 +308,33 @@ __global__ void __launch_bounds__(FA_WARPS * 32)
   const int qpos0 = start + q0 + 16 * warp + g;  // rows g and g+8 of this warp
   const int last_pos = start + q0 + nq - 1;
 
-  for (int kb = 0; kb <= last_pos; kb += FA_KB) {
-    __syncthreads();
+  // K/V tiles stream in with cp.async, double-buffered: the next tile's loads
+  // are in flight while this one's MMAs run (rows past the live end are
+  // zero-filled: their scores are masked, and 0 * V must stay finite)
+  auto load_kv = [&](int kb, int buf) {
+    __nv_bfloat16* Ks = Kb + buf * FA_KB * LD;
+    __nv_bfloat16* Vs = Vb + buf * FA_KB * LD;
     for (int e = threadIdx.x; e < FA_KB * DH / 8; e += FA_WARPS * 32) {
       const int r = e / (DH / 8), c = 8 * (e - r * (DH / 8));
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (kb + r <= last_pos) {
-        const int64_t row = kv_row(kvp, head, max_seq, kb + r) * DH;
-        kv = *reinterpret_cast<const uint4*>(k_cache + row + c);
-        vv = *reinterpret_cast<const uint4*>(v_cache + row + c);
-      }
-      *reinterpret_cast<uint4*>(&Ks[r * LD + c]) = kv;
-      *reinterpret_cast<uint4*>(&Vs[r * LD + c]) = vv;
+      const bool ok = kb + r <= last_pos;
+      const int64_t row = ok ? kv_row(kvp, head, max_seq, kb + r) * DH : 0;
+      cp_async16(&Ks[r * LD + c], k_cache + row + c, ok);
+      cp_async16(&Vs[r * LD + c], v_cache + row + c, ok);
     }
+    cp_async_commit();
+  };
+  load_kv(0, 0);
+  for (int kb = 0, it = 0; kb <= last_pos; kb += FA_KB, ++it) {
+    const int buf = it & 1;
+    const bool more = kb + FA_KB <= last_pos;
+    if (more) load_kv(kb + FA_KB, buf ^ 1);  // that buffer was released by the barrier ending the last iteration
+    if (more)
+      cp_async_wait<1>();
+    else
+      cp_async_wait<0>();
     __syncthreads();
+    const __nv_bfloat16* Ks = Kb + buf * FA_KB * LD;
+    const __nv_bfloat16* Vs = Vb + buf * FA_KB * LD;
     float sacc[FA_KB / 8][4];
 #pragma unroll
     for (int nb = 0; nb < FA_KB / 8; ++nb) sacc[nb][0] = sacc[nb][1] = sacc[nb][2] = sacc[nb][3] = 0.0f;
@@ -383,6 +406,7 @@ __global__ void __launch_bounds__(FA_WARPS * 32)
         mma_bf16(o[jn + 1], a, b2, b3);
       }
     }
+    __syncthreads();  // every warp is done with `buf` before it is refilled
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -434,7 +458,7 @@ static cudaError_t attn_dispatch(int dh, const float* Q, const void* k, const vo
 template <int DH>
 static cudaError_t fa_launch(const float* Q, const void* k, const void* v, int start, int P, int d, int n_heads,
                              int max_seq, float scale, void* out, cudaStream_t s, KvPaging kvp) {
-  const size_t smem = static_cast<size_t>(FA_QB + 2 * FA_KB) * (DH + 8) * 2;
+  const size_t smem = static_cast<size_t>(FA_QB + 4 * FA_KB) * (DH + 8) * 2;  // Q + 2 x (K, V)
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(prefill_fa_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -452,14 +452,18 @@ __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
 // reassociation only).
 constexpr int RN_THREADS = 512, RN_MAXV = 8, RN_SPLIT_GROUP = 4;  // M = d <= 16384
 constexpr int RN_NORM_THREADS = 256, RN_NORM_MAXV = 16;  // prefill_rmsnorm_kernel's thread shape
+// MAXV float4 per thread, the smallest that covers d (2 at d = 4096): registers
+// stay low enough for several rows' CTAs per SM -- at 8 the kernel held the SM's
+// whole register file and ran at 1 CTA per SM (P=500: 19.2 us per launch)
+template <int MAXV>
 __global__ void __launch_bounds__(RN_THREADS) prefill_resid_norm_kernel(const PrefillGemmParams p, const float* gamma,
                                                                         float eps, __nv_bfloat16* Xn) {
   __shared__ float red[32];
   extern __shared__ float4 xrow[];  // the updated row, for the reduction below
-  float4 g[RN_MAXV];
+  float4 g[MAXV];
   const int d = p.M, n4 = d >> 2;
 #pragma unroll
-  for (int u = 0; u < RN_MAXV; ++u) {
+  for (int u = 0; u < MAXV; ++u) {
     const int j = threadIdx.x + u * RN_THREADS;
     g[u] = j < n4 ? __ldg(reinterpret_cast<const float4*>(gamma) + j) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -467,9 +471,9 @@ __global__ void __launch_bounds__(RN_THREADS) prefill_resid_norm_kernel(const Pr
   const int n = blockIdx.x;
   const int n_tile = n / p.ntile, nn = n - n_tile * p.ntile;
   float* X = p.out + static_cast<int64_t>(n) * d;
-  float4 v[RN_MAXV];
+  float4 v[MAXV];
 #pragma unroll
-  for (int u = 0; u < RN_MAXV; ++u) {
+  for (int u = 0; u < MAXV; ++u) {
     const int j = threadIdx.x + u * RN_THREADS;
     v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (j >= n4) continue;
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(RN_THREADS) prefill_resid_norm_kernel(const Pr
   const float inv = 1.0f / sqrtf(red[0] / static_cast<float>(d) + eps);
   __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(Xn + static_cast<int64_t>(n) * d);
 #pragma unroll
-  for (int u = 0; u < RN_MAXV; ++u) {
+  for (int u = 0; u < MAXV; ++u) {
     const int j = threadIdx.x + u * RN_THREADS;
     if (j >= n4) continue;
     o[2 * j] = __floats2bfloat162_rn(v[u].x * inv * g[u].x, v[u].y * inv * g[u].y);
@@ -715,7 +719,12 @@ cudaError_t launch_prefill_resid_norm(const PrefillGemmParams& p, const float* g
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   rc.attrs = attr;
   rc.numAttrs = 1;
-  return cudaLaunchKernelEx(&rc, prefill_resid_norm_kernel, p, gamma, eps, static_cast<__nv_bfloat16*>(Xn));
+  const int n4 = p.M / 4;
+  if (n4 <= 2 * RN_THREADS)
+    return cudaLaunchKernelEx(&rc, prefill_resid_norm_kernel<2>, p, gamma, eps, static_cast<__nv_bfloat16*>(Xn));
+  if (n4 <= 4 * RN_THREADS)
+    return cudaLaunchKernelEx(&rc, prefill_resid_norm_kernel<4>, p, gamma, eps, static_cast<__nv_bfloat16*>(Xn));
+  return cudaLaunchKernelEx(&rc, prefill_resid_norm_kernel<RN_MAXV>, p, gamma, eps, static_cast<__nv_bfloat16*>(Xn));
 }
 
 }  // namespace grt
