@@ -7,3 +7,4 @@ timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/${T}_tests.log 2>&
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo rc=$? >> gpurun_out/${T}_smoke.log
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo rc=$? >> gpurun_out/${T}_bench.err
 timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${T}_ref.json 2> gpurun_out/${T}_ref.err
+timeout 900 python bench.py --steps 20 --warmup 5 --trials 100 --mixed 0 --ipc 0 --modes= --no-cpu-baseline > gpurun_out/${T}_sweep100.json 2> gpurun_out/${T}_sweep100.err
