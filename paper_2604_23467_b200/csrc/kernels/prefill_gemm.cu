@@ -324,6 +324,21 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      // The weights (A) never depend on the previous kernel: the A boxes of the
+      // first S stages are requested before the dependency wait (PDL), so the
+      // ring fills while the previous kernel drains; the activation boxes (B)
+      // of those stages follow the wait.
+      int pre = 0;
+      for (int w = blockIdx.x; w < n_items && pre < S; w += gridDim.x) {
+        int m_tile, n_tile, split, kb0, kb1;
+        decode(w, m_tile, n_tile, split, kb0, kb1);
+        for (int kb = kb0; kb < kb1 && pre < S; ++kb, ++pre) {
+          uint8_t* st = smem + static_cast<size_t>(pre) * stage_bytes;
+          mbar_arrive_expect_tx(&full[pre], stage_bytes);
+          for (int j = 0; j < p.kbox; ++j)
+            tma_load_2d(st + j * a_box, &map_w, kb * kstep + j * PG_BK, m_tile * PG_BM, &full[pre]);
+        }
+      }
       griddep_wait();
       int i = 0;  // global stage counter across items
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
@@ -331,12 +346,14 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
         decode(w, m_tile, n_tile, split, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int s = i % S;
-          mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
           uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
-          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          if (i >= pre) {
+            mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[s], stage_bytes);
+          }
           for (int j = 0; j < p.kbox; ++j) {
             const int k0 = kb * kstep + j * PG_BK;
-            tma_load_2d(st + j * a_box, &map_w, k0, m_tile * PG_BM, &full[s]);
+            if (i >= pre) tma_load_2d(st + j * a_box, &map_w, k0, m_tile * PG_BM, &full[s]);
             tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, k0, n_tile * p.ntile, &full[s]);
           }
         }
