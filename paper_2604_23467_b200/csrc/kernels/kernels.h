@@ -141,6 +141,10 @@ enum PgEpi : int {
 struct PrefillGemmParams {
   int M = 0, K = 0, P = 0;  // Y[P, M] = X[P, K] . W[M, K]^T  (bf16 operands, fp32 accumulate)
   int ntile = 0, n_ntiles = 0, ksplit = 1, stages = 0, kbox = 1;  // set by the launcher
+  // stream-K tail (set by the launcher; ksplit == 1 only): tiles [tail_first,
+  // m_tiles*n_ntiles) -- the last, partial wave -- are split tail_ks ways in K
+  // so their units fill the SMs; their partials go through a reduce kernel
+  int tail_first = 0, tail_ks = 0;
   int epi = PG_EPI_STORE;
   float* out = nullptr;
   void* out_bf16 = nullptr;

@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
-  const int n_items = m_tiles * p.n_ntiles * p.ksplit;
+  const int n_tiles_all = m_tiles * p.n_ntiles;
+  const bool tail = p.tail_ks > 1;  // stream-K tail (ksplit == 1)
+  const int n_items = tail ? p.tail_first + (n_tiles_all - p.tail_first) * p.tail_ks : n_tiles_all * p.ksplit;
   const int kstep = PG_BK * p.kbox;
   const int nkb = (p.K + kstep - 1) / kstep;  // a ragged last block reads zeros past K (TMA OOB fill)
   const int S = p.stages;
@@ -291,12 +293,27 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
   while (cols < static_cast<uint32_t>(2 * p.ntile)) cols <<= 1;
 
   auto decode = [&](int w, int& m_tile, int& n_tile, int& split, int& kb0, int& kb1) {
-    split = w % p.ksplit;
-    const int mn = w / p.ksplit;
+    int mn, ks;
+    if (tail) {
+      if (w < p.tail_first) {  // whole tile
+        mn = w;
+        split = 0;
+        ks = 1;
+      } else {
+        const int t = w - p.tail_first;
+        mn = p.tail_first + t / p.tail_ks;
+        split = t % p.tail_ks;
+        ks = p.tail_ks;
+      }
+    } else {
+      split = w % p.ksplit;
+      mn = w / p.ksplit;
+      ks = p.ksplit;
+    }
     n_tile = mn % p.n_ntiles;
     m_tile = mn / p.n_ntiles;
-    kb0 = static_cast<int>(static_cast<int64_t>(split) * nkb / p.ksplit);
-    kb1 = static_cast<int>(static_cast<int64_t>(split + 1) * nkb / p.ksplit);
+    kb0 = static_cast<int>(static_cast<int64_t>(split) * nkb / ks);
+    kb1 = static_cast<int>(static_cast<int64_t>(split + 1) * nkb / ks);
   };
 
   if (threadIdx.x == 0) {
@@ -324,21 +341,6 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // The weights (A) never depend on the previous kernel: the A boxes of the
-      // first S stages are requested before the dependency wait (PDL), so the
-      // ring fills while the previous kernel drains; the activation boxes (B)
-      // of those stages follow the wait.
-      int pre = 0;
-      for (int w = blockIdx.x; w < n_items && pre < S; w += gridDim.x) {
-        int m_tile, n_tile, split, kb0, kb1;
-        decode(w, m_tile, n_tile, split, kb0, kb1);
-        for (int kb = kb0; kb < kb1 && pre < S; ++kb, ++pre) {
-          uint8_t* st = smem + static_cast<size_t>(pre) * stage_bytes;
-          mbar_arrive_expect_tx(&full[pre], stage_bytes);
-          for (int j = 0; j < p.kbox; ++j)
-            tma_load_2d(st + j * a_box, &map_w, kb * kstep + j * PG_BK, m_tile * PG_BM, &full[pre]);
-        }
-      }
       griddep_wait();
       int i = 0;  // global stage counter across items
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
@@ -346,14 +348,12 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
         decode(w, m_tile, n_tile, split, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int s = i % S;
+          mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
           uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
-          if (i >= pre) {
-            mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full[s], stage_bytes);
-          }
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
           for (int j = 0; j < p.kbox; ++j) {
             const int k0 = kb * kstep + j * PG_BK;
-            if (i >= pre) tma_load_2d(st + j * a_box, &map_w, k0, m_tile * PG_BM, &full[s]);
+            tma_load_2d(st + j * a_box, &map_w, k0, m_tile * PG_BM, &full[s]);
             tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, k0, n_tile * p.ntile, &full[s]);
           }
         }
@@ -398,7 +398,6 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
     const int half = (warp - 2) >> 2;                      // column group of this warp
     const int groups = (static_cast<int>(blockDim.x) / 32 - 2) >> 2;  // warps per lane quadrant
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(lane_base) << 16);
-    const bool split_k = p.ksplit > 1;
     int it = 0;
     for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
       int m_tile, n_tile, split, kb0, kb1;
@@ -410,7 +409,12 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
       mbar_wait_sleep(&acc_full[buf], (it >> 1) & 1);
       tc_fence_after();
       const int tile_id = m_tile * p.n_ntiles + n_tile;
-      float* mypart = split_k ? p.part + (static_cast<int64_t>(tile_id) * p.ksplit + split) * p.ntile * PG_BM : nullptr;
+      // partials: every item of a split-K GEMM, or a stream-K tail unit
+      const bool split_k = tail ? w >= p.tail_first : p.ksplit > 1;
+      float* mypart = nullptr;
+      if (split_k)
+        mypart = tail ? p.part + (static_cast<int64_t>(tile_id - p.tail_first) * p.tail_ks + split) * p.ntile * PG_BM
+                      : p.part + (static_cast<int64_t>(tile_id) * p.ksplit + split) * p.ntile * PG_BM;
       for (int c0 = 16 * half; c0 < n_valid; c0 += 16 * groups) {
         float v[16];
         tc_ld16(t_lane + buf * p.ntile + c0, v);
@@ -452,6 +456,35 @@ __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
     const float* base = p.part + (static_cast<int64_t>(m_tile * p.n_ntiles + n_tile) * p.ksplit) * p.ntile * PG_BM;
     float va = 0.0f, vb = 0.0f;
     for (int sp = 0; sp < p.ksplit; ++sp) {
+      const float* q = base + (static_cast<int64_t>(sp) * p.ntile + nn) * PG_BM + r;
+      va += q[0];
+      vb += q[1];
+    }
+    pg_epilogue_pair(p, m, n, va, vb);
+  }
+}
+
+// Reduce of the stream-K tail: tiles [tail_first, m_tiles*n_ntiles), tail_ks
+// partials each ([tile - tail_first][split][token][128 rows]), summed in split
+// order, then the GEMM's epilogue; one thread per (row pair, token).
+__global__ void prefill_tail_reduce_kernel(const PrefillGemmParams p) {
+  griddep_wait();  // launched with PDL behind the GEMM: partials complete
+  const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
+  const int n_tail = m_tiles * p.n_ntiles - p.tail_first;
+  const int per_tile = (PG_BM / 2) * p.ntile;
+  const int64_t total = static_cast<int64_t>(n_tail) * per_tile;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(e / per_tile);
+    const int r2 = static_cast<int>(e - static_cast<int64_t>(t) * per_tile);
+    const int nn = r2 / (PG_BM / 2), r = 2 * (r2 - nn * (PG_BM / 2));
+    const int tile = p.tail_first + t;
+    const int m_tile = tile / p.n_ntiles, n_tile = tile - m_tile * p.n_ntiles;
+    const int m = m_tile * PG_BM + r, n = n_tile * p.ntile + nn;
+    if (m >= p.M || n >= p.P) continue;
+    const float* base = p.part + static_cast<int64_t>(t) * p.tail_ks * p.ntile * PG_BM;
+    float va = 0.0f, vb = 0.0f;
+    for (int sp = 0; sp < p.tail_ks; ++sp) {
       const float* q = base + (static_cast<int64_t>(sp) * p.ntile + nn) * PG_BM + r;
       va += q[0];
       vb += q[1];
@@ -646,14 +679,35 @@ static PgShape pg_shape(int M, int K, int P, int sms, bool wide_split = false) {
 
 int prefill_gemm_ksplit(int M, int K, int sms) { return pg_shape(M, K, 16, sms).ksplit; }
 
+// Stream-K tail of an unsplit GEMM: when the tiles leave a partial last wave,
+// its tiles are split ks ways in K (ks <= 4, their units fill the SMs) and
+// reduced afterwards; the first full waves stay whole tiles.
+static void pg_tail(int n_tiles_all, int nkb, int sms, int* tail_first, int* tail_ks) {
+  *tail_first = 0;
+  *tail_ks = 0;
+  if (n_tiles_all <= sms) return;
+  const int rem = n_tiles_all % sms;
+  if (rem == 0) return;
+  const int ks = std::min({4, sms / rem, nkb});
+  if (ks < 2) return;
+  *tail_first = n_tiles_all - rem;
+  *tail_ks = ks;
+}
+
 size_t prefill_gemm_part_floats(int M, int K, int P, int sms) {
   size_t worst = 0;
   (void)P;
   for (int q = 16; q <= PREFILL_CHUNK; q += 16) {  // size for the worst token count
     for (const bool wide : {false, true}) {
       const PgShape sh = pg_shape(M, K, q, sms, wide);
-      if (sh.ksplit == 1) continue;
       const int m_tiles = (M + PG_BM - 1) / PG_BM;
+      if (sh.ksplit == 1) {  // stream-K tail partials
+        int tf, tk;
+        pg_tail(m_tiles * sh.n_ntiles, (K + PG_BK * sh.kbox - 1) / (PG_BK * sh.kbox), sms, &tf, &tk);
+        if (tk > 1)
+          worst = std::max(worst, static_cast<size_t>(m_tiles * sh.n_ntiles - tf) * tk * sh.ntile * PG_BM);
+        continue;
+      }
       worst = std::max(worst, static_cast<size_t>(m_tiles) * sh.n_ntiles * sh.ksplit * sh.ntile * PG_BM);
     }
   }
@@ -679,7 +733,14 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   if (p.ksplit > 1 && (!p.part || !p.counters)) return cudaErrorInvalidValue;
   const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
   if (p.ksplit > 1 && m_tiles * p.n_ntiles > 4096) return cudaErrorInvalidValue;
-  const int n_items = m_tiles * p.n_ntiles * p.ksplit;
+  p.tail_first = 0;
+  p.tail_ks = 0;
+  if (p.ksplit == 1 && p.part)
+    pg_tail(m_tiles * p.n_ntiles, (p.K + PG_BK * p.kbox - 1) / (PG_BK * p.kbox), num_sms(dev), &p.tail_first,
+            &p.tail_ks);
+  const bool tail = p.tail_ks > 1;
+  const int n_items =
+      tail ? p.tail_first + (m_tiles * p.n_ntiles - p.tail_first) * p.tail_ks : m_tiles * p.n_ntiles * p.ksplit;
   const int stage_bytes = p.kbox * (PG_BM * PG_BK * 2 + p.ntile * PG_BK * 2);
   const int budget = 220 * 1024 - 1024;
   p.stages = std::min(8, budget / stage_bytes);
@@ -701,7 +762,18 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, prefill_gemm_kernel, mw, mx, p);
   if (out) *out = p;
-  if (e != cudaSuccess || p.ksplit == 1 || (p.defer_reduce && p.epi == PG_EPI_RESID)) return e;
+  if (e != cudaSuccess) return e;
+  if (tail) {  // reduce + epilogue of the tail tiles
+    const int64_t work = static_cast<int64_t>(m_tiles * p.n_ntiles - p.tail_first) * (PG_BM / 2) * p.ntile;
+    cudaLaunchConfig_t rc = {};
+    rc.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>((work + 255) / 256, 4 * num_sms(dev))));
+    rc.blockDim = dim3(256);
+    rc.stream = s;
+    rc.attrs = attr;
+    rc.numAttrs = 1;
+    return cudaLaunchKernelEx(&rc, prefill_tail_reduce_kernel, p);
+  }
+  if (p.ksplit == 1 || (p.defer_reduce && p.epi == PG_EPI_RESID)) return e;
   const int64_t work = static_cast<int64_t>((p.M + 1) / 2) * p.P;
   const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 4 * num_sms(dev)));
   cudaLaunchConfig_t rc = {};
