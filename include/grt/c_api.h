@@ -291,6 +291,9 @@ grt_status grt_plan_size(grt_session* s, int32_t key, int32_t* n);
 grt_status grt_session_replay(grt_session* s, int32_t key, int32_t fused, int32_t token, int32_t validate);
 /* arena of the model: bytes reserved, bytes used, sub-allocations (never grows per capture) */
 grt_status grt_model_arena_info(grt_model* m, uint64_t* capacity, uint64_t* used, uint64_t* allocations);
+/* tensor-parallel state: group size, rank, and whether the residual stream's
+ * allreduce buffer lives in an NCCL symmetric window (ncclCommWindowRegister) */
+grt_status grt_model_tp_info(grt_model* m, int32_t* tp_size, int32_t* tp_rank, int32_t* symmetric);
 
 /* ---- graph cache policy (replaces graphrt::GraphCache, graph_cache.hpp:29-81) ---
  * The session owns its own cache of cudaGraphExec_t; this standalone handle runs

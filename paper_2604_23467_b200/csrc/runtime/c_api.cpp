@@ -443,6 +443,15 @@ grt_status grt_model_arena_info(grt_model* m, uint64_t* capacity, uint64_t* used
   });
 }
 
+grt_status grt_model_tp_info(grt_model* m, int32_t* tp_size, int32_t* tp_rank, int32_t* symmetric) {
+  return guard([&] {
+    const grt::ModelConfig& c = m->m->config();
+    if (tp_size) *tp_size = c.tp_size;
+    if (tp_rank) *tp_rank = c.tp_rank;
+    if (symmetric) *symmetric = m->m->symmetric_exchange() ? 1 : 0;
+  });
+}
+
 grt_status grt_session_counters(grt_session* s, grt_counters* c) {
   return guard([&] { *c = s->s->device().counters(); });
 }

@@ -151,7 +151,28 @@ void* Arena::alloc(size_t bytes, size_t align) {
 
 bool Arena::contains(const void* p, size_t n) const {
   const char* c = static_cast<const char*>(p);
-  return base_ && c >= base_ && c + n <= base_ + cap_;
+  if (base_ && c >= base_ && c + n <= base_ + cap_) return true;
+  for (const auto& [b, len] : extra_)
+    if (c >= b && c + n <= b + len) return true;
+  return false;
+}
+
+// Collectives are planned whenever a communicator is attached (a 1-rank group
+// included).  The residual stream x -- the buffer every per-layer allreduce
+// reduces in place -- moves into memory registered with the communicator when
+// it supports that (NCCL symmetric windows: the low-latency symmetric
+// allreduce kernels); plans built before are dropped.
+void Model::attach_comm(TpComm* c) {
+  comm_ = c;
+  plans_.clear();
+  if (!c || x_sym_) return;
+  const size_t bytes = static_cast<size_t>(cfg_.d_model) * 4;
+  void* sym = c->alloc_symmetric(bytes);
+  if (!sym) return;
+  cuda_check(cudaMemcpy(sym, x_, bytes, cudaMemcpyDeviceToDevice), "x -> symmetric buffer");
+  x_sym_ = static_cast<float*>(sym);
+  x_ = x_sym_;
+  arena_.allow(x_sym_, bytes);
 }
 
 // ---------------------------------------------------------------------------
@@ -444,6 +465,7 @@ Model::Model(const ModelConfig& cfg) : cfg_(cfg) {
 Model::~Model() {
   cudaSetDevice(cfg_.device);
   cudaDeviceSynchronize();
+  if (x_sym_ && comm_) comm_->free_symmetric(x_sym_);  // the communicator outlives the model (c_api.cpp)
   if (h_out_tokens_) cudaFreeHost(const_cast<int*>(h_out_tokens_));
   if (h_out_stamps_) cudaFreeHost(const_cast<unsigned long long*>(h_out_stamps_));
 }

@@ -95,6 +95,8 @@ class Arena {
   void reserve(size_t bytes);
   void* alloc(size_t bytes, size_t align = 256);
   bool contains(const void* p, size_t n) const;
+  // memory outside the arena that bindings may use (the symmetric exchange buffer)
+  void allow(const void* p, size_t n) { extra_.push_back({static_cast<const char*>(p), n}); }
   size_t used() const { return used_; }
   size_t capacity() const { return cap_; }
   size_t allocations() const { return count_; }
@@ -103,6 +105,7 @@ class Arena {
  private:
   char* base_ = nullptr;
   size_t cap_ = 0, used_ = 0, count_ = 0;
+  std::vector<std::pair<const char*, size_t>> extra_;
 };
 
 // ---------------------------------------------------------------------------
@@ -138,6 +141,10 @@ class TpComm {
   virtual ~TpComm() = default;
   virtual cudaError_t allreduce_sum(float* buf, size_t n, cudaStream_t s) = 0;                   // in place
   virtual cudaError_t allgather(const float* in, float* out, size_t n_per_rank, cudaStream_t s) = 0;  // rank order
+  // Device memory registered with the communicator for symmetric collectives
+  // (NCCL: ncclMemAlloc + ncclCommWindowRegister); nullptr when unsupported.
+  virtual void* alloc_symmetric(size_t /*bytes*/) { return nullptr; }
+  virtual void free_symmetric(void* /*p*/) {}
 };
 enum CollectiveKind : int { COLL_NONE = 0, COLL_ALLREDUCE = 1, COLL_ALLGATHER = 2 };
 
@@ -264,10 +271,8 @@ class Model {
   // Collectives are planned whenever a communicator is attached -- including a
   // 1-rank group (tp_size 1), where they are identities: the NCCL capture path
   // exercised on one GPU.  Plans built before attaching are dropped.
-  void attach_comm(TpComm* c) {
-    comm_ = c;
-    plans_.clear();
-  }
+  void attach_comm(TpComm* c);
+  bool symmetric_exchange() const { return x_sym_ != nullptr; }
   TpComm* comm() const { return comm_; }
   float* logits_local_dev() const { return logits_local_; }
   const void* emb_dev() const { return emb_; }
@@ -309,6 +314,7 @@ class Model {
   void *pf_Xn_ = nullptr, *pf_A_ = nullptr, *pf_act_ = nullptr;
   int* pf_cnt_ = nullptr;
   int* pair_bar_ = nullptr;
+  float* x_sym_ = nullptr;     // the residual stream in communicator-registered memory (TP)
   KvPaging kvp_;
   int kv_pages_ = 0;
   size_t kv_layer_elems_ = 0;
@@ -693,9 +699,12 @@ class NcclComm : public TpComm {
   ~NcclComm() override;
   cudaError_t allreduce_sum(float* buf, size_t n, cudaStream_t s) override;
   cudaError_t allgather(const float* in, float* out, size_t n_per_rank, cudaStream_t s) override;
+  void* alloc_symmetric(size_t bytes) override;
+  void free_symmetric(void* p) override;
 
  private:
   void* comm_ = nullptr;  // ncclComm_t
+  std::vector<std::pair<void*, void*>> windows_;  // (buffer, ncclWindow_t)
 };
 std::vector<uint8_t> nccl_unique_id();
 

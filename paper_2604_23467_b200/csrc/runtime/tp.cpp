@@ -27,6 +27,11 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // optional (NCCL >= 2.27): symmetric memory windows
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*CommWindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+  ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -49,6 +54,12 @@ const NcclApi& nccl() {
     sym("ncclAllReduce", api.AllReduce);
     sym("ncclAllGather", api.AllGather);
     sym("ncclGetErrorString", api.GetErrorString);
+    // optional: absent in older NCCL builds (then the exchange buffer stays in the arena)
+    api.MemAlloc = reinterpret_cast<decltype(api.MemAlloc)>(dlsym(h, "ncclMemAlloc"));
+    api.MemFree = reinterpret_cast<decltype(api.MemFree)>(dlsym(h, "ncclMemFree"));
+    api.CommWindowRegister = reinterpret_cast<decltype(api.CommWindowRegister)>(dlsym(h, "ncclCommWindowRegister"));
+    api.CommWindowDeregister =
+        reinterpret_cast<decltype(api.CommWindowDeregister)>(dlsym(h, "ncclCommWindowDeregister"));
   });
   if (!err.empty()) raise(GRT_NcclError, err);
   return api;
@@ -77,6 +88,7 @@ NcclComm::NcclComm(const void* unique_id, int nranks, int rank, int device) {
 }
 
 NcclComm::~NcclComm() {
+  while (!windows_.empty()) free_symmetric(windows_.back().first);
   if (comm_) nccl().CommDestroy(static_cast<ncclComm_t>(comm_));
 }
 
@@ -84,6 +96,33 @@ cudaError_t NcclComm::allreduce_sum(float* buf, size_t n, cudaStream_t s) {
   return nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, static_cast<ncclComm_t>(comm_), s) == ncclSuccess
              ? cudaSuccess
              : cudaErrorUnknown;
+}
+
+// Symmetric exchange buffer: ncclMemAlloc'd and registered as a symmetric
+// window (collective over the communicator: every rank calls it, same size).
+void* NcclComm::alloc_symmetric(size_t bytes) {
+  const NcclApi& a = nccl();
+  if (!a.MemAlloc || !a.MemFree || !a.CommWindowRegister || !a.CommWindowDeregister) return nullptr;
+  void* p = nullptr;
+  if (a.MemAlloc(&p, bytes) != ncclSuccess || !p) return nullptr;
+  ncclWindow_t win = nullptr;
+  if (a.CommWindowRegister(static_cast<ncclComm_t>(comm_), p, bytes, &win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) {
+    a.MemFree(p);
+    return nullptr;
+  }
+  windows_.push_back({p, win});
+  return p;
+}
+
+void NcclComm::free_symmetric(void* p) {
+  const NcclApi& a = nccl();
+  for (size_t i = 0; i < windows_.size(); ++i)
+    if (windows_[i].first == p) {
+      a.CommWindowDeregister(static_cast<ncclComm_t>(comm_), static_cast<ncclWindow_t>(windows_[i].second));
+      a.MemFree(p);
+      windows_.erase(windows_.begin() + static_cast<std::ptrdiff_t>(i));
+      return;
+    }
 }
 
 cudaError_t NcclComm::allgather(const float* in, float* out, size_t n_per_rank, cudaStream_t s) {

@@ -171,6 +171,7 @@ EXPORTS = [
     "grt_ipc_client_generate", "grt_ipc_client_destroy",
     "grt_capture_begin", "grt_capture_record", "grt_capture_record_external", "grt_capture_end",
     "grt_capture_state_get", "grt_capture_destroy", "grt_plan_size", "grt_session_replay", "grt_model_arena_info",
+    "grt_model_tp_info",
 ]
 
 _lib = None
@@ -254,6 +255,7 @@ def lib():
         L.grt_capture_destroy.argtypes = [vp]
         L.grt_capture_destroy.restype = None
         L.grt_plan_size.argtypes = [vp, C.c_int32, C.POINTER(C.c_int32)]
+        L.grt_model_tp_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.grt_session_replay.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32]
         L.grt_model_arena_info.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.grt_graph_cache_create.argtypes = [C.c_uint64, C.c_int32, C.POINTER(vp)]
@@ -440,6 +442,12 @@ class Model:
             self.close()
         except Exception:
             pass
+
+    def tp_info(self):
+        """-> (tp_size, tp_rank, symmetric): symmetric = the allreduce buffer is an NCCL symmetric window."""
+        a, b, c = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().grt_model_tp_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, bool(c.value)
 
     def arena_info(self):
         """-> (capacity, used, allocations) of the model's single device arena."""

@@ -35,6 +35,7 @@ def test_one_rank_nccl_group_in_graph_matches_plain_model():
     want_logits = plain.logits()
     m = g.Model(g.ModelConfig(**KW))
     m.attach_nccl(g.tp_unique_id())  # tp_size 1: a 1-rank group
+    assert m.tp_info() == (1, 0, True)  # x moved into an NCCL symmetric window
     s = g.Session(m, _cache())
     r1 = s.run(g.GenerationRequest(prompt=prompt, gen_len=40))  # eager misses + inline captures (NCCL nodes)
     r2 = s.run(g.GenerationRequest(prompt=prompt, gen_len=40))  # prefill graph + step graphs replayed
