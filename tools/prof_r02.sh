@@ -1,12 +1,27 @@
-# Round-2 profile set (one GPU, run via gpurun): launch lists and one full ncu
-# capture per decode / prefill kernel of the current build, into gpurun_out/.
+# Round-2 profile set (one GPU; run via gpurun, outputs in gpurun_out/r02p_*):
+# launch lists of a decode token / a batched prefill / the sampler, and one
+# full ncu capture per decode and prefill kernel.  Summaries: tools/launch_summary.py,
+# tools/ncu_summary.py -> profiles/r02_*.txt.
 cd "$GRAFT_REPO_ROOT"
 NCU=/usr/local/cuda/bin/ncu
 O=gpurun_out/r02p
-# one full capture of each decode kernel (eager step API, 4 layers; skip layer 0)
-for k in "gemv_pair_kernel:2" "gemv_kernel<__nv_bfloat16, 2, 3>:2" "gemv_kernel<__nv_bfloat16, 0, 1>:2" "attn_decode_kernel:2" "gemv_kernel<__nv_bfloat16, 2, 0>:2"; do
-  name=${k%%:*}; skip=${k##*:}; tag=$(echo "$name" | tr -cd 'a-z0-9_')
-  timeout 600 $NCU --set full --clock-control none --import-source on -k "regex:${name//</\\<}" --launch-skip $skip -c 1 -o ${O}_${tag} -f python tools/decode_prof.py 10 4 2 > ${O}_${tag}.log 2>&1
+B="python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-profile --sweep= --mixed 0 --ipc 0 --modes="
+# launch lists (gpu__time_duration only): decode at P=10 / P=500, prefill at P=10 / P=500, sampler
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${O}_decode10_launches.csv $B > ${O}_l10.log 2>&1
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${O}_decode500_launches.csv $B --prompt-len 500 > ${O}_l500.log 2>&1
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${O}_prefill500_launches.csv python tools/prefill_prof.py 500 32 1 > ${O}_lp500.log 2>&1
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${O}_prefill10_launches.csv python tools/prefill_prof.py 10 32 1 > ${O}_lp10.log 2>&1
+for k in topp topk greedy; do
+  timeout 300 $NCU --metrics gpu__time_duration.sum --clock-control none -k regex:grt_sample --csv --log-file ${O}_sampler_$k.csv python tools/topp_prof.py $k > ${O}_s_$k.log 2>&1
 done
+# full captures (eager step API of tools/decode_prof.py, 4 layers; launch indices skip layer 0)
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemv_pair --launch-skip 2 -c 1 -o ${O}_gemv_pair_kernel -f python tools/decode_prof.py 10 4 2 > ${O}_pair.log 2>&1
+# gemv_kernel launches: 0 prefill head, then per step q0 d0 q1 d1 q2 d2 q3 d3 head
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemv_kernel --launch-skip 3 -c 2 -o ${O}_gemv_qkv_down -f python tools/decode_prof.py 10 4 2 > ${O}_gemv_qkv_down.log 2>&1
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemv_kernel --launch-skip 9 -c 1 -o ${O}_gemv_head -f python tools/decode_prof.py 10 4 2 > ${O}_gemv_head.log 2>&1
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:attn_decode --launch-skip 2 -c 1 -o ${O}_attn_decode_kernel -f python tools/decode_prof.py 10 4 2 > ${O}_attn10.log 2>&1
 timeout 600 $NCU --set full --clock-control none -k regex:attn_decode --launch-skip 2 -c 1 -o ${O}_attn500 -f python tools/decode_prof.py 500 4 2 > ${O}_attn500.log 2>&1
 timeout 600 $NCU --set full --clock-control none -k regex:grt_sample --launch-skip 4 -c 1 -o ${O}_sampler_topp -f python tools/topp_prof.py topp > ${O}_sampler_topp_full.log 2>&1
+# batched prefill P=500 (4 layers): the four GEMMs of layer 1 and one flash-attention launch
+timeout 600 $NCU --set full --clock-control none -k regex:prefill_gemm --launch-skip 4 -c 4 -o ${O}_pfgemm500 -f python tools/prefill_prof.py 500 4 1 > ${O}_pfgemm500.log 2>&1
+timeout 600 $NCU --set full --clock-control none -k regex:prefill_fa --launch-skip 1 -c 1 -o ${O}_pffa500 -f python tools/prefill_prof.py 500 4 1 > ${O}_pffa500.log 2>&1
