@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc05.cuh"
 
 namespace grt {
 
@@ -286,11 +287,22 @@ __global__ void __launch_bounds__(FA_WARPS * 32)
   const int g = lane >> 2, t = lane & 3;
   const int nq = min(FA_QB, P - q0);
 
-  for (int e = threadIdx.x; e < FA_QB * DH / 2; e += FA_WARPS * 32) {
-    const int r = e / (DH / 2), c = 2 * (e - r * (DH / 2));
-    float2 v = make_float2(0.f, 0.f);
-    if (r < nq) v = *reinterpret_cast<const float2*>(Q + static_cast<int64_t>(q0 + r) * d + head * DH + c);
-    *reinterpret_cast<__nv_bfloat162*>(&Qs[r * LD + c]) = __floats2bfloat162_rn(v.x, v.y);
+  // Q (fp32) -> bf16: 16-byte loads, 8 in flight per thread
+  constexpr int QV = FA_QB * DH / 4 / (FA_WARPS * 32);  // float4s per thread
+#pragma unroll
+  for (int h = 0; h < QV; h += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = threadIdx.x + (h + u) * FA_WARPS * 32, r = e / (DH / 4), c = 4 * (e - r * (DH / 4));
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nq) v[u] = *reinterpret_cast<const float4*>(Q + static_cast<int64_t>(q0 + r) * d + head * DH + c);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = threadIdx.x + (h + u) * FA_WARPS * 32, r = e / (DH / 4), c = 4 * (e - r * (DH / 4));
+      *reinterpret_cast<uint2*>(&Qs[r * LD + c]) = make_uint2(pack_bf16(v[u].x, v[u].y), pack_bf16(v[u].z, v[u].w));
+    }
   }
   __syncthreads();
   uint32_t qf[KS][4];
@@ -426,6 +438,300 @@ __global__ void __launch_bounds__(FA_WARPS * 32)
   }
 }
 
+// ---- causal attention on the 5th-generation tensor cores (head_dim 128) ------
+// One CTA = 128 queries of one head, 4 warps; warp w owns TMEM lanes 32w..32w+31,
+// i.e. thread = query row.  Per 128-key block:
+//   S = Q K^T     tcgen05.mma (M=128 queries, N=128 keys, K=head_dim) -> TMEM cols [0,128)
+//   softmax       the thread's S row in 4 tcgen05.ld x32 (one wait), online max /
+//                 sum in the log2 domain (ft_softmax), P (bf16) into shared memory
+//                 as the next A operand
+//   O += P V      tcgen05.mma (M=128 queries, N=128 head_dim, K=128 keys) into the
+//                 TMEM accumulator, cols [128,256); when a row's reference max
+//                 moves, the warp rescales its rows in place (tcgen05.ld/st).
+// The next block's S MMA is issued before this block's P V is waited on.
+// Q, K, V and P tiles are [128][128] bf16 in the K-major 128-byte swizzled layout
+// (two [128][64] halves).  K and V are both copied row by row (key = row, head
+// dim contiguous) with 16-byte cp.async through the page table; V is therefore
+// the MN-major B operand of the second MMA (N = head dim contiguous).  The next
+// block's K/V copies overlap this block's MMAs and softmax.
+constexpr int FT_ROWS = 128, FT_THREADS = 128;
+constexpr uint32_t FT_TILE = FT_ROWS * 128 * 2;  // 32 KB
+
+// byte offset of element (row r, col c) of a [128][128] bf16 tile, 128-byte swizzle
+__device__ __forceinline__ uint32_t ft_off(int r, int c) {
+  return static_cast<uint32_t>((c >> 6) * (FT_TILE / 2) + r * 128 + ((((c & 63) >> 3) ^ (r & 7)) << 4) + (c & 7) * 2);
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane; no wait (batch several,
+// then tc_wait_ld once)
+#define FT_R32(r) "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), \
+    "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),          \
+    "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),        \
+    "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+#define FT_W32(r) "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), \
+    "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),      \
+    "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),      \
+    "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+__device__ __forceinline__ void tc_ld32_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : FT_R32(r)
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      FT_W32(r)
+      : "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Online-softmax update of one query row over a 128-key block (log2 domain).
+// m = the row's reference max of s * sl2, moved only when the block max exceeds
+// it by more than FT_RESCALE (FlashAttention-4's conditional rescale: P values
+// up to 2^FT_RESCALE are exact in fp32/bf16 range, and most blocks then leave
+// the output accumulator alone); alpha = exp2(m_old - m_new) (1 if unmoved);
+// P = exp2(s * sl2 - m) as bf16 into the swizzled P tile; ls = sum of this
+// block's P.  MASK: keys c > lim are masked out (causal diagonal).  Independent
+// partial max / sum accumulators keep the dependency chains short.
+constexpr float FT_RESCALE = 8.0f;
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+template <bool MASK>
+__device__ __forceinline__ void ft_softmax(const uint32_t (&s)[128], int lim, float sl2, float& m, float& alpha,
+                                           float& ls, uint8_t* Ps, int r) {
+  float mx[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) mx[k] = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 128; ++i) {
+    const float v = __uint_as_float(s[i]);
+    if (!MASK || i <= lim) mx[i & 7] = fmaxf(mx[i & 7], v);
+  }
+  const float bm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+  const float cand = bm * sl2;
+  alpha = 1.0f;
+  if (m == -INFINITY) {
+    m = cand;  // first block (key 0 is visible to every row)
+  } else if (cand > m + FT_RESCALE) {
+    alpha = ex2_approx(m - cand);
+    m = cand;
+  }
+  const float mn = m;
+  float acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+#pragma unroll
+  for (int cc = 0; cc < 16; ++cc) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      const int c = 8 * cc + i;
+      float p0 = ex2_approx(fmaf(__uint_as_float(s[c]), sl2, -mn));
+      float p1 = ex2_approx(fmaf(__uint_as_float(s[c + 1]), sl2, -mn));
+      if (MASK) {
+        p0 = c <= lim ? p0 : 0.0f;
+        p1 = c + 1 <= lim ? p1 : 0.0f;
+      }
+      acc[i] += p0;
+      acc[i + 1] += p1;
+      pk[i / 2] = pack_bf16(p0, p1);
+    }
+    *reinterpret_cast<uint4*>(Ps + ft_off(r, 8 * cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+  ls = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
+__global__ void __launch_bounds__(FT_THREADS, 1)
+    prefill_fa_tc_kernel(const float* Q, const __nv_bfloat16* k_cache, const __nv_bfloat16* v_cache, int start, int P,
+                          int d, int max_seq, float scale, __nv_bfloat16* out, KvPaging kvp) {
+  extern __shared__ __align__(1024) uint8_t ft_raw[];
+  __shared__ uint64_t bar_s, bar_o;
+  __shared__ uint32_t tmem_base;
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ft_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Qs = sm;
+  uint8_t* Ks = sm + FT_TILE;
+  uint8_t* Vs = sm + 3 * FT_TILE;
+  uint8_t* Ps = sm + 5 * FT_TILE;
+  const int head = blockIdx.y, q0 = (gridDim.x - 1 - blockIdx.x) * FT_ROWS;
+  const int tid = threadIdx.x, warp = tid >> 5, r = tid;
+  const int nq = min(FT_ROWS, P - q0);
+  const int last_pos = start + q0 + nq - 1;
+  const int qpos = start + q0 + r;
+
+  if (tid == 0) {
+    mbar_init(&bar_s, 1);
+    mbar_init(&bar_o, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // K/V copies: thread = one 16-byte column chunk of rows tid/16 + 8i, so its
+  // swizzled shared offset is fixed up to i * 1024 B
+  const int ld_row = tid >> 4, ld_c = (tid & 15) * 8;
+  const uint32_t ld_off = ft_off(ld_row, ld_c);
+  auto load_kv = [&](int kb, int buf) {
+    uint8_t* ks = Ks + buf * FT_TILE + ld_off;
+    uint8_t* vs = Vs + buf * FT_TILE + ld_off;
+    if (kvp.page == 0) {
+      const int64_t g0 = (static_cast<int64_t>(head) * max_seq + kb + ld_row) * 128 + ld_c;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const bool ok = kb + ld_row + 8 * i <= last_pos;
+        const int64_t g = ok ? g0 + i * 1024 : 0;
+        cp_async16(ks + i * 1024, k_cache + g, ok);
+        cp_async16(vs + i * 1024, v_cache + g, ok);
+      }
+    } else {
+      for (int i = 0; i < 16; ++i) {
+        const bool ok = kb + ld_row + 8 * i <= last_pos;
+        const int64_t g = ok ? kv_row(kvp, head, max_seq, kb + ld_row + 8 * i) * 128 + ld_c : 0;
+        cp_async16(ks + i * 1024, k_cache + g, ok);
+        cp_async16(vs + i * 1024, v_cache + g, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  load_kv(0, 0);
+  // Q (fp32, just written by the QKV GEMM) -> bf16 tile: 8 rows' loads in flight per thread
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float4 a[8], b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + (8 * h + u) * FT_THREADS, row = e >> 4, c = (e & 15) * 8;
+      a[u] = b[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row < nq) {
+        const float4* src = reinterpret_cast<const float4*>(Q + static_cast<int64_t>(q0 + row) * d + head * 128 + c);
+        a[u] = src[0];
+        b[u] = src[1];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + (8 * h + u) * FT_THREADS, row = e >> 4, c = (e & 15) * 8;
+      *reinterpret_cast<uint4*>(Qs + ft_off(row, c)) = make_uint4(pack_bf16(a[u].x, a[u].y), pack_bf16(a[u].z, a[u].w),
+                                                                  pack_bf16(b[u].x, b[u].y), pack_bf16(b[u].z, b[u].w));
+    }
+  }
+  const uint32_t sQ = smem_u32(Qs), sK = smem_u32(Ks), sV = smem_u32(Vs), sP = smem_u32(Ps);
+  constexpr uint32_t idesc_s = idesc_bf16(128), idesc_o = idesc_bf16(128) | IDESC_B_MN_MAJOR;
+  const float sl2 = scale * 1.4426950408889634f;  // scores in log2 units: p = exp2(s * sl2 - m)
+  float m = -INFINITY, l = 0.0f;
+  int j = 0;
+  for (int kb = 0; kb <= last_pos; kb += FT_ROWS, ++j) {
+    const int buf = j & 1;
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tm = tmem_base + (static_cast<uint32_t>(32 * warp) << 16);
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t off = (ks >> 2) * (FT_TILE / 2) + (ks & 3) * 32;
+        tc_mma_bf16(tmem_base, sw128_desc(sQ + off), sw128_desc(sK + buf * FT_TILE + off), idesc_s, ks > 0);
+      }
+      tc_commit(&bar_s);
+    }
+    if (j > 0) mbar_wait(&bar_o, (j - 1) & 1);  // P V of block j-1: Ps and buffer buf^1 free, O settled
+    if (kb + FT_ROWS <= last_pos) load_kv(kb + FT_ROWS, buf ^ 1);
+    mbar_wait(&bar_s, j & 1);
+    tc_fence_after();
+    uint32_t s[128];  // this query's 128 scores: 4 TMEM loads in flight, one wait
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tc_ld32_nowait(tm + 32 * q, s + 32 * q);
+    tc_wait_ld();
+    float alpha, ls;
+    if (kb + FT_ROWS - 1 <= start + q0)  // block entirely below the diagonal for every row: no mask
+      ft_softmax<false>(s, 0, sl2, m, alpha, ls, Ps, r);
+    else
+      ft_softmax<true>(s, qpos - kb, sl2, m, alpha, ls, Ps, r);
+    l = l * alpha + ls;
+    if (j > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {  // rescale the running output in TMEM
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t v[64];
+        tc_ld32_nowait(tm + 128 + 64 * h, v);
+        tc_ld32_nowait(tm + 128 + 64 * h + 32, v + 32);
+        tc_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+        tc_st32(tm + 128 + 64 * h, v);
+        tc_st32(tm + 128 + 64 * h + 32, v + 32);
+      }
+      tc_wait_st();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t pa = (ks >> 2) * (FT_TILE / 2) + (ks & 3) * 32;
+        tc_mma_bf16(tmem_base + 128, sw128_desc(sP + pa), sw128_desc_mn(sV + buf * FT_TILE + ks * 2048, FT_TILE / 2, 1024),
+                    idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+      }
+      tc_commit(&bar_o);
+    }
+  }
+  mbar_wait(&bar_o, (j - 1) & 1);
+  tc_fence_after();
+  const uint32_t tm = tmem_base + (static_cast<uint32_t>(32 * warp) << 16);
+  const float inv = 1.0f / l;
+  uint4* op = reinterpret_cast<uint4*>(out + static_cast<int64_t>(q0 + r) * d + head * 128);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[64];
+    tc_ld32_nowait(tm + 128 + 64 * h, v);
+    tc_ld32_nowait(tm + 128 + 64 * h + 32, v + 32);
+    tc_wait_ld();
+    if (r < nq) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float* f = reinterpret_cast<const float*>(v + 8 * c);
+        op[8 * h + c] = make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
+                                   pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256) : "memory");
+  }
+}
+
+static cudaError_t fa_tc_launch(const float* Q, const void* k, const void* v, int start, int P, int d, int n_heads,
+                                int max_seq, float scale, void* out, cudaStream_t s, KvPaging kvp) {
+  const size_t smem = 6 * FT_TILE + 1024;  // Q, 2 x K, 2 x V, P tiles + 1 KB alignment slack
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_fa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((P + FT_ROWS - 1) / FT_ROWS, n_heads);
+  prefill_fa_tc_kernel<<<grid, FT_THREADS, smem, s>>>(Q, static_cast<const __nv_bfloat16*>(k),
+                                                      static_cast<const __nv_bfloat16*>(v), start, P, d, max_seq, scale,
+                                                      static_cast<__nv_bfloat16*>(out), kvp);
+  return cudaGetLastError();
+}
+
 template <typename KT, int DH>
 static cudaError_t attn_launch(const float* Q, const void* k, const void* v, int start, int P, int d, int n_heads,
                                int max_seq, float scale, void* out, cudaStream_t s, KvPaging kvp) {
@@ -477,6 +783,9 @@ cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, con
                                      int n_heads, int dh, int max_seq, float scale, void* out, cudaStream_t s,
                                      KvPaging kvp) {
   if (kvdt == Dt::BF16) {  // tensor cores for bf16 KV
+    // tcgen05 once there is a full 128-key block to attend over; a short prompt's
+    // single partial tile is cheaper on the mma.sync kernel's 64 x 64 tiles
+    if (dh == 128 && start + P >= FT_ROWS) return fa_tc_launch(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
     if (dh == 64) return fa_launch<64>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
     if (dh == 128) return fa_launch<128>(Q, k, v, start, P, d, n_heads, max_seq, scale, out, s, kvp);
   }

@@ -52,7 +52,7 @@ def test_llama_7b_dims_paged_bit_identical_to_contiguous(page, batched):
     mp.set_kv_block_table(rng.permutation(n).tolist())
     sp = g.Session(mp, g.CacheConfig(bucket_size=32, warmup_hi=0, batched_prefill=batched))
     sc = g.Session(_llama(0), g.CacheConfig(bucket_size=32, warmup_hi=0, batched_prefill=batched))
-    prompt = po.make_prompt(42, 70, 32000)
+    prompt = po.make_prompt(42, 150, 32000)  # > 128: the tcgen05 prefill attention reads through the page table
     sp.prefill(prompt)
     sc.prefill(prompt)
     assert np.array_equal(sp.logits(), sc.logits())
@@ -60,7 +60,7 @@ def test_llama_7b_dims_paged_bit_identical_to_contiguous(page, batched):
         sp.step(t)
         sc.step(t)
         assert np.array_equal(sp.logits(), sc.logits())
-    for row in (0, 33, 72):
+    for row in (0, 33, 152):
         assert np.array_equal(sp.kv_row(1, 0, row), sc.kv_row(1, 0, row))
         assert np.array_equal(sp.kv_row(0, 1, row), sc.kv_row(0, 1, row))
     a = sp.run(g.GenerationRequest(prompt=prompt, gen_len=24))

@@ -40,18 +40,25 @@ def raw(rep):
 
 
 def stalls(rep, n):
-    out = subprocess.run([NCU, "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--launch-count", "1"],
+    """Top stall lines of the FIRST kernel on the source page (the page holds one
+    header + body block per profiled kernel)."""
+    out = subprocess.run([NCU, "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    if len(rows) < 3:
+    key = "Warp Stall Sampling (All Samples)"
+    start = next((k for k, r in enumerate(rows) if key in r), None)
+    if start is None:
         return []
-    hdr = rows[1]
-    if "Warp Stall Sampling (All Samples)" not in hdr:
-        return []
-    i = hdr.index("Warp Stall Sampling (All Samples)")
-    body = [r for r in rows[2:] if len(r) > i]
-    tot = sum(int(r[i] or 0) for r in body) or 1
-    top = sorted(body, key=lambda r: -int(r[i] or 0))[:n]
+    hdr = rows[start]
+    i = hdr.index(key)
+    body = []
+    for r in rows[start + 1:]:
+        if key in r or (r and r[0] == "Kernel Name"):
+            break  # the next kernel's block
+        if len(r) > i and r[i].isdigit():
+            body.append(r)
+    tot = sum(int(r[i]) for r in body) or 1
+    top = sorted(body, key=lambda r: -int(r[i]))[:n]
     return [(int(r[i]) / tot, r[1].strip()) for r in top]
 
 
