@@ -98,7 +98,7 @@ def _logits_dev(lg):
     return torch.from_numpy(np.ascontiguousarray(lg, np.float32)).cuda()
 
 
-@pytest.mark.parametrize("vocab", [8, 256, 1000, 32000])
+@pytest.mark.parametrize("vocab", [8, 256, 1000, 8195, 32000, 50257])  # ragged vocabulary sizes; > 32768: the 8-bit-pass path
 def test_sampler_topkp_bitexact_vs_oracle(vocab):
     rs = np.random.RandomState(vocab)
     tok = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -117,7 +117,7 @@ def test_sampler_topkp_bitexact_vs_oracle(vocab):
                 assert int(tok.item()) == want, (vocab, rep, t, k, p, step)
 
 
-@pytest.mark.parametrize("vocab", [5, 256, 32000])
+@pytest.mark.parametrize("vocab", [5, 256, 8195, 32000])
 def test_sampler_greedy_and_temperature(vocab):
     rs = np.random.RandomState(3)
     tok = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -127,6 +127,8 @@ def test_sampler_greedy_and_temperature(vocab):
             lg[:] = 0.0
         if rep == 2 and vocab > 3:
             lg[1] = lg[3] = lg.max() + 1.0  # tie -> lowest index (tensor_kernels_test.cpp:293-301)
+        if rep == 3 and vocab > 8000:
+            lg[7999] = lg[4100] = lg.max() + 1.0  # a tie far apart (different threads and warps)
         ld = _logits_dev(lg)
         g.op_sample(ld.data_ptr(), vocab, g.SampleStrategy.greedy(), 0, 0, 0.0, tok.data_ptr())
         assert int(tok.item()) == po.sample_greedy(lg)
