@@ -137,6 +137,7 @@ enum PgEpi : int {
   PG_EPI_SWIGLU = 2,    // out_bf16[n][m/2] = silu(gate) * up   (rows 2j, 2j+1)
   PG_EPI_QKV = 3,       // q -> q_out[n], k/v -> KV rows start_pos + n
   PG_EPI_QKV_ROPE = 4,  // as QKV with rotate-half RoPE at position start_pos + n
+  PG_EPI_RELU = 5,      // out_bf16[n][m] = max(v, 0)  (reference arch W1, make_relu kernels.cpp:176-186)
 };
 struct PrefillGemmParams {
   int M = 0, K = 0, P = 0;  // Y[P, M] = X[P, K] . W[M, K]^T  (bf16 operands, fp32 accumulate)
@@ -174,8 +175,10 @@ cudaError_t prefill_gemm_prepare();
 int prefill_gemm_ksplit(int M, int K, int sms);
 size_t prefill_gemm_part_floats(int M, int K, int P, int sms);
 constexpr int PREFILL_CHUNK = 512;  // tokens per batched pass (two 256-token TMEM accumulators)
-cudaError_t launch_prefill_embed(Dt wdt, const int* tokens, int start, int P, const void* emb, int d, float* X,
-                                 int vocab, int* err, cudaStream_t s);
+cudaError_t launch_prefill_embed(Dt wdt, const int* tokens, int start, int P, const void* emb, const void* pos, int d,
+                                 float* X, int vocab, int* err, cudaStream_t s);  // pos: nullptr for LLaMA
+cudaError_t launch_prefill_layernorm(const float* X, int P, const float* gamma, const float* beta, float eps, int d,
+                                     void* Xn, cudaStream_t s);
 cudaError_t launch_prefill_rmsnorm(const float* X, int P, const float* gamma, float eps, int d, void* Xn,
                                    cudaStream_t s);
 cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, const void* v, int start, int P, int d,

@@ -19,10 +19,11 @@
 
 namespace grt {
 
-// x[i][:] = emb[tokens[start+i]][:]  (LLaMA: no position table)
+// x[i][:] = emb[tokens[start+i]][:] (+ pos[start+i][:] in the reference arch,
+// extend_position kernels.cpp:238-259; LLaMA: no position table)
 template <typename WT>
-__global__ void prefill_embed_kernel(const int* tokens, int start, int P, const WT* emb, int d, float* X, int vocab,
-                                     int* err) {
+__global__ void prefill_embed_kernel(const int* tokens, int start, int P, const WT* emb, const WT* pos, int d, float* X,
+                                     int vocab, int* err) {
   const int i = blockIdx.x;
   if (i >= P) return;
   const int tok = tokens[start + i];
@@ -31,7 +32,9 @@ __global__ void prefill_embed_kernel(const int* tokens, int start, int P, const 
     return;
   }
   const WT* row = emb + static_cast<int64_t>(tok) * d;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) X[static_cast<int64_t>(i) * d + j] = to_f32(row[j]);
+  const WT* prow = pos ? pos + static_cast<int64_t>(start + i) * d : nullptr;
+  for (int j = threadIdx.x; j < d; j += blockDim.x)
+    X[static_cast<int64_t>(i) * d + j] = prow ? to_f32(row[j]) + to_f32(prow[j]) : to_f32(row[j]);
 }
 
 // Xn[i] = bf16(rmsnorm(X[i]) * gamma): ss = sum x^2 ; inv = 1/sqrt(ss/d + eps).
@@ -70,6 +73,58 @@ __global__ void __launch_bounds__(PN_THREADS) prefill_rmsnorm_kernel(const float
     if (j >= n4) continue;
     o[2 * j] = __floats2bfloat162_rn(v[u].x * inv * g[u].x, v[u].y * inv * g[u].y);
     o[2 * j + 1] = __floats2bfloat162_rn(v[u].z * inv * g[u].z, v[u].w * inv * g[u].w);
+  }
+}
+
+// Xn[i] = bf16((X[i] - mean) / sqrt(var + eps) * gamma + beta): the reference
+// arch's make_layernorm (kernels.cpp:52-85) for all P rows, one CTA per row.
+__global__ void __launch_bounds__(PN_THREADS) prefill_layernorm_kernel(const float* X, const float* gamma,
+                                                                       const float* beta, float eps, int d,
+                                                                       __nv_bfloat16* Xn) {
+  __shared__ float red[32];
+  const int i = blockIdx.x;
+  const float4* x = reinterpret_cast<const float4*>(X + static_cast<int64_t>(i) * d);
+  const int n4 = d >> 2;
+  float4 v[PN_MAXV];
+#pragma unroll
+  for (int u = 0; u < PN_MAXV; ++u) {
+    const int j = threadIdx.x + u * PN_THREADS;
+    v[u] = j < n4 ? x[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  auto block_sum = [&](float t) {
+    t = warp_sum(t);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float a = threadIdx.x < (PN_THREADS >> 5) ? red[threadIdx.x] : 0.0f;
+      a = warp_sum(a);
+      if (threadIdx.x == 0) red[0] = a;
+    }
+    __syncthreads();
+    return red[0];
+  };
+  float s = 0.0f;
+#pragma unroll
+  for (int u = 0; u < PN_MAXV; ++u) s += (v[u].x + v[u].y) + (v[u].z + v[u].w);
+  const float mean = block_sum(s) / static_cast<float>(d);
+  float q = 0.0f;
+#pragma unroll
+  for (int u = 0; u < PN_MAXV; ++u) {
+    const int j = threadIdx.x + u * PN_THREADS;
+    if (j >= n4) continue;
+    const float a = v[u].x - mean, b = v[u].y - mean, c = v[u].z - mean, e = v[u].w - mean;
+    q += (a * a + b * b) + (c * c + e * e);
+  }
+  const float inv = 1.0f / sqrtf(block_sum(q) / static_cast<float>(d) + eps);
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(Xn + static_cast<int64_t>(i) * d);
+#pragma unroll
+  for (int u = 0; u < PN_MAXV; ++u) {
+    const int j = threadIdx.x + u * PN_THREADS;
+    if (j >= n4) continue;
+    const float4 g = reinterpret_cast<const float4*>(gamma)[j], b = reinterpret_cast<const float4*>(beta)[j];
+    o[2 * j] = __floats2bfloat162_rn((v[u].x - mean) * inv * g.x + b.x, (v[u].y - mean) * inv * g.y + b.y);
+    o[2 * j + 1] = __floats2bfloat162_rn((v[u].z - mean) * inv * g.z + b.z, (v[u].w - mean) * inv * g.w + b.w);
   }
 }
 
@@ -215,12 +270,21 @@ __global__ void prefill_handoff_kernel(const float* X_last, int d, float* x, int
 
 // ---- host -----------------------------------------------------------------------
 
-cudaError_t launch_prefill_embed(Dt wdt, const int* tokens, int start, int P, const void* emb, int d, float* X,
-                                 int vocab, int* err, cudaStream_t s) {
+cudaError_t launch_prefill_embed(Dt wdt, const int* tokens, int start, int P, const void* emb, const void* pos, int d,
+                                 float* X, int vocab, int* err, cudaStream_t s) {
   if (wdt == Dt::BF16)
-    prefill_embed_kernel<<<P, 256, 0, s>>>(tokens, start, P, static_cast<const __nv_bfloat16*>(emb), d, X, vocab, err);
+    prefill_embed_kernel<<<P, 256, 0, s>>>(tokens, start, P, static_cast<const __nv_bfloat16*>(emb),
+                                           static_cast<const __nv_bfloat16*>(pos), d, X, vocab, err);
   else
-    prefill_embed_kernel<<<P, 256, 0, s>>>(tokens, start, P, static_cast<const float*>(emb), d, X, vocab, err);
+    prefill_embed_kernel<<<P, 256, 0, s>>>(tokens, start, P, static_cast<const float*>(emb),
+                                           static_cast<const float*>(pos), d, X, vocab, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefill_layernorm(const float* X, int P, const float* gamma, const float* beta, float eps, int d,
+                                     void* Xn, cudaStream_t s) {
+  if (d % 4 != 0 || d > 4 * PN_MAXV * PN_THREADS || !beta) return cudaErrorInvalidValue;
+  prefill_layernorm_kernel<<<P, PN_THREADS, 0, s>>>(X, gamma, beta, eps, d, static_cast<__nv_bfloat16*>(Xn));
   return cudaGetLastError();
 }
 
@@ -231,13 +295,13 @@ cudaError_t launch_prefill_rmsnorm(const float* X, int P, const float* gamma, fl
   return cudaGetLastError();
 }
 
-// ---- tensor-core flash attention (bf16 KV) ------------------------------------
+// ---- tensor-core flash attention (bf16 KV), short prompts and head_dim 64 -----
 // FA2-style on mma.sync.m16n8k16 (bf16 in, fp32 accumulate): a CTA = one head x
 // 64 queries (4 warps x 16 rows); 64-key K/V tiles staged in shared memory
 // (zero rows past the causal end); S = Q K^T and O += P V from ldmatrix
 // fragments, the S accumulator re-packed in registers as the P operand; online
-// softmax per row.  Attention is ~1% of the prefill flops, so the
-// legacy tensor path is enough here; the projections are the tcgen05 GEMMs.
+// softmax per row.  head_dim 128 with a full 128-key block goes to the tcgen05
+// kernel below (prefill_fa_tc_kernel).
 constexpr int FA_WARPS = 4, FA_QB = 64, FA_KB = 64;
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {

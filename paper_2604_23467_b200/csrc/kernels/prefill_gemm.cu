@@ -76,6 +76,13 @@ __device__ __forceinline__ void pg_epilogue16(const PrefillGemmParams& p, int m,
         if (j < nv) p.out[static_cast<int64_t>(n0 + j) * p.M + m] = old[j] + v[j];
       break;
     }
+    case PG_EPI_RELU: {
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out_bf16) + m;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nv) o[static_cast<int64_t>(n0 + j) * p.M] = __float2bfloat16_rn(fmaxf(v[j], 0.0f));
+      break;
+    }
     case PG_EPI_SWIGLU: {
       if (m & 1) return;
       __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out_bf16) + (m >> 1);
@@ -161,6 +168,12 @@ __device__ __forceinline__ void pg_epilogue_pair(const PrefillGemmParams& p, int
       p.out[static_cast<int64_t>(n) * p.M + m] += va;
       if (has_b) p.out[static_cast<int64_t>(n) * p.M + m + 1] += vb;
       break;
+    case PG_EPI_RELU: {
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out_bf16) + static_cast<int64_t>(n) * p.M + m;
+      o[0] = __float2bfloat16_rn(fmaxf(va, 0.0f));
+      if (has_b) o[1] = __float2bfloat16_rn(fmaxf(vb, 0.0f));
+      break;
+    }
     case PG_EPI_SWIGLU:
       static_cast<__nv_bfloat16*>(p.out_bf16)[static_cast<int64_t>(n) * (p.M >> 1) + (m >> 1)] =
           __float2bfloat16_rn(va / (1.0f + expf(-va)) * vb);

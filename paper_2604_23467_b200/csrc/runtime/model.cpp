@@ -576,14 +576,17 @@ uint64_t Model::decode_bytes(int length) const {
 // ---------------------------------------------------------------------------
 // batched prefill
 
+// Both architectures: LLaMA (RMSNorm, RoPE, SwiGLU) and the reference's own
+// (LayerNorm with beta, learned position table, ReLU MLP); bf16 weights (the
+// tcgen05 GEMM operands are the stored weights).
 bool Model::supports_batched_prefill() const {
   const int dh = cfg_.head_dim();
-  return cfg_.llama() && cfg_.weight_dtype == GRT_BF16 && cfg_.d_model % 8 == 0 && cfg_.d_ff() % 8 == 0 &&
+  return cfg_.weight_dtype == GRT_BF16 && cfg_.d_model % 8 == 0 && cfg_.d_ff() % 8 == 0 &&
          (dh == 16 || dh == 32 || dh == 64 || dh == 128);
 }
 
 void Model::prefill_batched(int p, cudaStream_t s, bool fuse_norm) {
-  if (!supports_batched_prefill()) raise(GRT_Unsupported, "batched prefill needs the LLaMA arch with bf16 weights");
+  if (!supports_batched_prefill()) raise(GRT_Unsupported, "batched prefill needs bf16 weights");
   if (p < 1 || p > cfg_.max_seq_len) raise(GRT_PromptTooLong, "batched prefill length out of range");
   const int d = cfg_.d_model, dh = cfg_.head_dim(), S = cfg_.max_seq_len;
   const int T = cfg_.tp_size, dq = dq_, ffl = ffl_, hl = hl_;  // this rank's shard
@@ -591,27 +594,35 @@ void Model::prefill_batched(int p, cudaStream_t s, bool fuse_norm) {
   const int resid_epi = (T == 1 || cfg_.tp_rank == 0) ? PG_EPI_RESID : PG_EPI_STORE;
   const Dt kvdt = cfg_.kv_dtype == GRT_BF16 ? Dt::BF16 : Dt::F32;
   const float scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:119
+  const bool llama = cfg_.llama();
   int last_P = 0;
   for (int start = 0; start < p; start += PREFILL_CHUNK) {
     const int P = std::min(PREFILL_CHUNK, p - start);
     last_P = P;
-    cuda_check(launch_prefill_embed(Dt::BF16, tokens_, start, P, emb_, d, pf_X_, cfg_.vocab_size, &ctrl_->err, s),
+    cuda_check(launch_prefill_embed(Dt::BF16, tokens_, start, P, emb_, llama ? nullptr : pos_, d, pf_X_,
+                                    cfg_.vocab_size, &ctrl_->err, s),
                "prefill embed");
     // Single GPU: a residual GEMM that splits K leaves its partials to the next
     // RMSNorm launch (reduce + residual + norm in one kernel, bit-identical).
-    const bool fuse_rn = !comm_ && fuse_norm;
+    const bool fuse_rn = !comm_ && fuse_norm && llama;
+    auto norm = [&](const float* g, const float* b, const char* what) {
+      if (llama)
+        cuda_check(launch_prefill_rmsnorm(pf_X_, P, g, cfg_.norm_eps, d, pf_Xn_, s), what);
+      else
+        cuda_check(launch_prefill_layernorm(pf_X_, P, g, b, cfg_.norm_eps, d, pf_Xn_, s), what);
+    };
     PrefillGemmParams prev_down;  // previous layer's down GEMM, if its reduce was deferred
     for (int l = 0; l < cfg_.n_layers; ++l) {
       const LayerBuffers& L = layers_[l];
       if (prev_down.defer_reduce && prev_down.ksplit > 1)
         cuda_check(launch_prefill_resid_norm(prev_down, L.ln1_g, cfg_.norm_eps, pf_Xn_, s), "prefill resid+rmsnorm1");
       else
-        cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln1_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm1");
+        norm(L.ln1_g, L.ln1_b, "prefill norm1");
       PrefillGemmParams q;
       q.M = 3 * dq;
       q.K = d;
       q.P = P;
-      q.epi = PG_EPI_QKV_ROPE;
+      q.epi = llama ? PG_EPI_QKV_ROPE : PG_EPI_QKV;
       q.q_out = pf_Q_;
       q.k_cache = L.k;
       q.kvp = kvp_;
@@ -642,12 +653,12 @@ void Model::prefill_batched(int p, cudaStream_t s, bool fuse_norm) {
       if (o.defer_reduce && o.ksplit > 1)
         cuda_check(launch_prefill_resid_norm(o, L.ln2_g, cfg_.norm_eps, pf_Xn_, s), "prefill resid+rmsnorm2");
       else
-        cuda_check(launch_prefill_rmsnorm(pf_X_, P, L.ln2_g, cfg_.norm_eps, d, pf_Xn_, s), "prefill rmsnorm2");
-      PrefillGemmParams u;
-      u.M = 2 * ffl;
+        norm(L.ln2_g, L.ln2_b, "prefill norm2");
+      PrefillGemmParams u;  // gate/up + SwiGLU (LLaMA) | W1 + ReLU (reference arch)
+      u.M = llama ? 2 * ffl : ffl;
       u.K = d;
       u.P = P;
-      u.epi = PG_EPI_SWIGLU;
+      u.epi = llama ? PG_EPI_SWIGLU : PG_EPI_RELU;
       u.out_bf16 = pf_act_;
       u.part = pf_part_;
       u.counters = pf_cnt_;
@@ -679,7 +690,7 @@ void Model::prefill_batched(int p, cudaStream_t s, bool fuse_norm) {
   hp.beta = lnf_b_;
   hp.eps = cfg_.norm_eps;
   hp.out = logits_local_;
-  cuda_check(launch_gemv(Dt::BF16, NORM_RMS, EPI_STORE, hp, s, false, 0), "prefill head");
+  cuda_check(launch_gemv(Dt::BF16, llama ? NORM_RMS : NORM_LN, EPI_STORE, hp, s, false, 0), "prefill head");
   if (comm_) cuda_check(comm_->allgather(logits_local_, logits_, static_cast<size_t>(vl_), s), "prefill allgather");
 }
 

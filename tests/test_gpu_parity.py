@@ -434,6 +434,51 @@ def test_batched_prefill_matches_oracle(kw, plen):
         assert err <= 2e-2, err
 
 
+@pytest.mark.parametrize("plen", [6, 150, 600])
+def test_batched_prefill_reference_arch_matches_oracle(plen):
+    """The reference's own architecture (LayerNorm with beta, learned position
+    table, ReLU MLP; kernels.cpp:52-85,176-186,238-259) through the batched
+    tcgen05 prefill: last-token logits vs the oracle's token-by-token prefill
+    (tolerance 2e-2), then two single-token steps on the handed-off state."""
+    import pyoracle as po
+    kw = dict(n_layers=2, d_model=128, n_heads=2, vocab_size=512, max_seq_len=640, seed=13)
+    o = po.OracleModel(arch=po.ARCH_REF, weight_dtype=po.BF16, kv_dtype=po.BF16, init=po.INIT_PHILOX, **kw)
+    s = g.Session(g.ModelConfig(arch=g.ARCH_REF, weight_dtype=g.BF16, kv_dtype=g.BF16, init=g.INIT_PHILOX,
+                                d_ff_=o.cfg.d_ff, **kw), g.CacheConfig(bucket_size=64, batched_prefill=True))
+    prompt = po.make_prompt(42, plen, kw["vocab_size"])
+    o.prefill(prompt)
+    r = s.run(g.GenerationRequest(prompt=prompt, gen_len=1))
+    assert r.prefill_paths == [g.StepPath.Batched] * plen
+    s.reset()
+    s.prefill(prompt)
+    err = float(np.abs(s.logits() - o.logits()).max())
+    assert err <= 2e-2, err
+    for t in (5, 7):
+        o.step(t)
+        s.step(t)
+        err = float(np.abs(s.logits() - o.logits()).max())
+        assert err <= 2e-2, err
+
+
+def test_batched_prefill_reference_arch_7b_dims_vs_token_by_token():
+    """The reference architecture at 7B dims (head_dim 128: the tcgen05 flash
+    attention, d_ff 16384 ReLU MLP): batched prefill of 200 tokens vs the
+    token-by-token GPU path on the same weights (tolerance 2e-2)."""
+    import pyoracle as po
+    kw = dict(arch=g.ARCH_REF, n_layers=2, d_model=4096, n_heads=32, vocab_size=32000, max_seq_len=256, seed=17,
+              weight_dtype=g.BF16, kv_dtype=g.BF16, init=g.INIT_PHILOX)
+    prompt = po.make_prompt(42, 200, 32000)
+    m = g.Model(g.ModelConfig(**kw))
+    a = g.Session(m, g.CacheConfig(bucket_size=64, warmup_hi=0, batched_prefill=True))
+    a.prefill(prompt)
+    la = a.logits()
+    a.close()
+    b = g.Session(m, g.CacheConfig(bucket_size=64, warmup_hi=0, batched_prefill=False))
+    b.prefill(prompt)
+    err = float(np.abs(la - b.logits()).max())
+    assert np.isfinite(la).all() and err <= 2e-2, err
+
+
 def test_batched_prefill_run_tokens_match_token_by_token():
     """Session.run with batched prefill reproduces the token-by-token run's greedy
     stream wherever the logit margins allow (same weights, same prompt)."""
