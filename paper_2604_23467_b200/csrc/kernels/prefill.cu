@@ -22,8 +22,8 @@ namespace grt {
 // x[i][:] = emb[tokens[start+i]][:] (+ pos[start+i][:] in the reference arch,
 // extend_position kernels.cpp:238-259; LLaMA: no position table)
 template <typename WT>
-__global__ void prefill_embed_kernel(const int* tokens, int start, int P, const WT* emb, const WT* pos, int d, float* X,
-                                     int vocab, int* err) {
+__global__ void prefill_embed_kernel(const int* tokens, int start, int P, const WT* __restrict__ emb,
+                                     const WT* __restrict__ pos, int d, float* __restrict__ X, int vocab, int* err) {
   const int i = blockIdx.x;
   if (i >= P) return;
   const int tok = tokens[start + i];
@@ -33,8 +33,19 @@ __global__ void prefill_embed_kernel(const int* tokens, int start, int P, const 
   }
   const WT* row = emb + static_cast<int64_t>(tok) * d;
   const WT* prow = pos ? pos + static_cast<int64_t>(start + i) * d : nullptr;
-  for (int j = threadIdx.x; j < d; j += blockDim.x)
-    X[static_cast<int64_t>(i) * d + j] = prow ? to_f32(row[j]) + to_f32(prow[j]) : to_f32(row[j]);
+  float* out = X + static_cast<int64_t>(i) * d;
+  constexpr int U = 8;  // a thread's loads of the row issued together
+  for (int j0 = threadIdx.x; j0 < d; j0 += U * blockDim.x) {
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * blockDim.x;
+      v[u] = j < d ? to_f32(row[j]) + (prow ? to_f32(prow[j]) : 0.0f) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j0 + u * blockDim.x < d) out[j0 + u * blockDim.x] = v[u];
+  }
 }
 
 // Xn[i] = bf16(rmsnorm(X[i]) * gamma): ss = sum x^2 ; inv = 1/sqrt(ss/d + eps).
@@ -264,8 +275,9 @@ __global__ void __launch_bounds__(PA_THREADS)
 
 // decode hand-off: residual row of the last prompt token -> x, seq_len = len
 __global__ void prefill_handoff_kernel(const float* X_last, int d, float* x, int* seq_len, int len) {
-  for (int j = threadIdx.x; j < d; j += blockDim.x) x[j] = X_last[j];
-  if (threadIdx.x == 0) *seq_len = len;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;  // one element per thread: one memory round trip
+  if (j < d) x[j] = X_last[j];
+  if (j == 0) *seq_len = len;
 }
 
 // ---- host -----------------------------------------------------------------------
@@ -858,7 +870,7 @@ cudaError_t launch_prefill_attention(Dt kvdt, const float* Q, const void* k, con
 }
 
 cudaError_t launch_prefill_handoff(const float* X_last, int d, float* x, int* seq_len, int len, cudaStream_t s) {
-  prefill_handoff_kernel<<<1, 256, 0, s>>>(X_last, d, x, seq_len, len);
+  prefill_handoff_kernel<<<(d + 255) / 256, 256, 0, s>>>(X_last, d, x, seq_len, len);
   return cudaGetLastError();
 }
 
