@@ -157,7 +157,24 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 // Epilogue of one row pair (m even, m+1) for one token: the split-K reduce path.
-__device__ __forceinline__ void pg_epilogue_pair(const PrefillGemmParams& p, int m, int n, float va, float vb) {
+// RoPE factors of row pair m at token n (QKV_ROPE, q/k sections), loaded before
+// the reduce kernels' dependency wait -- the tables do not depend on the GEMM
+struct PgRope {
+  float c = 1.0f, s = 0.0f;
+};
+__device__ __forceinline__ PgRope pg_rope_load(const PrefillGemmParams& p, int m, int n) {
+  PgRope r;
+  if (p.epi != PG_EPI_QKV_ROPE || m / p.d_model >= 2) return r;
+  const int half = p.head_dim >> 1;
+  const int lp = (m >> 1) - (m / p.d_model) * (p.d_model >> 1);
+  const int64_t t = static_cast<int64_t>(p.start_pos + n) * half + (lp - (lp / half) * half);
+  r.c = __ldg(p.rope_cos + t);
+  r.s = __ldg(p.rope_sin + t);
+  return r;
+}
+
+__device__ __forceinline__ void pg_epilogue_pair(const PrefillGemmParams& p, int m, int n, float va, float vb,
+                                                 PgRope rp) {
   const bool has_b = m + 1 < p.M;
   switch (p.epi) {
     case PG_EPI_STORE:
@@ -189,8 +206,7 @@ __device__ __forceinline__ void pg_epilogue_pair(const PrefillGemmParams& p, int
         const int half = dh >> 1;
         head = lp / half;
         const int i = lp - head * half;
-        const float c = p.rope_cos[static_cast<int64_t>(pos) * half + i];
-        const float sn = p.rope_sin[static_cast<int64_t>(pos) * half + i];
+        const float c = rp.c, sn = rp.s;
         ra = va * c - vb * sn;
         rb = vb * c + va * sn;
         e0 = i;
@@ -409,11 +425,14 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
 // (deterministic) and applies the epilogue, one thread per (row pair, token):
 // fully parallel, instead of one CTA per tile serialising a tail reduction.
 __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
-  griddep_wait();  // launched with PDL behind the GEMM: partials complete
   const int n_pairs = (p.M + 1) >> 1;
   const int64_t total = static_cast<int64_t>(n_pairs) * p.P;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t e0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  // this thread's first element's RoPE factors, before the wait
+  const PgRope r0 = e0 < total ? pg_rope_load(p, 2 * static_cast<int>(e0 % n_pairs), static_cast<int>(e0 / n_pairs))
+                               : PgRope{};
+  griddep_wait();  // launched with PDL behind the GEMM: partials complete
+  for (int64_t e = e0; e < total; e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int n = static_cast<int>(e / n_pairs);
     const int pr = static_cast<int>(e - static_cast<int64_t>(n) * n_pairs);
     const int m = 2 * pr;
@@ -426,7 +445,7 @@ __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
       va += q[0];
       vb += q[1];
     }
-    pg_epilogue_pair(p, m, n, va, vb);
+    pg_epilogue_pair(p, m, n, va, vb, e == e0 ? r0 : pg_rope_load(p, m, n));
   }
 }
 
@@ -434,19 +453,26 @@ __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
 // partials each ([tile - tail_first][split][token][128 rows]), summed in split
 // order, then the GEMM's epilogue; one thread per (row pair, token).
 __global__ void prefill_tail_reduce_kernel(const PrefillGemmParams p) {
-  griddep_wait();  // launched with PDL behind the GEMM: partials complete
   const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
   const int n_tail = m_tiles * p.n_ntiles - p.tail_first;
   const int per_tile = (PG_BM / 2) * p.ntile;
   const int64_t total = static_cast<int64_t>(n_tail) * per_tile;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int t = static_cast<int>(e / per_tile);
+  auto coords = [&](int64_t e, int& t, int& nn, int& r, int& m, int& n) {
+    t = static_cast<int>(e / per_tile);
     const int r2 = static_cast<int>(e - static_cast<int64_t>(t) * per_tile);
-    const int nn = r2 / (PG_BM / 2), r = 2 * (r2 - nn * (PG_BM / 2));
+    nn = r2 / (PG_BM / 2);
+    r = 2 * (r2 - nn * (PG_BM / 2));
     const int tile = p.tail_first + t;
     const int m_tile = tile / p.n_ntiles, n_tile = tile - m_tile * p.n_ntiles;
-    const int m = m_tile * PG_BM + r, n = n_tile * p.ntile + nn;
+    m = m_tile * PG_BM + r;
+    n = n_tile * p.ntile + nn;
+  };
+  griddep_wait();  // launched with PDL behind the GEMM: partials complete
+  // (no pre-wait RoPE loads here: measured slower at P >= 200, unlike the short-prompt reduce)
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int t, nn, r, m, n;
+    coords(e, t, nn, r, m, n);
     if (m >= p.M || n >= p.P) continue;
     const float* base = p.part + static_cast<int64_t>(t) * p.tail_ks * p.ntile * PG_BM;
     float va = 0.0f, vb = 0.0f;
@@ -455,7 +481,7 @@ __global__ void prefill_tail_reduce_kernel(const PrefillGemmParams p) {
       va += q[0];
       vb += q[1];
     }
-    pg_epilogue_pair(p, m, n, va, vb);
+    pg_epilogue_pair(p, m, n, va, vb, pg_rope_load(p, m, n));
   }
 }
 
