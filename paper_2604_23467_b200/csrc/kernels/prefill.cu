@@ -24,6 +24,7 @@ namespace grt {
 template <typename WT>
 __global__ void prefill_embed_kernel(const int* tokens, int start, int P, const WT* __restrict__ emb,
                                      const WT* __restrict__ pos, int d, float* __restrict__ X, int vocab, int* err) {
+  griddep_launch_dependents();  // PDL successors wait for this grid before reading X
   const int i = blockIdx.x;
   if (i >= P) return;
   const int tok = tokens[start + i];
@@ -53,6 +54,7 @@ __global__ void prefill_embed_kernel(const int* tokens, int start, int P, const 
 constexpr int PN_THREADS = 256, PN_MAXV = 16;  // d <= 16384
 __global__ void __launch_bounds__(PN_THREADS) prefill_rmsnorm_kernel(const float* X, const float* gamma, float eps, int d,
                                                                      __nv_bfloat16* Xn) {
+  griddep_launch_dependents();  // the next GEMM may start its weight stream
   __shared__ float red[32];
   const int i = blockIdx.x;
   const float4* x = reinterpret_cast<const float4*>(X + static_cast<int64_t>(i) * d);
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(PN_THREADS) prefill_rmsnorm_kernel(const float
 __global__ void __launch_bounds__(PN_THREADS) prefill_layernorm_kernel(const float* X, const float* gamma,
                                                                        const float* beta, float eps, int d,
                                                                        __nv_bfloat16* Xn) {
+  griddep_launch_dependents();
   __shared__ float red[32];
   const int i = blockIdx.x;
   const float4* x = reinterpret_cast<const float4*>(X + static_cast<int64_t>(i) * d);
@@ -163,6 +166,7 @@ template <typename KT, int DH>
 __global__ void __launch_bounds__(PA_THREADS)
     prefill_attn_kernel(const float* Q, const void* k_cache, const void* v_cache, int start, int P, int d,
                         int max_seq, float scale, __nv_bfloat16* out, KvPaging kvp) {
+  griddep_launch_dependents();
   extern __shared__ __align__(16) float sm[];
   constexpr int KS = DH + 1;   // odd row stride: conflict-free column reads of K
   constexpr int DPT = DH / 16; // output dims per thread
@@ -353,6 +357,7 @@ __global__ void __launch_bounds__(FA_WARPS * 32)
                       int d, int max_seq, float scale, __nv_bfloat16* out, KvPaging kvp) {
   constexpr int LD = DH + 8;  // bf16 row stride: 16-byte aligned, conflict-free ldmatrix
   constexpr int KS = DH / 16, NB = DH / 8;
+  griddep_launch_dependents();  // the Wo GEMM's CTAs may take the SMs this grid leaves free
   extern __shared__ __align__(16) uint8_t fa_smem[];
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(fa_smem);
   __nv_bfloat16* Kb = Qs + FA_QB * LD;      // [2][FA_KB][LD] double-buffered K tiles
@@ -627,6 +632,7 @@ __device__ __forceinline__ void ft_softmax(const uint32_t (&s)[128], int lim, fl
 __global__ void __launch_bounds__(FT_THREADS, 1)
     prefill_fa_tc_kernel(const float* Q, const __nv_bfloat16* k_cache, const __nv_bfloat16* v_cache, int start, int P,
                           int d, int max_seq, float scale, __nv_bfloat16* out, KvPaging kvp) {
+  griddep_launch_dependents();  // the Wo GEMM's CTAs may take the SMs this grid leaves free
   extern __shared__ __align__(1024) uint8_t ft_raw[];
   __shared__ uint64_t bar_s, bar_o;
   __shared__ uint32_t tmem_base;

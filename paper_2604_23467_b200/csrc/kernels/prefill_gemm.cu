@@ -323,6 +323,21 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      // The weight (A) boxes of the first S stages do not depend on the previous
+      // kernel: requested before the dependency wait (the small kernels ahead of
+      // a GEMM trigger their dependents at entry, so this CTA can be resident and
+      // streaming while they run); the token (B) boxes follow after the wait.
+      int npre = 0;
+      for (int w = blockIdx.x; w < n_items && npre < S; w += gridDim.x) {
+        int m_tile, n_tile, split, kb0, kb1;
+        decode(w, m_tile, n_tile, split, kb0, kb1);
+        for (int kb = kb0; kb < kb1 && npre < S; ++kb, ++npre) {
+          uint8_t* st = smem + static_cast<size_t>(npre) * stage_bytes;
+          mbar_arrive_expect_tx(&full[npre], stage_bytes);
+          for (int j = 0; j < p.kbox; ++j)
+            tma_load_2d(st + j * a_box, &map_w, kb * kstep + j * PG_BK, m_tile * PG_BM, &full[npre]);
+        }
+      }
       griddep_wait();
       int i = 0;  // global stage counter across items
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
@@ -330,12 +345,14 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
         decode(w, m_tile, n_tile, split, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int s = i % S;
-          mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
           uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
-          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          if (i >= npre) {
+            mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[s], stage_bytes);
+          }
           for (int j = 0; j < p.kbox; ++j) {
             const int k0 = kb * kstep + j * PG_BK;
-            tma_load_2d(st + j * a_box, &map_w, k0, m_tile * PG_BM, &full[s]);
+            if (i >= npre) tma_load_2d(st + j * a_box, &map_w, k0, m_tile * PG_BM, &full[s]);
             tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, k0, n_tile * p.ntile, &full[s]);
           }
         }
@@ -425,6 +442,7 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
 // (deterministic) and applies the epilogue, one thread per (row pair, token):
 // fully parallel, instead of one CTA per tile serialising a tail reduction.
 __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
+  griddep_launch_dependents();  // the next GEMM may start its weight stream (it waits for us before its tokens)
   const int n_pairs = (p.M + 1) >> 1;
   const int64_t total = static_cast<int64_t>(n_pairs) * p.P;
   const int64_t e0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -453,6 +471,7 @@ __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
 // partials each ([tile - tail_first][split][token][128 rows]), summed in split
 // order, then the GEMM's epilogue; one thread per (row pair, token).
 __global__ void prefill_tail_reduce_kernel(const PrefillGemmParams p) {
+  griddep_launch_dependents();
   const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
   const int n_tail = m_tiles * p.n_ntiles - p.tail_first;
   const int per_tile = (PG_BM / 2) * p.ntile;
@@ -500,6 +519,7 @@ constexpr int RN_NORM_THREADS = 256, RN_NORM_MAXV = 16;  // prefill_rmsnorm_kern
 template <int MAXV>
 __global__ void __launch_bounds__(RN_THREADS) prefill_resid_norm_kernel(const PrefillGemmParams p, const float* gamma,
                                                                         float eps, __nv_bfloat16* Xn) {
+  griddep_launch_dependents();  // the next GEMM may start its weight stream
   __shared__ float red[32];
   extern __shared__ float4 xrow[];  // the updated row, for the reduction below
   float4 g[MAXV];

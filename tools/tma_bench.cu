@@ -84,6 +84,48 @@ __global__ void __launch_bounds__(64) stream(const __grid_constant__ CUtensorMap
   }
 }
 
+
+// the decode GEMV's pattern: 8 warps, each with a private ring of `depth`
+// slots of 2 rows x `ch` elements, filled by cp.async.bulk (1D, contiguous)
+__global__ void __launch_bounds__(256) bulk_stream(const __nv_bfloat16* __restrict__ w, int R, int K, int ch, int depth) {
+  extern __shared__ __align__(128) uint8_t raw[];
+  __shared__ uint64_t bars[8][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = K / ch;
+  const uint32_t rowb = ch * 2, stageb = 2 * rowb;
+  uint8_t* mine = raw + warp * depth * stageb;
+  const int n_pairs = R / 2;
+  const int pb = static_cast<int>(static_cast<int64_t>(blockIdx.x) * n_pairs / gridDim.x);
+  const int pe = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * n_pairs / gridDim.x);
+  const int tc = (pe - pb) * nch;
+  const int nt = tc > warp ? (tc - warp + 7) / 8 : 0;
+  if (lane == 0) {
+    for (int s = 0; s < depth; ++s) mbar_init(&bars[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncwarp();
+  auto issue = [&](int i) {
+    const int t = warp + i * 8, pl = t / nch, c = t - pl * nch;
+    const int slot = i % depth;
+    uint64_t* bar = &bars[warp][slot];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(stageb));
+    const __nv_bfloat16* src = w + static_cast<int64_t>(2 * (pb + pl)) * K + c * ch;
+    for (int r = 0; r < 2; ++r)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(mine + slot * stageb + r * rowb)),
+                   "l"(src + r * K), "r"(rowb), "r"(smem_u32(bar))
+                   : "memory");
+  };
+  if (lane == 0)
+    for (int i = 0; i < nt && i < depth; ++i) issue(i);
+  for (int i = 0; i < nt; ++i) {
+    while (!mbar_try(&bars[warp][i % depth], (i / depth) & 1)) {
+    }
+    __syncwarp();
+    if (lane == 0 && i + depth < nt) issue(i + depth);
+  }
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -137,6 +179,37 @@ int main() {
         }
         printf("R=%5d K=%5d stages=%2d boxes=%d ring=%3zu KB ctas/SM=%d ks=%2d items=%4d : %7.2f us %7.1f GB/s\n", R, K, S,
                KB, smem / 1024, cps, ks, items, tot / 5 * 1e3, bytes / (tot / 5 * 1e-3) / 1e9);
+      }
+    }
+    cudaFree(w);
+  }
+  // decode-GEMV-style bulk rings on the same shapes
+  cudaFuncSetAttribute(bulk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const int bshapes[][2] = {{12288, 4096}, {4096, 11008}, {22016, 4096}};
+  for (auto& sh : bshapes) {
+    const int R = sh[0], K = sh[1];
+    void* w = nullptr;
+    const size_t bytes = static_cast<size_t>(R) * K * 2;
+    cudaMalloc(&w, bytes);
+    cudaMemset(w, 0x3c, bytes);
+    for (int ch : {2048, 1376, 1024, 512}) {
+      if (K % ch) continue;
+      for (int depth : {3, 2}) {
+        const size_t smem = static_cast<size_t>(8) * depth * 2 * ch * 2;
+        if (smem > 200 * 1024) continue;
+        float tot = 0;
+        for (int r = 0; r < 6; ++r) {
+          cudaMemsetAsync(flush, r, 256u << 20);
+          cudaEventRecord(e0);
+          bulk_stream<<<sms, 256, smem>>>(static_cast<const __nv_bfloat16*>(w), R, K, ch, depth);
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (r > 0) tot += ms;
+        }
+        printf("bulk R=%5d K=%5d chunk=%5d B depth=%d : %7.2f us %7.1f GB/s\n", R, K, ch * 2, depth, tot / 5 * 1e3,
+               bytes / (tot / 5 * 1e-3) / 1e9);
       }
     }
     cudaFree(w);
