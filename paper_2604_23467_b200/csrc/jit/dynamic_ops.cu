@@ -38,6 +38,10 @@ typedef unsigned int u32;
 #ifndef INFINITY
 #define INFINITY __int_as_float(0x7f800000)
 #endif
+// phase stamps for the sampler timing probe (tools/sampler_timing.cu); no-op here
+#ifndef GRT_STAMP
+#define GRT_STAMP(i)
+#endif
 
 __device__ __forceinline__ void grt_griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grt_launch_dependents() {
@@ -163,13 +167,15 @@ __device__ __forceinline__ float grt_expf(float z) {
   const float r2 = r * r;
   float y = fmaf(p, r2, r);
   y = y + 1.0f;
-  return ldexpf(y, (int)n);
+  // y * 2^n with n in [-44, 0] and y in [0.7, 1.5): always a normal float, so
+  // adding n to the exponent field is ldexpf's result exactly
+  return __int_as_float(__float_as_int(y) + ((int)n << 23));
 }
 
 __device__ __forceinline__ u64 topkp_weight_v(float logit, float m, float t) {
   const float z = (logit - m) / t;
   const float e = grt_expf(z);
-  return (u64)(e * 2147483648.0f);
+  return (u64)(u32)(e * 2147483648.0f);  // e <= 1: the product fits 32 bits (same truncation)
 }
 __device__ __forceinline__ u64 topkp_weight(const float* logits, int i, float m, float t) {
   const float z = (logits[i] - m) / t;
@@ -377,17 +383,31 @@ __device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kf
       }
     };
     if (n < 0) {  // pass 0 (sh = 37 >= 16): the digit is w's top bits, 32-bit arithmetic
+      // digit 0 (weights below 2^21: most of the vocabulary) is summed per thread
+      // and added once per warp -- 32000 atomics on one shared word serialise
+      u32 z_lo = 0, z_hi = 0;
       for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
         const u32 w = wsm[i];
         if (kfloor == 0 || rs_ge(w, i, kfloor)) {
           const int b = (int)((w >> (sh - 16)) & (RS_B - 1));
-          if (!by_weight) {
+          if (b == 0) {
+            z_lo += by_weight ? (w & 0xFFFFu) : 1u;
+            z_hi += by_weight ? (w >> 16) : 0u;
+          } else if (!by_weight) {
             atomicAdd(&hist[b], 1u);
           } else {
             atomicAdd(&hist[b], w & 0xFFFFu);
             if (w >> 16) atomicAdd(&hist[RS_B + b], w >> 16);
           }
         }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        z_lo += __shfl_xor_sync(0xffffffffu, z_lo, o);
+        z_hi += __shfl_xor_sync(0xffffffffu, z_hi, o);
+      }
+      if ((tid & 31) == 0) {
+        if (z_lo) atomicAdd(&hist[0], z_lo);
+        if (z_hi) atomicAdd(&hist[RS_B], z_hi);
       }
     } else {
       for (int j = tid; j < n; j += GRT_SAMPLE_THREADS) {
@@ -438,7 +458,10 @@ __device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kf
     if (tid == 0) s_n = n;
     __syncthreads();
     n = s_n;
-    if (n <= 0) break;  // cannot happen (need <= total at every pass); the prefix stands
+    // one candidate left: it is the threshold key (the running total reaches
+    // `need` inside its bucket); the remaining passes would only re-derive its
+    // low digits.  n <= 0 cannot happen (need <= total at every pass).
+    if (n <= 1) break;
   }
   const u64 r = n == 1 ? rs_key(wsm, cand[0]) : prefix;
   __syncthreads();
@@ -578,6 +601,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
 #if GRT_TOPKP_SMEM
     // the logits are read ONCE (all loads of a thread in flight together), the
     // weights computed from registers into dynamic shared memory
+    GRT_STAMP(0);
     constexpr int NV4 = GRT_V / 4;
     constexpr int PER = NV4 > 0 ? (NV4 + GRT_SAMPLE_THREADS - 1) / GRT_SAMPLE_THREADS : 1;
     float4 lv[PER];
@@ -592,6 +616,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
     for (int i = 4 * NV4 + tid; i < GRT_V; i += GRT_SAMPLE_THREADS) m = fmaxf(m, logits[i]);
     m = block_max_f(m, redf);
     extern __shared__ u32 wsm[];  // [GRT_V] weights, computed once (every pass below reads them)
+    GRT_STAMP(1);
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int j4 = tid + k * GRT_SAMPLE_THREADS;
@@ -603,6 +628,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
     }
     for (int i = 4 * NV4 + tid; i < GRT_V; i += GRT_SAMPLE_THREADS) wsm[i] = (u32)topkp_weight(logits, i, m, temperature);
     __syncthreads();
+    GRT_STAMP(2);
 #define GRT_W(i) ((u64)wsm[i])
 #define GRT_GE(w, i, floor) rs_ge((u32)(w), (i), (floor))
 #else
@@ -620,6 +646,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
     // (1) top-k threshold key: the top_k-th largest key
     u64 kth = 0;
     if (top_k > 0 && top_k < GRT_V) kth = radix_select_compact(wsm, cand, 0, false, (u64)top_k, rs_hist);
+    GRT_STAMP(3);
     // (2) top-p threshold key among keys >= kth
     u64 W = 0;
     for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
@@ -628,12 +655,14 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
     }
     W = block_sum_u64(W, redu);
     u64 kappa = kth;
+    GRT_STAMP(4);
     if (top_p > 0.0f && top_p < 1.0f) {
       u64 thresh = (u64)((double)top_p * (double)W);
       if (thresh < 1) thresh = 1;
       const u64 kp = radix_select_compact(wsm, cand, kth, true, thresh, rs_hist);
       kappa = kp > kth ? kp : kth;
     }
+    GRT_STAMP(5);
 #else
     // (1) top-k threshold key
     u64 kth = 0;
@@ -734,25 +763,41 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
       if (r >= S) r = S - 1;
       u64 acc = wtot[wp];
       if (S > 0 && acc <= r && r < acc + t) {  // this warp's block holds the draw
-        for (int base = i0; base < i1; base += 32) {
-          const int i = base + lane;
-          u64 w = 0;
+        // lane c sums chunk c = indices [i0 + 32c, i0 + 32c + 32) (rotated reads:
+        // no bank conflicts), a scan over the 32 chunk sums finds the chunk, a
+        // scan inside it the index -- the serial walk's token exactly
+        static_assert(VB <= 32 * 32, "one chunk per lane");
+        const int cb = i0 + 32 * lane;
+        u64 cs = 0;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+          const int i = cb + ((k + lane) & 31);
           if (i < i1) {
-            w = GRT_W(i);
-            if (!GRT_GE(w, i, kappa)) w = 0;
+            const u64 w = GRT_W(i);
+            if (GRT_GE(w, i, kappa)) cs += w;
           }
-          u64 incl = w;
-          for (int o = 1; o < 32; o <<= 1) {
-            const u64 n2 = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += n2;
-          }
-          const unsigned hit = __ballot_sync(0xffffffffu, w > 0 && acc + incl > r);
-          if (hit) {
-            if (lane == 0) s_tok = base + __ffs(hit) - 1;
-            break;
-          }
-          acc += __shfl_sync(0xffffffffu, incl, 31);
         }
+        u64 cincl = cs;
+        for (int o = 1; o < 32; o <<= 1) {
+          const u64 n2 = __shfl_up_sync(0xffffffffu, cincl, o);
+          if (lane >= o) cincl += n2;
+        }
+        const unsigned hc = __ballot_sync(0xffffffffu, acc + cincl > r);
+        const int ch = __ffs(hc) - 1;  // r < acc + t: some chunk reaches it
+        acc += __shfl_sync(0xffffffffu, cincl - cs, ch);
+        const int base = i0 + 32 * ch, i = base + lane;
+        u64 w = 0;
+        if (i < i1) {
+          w = GRT_W(i);
+          if (!GRT_GE(w, i, kappa)) w = 0;
+        }
+        u64 incl = w;
+        for (int o = 1; o < 32; o <<= 1) {
+          const u64 n2 = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += n2;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, w > 0 && acc + incl > r);
+        if (lane == 0 && hit) s_tok = base + __ffs(hit) - 1;
       }
       __syncthreads();
     }
@@ -817,6 +862,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
 #endif
   }
 
+  GRT_STAMP(6);
   if (tid == 0) {
     const int tok = s_tok;
     ctrl->tokens[pos] = tok;
