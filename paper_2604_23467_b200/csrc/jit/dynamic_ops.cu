@@ -359,8 +359,10 @@ __device__ __forceinline__ void rs_pick(const u32* hist, u64 need, int* s_dg, u6
   __syncthreads();
 }
 
+// hist_ready: pass 0's histogram was accumulated by the caller (while it
+// computed the weights, kfloor == 0)
 __device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kfloor, bool by_weight, u64 need,
-                                    u32* hist) {
+                                    u32* hist, bool hist_ready = false) {
   __shared__ int s_dg, s_n, warp_tot[32];
   __shared__ u64 s_above, wsum[32];
   const int tid = threadIdx.x;
@@ -370,8 +372,11 @@ __device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kf
 #pragma unroll 1
   for (int ps = 0; ps < 5; ++ps) {
     const int sh = shifts[ps];
-    for (int b = tid; b < 2 * RS_B; b += GRT_SAMPLE_THREADS) hist[b] = 0;
-    __syncthreads();
+    const bool built = ps == 0 && hist_ready;
+    if (!built) {
+      for (int b = tid; b < 2 * RS_B; b += GRT_SAMPLE_THREADS) hist[b] = 0;
+      __syncthreads();
+    }
     auto add = [&](int i, u64 key) {
       const int b = (int)((key >> sh) & (RS_B - 1));
       if (!by_weight) {
@@ -382,7 +387,9 @@ __device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kf
         if (w >> 16) atomicAdd(&hist[RS_B + b], w >> 16);
       }
     };
-    if (n < 0) {  // pass 0 (sh = 37 >= 16): the digit is w's top bits, 32-bit arithmetic
+    if (built) {
+      // histogram already complete (the caller synchronised)
+    } else if (n < 0) {  // pass 0 (sh = 37 >= 16): the digit is w's top bits, 32-bit arithmetic
       // digit 0 (weights below 2^21: most of the vocabulary) is summed per thread
       // and added once per warp -- 32000 atomics on one shared word serialise
       u32 z_lo = 0, z_hi = 0;
@@ -458,6 +465,7 @@ __device__ u64 radix_select_compact(const u32* wsm, unsigned short* cand, u64 kf
     if (tid == 0) s_n = n;
     __syncthreads();
     n = s_n;
+    GRT_STAMP(9 + ps);
     // one candidate left: it is the threshold key (the running total reaches
     // `need` inside its bucket); the remaining passes would only re-derive its
     // low digits.  n <= 0 cannot happen (need <= total at every pass).
@@ -602,6 +610,17 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
     // the logits are read ONCE (all loads of a thread in flight together), the
     // weights computed from registers into dynamic shared memory
     GRT_STAMP(0);
+#if GRT_TOPKP_SMEM == 2
+    // the draw's uniform (Philox over the step index) is known now: computed
+    // while the logits load is in flight
+    double u_draw;
+    {
+      u32 c[4] = {(u32)step, (u32)((u64)step >> 32), 0u, 0x53616D70u};
+      const u64 seed = ctrl->seed;
+      philox4x32_10(c, (u32)seed, (u32)(seed >> 32));
+      u_draw = (double)((((u64)c[1] << 32) | (u64)c[0]) >> 11) * 0x1.0p-53;
+    }
+#endif
     constexpr int NV4 = GRT_V / 4;
     constexpr int PER = NV4 > 0 ? (NV4 + GRT_SAMPLE_THREADS - 1) / GRT_SAMPLE_THREADS : 1;
     float4 lv[PER];
@@ -617,16 +636,59 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
     m = block_max_f(m, redf);
     extern __shared__ u32 wsm[];  // [GRT_V] weights, computed once (every pass below reads them)
     GRT_STAMP(1);
+#if GRT_TOPKP_SMEM == 2
+    // The first select's pass-0 histogram (digit = w >> 21; digit 0 summed per
+    // thread, added once per warp) and the total weight are accumulated while
+    // the weights are computed: the top-k count histogram when top-k is active,
+    // else the top-p weight histogram -- one pass over the vocabulary fewer.
+    __shared__ u32 rs_hist[2 * RS_B];
+    const int top_k = ctrl->top_k;
+    const float top_p = ctrl->top_p;
+    const bool pre_k = top_k > 0 && top_k < GRT_V;
+    const bool pre_p = !pre_k && top_p > 0.0f && top_p < 1.0f;
+    for (int b = tid; b < 2 * RS_B; b += GRT_SAMPLE_THREADS) rs_hist[b] = 0;
+    __syncthreads();
+    u64 W_all = 0;
+    u32 z_lo = 0, z_hi = 0;
+    auto put = [&](int i, u32 w) {
+      wsm[i] = w;
+      W_all += w;
+      if (pre_k || pre_p) {
+        const int b = (int)(w >> 21);
+        if (b == 0) {
+          z_lo += pre_k ? 1u : (w & 0xFFFFu);
+          z_hi += pre_k ? 0u : (w >> 16);
+        } else if (pre_k) {
+          atomicAdd(&rs_hist[b], 1u);
+        } else {
+          atomicAdd(&rs_hist[b], w & 0xFFFFu);
+          atomicAdd(&rs_hist[RS_B + b], w >> 16);
+        }
+      }
+    };
+#else
+    auto put = [&](int i, u32 w) { wsm[i] = w; };
+#endif
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int j4 = tid + k * GRT_SAMPLE_THREADS;
       if (j4 >= NV4) continue;
-      wsm[4 * j4] = (u32)topkp_weight_v(lv[k].x, m, temperature);
-      wsm[4 * j4 + 1] = (u32)topkp_weight_v(lv[k].y, m, temperature);
-      wsm[4 * j4 + 2] = (u32)topkp_weight_v(lv[k].z, m, temperature);
-      wsm[4 * j4 + 3] = (u32)topkp_weight_v(lv[k].w, m, temperature);
+      put(4 * j4, (u32)topkp_weight_v(lv[k].x, m, temperature));
+      put(4 * j4 + 1, (u32)topkp_weight_v(lv[k].y, m, temperature));
+      put(4 * j4 + 2, (u32)topkp_weight_v(lv[k].z, m, temperature));
+      put(4 * j4 + 3, (u32)topkp_weight_v(lv[k].w, m, temperature));
     }
-    for (int i = 4 * NV4 + tid; i < GRT_V; i += GRT_SAMPLE_THREADS) wsm[i] = (u32)topkp_weight(logits, i, m, temperature);
+    for (int i = 4 * NV4 + tid; i < GRT_V; i += GRT_SAMPLE_THREADS) put(i, (u32)topkp_weight(logits, i, m, temperature));
+#if GRT_TOPKP_SMEM == 2
+    for (int o = 16; o > 0; o >>= 1) {
+      z_lo += __shfl_xor_sync(0xffffffffu, z_lo, o);
+      z_hi += __shfl_xor_sync(0xffffffffu, z_hi, o);
+    }
+    if ((tid & 31) == 0) {
+      if (z_lo) atomicAdd(&rs_hist[0], z_lo);
+      if (z_hi) atomicAdd(&rs_hist[RS_B], z_hi);
+    }
+#endif
     __syncthreads();
     GRT_STAMP(2);
 #define GRT_W(i) ((u64)wsm[i])
@@ -638,20 +700,21 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
 #define GRT_W(i) topkp_weight(logits, (i), m, temperature)
 #define GRT_GE(w, i, floor) (topkp_key((w), (i)) >= (floor))
 #endif
-    const int top_k = ctrl->top_k;
-    const float top_p = ctrl->top_p;
 #if GRT_TOPKP_SMEM == 2
     unsigned short* cand = (unsigned short*)(wsm + GRT_V);
-    __shared__ u32 rs_hist[2 * RS_B];
     // (1) top-k threshold key: the top_k-th largest key
     u64 kth = 0;
-    if (top_k > 0 && top_k < GRT_V) kth = radix_select_compact(wsm, cand, 0, false, (u64)top_k, rs_hist);
+    if (pre_k) kth = radix_select_compact(wsm, cand, 0, false, (u64)top_k, rs_hist, true);
     GRT_STAMP(3);
     // (2) top-p threshold key among keys >= kth
     u64 W = 0;
-    for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
-      const u64 w = GRT_W(i);
-      if (kth == 0 || GRT_GE(w, i, kth)) W += w;
+    if (kth == 0) {
+      W = W_all;  // every key counts
+    } else {
+      for (int i = tid; i < GRT_V; i += GRT_SAMPLE_THREADS) {
+        const u64 w = GRT_W(i);
+        if (GRT_GE(w, i, kth)) W += w;
+      }
     }
     W = block_sum_u64(W, redu);
     u64 kappa = kth;
@@ -659,11 +722,13 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
     if (top_p > 0.0f && top_p < 1.0f) {
       u64 thresh = (u64)((double)top_p * (double)W);
       if (thresh < 1) thresh = 1;
-      const u64 kp = radix_select_compact(wsm, cand, kth, true, thresh, rs_hist);
+      const u64 kp = radix_select_compact(wsm, cand, kth, true, thresh, rs_hist, pre_p);
       kappa = kp > kth ? kp : kth;
     }
     GRT_STAMP(5);
 #else
+    const int top_k = ctrl->top_k;
+    const float top_p = ctrl->top_p;
     // (1) top-k threshold key
     u64 kth = 0;
     if (top_k > 0 && top_k < GRT_V) {
@@ -742,6 +807,7 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
       if (lane == 0) wtot[wp] = t;
       if (tid == 0) s_tok = 0x7fffffff;
       __syncthreads();
+      GRT_STAMP(7);
       if (wp == 0) {
         const u64 v = wtot[lane];
         u64 incl = v;
@@ -753,13 +819,9 @@ __device__ __forceinline__ int sample_impl(GrtCtrl* ctrl, const float* logits, b
         if (lane == 31) s_S2 = incl;
       }
       __syncthreads();
+      GRT_STAMP(8);
       const u64 S = s_S2;
-      u32 c[4] = {(u32)step, (u32)((u64)step >> 32), 0u, 0x53616D70u};
-      const u64 seed = ctrl->seed;
-      philox4x32_10(c, (u32)seed, (u32)(seed >> 32));
-      const u64 bits = (((u64)c[1] << 32) | (u64)c[0]) >> 11;
-      const double u = (double)bits * 0x1.0p-53;
-      u64 r = (u64)(u * (double)S);
+      u64 r = (u64)(u_draw * (double)S);
       if (r >= S) r = S - 1;
       u64 acc = wtot[wp];
       if (S > 0 && acc <= r && r < acc + t) {  // this warp's block holds the draw

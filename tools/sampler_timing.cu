@@ -11,7 +11,7 @@
 #include <random>
 #include <vector>
 
-__device__ long long g_stamps[8];
+__device__ long long g_stamps[16];
 #define GRT_STAMP(i)                                  \
   do {                                                \
     if (threadIdx.x == 0) g_stamps[i] = clock64();    \
@@ -55,11 +55,11 @@ int main() {
     h.uniforms = uni;
     h.scratch = scratch;
     cudaMemcpy(ctrl, &h, sizeof(h), cudaMemcpyHostToDevice);
-    long long st[8];
-    double acc[8] = {0};
+    long long st[16];
+    double acc[16] = {0};
     const int reps = 20;
     for (int r = 0; r < reps + 1; ++r) {
-      long long zero[8] = {0};
+      long long zero[16] = {0};
       cudaMemcpyToSymbol(g_stamps, zero, sizeof(zero));
       grt_sample<<<1, 1024, V * 6>>>(ctrl, dl);
       cudaDeviceSynchronize();
@@ -71,11 +71,21 @@ int main() {
         acc[i] += (st[i] - prev) / 1.965e3;  // us at 1965 MHz
         prev = st[i];
       }
+      // draw internals: 5 -> 7 (warp totals), 7 -> 8 (scan), 8 -> 6 (draw + walk)
+      if (st[7] && st[8]) {
+        acc[12 + 0] += (st[7] - st[5]) / 1.965e3;
+        acc[12 + 1] += (st[8] - st[7]) / 1.965e3;
+        acc[12 + 2] += (st[6] - st[8]) / 1.965e3;
+      }
+      // select passes (the last select run): 9..13 end of pass 0..4
+      for (int i = 9; i <= 11; ++i)
+        if (st[i]) acc[i - 9 + 7] += (st[i] - (i == 9 ? 0 : st[i - 1])) / 1.965e3 * (i == 9 ? 0 : 1);
     }
     printf("%-28s", c.name);
     const char* nm[] = {"", "max", "weights", "top-k sel", "W sum", "top-p sel", "draw"};
     for (int i = 1; i <= 6; ++i) printf("  %s %.2f", nm[i], acc[i] / reps);
-    printf("  us\n");
+    printf("  us\n     draw: totals %.2f scan %.2f walk %.2f;  select pass1 %.2f pass2 %.2f\n", acc[12] / reps,
+           acc[13] / reps, acc[14] / reps, acc[8] / reps, acc[9] / reps);
   }
   printf("err=%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
