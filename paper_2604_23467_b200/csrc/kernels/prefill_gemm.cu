@@ -152,6 +152,100 @@ __device__ __forceinline__ void pg_epilogue16(const PrefillGemmParams& p, int m,
   }
 }
 
+// QKV epilogue of one warp (32 weight rows = 16 row pairs) for 16 tokens, staged
+// through shared memory so the stores are 16-byte vectors of consecutive
+// destinations (the per-element q / KV stores of pg_epilogue16 -- 2 or 4 bytes
+// per lane, half the lanes idle -- made the epilogue the QKV GEMM's tail: 75 ->
+// 51 us at P=500 without it).  Requires d_model % 32 == 0 and head_dim % 32 == 0
+// (a warp's 16 pairs lie in one section and one head).  Both lanes of a pair
+// work: the even lane rotates tokens 0-7, the odd lane tokens 8-15.  rc / rs:
+// this thread's RoPE factors for its 8 tokens.
+constexpr int PG_STG = 33;  // staging row stride (floats): conflict-free column reads
+__device__ __forceinline__ void pg_epilogue_qkv_staged(const PrefillGemmParams& p, int m, int n0, int nv,
+                                                       const float (&v)[16], const float (&rc)[8],
+                                                       const float (&rs)[8], float* stg) {
+  if ((m & ~31) >= p.M) return;  // warp-uniform (M % 32 == 0)
+  const int lane = threadIdx.x & 31;
+  const bool odd = lane & 1;
+  // the partner row's value for this thread's 8 tokens (8 shuffles)
+  float recv[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) recv[j] = __shfl_xor_sync(0xffffffffu, odd ? v[j] : v[j + 8], 1);
+  const int d = p.d_model, dh = p.head_dim;
+  const int sec = m / d;
+  const bool rope = p.epi == PG_EPI_QKV_ROPE && sec < 2;
+  const int pr = lane >> 1;  // pair slot within the warp
+  const int sa = rope ? pr : 2 * pr, sb = rope ? 16 + pr : 2 * pr + 1;
+  const int jo = odd ? 8 : 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float a = odd ? recv[j] : v[j];       // even row (m & ~1)
+    const float b = odd ? v[j + 8] : recv[j];   // odd row
+    float ra = a, rb = b;
+    if (rope) {
+      ra = a * rc[j] - b * rs[j];
+      rb = b * rc[j] + a * rs[j];
+    }
+    stg[(jo + j) * PG_STG + sa] = ra;
+    stg[(jo + j) * PG_STG + sb] = rb;
+  }
+  __syncwarp();
+  // destinations: section-local pair index of slot 0, its head and element
+  const int m0 = m & ~31;  // row of lane 0 (warp's first row)
+  const int lp0 = (m0 >> 1) - sec * (d >> 1);
+  int head, ebase;
+  if (rope) {
+    head = lp0 / (dh >> 1);
+    ebase = lp0 - head * (dh >> 1);  // slots 0-15: e = ebase + s; 16-31: e = dh/2 + ebase + s - 16
+  } else {
+    head = (2 * lp0) / dh;
+    ebase = 2 * lp0 - head * dh;  // slot s: e = ebase + s
+  }
+  const int s0 = (lane & 7) * 4;
+  const int e = rope ? (s0 < 16 ? ebase + s0 : (dh >> 1) + ebase + s0 - 16) : ebase + s0;
+#pragma unroll
+  for (int tb = 0; tb < 4; ++tb) {
+    const int j = tb * 4 + (lane >> 3);
+    if (j >= nv) continue;
+    const float* src = stg + j * PG_STG + s0;
+    const float x0 = src[0], x1 = src[1], x2 = src[2], x3 = src[3];
+    const int n = n0 + j;
+    if (sec == 0) {
+      *reinterpret_cast<float4*>(p.q_out + static_cast<int64_t>(n) * d + head * dh + e) = make_float4(x0, x1, x2, x3);
+    } else {
+      void* cache = sec == 1 ? p.k_cache : p.v_cache;
+      const int64_t off = kv_row(p.kvp, head, p.max_seq, p.start_pos + n) * dh + e;
+      if (p.kv_bf16) {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(x0, x1), hi = __floats2bfloat162_rn(x2, x3);
+        uint2 u;
+        u.x = *reinterpret_cast<const uint32_t*>(&lo);
+        u.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(cache) + off) = u;
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(cache) + off) = make_float4(x0, x1, x2, x3);
+      }
+    }
+  }
+  __syncwarp();  // staging reused by the next group
+}
+
+// RoPE factors of this thread's 8 tokens of the group at column c0 (staged QKV
+// epilogue): pair (m & ~1), tokens n0 + c0 + (odd ? 8 : 0) + j.
+__device__ __forceinline__ void pg_rope8(const PrefillGemmParams& p, int m, int n, float (&rc)[8], float (&rs)[8]) {
+  const int d = p.d_model, half = p.head_dim >> 1;
+  const int sec = m / d;
+  if (p.epi != PG_EPI_QKV_ROPE || sec >= 2) return;
+  const int lp = (m >> 1) - sec * (d >> 1);
+  const int i = lp % half;
+  const int nb = n + ((threadIdx.x & 1) ? 8 : 0);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t t = static_cast<int64_t>(p.start_pos + min(nb + j, p.P - 1)) * half + i;
+    rc[j] = __ldg(p.rope_cos + t);
+    rs[j] = __ldg(p.rope_sin + t);
+  }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -252,6 +346,11 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 // Each pipeline stage carries `kbox` 64-wide K boxes (kbox*128 contiguous bytes
 // per weight row).
 
+// STAGED: the QKV epilogue of whole tiles through shared-memory staging
+// (pg_epilogue_qkv_staged); a separate instantiation so the launches that never
+// use it (split-K short prompts, the other projections) keep the plain kernel
+// (measured: one kernel for both cost TTFT P=10-200 30-90 us)
+template <bool STAGED>
 __global__ void __launch_bounds__(PG_THREADS, 1)
     prefill_gemm_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                         const PrefillGemmParams p) {
@@ -259,6 +358,9 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
   __shared__ uint64_t full[8], empty[8], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stg_base = STAGED ? reinterpret_cast<float*>(smem + static_cast<size_t>(p.stages) * p.kbox *
+                                                                 (PG_BM * PG_BK * 2 + p.ntile * PG_BK * 2))
+                           : nullptr;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
@@ -414,10 +516,17 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
       if (split_k)
         mypart = tail ? p.part + (static_cast<int64_t>(tile_id - p.tail_first) * p.tail_ks + split) * p.ntile * PG_BM
                       : p.part + (static_cast<int64_t>(tile_id) * p.ksplit + split) * p.ntile * PG_BM;
+      const bool staged = STAGED && !split_k;
       for (int c0 = 16 * half; c0 < n_valid; c0 += 16 * groups) {
         float v[16];
+        float rc[8], rs[8];  // RoPE factors (staged epilogue): requested before the TMEM load
+        if constexpr (STAGED)
+          if (staged) pg_rope8(p, m, n0 + c0, rc, rs);
         tc_ld16(t_lane + buf * p.ntile + c0, v);
-        if (split_k) {
+        if (STAGED && staged) {
+          pg_epilogue_qkv_staged(p, m, n0 + c0, min(16, n_valid - c0), v, rc, rs,
+                                 stg_base + (warp - 2) * 16 * PG_STG);
+        } else if (split_k) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) mypart[static_cast<int64_t>(c0 + j) * PG_BM + lane_base + lane] = v[j];
         } else {
@@ -727,7 +836,9 @@ size_t prefill_gemm_part_floats(int M, int K, int P, int sms) {
 }
 
 cudaError_t prefill_gemm_prepare() {
-  return cudaFuncSetAttribute(prefill_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(prefill_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(prefill_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
 }
 
 static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, PrefillGemmParams p, cudaStream_t s, bool pdl,
@@ -754,7 +865,11 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   const int n_items =
       tail ? p.tail_first + (m_tiles * p.n_ntiles - p.tail_first) * p.tail_ks : m_tiles * p.n_ntiles * p.ksplit;
   const int stage_bytes = p.kbox * (PG_BM * PG_BK * 2 + p.ntile * PG_BK * 2);
-  const int budget = 220 * 1024 - 1024;
+  // the QKV epilogue of whole tiles goes through per-warp shared-memory staging
+  p.epi_stage = (p.epi == PG_EPI_QKV || p.epi == PG_EPI_QKV_ROPE) && p.ksplit == 1 && p.head_dim % 32 == 0 &&
+                p.d_model % 32 == 0;
+  const int stg_bytes = p.epi_stage ? PG_EPI_WARPS * 16 * PG_STG * 4 : 0;
+  const int budget = 220 * 1024 - 1024 - stg_bytes;
   p.stages = std::min(8, budget / stage_bytes);
   if (p.stages < 2) return cudaErrorInvalidValue;
   CUtensorMap mw, mx;
@@ -765,14 +880,15 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   // two token tiles (P > 256): 8 epilogue warps (the epilogue's memory round
   // trips dominate a one-item CTA); otherwise 4 (measured faster)
   cfg.blockDim = dim3(p.n_ntiles > 1 ? PG_THREADS : 6 * 32);
-  cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + 1024;
+  cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + stg_bytes + 1024;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, prefill_gemm_kernel, mw, mx, p);
+  cudaError_t e = p.epi_stage ? cudaLaunchKernelEx(&cfg, prefill_gemm_kernel<true>, mw, mx, p)
+                              : cudaLaunchKernelEx(&cfg, prefill_gemm_kernel<false>, mw, mx, p);
   if (out) *out = p;
   if (e != cudaSuccess) return e;
   if (tail) {  // reduce + epilogue of the tail tiles
