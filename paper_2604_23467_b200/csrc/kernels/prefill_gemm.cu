@@ -229,6 +229,43 @@ __device__ __forceinline__ void pg_epilogue_qkv_staged(const PrefillGemmParams& 
   __syncwarp();  // staging reused by the next group
 }
 
+// SwiGLU epilogue of one warp (16 gate/up row pairs) for 16 tokens, staged like
+// the QKV one: h = silu(gate) * up (same expression as pg_epilogue16) for 8
+// tokens per lane, then 8-byte stores of 4 consecutive bf16 outputs (16 per
+// token and warp).  Requires M % 32 == 0.
+__device__ __forceinline__ void pg_epilogue_swiglu_staged(const PrefillGemmParams& p, int m, int n0, int nv,
+                                                          const float (&v)[16], float* stg) {
+  if ((m & ~31) >= p.M) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const bool odd = lane & 1;
+  float recv[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) recv[j] = __shfl_xor_sync(0xffffffffu, odd ? v[j] : v[j + 8], 1);
+  const int pr = lane >> 1, jo = odd ? 8 : 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float a = odd ? recv[j] : v[j];      // gate (even row)
+    const float b = odd ? v[j + 8] : recv[j];  // up (odd row)
+    const float sg = a / (1.0f + expf(-a));
+    stg[(jo + j) * PG_STG + pr] = sg * b;
+  }
+  __syncwarp();
+  const int half_m = p.M >> 1;
+  const int col = ((m & ~31) >> 1) + (lane & 3) * 4;
+#pragma unroll
+  for (int tb = 0; tb < 2; ++tb) {
+    const int j = tb * 8 + (lane >> 2);
+    if (j >= nv) continue;
+    const float* src = stg + j * PG_STG + (lane & 3) * 4;
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(src[0], src[1]), hi = __floats2bfloat162_rn(src[2], src[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&lo);
+    u.y = *reinterpret_cast<const uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.out_bf16) + static_cast<int64_t>(n0 + j) * half_m + col) = u;
+  }
+  __syncwarp();
+}
+
 // RoPE factors of this thread's 8 tokens of the group at column c0 (staged QKV
 // epilogue): pair (m & ~1), tokens n0 + c0 + (odd ? 8 : 0) + j.
 __device__ __forceinline__ void pg_rope8(const PrefillGemmParams& p, int m, int n, float (&rc)[8], float (&rs)[8]) {
@@ -521,11 +558,14 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
         float v[16];
         float rc[8], rs[8];  // RoPE factors (staged epilogue): requested before the TMEM load
         if constexpr (STAGED)
-          if (staged) pg_rope8(p, m, n0 + c0, rc, rs);
+          if (staged && p.epi != PG_EPI_SWIGLU) pg_rope8(p, m, n0 + c0, rc, rs);
         tc_ld16(t_lane + buf * p.ntile + c0, v);
         if (STAGED && staged) {
-          pg_epilogue_qkv_staged(p, m, n0 + c0, min(16, n_valid - c0), v, rc, rs,
-                                 stg_base + (warp - 2) * 16 * PG_STG);
+          float* stg = stg_base + (warp - 2) * 16 * PG_STG;
+          if (p.epi == PG_EPI_SWIGLU)
+            pg_epilogue_swiglu_staged(p, m, n0 + c0, min(16, n_valid - c0), v, stg);
+          else
+            pg_epilogue_qkv_staged(p, m, n0 + c0, min(16, n_valid - c0), v, rc, rs, stg);
         } else if (split_k) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) mypart[static_cast<int64_t>(c0 + j) * PG_BM + lane_base + lane] = v[j];
@@ -865,9 +905,10 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   const int n_items =
       tail ? p.tail_first + (m_tiles * p.n_ntiles - p.tail_first) * p.tail_ks : m_tiles * p.n_ntiles * p.ksplit;
   const int stage_bytes = p.kbox * (PG_BM * PG_BK * 2 + p.ntile * PG_BK * 2);
-  // the QKV epilogue of whole tiles goes through per-warp shared-memory staging
-  p.epi_stage = (p.epi == PG_EPI_QKV || p.epi == PG_EPI_QKV_ROPE) && p.ksplit == 1 && p.head_dim % 32 == 0 &&
-                p.d_model % 32 == 0;
+  // the QKV / SwiGLU epilogue of whole tiles goes through per-warp shared-memory staging
+  p.epi_stage = p.ksplit == 1 && (((p.epi == PG_EPI_QKV || p.epi == PG_EPI_QKV_ROPE) && p.head_dim % 32 == 0 &&
+                                    p.d_model % 32 == 0) ||
+                                   (p.epi == PG_EPI_SWIGLU && p.M % 32 == 0));
   const int stg_bytes = p.epi_stage ? PG_EPI_WARPS * 16 * PG_STG * 4 : 0;
   const int budget = 220 * 1024 - 1024 - stg_bytes;
   p.stages = std::min(8, budget / stage_bytes);
