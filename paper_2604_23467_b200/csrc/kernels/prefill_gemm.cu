@@ -590,67 +590,55 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
 // [tile][split][token][128 rows]; this kernel sums them in split order
 // (deterministic) and applies the epilogue, one thread per (row pair, token):
 // fully parallel, instead of one CTA per tile serialising a tail reduction.
+// 2D grid: blockIdx.y = token, x * blockDim + tid = row pair -- no 64-bit index
+// division per element (the 1D version spent most of its time there: P=200
+// QKV 20.7 us for ~37 MB of traffic).
 __global__ void prefill_splitk_reduce_kernel(const PrefillGemmParams p) {
   griddep_launch_dependents();  // the next GEMM may start its weight stream (it waits for us before its tokens)
   const int n_pairs = (p.M + 1) >> 1;
-  const int64_t total = static_cast<int64_t>(n_pairs) * p.P;
-  const int64_t e0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  // this thread's first element's RoPE factors, before the wait
-  const PgRope r0 = e0 < total ? pg_rope_load(p, 2 * static_cast<int>(e0 % n_pairs), static_cast<int>(e0 / n_pairs))
-                               : PgRope{};
+  const int pr = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = blockIdx.y;
+  const bool live = pr < n_pairs;
+  const int m = 2 * pr;
+  // this thread's RoPE factors, before the wait
+  const PgRope r0 = live ? pg_rope_load(p, m, n) : PgRope{};
   griddep_wait();  // launched with PDL behind the GEMM: partials complete
-  for (int64_t e = e0; e < total; e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int n = static_cast<int>(e / n_pairs);
-    const int pr = static_cast<int>(e - static_cast<int64_t>(n) * n_pairs);
-    const int m = 2 * pr;
-    const int m_tile = m / PG_BM, n_tile = n / p.ntile;
-    const int r = m - m_tile * PG_BM, nn = n - n_tile * p.ntile;
-    const float* base = p.part + (static_cast<int64_t>(m_tile * p.n_ntiles + n_tile) * p.ksplit) * p.ntile * PG_BM;
-    float va = 0.0f, vb = 0.0f;
-    for (int sp = 0; sp < p.ksplit; ++sp) {
-      const float* q = base + (static_cast<int64_t>(sp) * p.ntile + nn) * PG_BM + r;
-      va += q[0];
-      vb += q[1];
-    }
-    pg_epilogue_pair(p, m, n, va, vb, e == e0 ? r0 : pg_rope_load(p, m, n));
+  if (!live) return;
+  const int m_tile = m / PG_BM, n_tile = n / p.ntile;
+  const int r = m - m_tile * PG_BM, nn = n - n_tile * p.ntile;
+  const float* base = p.part + (static_cast<int64_t>(m_tile * p.n_ntiles + n_tile) * p.ksplit) * p.ntile * PG_BM;
+  float va = 0.0f, vb = 0.0f;
+  for (int sp = 0; sp < p.ksplit; ++sp) {
+    const float2 q = *reinterpret_cast<const float2*>(base + (static_cast<int64_t>(sp) * p.ntile + nn) * PG_BM + r);
+    va += q.x;
+    vb += q.y;
   }
+  pg_epilogue_pair(p, m, n, va, vb, r0);
 }
 
 // Reduce of the stream-K tail: tiles [tail_first, m_tiles*n_ntiles), tail_ks
 // partials each ([tile - tail_first][split][token][128 rows]), summed in split
-// order, then the GEMM's epilogue; one thread per (row pair, token).
+// order, then the GEMM's epilogue; one thread per (row pair, token): block
+// (x, y) = 4 tokens [4x, 4x+4) of tail tile y, 64 row pairs per token.
 __global__ void prefill_tail_reduce_kernel(const PrefillGemmParams p) {
   griddep_launch_dependents();
-  const int m_tiles = (p.M + PG_BM - 1) / PG_BM;
-  const int n_tail = m_tiles * p.n_ntiles - p.tail_first;
-  const int per_tile = (PG_BM / 2) * p.ntile;
-  const int64_t total = static_cast<int64_t>(n_tail) * per_tile;
-  auto coords = [&](int64_t e, int& t, int& nn, int& r, int& m, int& n) {
-    t = static_cast<int>(e / per_tile);
-    const int r2 = static_cast<int>(e - static_cast<int64_t>(t) * per_tile);
-    nn = r2 / (PG_BM / 2);
-    r = 2 * (r2 - nn * (PG_BM / 2));
-    const int tile = p.tail_first + t;
-    const int m_tile = tile / p.n_ntiles, n_tile = tile - m_tile * p.n_ntiles;
-    m = m_tile * PG_BM + r;
-    n = n_tile * p.ntile + nn;
-  };
+  const int t = blockIdx.y;
+  const int nn = blockIdx.x * 4 + (threadIdx.x >> 6);
+  const int r = 2 * (threadIdx.x & 63);
+  const int tile = p.tail_first + t;
+  const int m_tile = tile / p.n_ntiles, n_tile = tile - m_tile * p.n_ntiles;
+  const int m = m_tile * PG_BM + r, n = n_tile * p.ntile + nn;
   griddep_wait();  // launched with PDL behind the GEMM: partials complete
   // (no pre-wait RoPE loads here: measured slower at P >= 200, unlike the short-prompt reduce)
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int t, nn, r, m, n;
-    coords(e, t, nn, r, m, n);
-    if (m >= p.M || n >= p.P) continue;
-    const float* base = p.part + static_cast<int64_t>(t) * p.tail_ks * p.ntile * PG_BM;
-    float va = 0.0f, vb = 0.0f;
-    for (int sp = 0; sp < p.tail_ks; ++sp) {
-      const float* q = base + (static_cast<int64_t>(sp) * p.ntile + nn) * PG_BM + r;
-      va += q[0];
-      vb += q[1];
-    }
-    pg_epilogue_pair(p, m, n, va, vb, pg_rope_load(p, m, n));
+  if (nn >= p.ntile || m >= p.M || n >= p.P) return;
+  const float* base = p.part + static_cast<int64_t>(t) * p.tail_ks * p.ntile * PG_BM;
+  float va = 0.0f, vb = 0.0f;
+  for (int sp = 0; sp < p.tail_ks; ++sp) {
+    const float2 q = *reinterpret_cast<const float2*>(base + (static_cast<int64_t>(sp) * p.ntile + nn) * PG_BM + r);
+    va += q.x;
+    vb += q.y;
   }
+  pg_epilogue_pair(p, m, n, va, vb, pg_rope_load(p, m, n));
 }
 
 // Deferred reduce of a residual GEMM (epi RESID, split K) + RMSNorm of the
@@ -933,11 +921,10 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   if (out) *out = p;
   if (e != cudaSuccess) return e;
   if (tail) {  // reduce + epilogue of the tail tiles
-    const int64_t work = static_cast<int64_t>(m_tiles * p.n_ntiles - p.tail_first) * (PG_BM / 2) * p.ntile;
+    const int n_tail = m_tiles * p.n_ntiles - p.tail_first;
     cudaLaunchConfig_t rc = {};
-    // one (row pair, token) per thread: every partial load of the grid is in
-    // flight at once (a grid-stride loop of dependent round trips measured 13 us)
-    rc.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>((work + 255) / 256, 64 * num_sms(dev))));
+    // one (row pair, token) per thread: every partial load of the grid in flight at once
+    rc.gridDim = dim3((p.ntile + 3) / 4, n_tail);
     rc.blockDim = dim3(256);
     rc.stream = s;
     rc.attrs = attr;
@@ -945,10 +932,8 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
     return cudaLaunchKernelEx(&rc, prefill_tail_reduce_kernel, p);
   }
   if (p.ksplit == 1 || (p.defer_reduce && p.epi == PG_EPI_RESID)) return e;
-  const int64_t work = static_cast<int64_t>((p.M + 1) / 2) * p.P;
-  const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 64 * num_sms(dev)));
   cudaLaunchConfig_t rc = {};
-  rc.gridDim = dim3(blocks);
+  rc.gridDim = dim3(((p.M + 1) / 2 + 255) / 256, p.P);
   rc.blockDim = dim3(256);
   rc.stream = s;
   rc.attrs = attr;
