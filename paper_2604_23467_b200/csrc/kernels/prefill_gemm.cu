@@ -36,7 +36,10 @@ constexpr int PG_BM = 128;        // weight rows per CTA (UMMA M)
 constexpr int PG_BK = 64;         // K elements per stage (one 128-byte swizzle row)
 constexpr int PG_UK = 16;         // K per tcgen05.mma (kind::f16)
 constexpr int PG_EPI_WARPS = 8;    // max: two warps per TMEM lane quadrant, splitting the token columns
-constexpr int PG_THREADS = (2 + PG_EPI_WARPS) * 32;  // TMA warp, MMA warp, epilogue warps (max)
+// weight (A) TMA warp, MMA warp, epilogue warps (max), token (B) TMA warp -- two
+// producer warps: one thread issuing both operands' boxes took ~300 cycles per
+// TMA instruction, longer than a stage's MMAs (tools/tma_rows_bench.cu)
+constexpr int PG_THREADS = (3 + PG_EPI_WARPS) * 32;
 constexpr int PG_MAX_NT = 256;    // tokens per N tile (UMMA N max)
 
 // ---- tcgen05 / TMA primitives (inline PTX) --------------------------------------
@@ -439,12 +442,12 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 2);  // the A and the B producer
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], blockDim.x / 32 - 2);  // one arrival per epilogue warp
+      mbar_init(&acc_empty[b], blockDim.x / 32 - 3);  // one arrival per epilogue warp
     }
     mbar_fence_init();
   }
@@ -460,40 +463,54 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
   const uint32_t tmem = tmem_base;
   griddep_launch_dependents();
 
+  const int b_warp = static_cast<int>(blockDim.x / 32) - 1;  // the token (B) producer
+  const uint32_t a_bytes = p.kbox * a_box, b_bytes = p.kbox * b_box;
   if (warp == 0) {
     if (lane == 0) {
       // The weight (A) boxes of the first S stages do not depend on the previous
       // kernel: requested before the dependency wait (the small kernels ahead of
       // a GEMM trigger their dependents at entry, so this CTA can be resident and
-      // streaming while they run); the token (B) boxes follow after the wait.
+      // streaming while they run); the token (B) boxes come from warp b_warp.
       int npre = 0;
       for (int w = blockIdx.x; w < n_items && npre < S; w += gridDim.x) {
         int m_tile, n_tile, split, kb0, kb1;
         decode(w, m_tile, n_tile, split, kb0, kb1);
         for (int kb = kb0; kb < kb1 && npre < S; ++kb, ++npre) {
           uint8_t* st = smem + static_cast<size_t>(npre) * stage_bytes;
-          mbar_arrive_expect_tx(&full[npre], stage_bytes);
+          mbar_arrive_expect_tx(&full[npre], a_bytes);
           for (int j = 0; j < p.kbox; ++j)
             tma_load_2d(st + j * a_box, &map_w, kb * kstep + j * PG_BK, m_tile * PG_BM, &full[npre]);
         }
       }
-      griddep_wait();
       int i = 0;  // global stage counter across items
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+        int m_tile, n_tile, split, kb0, kb1;
+        decode(w, m_tile, n_tile, split, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+          if (i < npre) continue;
+          const int s = i % S;
+          uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
+          mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], a_bytes);
+          for (int j = 0; j < p.kbox; ++j)
+            tma_load_2d(st + j * a_box, &map_w, kb * kstep + j * PG_BK, m_tile * PG_BM, &full[s]);
+        }
+      }
+    }
+  } else if (warp == b_warp) {
+    if (lane == 0) {
+      griddep_wait();  // the tokens are the previous kernel's output
+      int i = 0;
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
         int m_tile, n_tile, split, kb0, kb1;
         decode(w, m_tile, n_tile, split, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int s = i % S;
           uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
-          if (i >= npre) {
-            mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full[s], stage_bytes);
-          }
-          for (int j = 0; j < p.kbox; ++j) {
-            const int k0 = kb * kstep + j * PG_BK;
-            if (i >= npre) tma_load_2d(st + j * a_box, &map_w, k0, m_tile * PG_BM, &full[s]);
-            tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, k0, n_tile * p.ntile, &full[s]);
-          }
+          mbar_wait(&empty[s], ((i / S) & 1) ^ 1);  // a fresh slot passes at once
+          mbar_arrive_expect_tx(&full[s], b_bytes);
+          for (int j = 0; j < p.kbox; ++j)
+            tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, kb * kstep + j * PG_BK, n_tile * p.ntile, &full[s]);
         }
       }
     }
@@ -534,7 +551,7 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
     // epilogue's own memory round trips -- RoPE table, residual -- halve)
     const int lane_base = 32 * (warp & 3);
     const int half = (warp - 2) >> 2;                      // column group of this warp
-    const int groups = (static_cast<int>(blockDim.x) / 32 - 2) >> 2;  // warps per lane quadrant
+    const int groups = (static_cast<int>(blockDim.x) / 32 - 3) >> 2;  // warps per lane quadrant
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(lane_base) << 16);
     int it = 0;
     for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
@@ -908,7 +925,7 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   cfg.gridDim = dim3(std::min(n_items, num_sms(dev)));
   // two token tiles (P > 256): 8 epilogue warps (the epilogue's memory round
   // trips dominate a one-item CTA); otherwise 4 (measured faster)
-  cfg.blockDim = dim3(p.n_ntiles > 1 ? PG_THREADS : 6 * 32);
+  cfg.blockDim = dim3(p.n_ntiles > 1 ? PG_THREADS : 7 * 32);
   cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + stg_bytes + 1024;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
