@@ -71,7 +71,10 @@ class ClockSampler:
         self.mem = None  # [current, max] memory clock MHz (box-to-box context for HBM-bound numbers)
 
     def _nvml_loop(self, nv, h):
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception:
+            return self._smi_loop()
         while not self.stop.is_set():
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
@@ -121,6 +124,19 @@ class ClockSampler:
         self.stop.set()
         if self.thread:
             self.thread.join(timeout=5)
+        if not self.rows:  # NVML loop died (seen once on a pool box): one nvidia-smi sample, labelled as such
+            try:
+                fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                          "clocks_event_reasons.sw_power_cap")
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + fields,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+                r = [x.strip() for x in out.stdout.strip().splitlines()[0].split(",")]
+                rb = sum(b for b, v in zip([0x8, 0x20, 0x40, 0x4], r[2:6]) if v.lower() == "active")
+                self.rows.append((float(r[0]), float(r[1]), rb))
+                self.source = "nvidia-smi (one sample right after the timed region; NVML unavailable)"
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
