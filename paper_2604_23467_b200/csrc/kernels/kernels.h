@@ -146,6 +146,7 @@ struct PrefillGemmParams {
   // m_tiles*n_ntiles) -- the last, partial wave -- are split tail_ks ways in K
   // so their units fill the SMs; their partials go through a reduce kernel
   int tail_first = 0, tail_ks = 0;
+  int box3d = 0;      // set by the launcher: both maps are 3D ({64, rows, K/64}): one TMA box per stage and operand
   int epi_stage = 0;  // set by the launcher: QKV epilogue through per-warp shared-memory staging
   int epi = PG_EPI_STORE;
   float* out = nullptr;

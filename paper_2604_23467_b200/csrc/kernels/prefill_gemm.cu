@@ -52,6 +52,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// 3D box {64 K, rows, kbox K blocks} of a {64, rows, K/64} view (row stride K*2 B,
+// K-block stride 128 B): kbox 128-byte-swizzled [rows][64] tiles, one after the
+// other -- the stage layout of kbox 2D boxes, in one instruction.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---- epilogue -------------------------------------------------------------------
 // One thread = one weight row m, 16 tokens at a time (the 16 TMEM columns of
 // one tcgen05.ld); every global load the epilogue needs for those tokens (RoPE
@@ -478,8 +489,11 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
         for (int kb = kb0; kb < kb1 && npre < S; ++kb, ++npre) {
           uint8_t* st = smem + static_cast<size_t>(npre) * stage_bytes;
           mbar_arrive_expect_tx(&full[npre], a_bytes);
-          for (int j = 0; j < p.kbox; ++j)
-            tma_load_2d(st + j * a_box, &map_w, kb * kstep + j * PG_BK, m_tile * PG_BM, &full[npre]);
+          if (p.box3d)
+            tma_load_3d(st, &map_w, 0, m_tile * PG_BM, kb * p.kbox, &full[npre]);
+          else
+            for (int j = 0; j < p.kbox; ++j)
+              tma_load_2d(st + j * a_box, &map_w, kb * kstep + j * PG_BK, m_tile * PG_BM, &full[npre]);
         }
       }
       int i = 0;  // global stage counter across items
@@ -492,8 +506,11 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
           uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
           mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[s], a_bytes);
-          for (int j = 0; j < p.kbox; ++j)
-            tma_load_2d(st + j * a_box, &map_w, kb * kstep + j * PG_BK, m_tile * PG_BM, &full[s]);
+          if (p.box3d)
+            tma_load_3d(st, &map_w, 0, m_tile * PG_BM, kb * p.kbox, &full[s]);
+          else
+            for (int j = 0; j < p.kbox; ++j)
+              tma_load_2d(st + j * a_box, &map_w, kb * kstep + j * PG_BK, m_tile * PG_BM, &full[s]);
         }
       }
     }
@@ -509,8 +526,11 @@ __global__ void __launch_bounds__(PG_THREADS, 1)
           uint8_t* st = smem + static_cast<size_t>(s) * stage_bytes;
           mbar_wait(&empty[s], ((i / S) & 1) ^ 1);  // a fresh slot passes at once
           mbar_arrive_expect_tx(&full[s], b_bytes);
-          for (int j = 0; j < p.kbox; ++j)
-            tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, kb * kstep + j * PG_BK, n_tile * p.ntile, &full[s]);
+          if (p.box3d)
+            tma_load_3d(st + p.kbox * a_box, &map_x, 0, n_tile * p.ntile, kb * p.kbox, &full[s]);
+          else
+            for (int j = 0; j < p.kbox; ++j)
+              tma_load_2d(st + p.kbox * a_box + j * b_box, &map_x, kb * kstep + j * PG_BK, n_tile * p.ntile, &full[s]);
         }
       }
     }
@@ -782,6 +802,20 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int 
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// {64, rows, K/64} view of a row-major [rows, K] bf16 matrix (K % 64 == 0), box
+// {64, box_rows, kbox}, 128-byte swizzle: kbox K blocks in one TMA instruction.
+bool make_map3(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows, int kbox) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || cols % PG_BK) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(PG_BK), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(cols / PG_BK)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2, static_cast<cuuint64_t>(PG_BK) * 2};
+  const cuuint32_t box[3] = {PG_BK, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(kbox)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 }  // namespace
 
 // Tiling policy: tokens are split into N tiles of <= 128 (P > 128) so large
@@ -919,8 +953,18 @@ static cudaError_t launch_prefill_gemm_impl(const void* w, const void* x, Prefil
   p.stages = std::min(8, budget / stage_bytes);
   if (p.stages < 2) return cudaErrorInvalidValue;
   CUtensorMap mw, mx;
-  if (!make_map(&mw, w, p.M, p.K, PG_BM)) return cudaErrorInvalidValue;
-  if (!make_map(&mx, x, p.P, p.K, p.ntile)) return cudaErrorInvalidValue;
+  // several K blocks per stage (short prompts): one 3D box per operand and stage
+  // instead of kbox 2D boxes when K is a whole number of blocks
+  p.box3d = 0;
+#ifndef GRT_NO_BOX3D
+  if (p.kbox > 1 && p.K % (PG_BK * p.kbox) == 0 && make_map3(&mw, w, p.M, p.K, PG_BM, p.kbox) &&
+      make_map3(&mx, x, p.P, p.K, p.ntile, p.kbox))
+    p.box3d = 1;
+#endif
+  if (!p.box3d) {
+    if (!make_map(&mw, w, p.M, p.K, PG_BM)) return cudaErrorInvalidValue;
+    if (!make_map(&mx, x, p.P, p.K, p.ntile)) return cudaErrorInvalidValue;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(std::min(n_items, num_sms(dev)));
   // two token tiles (P > 256): 8 epilogue warps (the epilogue's memory round
