@@ -69,11 +69,13 @@ class ClockSampler:
         self.thread = None
         self.source = None
         self.mem = None  # [current, max] memory clock MHz (box-to-box context for HBM-bound numbers)
+        self.err = None
 
     def _nvml_loop(self, nv, h):
         try:
             mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        except Exception:
+        except Exception as e:
+            self.err = f"{type(e).__name__}: {e}"[:120]
             return self._smi_loop()
         while not self.stop.is_set():
             try:
@@ -83,8 +85,9 @@ class ClockSampler:
                 if not self.mem:
                     self.mem = [nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM),
                                 nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_MEM)]
-            except Exception:
-                pass
+            except Exception as e:  # keep the first failure for the line (diagnosis)
+                if not self.err:
+                    self.err = f"{type(e).__name__}: {e}"[:120]
             self.stop.wait(0.005)
 
     def _smi_loop(self):
@@ -140,11 +143,12 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0, "error": self.err}
         reasons = sorted(n for n, b in self.REASONS.items() if any(r[2] & b for r in self.rows))
         return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
                 "reasons": reasons, "samples": len(self.rows), "source": self.source,
-                "mem_mhz": self.mem[0] if self.mem else None, "mem_max_mhz": self.mem[1] if self.mem else None}
+                "mem_mhz": self.mem[0] if self.mem else None, "mem_max_mhz": self.mem[1] if self.mem else None,
+                **({"nvml_error": self.err} if self.err else {})}
 
 
 def cpu_reference_sample(layers=(1, 2), gen=4, warmup=1, timeout=600):
